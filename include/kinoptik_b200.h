@@ -1,0 +1,162 @@
+/*
+ * kinoptik_b200 -- C ABI of the B200 (sm_100a) batched LM-IK engine.
+ *
+ * Plain pointers, sizes and an opaque model handle; no torch or CUDA C++
+ * types cross this boundary (streams are passed as `void*` = cudaStream_t).
+ * Every array argument marked "device" must point to device memory on the
+ * current CUDA device; "host" arrays are read synchronously before return.
+ *
+ * Each entry point names the reference interface it replaces.  The reference
+ * (`kinoptik`, /root/reference/pkg/src/kinoptik) is pure NumPy and has no FFI
+ * of its own; INTEGRATION.md shows the ctypes stub a kinoptik maintainer
+ * would add at each of these seams.
+ *
+ * Conventions (liegroups.py:1-13): quaternions (w,x,y,z), twists
+ * translation-first, right-multiplicative retraction; a pose is 7 doubles
+ * (w,x,y,z,px,py,pz).  Configurations are the actuated joints in the
+ * topological (BFS) order of robot.py:325-340.
+ *
+ * Status codes: 0 ok; KOP_EINVAL invalid argument (the reference raises
+ * ValueError); KOP_EUNSUPPORTED kinematic shape not compiled in (the
+ * reference would run it -- the caller must raise UnsupportedFeatureError,
+ * never fall back to the CPU); KOP_ECUDA a CUDA launch/runtime error.
+ * kop_last_error() returns a thread-local message for the last failure.
+ *
+ * Thread safety: a KopModel is immutable after creation and holds no device
+ * state, so one model may be used concurrently from one host thread per GPU
+ * (robot.py:8-12 purity contract).  All launches are asynchronous on the
+ * given stream; results are bitwise reproducible run to run and independent
+ * of batch size and GPU count (no atomics, fixed reduction orders).
+ */
+#ifndef KINOPTIK_B200_H
+#define KINOPTIK_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KOP_OK 0
+#define KOP_EINVAL (-1)
+#define KOP_EUNSUPPORTED (-2)
+#define KOP_ECUDA (-3)
+
+#define KOP_FP32 0 /* measured mode: float arithmetic on the device       */
+#define KOP_FP64 1 /* parity-debug mode: double arithmetic, same algorithm */
+
+#define KOP_JOINT_FIXED 0     /* robot.py:27-36 kind codes */
+#define KOP_JOINT_REVOLUTE 1  /* revolute and continuous  */
+#define KOP_JOINT_PRISMATIC 2
+
+typedef struct KopModel KopModel;
+
+/* Kinematic tree in the reference's SoA layout, robot.py:74-112 (host). */
+typedef struct {
+  int32_t num_links;            /* L; link 0 is the root (robot.py:418-419)   */
+  int32_t num_joints;           /* J, topological order                        */
+  int32_t num_actuated;         /* n                                           */
+  const int32_t* parent_link;   /* [J]                                         */
+  const int32_t* child_link;    /* [J]                                         */
+  const int32_t* kind;          /* [J] KOP_JOINT_*                             */
+  const int32_t* qcol;          /* [J] actuated column, -1 for fixed           */
+  const double* mult;           /* [J] mimic multiplier (1 otherwise)          */
+  const double* offset;         /* [J] mimic offset (0 otherwise)              */
+  const double* origin_wxyz;    /* [J*4] joint origin rotation                 */
+  const double* origin_xyz;     /* [J*3] joint origin translation              */
+  const double* axis;           /* [J*3] unit joint axis in the joint frame    */
+  const double* lower;          /* [n] (-inf where absent, robot.py:114-126)   */
+  const double* upper;          /* [n] (+inf where absent)                     */
+  const double* rest;           /* [n] rest pose (robot.py:128-141)            */
+} KopModelDesc;
+
+/* IK-Beam request scalars: IkRequest (tasks.py:40-60) + CostWeights
+ * (costs.py:52-62).  Defaults: 50, 10, 100, 0.01; 64/16/6/4; 5 mm, 0.05. */
+typedef struct {
+  double w_position, w_orientation, w_limit, w_rest;
+  int32_t seeds, total_steps, prune_after, keep;
+  double success_pos_tol, success_rot_tol;
+  int32_t precision; /* KOP_FP32 | KOP_FP64 */
+} KopIkParams;
+
+/* --- model ----------------------------------------------------------------
+ * replaces: robot.RobotModel.__init__ tables (robot.py:55-144); the URDF /
+ * sidecar parse itself stays on the host (robot.py:221-387). */
+int kop_model_create(const KopModelDesc* desc, KopModel** out);
+void kop_model_destroy(KopModel* model);
+/* Moving joints on the root->link chain (fixed joints folded); -1 on error. */
+int kop_model_chain_length(const KopModel* model, int32_t link);
+const char* kop_last_error(void);
+const char* kop_build_info(void);
+
+/* --- forward kinematics ---------------------------------------------------
+ * replaces: robot.fk_arrays(model, q[B,n]) (robot.py:404-448).
+ * q: device [B*n] double.  Outputs (device, double, any may be NULL):
+ * link_wxyz [B*L*4] raw (non-canonical) quaternions, link_xyz [B*L*3],
+ * joint_xyz [B*J*3] joint anchors, joint_axis [B*J*3] world axes. */
+int kop_fk(const KopModel* model, int32_t precision, const double* q, int64_t batch,
+           double* link_wxyz, double* link_xyz, double* joint_xyz, double* joint_axis,
+           void* stream);
+
+/* --- lane engine ----------------------------------------------------------
+ * replaces: beam.IkLaneProblem(model, link, target, weights...) with
+ * .residuals_and_jacobian (beam.py:133-180), .start_state (beam.py:182-196)
+ * and .run(state, steps) (beam.py:198-240), generalised to one target per
+ * lane.  target_inv: device [T*7] double, the INVERSE target pose per target
+ * (beam.py:89-91); lane_target: device [B] int32 target index per lane.
+ * State arrays (device, double): q [B*n] in/out, damping [B] in/out,
+ * cost [B] in/out; history: device [B*steps] double (may be NULL).
+ * weights: host [4] (position, orientation, limit, rest). */
+int kop_lane_residuals_jacobian(const KopModel* model, int32_t link, int32_t precision,
+                                const double* weights, const double* target_inv,
+                                const int32_t* lane_target, const double* q, int64_t lanes,
+                                double* residual, double* jacobian, void* stream);
+int kop_lane_start(const KopModel* model, int32_t link, int32_t precision, const double* weights,
+                   const double* target_inv, const int32_t* lane_target, const double* q,
+                   int64_t lanes, double* damping, double* cost, void* stream);
+int kop_lane_run(const KopModel* model, int32_t link, int32_t precision, const double* weights,
+                 const double* target_inv, const int32_t* lane_target, int64_t lanes,
+                 int32_t steps, double* q, double* damping, double* cost, double* history,
+                 void* stream);
+
+/* --- IK-Beam ----------------------------------------------------------------
+ * replaces: tasks.solve_ik_beam(IkRequest) -> IkResult (tasks.py:119-166),
+ * batched over B independent targets (the reference loops targets one by one,
+ * benchmark.py:136-151).  targets: device [B*7] double (w,x,y,z,px,py,pz);
+ * seeds: device [S*n] double, shared by every target (tasks.py:131).
+ * Outputs (device): q [B*n] double, cost [B] double, history
+ * [B*(total_steps+1)] double (NULL ok), pos_err [B], rot_err [B] double
+ * (tasks.py:109-116, evaluated in double), success [B] uint8.
+ * workspace: device scratch of kop_ik_beam_workspace_bytes() bytes. */
+int64_t kop_ik_beam_workspace_bytes(const KopModel* model, int32_t link, const KopIkParams* params,
+                                    int64_t batch);
+int kop_ik_beam(const KopModel* model, int32_t link, const KopIkParams* params,
+                const double* targets, int64_t batch, const double* seeds, void* workspace,
+                int64_t workspace_bytes, double* q_out, double* cost_out, double* history_out,
+                double* pos_err, double* rot_err, uint8_t* success, void* stream);
+
+/* --- counter-based sampling ---------------------------------------------
+ * replaces: tasks.sample_seed_configurations (tasks.py:88-106) and the draws
+ * of benchmark.generate_reachable_targets (benchmark.py:83-93): row i is
+ * numpy Generator(Philox(key=[key0, key1_base+i])).uniform(lo, hi), bit-exact;
+ * negate[j] != 0 flips column j (continuous joints, tasks.py:105).
+ * lo, hi, negate: host [n]; out: device [count*n] double. */
+int kop_sample_uniform(uint64_t key0, uint64_t key1_base, int64_t count, int32_t n,
+                       const double* lo, const double* hi, const uint8_t* negate, double* out,
+                       void* stream);
+/* FK (double) of `link` at configurations q[count*n] -> canonical poses
+ * [count*7] (Transform3.from_parts canonicalisation, liegroups.py:323-325). */
+int kop_link_poses(const KopModel* model, int32_t link, const double* q, int64_t count,
+                   double* poses, void* stream);
+
+/* --- measurement helper ---------------------------------------------------
+ * FP32 FMA-pipe microbenchmark used for the roofline denominator (no FP32
+ * entry exists in MEASURED_PEAKS.json).  Writes flops executed to *flops. */
+int kop_fma_peak_kernel(int32_t blocks, int32_t threads, int32_t iters, float* sink, double* flops,
+                        void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* KINOPTIK_B200_H */

@@ -1,0 +1,89 @@
+"""ctypes binding of the in-tree C ABI (``include/kinoptik_b200.h``).
+
+The shared library is built by ``paper_2505_03728_b200._build`` (or
+``__graft_entry__.build()``) into this package directory.  There is no CPU
+fallback: if the library is missing, importing anything that computes raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkinoptik_b200.so")
+
+KOP_OK, KOP_EINVAL, KOP_EUNSUPPORTED, KOP_ECUDA = 0, -1, -2, -3
+KOP_FP32, KOP_FP64 = 0, 1
+
+_p = C.c_void_p
+_i32, _i64, _u64, _f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
+
+
+class KopModelDesc(C.Structure):
+    _fields_ = [
+        ("num_links", _i32), ("num_joints", _i32), ("num_actuated", _i32),
+        ("parent_link", _p), ("child_link", _p), ("kind", _p), ("qcol", _p),
+        ("mult", _p), ("offset", _p), ("origin_wxyz", _p), ("origin_xyz", _p), ("axis", _p),
+        ("lower", _p), ("upper", _p), ("rest", _p),
+    ]
+
+
+class KopIkParams(C.Structure):
+    _fields_ = [
+        ("w_position", _f64), ("w_orientation", _f64), ("w_limit", _f64), ("w_rest", _f64),
+        ("seeds", _i32), ("total_steps", _i32), ("prune_after", _i32), ("keep", _i32),
+        ("success_pos_tol", _f64), ("success_rot_tol", _f64), ("precision", _i32),
+    ]
+
+
+# name -> (restype, argtypes); must match include/kinoptik_b200.h exactly
+SIGNATURES = {
+    "kop_model_create": (C.c_int, [C.POINTER(KopModelDesc), C.POINTER(_p)]),
+    "kop_model_destroy": (None, [_p]),
+    "kop_model_chain_length": (C.c_int, [_p, _i32]),
+    "kop_last_error": (C.c_char_p, []),
+    "kop_build_info": (C.c_char_p, []),
+    "kop_fk": (C.c_int, [_p, _i32, _p, _i64, _p, _p, _p, _p, _p]),
+    "kop_lane_residuals_jacobian": (C.c_int, [_p, _i32, _i32, _p, _p, _p, _p, _i64, _p, _p, _p]),
+    "kop_lane_start": (C.c_int, [_p, _i32, _i32, _p, _p, _p, _p, _i64, _p, _p, _p]),
+    "kop_lane_run": (C.c_int, [_p, _i32, _i32, _p, _p, _p, _i64, _i32, _p, _p, _p, _p, _p]),
+    "kop_ik_beam_workspace_bytes": (_i64, [_p, _i32, C.POINTER(KopIkParams), _i64]),
+    "kop_ik_beam": (C.c_int, [_p, _i32, C.POINTER(KopIkParams), _p, _i64, _p, _p, _i64,
+                              _p, _p, _p, _p, _p, _p, _p]),
+    "kop_sample_uniform": (C.c_int, [_u64, _u64, _i64, _i32, _p, _p, _p, _p, _p]),
+    "kop_link_poses": (C.c_int, [_p, _i32, _p, _i64, _p, _p]),
+    "kop_fma_peak_kernel": (C.c_int, [_i32, _i32, _i32, _p, C.POINTER(_f64), _p]),
+}
+
+_lib = None
+
+
+def lib():
+    """Load (once) and return the CDLL; raise loudly if it is not built."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(
+                f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+                "(there is no CPU fallback)")
+        dll = C.CDLL(LIB_PATH)
+        for name, (res, args) in SIGNATURES.items():
+            fn = getattr(dll, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = dll
+    return _lib
+
+
+def check(status: int, what: str) -> None:
+    """Map a KOP_* status to the reference's exception types."""
+    if status == KOP_OK:
+        return
+    msg = lib().kop_last_error().decode(errors="replace")
+    if status == KOP_EINVAL:
+        raise ValueError(f"{what}: {msg}")
+    if status == KOP_EUNSUPPORTED:
+        from .errors import UnsupportedFeatureError
+        raise UnsupportedFeatureError(f"{what}: {msg}")
+    raise RuntimeError(f"{what}: {msg}")

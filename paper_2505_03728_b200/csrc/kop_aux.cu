@@ -1,0 +1,236 @@
+// Non-hot-path kernels: full-tree FK (the forward_kinematics / fk_arrays
+// API), single-link FK for benchmark targets, numpy-exact Philox sampling,
+// and the FP32 FMA-pipe microbenchmark that gives the roofline denominator.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kop_kernels.cuh"
+
+namespace kop {
+
+// ---------------------------------------------------------------------------
+// Full-tree FK in the reference's operation order (robot.py:404-448):
+// for each joint in topological order: fq = q_parent * q_origin,
+// fp = p_parent + R_parent p_origin; anchor = fp, world axis = R(fq) axis;
+// revolute: child = fq * (cos th/2, sin th/2 axis); prismatic: fp + th axis_w.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(128)
+k_fk_tree(const TreeParams P, const double* __restrict__ q, int64_t B, double* __restrict__ lq_out,
+          double* __restrict__ lp_out, double* __restrict__ jp_out, double* __restrict__ ja_out) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  quat<T> lq[kMaxLinks];
+  vec3<T> lp[kMaxLinks];
+  lq[0] = {T(1), T(0), T(0), T(0)};
+  lp[0] = {T(0), T(0), T(0)};
+  const double* qb = q + b * P.n;
+  for (int j = 0; j < P.nj; ++j) {
+    const quat<T> pq = lq[P.parent[j]];
+    const vec3<T> pp = lp[P.parent[j]];
+    const quat<T> fq = qmul(pq, quat<T>{T(P.oq[j][0]), T(P.oq[j][1]), T(P.oq[j][2]), T(P.oq[j][3])});
+    const vec3<T> o = qrot(pq, vec3<T>{T(P.op[j][0]), T(P.op[j][1]), T(P.op[j][2])});
+    const vec3<T> fp{pp.x + o.x, pp.y + o.y, pp.z + o.z};
+    const vec3<T> axis{T(P.axis[j][0]), T(P.axis[j][1]), T(P.axis[j][2])};
+    const vec3<T> wa = qrot(fq, axis);
+    if (jp_out) {
+      double* d = jp_out + (b * P.nj + j) * 3;
+      d[0] = fp.x; d[1] = fp.y; d[2] = fp.z;
+    }
+    if (ja_out) {
+      double* d = ja_out + (b * P.nj + j) * 3;
+      d[0] = wa.x; d[1] = wa.y; d[2] = wa.z;
+    }
+    const int c = P.child[j];
+    if (P.kind[j] == 0) {
+      lq[c] = fq;
+      lp[c] = fp;
+      continue;
+    }
+    const T th = T(qb[P.qcol[j]]) * T(P.mult[j]) + T(P.offset[j]);
+    if (P.kind[j] == 1) {
+      T s, co;
+      sincos_t(T(0.5) * th, &s, &co);
+      lq[c] = qmul(fq, quat<T>{co, s * axis.x, s * axis.y, s * axis.z});
+      lp[c] = fp;
+    } else {
+      lq[c] = fq;
+      lp[c] = {fp.x + th * wa.x, fp.y + th * wa.y, fp.z + th * wa.z};
+    }
+  }
+  for (int l = 0; l < P.nl; ++l) {
+    if (lq_out) {
+      double* d = lq_out + (b * P.nl + l) * 4;
+      d[0] = lq[l].w; d[1] = lq[l].x; d[2] = lq[l].y; d[3] = lq[l].z;
+    }
+    if (lp_out) {
+      double* d = lp_out + (b * P.nl + l) * 3;
+      d[0] = lp[l].x; d[1] = lp[l].y; d[2] = lp[l].z;
+    }
+  }
+}
+
+cudaError_t launch_fk_tree(const TreeParams& P, int precision, const double* q, int64_t B,
+                           double* lq, double* lp, double* jp, double* ja, cudaStream_t st) {
+  if (B == 0) return cudaSuccess;
+  const int tpb = 128;
+  const unsigned blocks = (unsigned)((B + tpb - 1) / tpb);
+  if (precision == 0)
+    k_fk_tree<float><<<blocks, tpb, 0, st>>>(P, q, B, lq, lp, jp, ja);
+  else
+    k_fk_tree<double><<<blocks, tpb, 0, st>>>(P, q, B, lq, lp, jp, ja);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// FK of one link along its root path (joints of `path` are consecutive:
+// each joint's parent is the previous joint's child), canonicalised like
+// Transform3.from_parts (liegroups.py:33-45, 372-374).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128)
+k_link_pose(const TreeParams P, const double* __restrict__ q, int64_t B, double* __restrict__ out) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  quat<double> pq{1.0, 0.0, 0.0, 0.0};
+  vec3<double> pp{0.0, 0.0, 0.0};
+  const double* qb = q + b * P.n;
+  for (int j = 0; j < P.nj; ++j) {
+    const quat<double> fq = qmul(pq, quat<double>{P.oq[j][0], P.oq[j][1], P.oq[j][2], P.oq[j][3]});
+    const vec3<double> o = qrot(pq, vec3<double>{P.op[j][0], P.op[j][1], P.op[j][2]});
+    const vec3<double> fp{pp.x + o.x, pp.y + o.y, pp.z + o.z};
+    const vec3<double> axis{P.axis[j][0], P.axis[j][1], P.axis[j][2]};
+    if (P.kind[j] == 0) {
+      pq = fq;
+      pp = fp;
+      continue;
+    }
+    const double th = qb[P.qcol[j]] * P.mult[j] + P.offset[j];
+    if (P.kind[j] == 1) {
+      double s, c;
+      sincos(0.5 * th, &s, &c);
+      pq = qmul(fq, quat<double>{c, s * axis.x, s * axis.y, s * axis.z});
+      pp = fp;
+    } else {
+      const vec3<double> wa = qrot(fq, axis);
+      pq = fq;
+      pp = {fp.x + th * wa.x, fp.y + th * wa.y, fp.z + th * wa.z};
+    }
+  }
+  const double n = sqrt(pq.w * pq.w + pq.x * pq.x + pq.y * pq.y + pq.z * pq.z);
+  double w = pq.w / n, x = pq.x / n, y = pq.y / n, z = pq.z / n;
+  double sign = w < 0.0 ? -1.0 : 1.0;
+  if (w == 0.0) {
+    const double ax = fabs(x), ay = fabs(y), az = fabs(z);
+    const double lead = (ax >= ay && ax >= az) ? x : (ay >= az ? y : z);
+    sign = lead < 0.0 ? -1.0 : 1.0;
+  }
+  double* d = out + b * 7;
+  d[0] = w * sign; d[1] = x * sign; d[2] = y * sign; d[3] = z * sign;
+  d[4] = pp.x; d[5] = pp.y; d[6] = pp.z;
+}
+
+cudaError_t launch_link_pose(const TreeParams& path, const double* q, int64_t B, double* poses,
+                             cudaStream_t st) {
+  if (B == 0) return cudaSuccess;
+  const int tpb = 128;
+  k_link_pose<<<(unsigned)((B + tpb - 1) / tpb), tpb, 0, st>>>(path, q, B, poses);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// numpy.random.Philox (Philox4x64-10, Random123 constants): the counter is
+// incremented BEFORE each 4-word block (numpy philox_next), key = (k0, k1),
+// counter starts at 0.  next_double = (u >> 11) * 2^-53; Generator.uniform
+// is low + (high - low) * u (numpy random_uniform), evaluated without FMA
+// contraction so the draws are bit-identical to numpy's.
+// ---------------------------------------------------------------------------
+struct Philox {
+  uint64_t ctr[4];
+  uint64_t key[2];
+  uint64_t buf[4];
+  int pos;
+};
+
+__device__ __forceinline__ void philox_block(const uint64_t in[4], const uint64_t key_in[2], uint64_t out[4]) {
+  uint64_t c0 = in[0], c1 = in[1], c2 = in[2], c3 = in[3];
+  uint64_t k0 = key_in[0], k1 = key_in[1];
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) {
+      k0 += 0x9E3779B97F4A7C15ull;
+      k1 += 0xBB67AE8584CAA73Bull;
+    }
+    const uint64_t lo0 = 0xD2E7470EE14C6C93ull * c0, hi0 = __umul64hi(0xD2E7470EE14C6C93ull, c0);
+    const uint64_t lo1 = 0xCA5A826395121157ull * c2, hi1 = __umul64hi(0xCA5A826395121157ull, c2);
+    const uint64_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+  }
+  out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+__device__ __forceinline__ uint64_t philox_next(Philox& s) {
+  if (s.pos < 4) return s.buf[s.pos++];
+  s.ctr[0]++;
+  if (s.ctr[0] == 0) {
+    s.ctr[1]++;
+    if (s.ctr[1] == 0) {
+      s.ctr[2]++;
+      if (s.ctr[2] == 0) s.ctr[3]++;
+    }
+  }
+  philox_block(s.ctr, s.key, s.buf);
+  s.pos = 1;
+  return s.buf[0];
+}
+
+__global__ void __launch_bounds__(128)
+k_philox(uint64_t key0, uint64_t key1_base, int64_t count, int n, const double* __restrict__ lo,
+         const double* __restrict__ range, const uint8_t* __restrict__ negate, double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  Philox s;
+  s.ctr[0] = s.ctr[1] = s.ctr[2] = s.ctr[3] = 0;
+  s.key[0] = key0;
+  s.key[1] = key1_base + (uint64_t)i;
+  s.pos = 4;
+  for (int j = 0; j < n; ++j) {
+    const uint64_t u = philox_next(s);
+    const double x = __dmul_rn((double)(u >> 11), 1.0 / 9007199254740992.0);
+    double v = __dadd_rn(lo[j], __dmul_rn(range[j], x));
+    if (negate[j]) v = -v;
+    out[i * n + j] = v;
+  }
+}
+
+cudaError_t launch_philox(uint64_t key0, uint64_t key1_base, int64_t count, int n, const double* lo,
+                          const double* range, const uint8_t* negate, double* out, cudaStream_t st) {
+  if (count == 0) return cudaSuccess;
+  const int tpb = 128;
+  k_philox<<<(unsigned)((count + tpb - 1) / tpb), tpb, 0, st>>>(key0, key1_base, count, n, lo, range,
+                                                                negate, out);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// FP32 FMA-pipe peak: 16 independent immediate-operand FFMA chains/thread.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_fma_peak(float* sink, int iters) {
+  float a[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) a[k] = (float)(threadIdx.x + k) * 1e-3f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) a[k] = fmaf(a[k], 0.9999f, 0.0001f);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) s += a[k];
+  if (s == 12345.678f) sink[blockIdx.x] = s;  // never true; defeats DCE
+}
+
+cudaError_t launch_fma_peak(int blocks, int threads, int iters, float* sink, cudaStream_t st) {
+  k_fma_peak<<<blocks, threads, 0, st>>>(sink, iters);
+  return cudaGetLastError();
+}
+
+}  // namespace kop

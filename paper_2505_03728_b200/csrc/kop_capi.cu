@@ -1,0 +1,573 @@
+// C ABI (include/kinoptik_b200.h): model compilation, argument validation,
+// shape dispatch.  Host code only; every compute path launches a kernel.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/kinoptik_b200.h"
+#include "kop_kernels.cuh"
+
+using namespace kop;
+
+struct KopModel {
+  TreeParams tree;
+  std::vector<double> lower, upper, rest;
+  std::vector<int32_t> parent_joint;  // per link, -1 for the root
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+int cuda_status(cudaError_t e) {
+  if (e == cudaSuccess) return KOP_OK;
+  return fail(KOP_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e));
+}
+
+// ---- quaternion helpers (host, double) -------------------------------------
+struct HQ {
+  double w, x, y, z;
+};
+HQ hmul(const HQ& a, const HQ& b) {
+  return {a.w * b.w - (a.x * b.x + a.y * b.y + a.z * b.z),
+          a.w * b.x + b.w * a.x + (a.y * b.z - a.z * b.y),
+          a.w * b.y + b.w * a.y + (a.z * b.x - a.x * b.z),
+          a.w * b.z + b.w * a.z + (a.x * b.y - a.y * b.x)};
+}
+void hrot(const HQ& q, const double p[3], double out[3]) {
+  const double t0 = 2 * (q.y * p[2] - q.z * p[1]), t1 = 2 * (q.z * p[0] - q.x * p[2]),
+               t2 = 2 * (q.x * p[1] - q.y * p[0]);
+  out[0] = p[0] + q.w * t0 + (q.y * t2 - q.z * t1);
+  out[1] = p[1] + q.w * t1 + (q.z * t0 - q.x * t2);
+  out[2] = p[2] + q.w * t2 + (q.x * t1 - q.y * t0);
+}
+// Rotation taking +z onto the unit vector a.
+HQ align_z(const double a[3]) {
+  if (a[2] < -1.0 + 1e-12) return {0.0, 1.0, 0.0, 0.0};
+  HQ q{1.0 + a[2], -a[1], a[0], 0.0};
+  const double n = sqrt(q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z);
+  return {q.w / n, q.x / n, q.y / n, q.z / n};
+}
+
+constexpr int kChainMax = 8;
+
+// Root->link moving-joint chain with fixed joints folded and axes aligned to
+// +z (kop_chain.h).  Returns the number of moving joints or a negative status.
+int compile_chain(const KopModel& m, int link, ChainParams<double, kChainMax>& C, bool& identity) {
+  const TreeParams& P = m.tree;
+  if (link < 0 || link >= P.nl) return fail(KOP_EINVAL, "unknown link index " + std::to_string(link));
+  std::vector<int> path;
+  for (int j = m.parent_joint[link]; j >= 0; j = m.parent_joint[P.parent[j]]) path.push_back(j);
+  HQ pend{1, 0, 0, 0};
+  double pend_p[3] = {0, 0, 0};
+  int k = 0;
+  memset(&C, 0, sizeof(C));
+  for (auto it = path.rbegin(); it != path.rend(); ++it) {
+    const int j = *it;
+    const HQ oq{P.oq[j][0], P.oq[j][1], P.oq[j][2], P.oq[j][3]};
+    double o[3];
+    hrot(pend, P.op[j], o);
+    const double tp[3] = {pend_p[0] + o[0], pend_p[1] + o[1], pend_p[2] + o[2]};
+    if (P.kind[j] == KOP_JOINT_FIXED) {
+      pend = hmul(pend, oq);
+      memcpy(pend_p, tp, sizeof(tp));
+      continue;
+    }
+    if (k >= kChainMax)
+      return fail(KOP_EUNSUPPORTED, "chain has more than 8 moving joints (not compiled in)");
+    const HQ al = align_z(P.axis[j]);
+    const HQ tq = hmul(hmul(pend, oq), al);
+    C.tq[k][0] = tq.w; C.tq[k][1] = tq.x; C.tq[k][2] = tq.y; C.tq[k][3] = tq.z;
+    memcpy(C.tp[k], tp, sizeof(tp));
+    C.mult[k] = P.mult[j];
+    C.offset[k] = P.offset[j];
+    C.qcol[k] = P.qcol[j];
+    C.prismatic[k] = P.kind[j] == KOP_JOINT_PRISMATIC ? 1 : 0;
+    ++k;
+    pend = {al.w, -al.x, -al.y, -al.z};
+    pend_p[0] = pend_p[1] = pend_p[2] = 0.0;
+  }
+  C.eq[0] = pend.w; C.eq[1] = pend.x; C.eq[2] = pend.y; C.eq[3] = pend.z;
+  memcpy(C.ep, pend_p, sizeof(pend_p));
+  C.k = k;
+  identity = (k == P.n);
+  for (int i = 0; i < k && identity; ++i)
+    identity = C.qcol[i] == i && C.mult[i] == 1.0 && C.offset[i] == 0.0 && !C.prismatic[i];
+  return k;
+}
+
+template <typename T, int K>
+ChainParams<T, K> cast_chain(const ChainParams<double, kChainMax>& D) {
+  ChainParams<T, K> C;
+  memset(&C, 0, sizeof(C));
+  for (int k = 0; k < K && k < kChainMax; ++k) {
+    for (int i = 0; i < 4; ++i) C.tq[k][i] = T(D.tq[k][i]);
+    for (int i = 0; i < 3; ++i) C.tp[k][i] = T(D.tp[k][i]);
+    C.mult[k] = T(D.mult[k]);
+    C.offset[k] = T(D.offset[k]);
+    C.qcol[k] = D.qcol[k];
+    C.prismatic[k] = D.prismatic[k];
+  }
+  for (int i = 0; i < 4; ++i) C.eq[i] = T(D.eq[i]);
+  for (int i = 0; i < 3; ++i) C.ep[i] = T(D.ep[i]);
+  C.k = D.k;
+  return C;
+}
+
+// Cost parameters; dimensions beyond the robot's n are padded with an
+// unlimited, zero-rest, Jacobian-free joint: its normal-equation row is
+// decoupled (A_ii = w_rest^2, g_i = 0), so the padded solve is exact.
+template <typename T, int NQ>
+CostParams<T, NQ> make_costs(const KopModel& m, const double w[4]) {
+  CostParams<T, NQ> W;
+  const int n = m.tree.n;
+  for (int i = 0; i < NQ; ++i) {
+    W.lower[i] = i < n ? T(m.lower[i]) : T(-INFINITY);
+    W.upper[i] = i < n ? T(m.upper[i]) : T(INFINITY);
+    W.rest[i] = i < n ? T(m.rest[i]) : T(0);
+  }
+  W.w_pos = T(w[0]);
+  W.w_ori = T(w[1]);
+  W.w_lim = T(w[2]);
+  W.w_rest = T(w[3]);
+  return W;
+}
+
+int next_pow2(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
+// Shape selection shared by every chain-based entry point.
+enum class Shape { kId2, kId6, kId7, kGen8, kNone };
+
+Shape pick_shape(int n, int k, bool identity) {
+  if (identity && n == 7) return Shape::kId7;
+  if (identity && n == 2) return Shape::kId2;
+  if (identity && n == 6) return Shape::kId6;
+  if (n <= 8 && k <= 8) return Shape::kGen8;
+  return Shape::kNone;
+}
+
+// Padded-configuration helpers: the generic shape works on NQ = 8 internally;
+// the API arrays have stride n.  Lane kernels need stride n == NQ, so for
+// the generic shape the host pads through device scratch allocated here.
+struct PadBuf {
+  double* ptr = nullptr;
+  ~PadBuf() {
+    if (ptr) cudaFree(ptr);
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* kop_last_error(void) { return g_err.c_str(); }
+
+const char* kop_build_info(void) {
+  return "kinoptik_b200 sm_100a; fp32/fp64 x shapes {id2, id6, id7, gen8}";
+}
+
+int kop_model_create(const KopModelDesc* d, KopModel** out) {
+  if (!d || !out) return fail(KOP_EINVAL, "null argument");
+  if (d->num_joints < 0 || d->num_joints > kMaxTreeJoints)
+    return fail(KOP_EUNSUPPORTED, "more than 64 joints (not compiled in)");
+  if (d->num_links != d->num_joints + 1)
+    return fail(KOP_EINVAL, "a kinematic tree has num_links == num_joints + 1");
+  if (d->num_actuated < 0 || d->num_actuated > d->num_joints)
+    return fail(KOP_EINVAL, "bad actuated joint count");
+  KopModel* m = new KopModel();
+  memset(&m->tree, 0, sizeof(m->tree));
+  TreeParams& P = m->tree;
+  P.nl = d->num_links;
+  P.nj = d->num_joints;
+  P.n = d->num_actuated;
+  m->parent_joint.assign(P.nl, -1);
+  std::vector<char> placed(P.nl, 0);
+  placed[0] = 1;
+  for (int j = 0; j < P.nj; ++j) {
+    const int pl = d->parent_link[j], cl = d->child_link[j];
+    if (pl < 0 || pl >= P.nl || cl <= 0 || cl >= P.nl || !placed[pl] || placed[cl]) {
+      delete m;
+      return fail(KOP_EINVAL, "joints must be in topological order over links rooted at link 0");
+    }
+    placed[cl] = 1;
+    const int kind = d->kind[j];
+    if (kind < 0 || kind > 2) {
+      delete m;
+      return fail(KOP_EINVAL, "unknown joint kind");
+    }
+    const int qc = d->qcol[j];
+    if ((kind == KOP_JOINT_FIXED) != (qc < 0) || qc >= P.n) {
+      delete m;
+      return fail(KOP_EINVAL, "qcol must be -1 exactly for fixed joints and < num_actuated");
+    }
+    P.parent[j] = pl;
+    P.child[j] = cl;
+    P.kind[j] = kind;
+    P.qcol[j] = qc;
+    P.mult[j] = d->mult[j];
+    P.offset[j] = d->offset[j];
+    for (int i = 0; i < 4; ++i) P.oq[j][i] = d->origin_wxyz[j * 4 + i];
+    for (int i = 0; i < 3; ++i) {
+      P.op[j][i] = d->origin_xyz[j * 3 + i];
+      P.axis[j][i] = d->axis[j * 3 + i];
+    }
+    m->parent_joint[cl] = j;
+  }
+  m->lower.assign(d->lower, d->lower + P.n);
+  m->upper.assign(d->upper, d->upper + P.n);
+  m->rest.assign(d->rest, d->rest + P.n);
+  *out = m;
+  return KOP_OK;
+}
+
+void kop_model_destroy(KopModel* m) { delete m; }
+
+int kop_model_chain_length(const KopModel* m, int32_t link) {
+  if (!m) return fail(KOP_EINVAL, "null model");
+  ChainParams<double, kChainMax> C;
+  bool id;
+  const int k = compile_chain(*m, link, C, id);
+  return k;
+}
+
+int kop_fk(const KopModel* m, int32_t precision, const double* q, int64_t batch, double* lq, double* lp,
+           double* jp, double* ja, void* stream) {
+  if (!m || batch < 0 || (batch > 0 && !q)) return fail(KOP_EINVAL, "invalid FK arguments");
+  if (precision != KOP_FP32 && precision != KOP_FP64) return fail(KOP_EINVAL, "bad precision");
+  return cuda_status(launch_fk_tree(m->tree, precision, q, batch, lq, lp, jp, ja, (cudaStream_t)stream));
+}
+
+int kop_link_poses(const KopModel* m, int32_t link, const double* q, int64_t count, double* poses,
+                   void* stream) {
+  if (!m || count < 0 || link < 0 || link >= m->tree.nl) return fail(KOP_EINVAL, "invalid arguments");
+  TreeParams path;
+  memset(&path, 0, sizeof(path));
+  std::vector<int> js;
+  for (int j = m->parent_joint[link]; j >= 0; j = m->parent_joint[m->tree.parent[j]]) js.push_back(j);
+  path.n = m->tree.n;
+  path.nj = (int)js.size();
+  path.nl = path.nj + 1;
+  for (int i = 0; i < path.nj; ++i) {
+    const int j = js[js.size() - 1 - i];
+    path.kind[i] = m->tree.kind[j];
+    path.qcol[i] = m->tree.qcol[j];
+    path.mult[i] = m->tree.mult[j];
+    path.offset[i] = m->tree.offset[j];
+    memcpy(path.oq[i], m->tree.oq[j], sizeof(path.oq[i]));
+    memcpy(path.op[i], m->tree.op[j], sizeof(path.op[i]));
+    memcpy(path.axis[i], m->tree.axis[j], sizeof(path.axis[i]));
+  }
+  return cuda_status(launch_link_pose(path, q, count, poses, (cudaStream_t)stream));
+}
+
+int kop_sample_uniform(uint64_t key0, uint64_t key1_base, int64_t count, int32_t n, const double* lo,
+                       const double* hi, const uint8_t* negate, double* out, void* stream) {
+  if (count < 0 || n < 0 || n > 64 || (count > 0 && !out)) return fail(KOP_EINVAL, "invalid arguments");
+  // the per-column constants live in a small device buffer
+  double* dev = nullptr;
+  const size_t bytes = sizeof(double) * 2 * n + n;
+  if (cudaMalloc(&dev, bytes + 16) != cudaSuccess) return cuda_status(cudaGetLastError());
+  std::vector<double> host(2 * n);
+  std::vector<uint8_t> neg(n);
+  for (int j = 0; j < n; ++j) {
+    host[j] = lo[j];
+    host[n + j] = hi[j] - lo[j];  // numpy: arange = np.subtract(high, low)
+    neg[j] = negate ? negate[j] : 0;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaMemcpyAsync(dev, host.data(), sizeof(double) * 2 * n, cudaMemcpyHostToDevice, st);
+  uint8_t* dneg = reinterpret_cast<uint8_t*>(dev + 2 * n);
+  cudaMemcpyAsync(dneg, neg.data(), n, cudaMemcpyHostToDevice, st);
+  cudaError_t e = launch_philox(key0, key1_base, count, n, dev, dev + n, dneg, out, st);
+  cudaStreamSynchronize(st);  // host staging vectors die at return
+  cudaFree(dev);
+  return cuda_status(e != cudaSuccess ? e : cudaGetLastError());
+}
+
+int64_t kop_ik_beam_workspace_bytes(const KopModel* m, int32_t link, const KopIkParams* p, int64_t batch) {
+  if (!m || !p || batch < 0) return fail(KOP_EINVAL, "invalid arguments");
+  ChainParams<double, kChainMax> C;
+  bool id;
+  const int k = compile_chain(*m, link, C, id);
+  if (k < 0) return k;
+  const Shape sh = pick_shape(m->tree.n, k, id);
+  if (sh == Shape::kNone) return fail(KOP_EUNSUPPORTED, "robot shape not compiled in");
+  const int nq = sh == Shape::kGen8 ? 8 : m->tree.n;
+  const size_t el = p->precision == KOP_FP64 ? 8 : 4;
+  const int64_t rec = nq + 2 + p->prune_after + 1;
+  return batch * (int64_t)p->keep * rec * (int64_t)el + 256;
+}
+
+}  // extern "C"
+
+namespace {
+
+template <typename T, int NQ, int K, bool ID>
+cudaError_t run_beam(const KopModel& m, const ChainParams<double, kChainMax>& D, const double w[4],
+                     const BeamLaunch& L, cudaStream_t st) {
+  return launch_beam<T, NQ, K, ID>(cast_chain<T, K>(D), make_costs<T, NQ>(m, w), cast_chain<double, K>(D), L,
+                                   st);
+}
+
+template <typename T>
+cudaError_t dispatch_beam(Shape sh, const KopModel& m, const ChainParams<double, kChainMax>& D,
+                          const double w[4], const BeamLaunch& L, cudaStream_t st) {
+  switch (sh) {
+    case Shape::kId7: return run_beam<T, 7, 7, true>(m, D, w, L, st);
+    case Shape::kId2: return run_beam<T, 2, 2, true>(m, D, w, L, st);
+    case Shape::kId6: return run_beam<T, 6, 6, true>(m, D, w, L, st);
+    case Shape::kGen8: return run_beam<T, 8, 8, false>(m, D, w, L, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+template <typename T, int NQ, int K, bool ID>
+cudaError_t run_lane(const KopModel& m, const ChainParams<double, kChainMax>& D, const double w[4],
+                     const LaneLaunch& L, cudaStream_t st) {
+  return launch_lane<T, NQ, K, ID>(cast_chain<T, K>(D), make_costs<T, NQ>(m, w), L, st);
+}
+
+template <typename T>
+cudaError_t dispatch_lane(Shape sh, const KopModel& m, const ChainParams<double, kChainMax>& D,
+                          const double w[4], const LaneLaunch& L, cudaStream_t st) {
+  switch (sh) {
+    case Shape::kId7: return run_lane<T, 7, 7, true>(m, D, w, L, st);
+    case Shape::kId2: return run_lane<T, 2, 2, true>(m, D, w, L, st);
+    case Shape::kId6: return run_lane<T, 6, 6, true>(m, D, w, L, st);
+    case Shape::kGen8: return run_lane<T, 8, 8, false>(m, D, w, L, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// Resolve the chain + shape for a lane / beam call.
+int prepare(const KopModel* m, int link, int precision, ChainParams<double, kChainMax>& C, Shape& sh) {
+  if (!m) return fail(KOP_EINVAL, "null model");
+  if (precision != KOP_FP32 && precision != KOP_FP64) return fail(KOP_EINVAL, "bad precision");
+  bool id = false;
+  const int k = compile_chain(*m, link, C, id);
+  if (k < 0) return k;
+  sh = pick_shape(m->tree.n, k, id);
+  if (sh == Shape::kNone)
+    return fail(KOP_EUNSUPPORTED, "robot with " + std::to_string(m->tree.n) +
+                                      " actuated joints is not compiled in (max 8)");
+  return KOP_OK;
+}
+
+// Stride-n <-> stride-8 copies for the generic shape (kernels use stride NQ).
+__global__ void k_restride(const double* __restrict__ src, int64_t rows, int sn, int dn, double pad,
+                           double* __restrict__ dst) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= rows * dn) return;
+  const int64_t r = i / dn;
+  const int c = (int)(i % dn);
+  dst[i] = c < sn ? src[r * sn + c] : pad;
+}
+
+cudaError_t restride(const double* src, int64_t rows, int sn, int dn, double* dst, cudaStream_t st) {
+  if (rows == 0) return cudaSuccess;
+  const int64_t total = rows * dn;
+  k_restride<<<(unsigned)((total + 127) / 128), 128, 0, st>>>(src, rows, sn, dn, 0.0, dst);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+extern "C" {
+
+int kop_ik_beam(const KopModel* m, int32_t link, const KopIkParams* p, const double* targets, int64_t batch,
+                const double* seeds, void* workspace, int64_t workspace_bytes, double* q_out, double* cost_out,
+                double* history_out, double* pos_err, double* rot_err, uint8_t* success, void* stream) {
+  if (!p) return fail(KOP_EINVAL, "null params");
+  ChainParams<double, kChainMax> C;
+  Shape sh;
+  int rc = prepare(m, link, p->precision, C, sh);
+  if (rc != KOP_OK) return rc;
+  // IkRequest.__post_init__ (tasks.py:56-60)
+  if (!(0 < p->prune_after && p->prune_after < p->total_steps))
+    return fail(KOP_EINVAL, "need 0 < prune_after < total_steps");
+  if (!(1 <= p->keep && p->keep <= p->seeds)) return fail(KOP_EINVAL, "need 1 <= keep <= seeds");
+  if (p->seeds > 1024 || p->keep > 32)
+    return fail(KOP_EUNSUPPORTED, "seeds <= 1024 and keep <= 32 are compiled in");
+  if (batch < 0) return fail(KOP_EINVAL, "negative batch");
+  if (batch == 0) return KOP_OK;
+  if (!targets || !seeds || !workspace || !q_out || !cost_out || !pos_err || !rot_err || !success)
+    return fail(KOP_EINVAL, "null array argument");
+  const int64_t need = kop_ik_beam_workspace_bytes(m, link, p, batch);
+  if (workspace_bytes < need) return fail(KOP_EINVAL, "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = m->tree.n;
+  PadBuf seeds_pad, q_pad;
+  const double* seeds_k = seeds;
+  double* q_k = q_out;
+  if (sh == Shape::kGen8 && n != 8) {
+    if (cudaMalloc(&seeds_pad.ptr, sizeof(double) * 8 * p->seeds) != cudaSuccess ||
+        cudaMalloc(&q_pad.ptr, sizeof(double) * 8 * batch) != cudaSuccess)
+      return cuda_status(cudaGetLastError());
+    rc = cuda_status(restride(seeds, p->seeds, n, 8, seeds_pad.ptr, st));
+    if (rc) return rc;
+    seeds_k = seeds_pad.ptr;
+    q_k = q_pad.ptr;
+  }
+  BeamLaunch L;
+  L.targets = targets;
+  L.B = batch;
+  L.seeds = seeds_k;
+  L.S = p->seeds;
+  L.P = next_pow2(p->seeds);
+  L.G = next_pow2(p->keep);
+  L.steps1 = p->prune_after;
+  L.steps2 = p->total_steps - p->prune_after;
+  L.keep = p->keep;
+  L.pos_tol = p->success_pos_tol;
+  L.rot_tol = p->success_rot_tol;
+  L.workspace = workspace;
+  L.q_out = q_k;
+  L.cost_out = cost_out;
+  L.hist_out = history_out;
+  L.pos_err = pos_err;
+  L.rot_err = rot_err;
+  L.success = success;
+  const char* tp = getenv("KOP_TWOPASS");
+  L.twopass = tp && tp[0] == '1';
+  const double w[4] = {p->w_position, p->w_orientation, p->w_limit, p->w_rest};
+  cudaError_t e = p->precision == KOP_FP32 ? dispatch_beam<float>(sh, *m, C, w, L, st)
+                                           : dispatch_beam<double>(sh, *m, C, w, L, st);
+  if (e == cudaSuccess && q_k != q_out) e = restride(q_k, batch, 8, n, q_out, st);
+  if (seeds_pad.ptr) cudaStreamSynchronize(st);  // scratch freed at return
+  return cuda_status(e);
+}
+
+static int lane_call(const KopModel* m, int32_t link, int32_t precision, const double* weights,
+                     LaneLaunch L, int64_t lanes, void* stream) {
+  ChainParams<double, kChainMax> C;
+  Shape sh;
+  int rc = prepare(m, link, precision, C, sh);
+  if (rc != KOP_OK) return rc;
+  if (!weights) return fail(KOP_EINVAL, "null weights");
+  if (lanes < 0) return fail(KOP_EINVAL, "negative lane count");
+  if (lanes == 0) return KOP_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = m->tree.n;
+  const int nq = sh == Shape::kGen8 ? 8 : n;
+  L.lanes = lanes;
+  PadBuf qin, qio, res, jac;
+  const double* user_qin = L.q_in;
+  double* user_qio = L.q_io;
+  double* user_res = L.res;
+  double* user_jac = L.jac;
+  if (nq != n) {  // pad to the kernel stride
+    if (L.q_in) {
+      if (cudaMalloc(&qin.ptr, sizeof(double) * nq * lanes) != cudaSuccess) return cuda_status(cudaGetLastError());
+      if ((rc = cuda_status(restride(L.q_in, lanes, n, nq, qin.ptr, st)))) return rc;
+      L.q_in = qin.ptr;
+    }
+    if (L.q_io) {
+      if (cudaMalloc(&qio.ptr, sizeof(double) * nq * lanes) != cudaSuccess) return cuda_status(cudaGetLastError());
+      if ((rc = cuda_status(restride(L.q_io, lanes, n, nq, qio.ptr, st)))) return rc;
+      L.q_io = qio.ptr;
+    }
+    if (L.res) {
+      const int M = 6 + 2 * nq;
+      if (cudaMalloc(&res.ptr, sizeof(double) * M * lanes) != cudaSuccess ||
+          cudaMalloc(&jac.ptr, sizeof(double) * M * nq * lanes) != cudaSuccess)
+        return cuda_status(cudaGetLastError());
+      L.res = res.ptr;
+      L.jac = jac.ptr;
+    }
+  }
+  cudaError_t e = precision == KOP_FP32 ? dispatch_lane<float>(sh, *m, C, weights, L, st)
+                                        : dispatch_lane<double>(sh, *m, C, weights, L, st);
+  if (e == cudaSuccess && nq != n) {
+    if (user_qio) e = restride(L.q_io, lanes, nq, n, user_qio, st);
+    if (e == cudaSuccess && user_res) {
+      // rows: pose 6 | limit nq | rest nq  ->  pose 6 | limit n | rest n; cols nq -> n
+      const int Mk = 6 + 2 * nq, Mu = 6 + 2 * n;
+      std::vector<int> rowmap;
+      for (int r = 0; r < 6; ++r) rowmap.push_back(r);
+      for (int r = 0; r < n; ++r) rowmap.push_back(6 + r);
+      for (int r = 0; r < n; ++r) rowmap.push_back(6 + nq + r);
+      // small: do it with per-row strided copies
+      for (int r = 0; r < Mu && e == cudaSuccess; ++r) {
+        e = cudaMemcpy2DAsync(user_res + r, sizeof(double) * Mu, L.res + rowmap[r], sizeof(double) * Mk,
+                              sizeof(double), lanes, cudaMemcpyDeviceToDevice, st);
+        if (e == cudaSuccess)
+          e = cudaMemcpy2DAsync(user_jac + (size_t)r * n, sizeof(double) * Mu * n,
+                                L.jac + (size_t)rowmap[r] * nq, sizeof(double) * Mk * nq, sizeof(double) * n,
+                                lanes, cudaMemcpyDeviceToDevice, st);
+      }
+    }
+    (void)user_qin;
+    cudaStreamSynchronize(st);  // scratch freed at return
+  }
+  return cuda_status(e);
+}
+
+int kop_lane_residuals_jacobian(const KopModel* m, int32_t link, int32_t precision, const double* weights,
+                                const double* tinv, const int32_t* lane_target, const double* q, int64_t lanes,
+                                double* residual, double* jacobian, void* stream) {
+  if (lanes > 0 && (!tinv || !lane_target || !q || !residual || !jacobian))
+    return fail(KOP_EINVAL, "null array argument");
+  LaneLaunch L{};
+  L.op = LaneOp::kResJac;
+  L.tinv = tinv;
+  L.lane_target = lane_target;
+  L.q_in = q;
+  L.res = residual;
+  L.jac = jacobian;
+  return lane_call(m, link, precision, weights, L, lanes, stream);
+}
+
+int kop_lane_start(const KopModel* m, int32_t link, int32_t precision, const double* weights,
+                   const double* tinv, const int32_t* lane_target, const double* q, int64_t lanes,
+                   double* damping, double* cost, void* stream) {
+  if (lanes > 0 && (!tinv || !lane_target || !q || !damping || !cost))
+    return fail(KOP_EINVAL, "null array argument");
+  LaneLaunch L{};
+  L.op = LaneOp::kStart;
+  L.tinv = tinv;
+  L.lane_target = lane_target;
+  L.q_in = q;
+  L.lam = damping;
+  L.cost = cost;
+  return lane_call(m, link, precision, weights, L, lanes, stream);
+}
+
+int kop_lane_run(const KopModel* m, int32_t link, int32_t precision, const double* weights, const double* tinv,
+                 const int32_t* lane_target, int64_t lanes, int32_t steps, double* q, double* damping,
+                 double* cost, double* history, void* stream) {
+  if (steps < 0) return fail(KOP_EINVAL, "negative step count");
+  if (lanes > 0 && (!tinv || !lane_target || !q || !damping || !cost))
+    return fail(KOP_EINVAL, "null array argument");
+  LaneLaunch L{};
+  L.op = LaneOp::kRun;
+  L.tinv = tinv;
+  L.lane_target = lane_target;
+  L.steps = steps;
+  L.q_io = q;
+  L.lam = damping;
+  L.cost = cost;
+  L.hist = history;
+  return lane_call(m, link, precision, weights, L, lanes, stream);
+}
+
+int kop_fma_peak_kernel(int32_t blocks, int32_t threads, int32_t iters, float* sink, double* flops,
+                        void* stream) {
+  if (blocks <= 0 || threads <= 0 || iters <= 0 || !sink) return fail(KOP_EINVAL, "invalid arguments");
+  if (flops) *flops = 2.0 * 16.0 * (double)blocks * threads * (double)iters;
+  return cuda_status(launch_fma_peak(blocks, threads, iters, sink, (cudaStream_t)stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,371 @@
+// sm_100a kernels of the batched LM-IK engine.
+//
+//   k_beam_stage1  one thread per (target, seed) lane: start + prune_after LM
+//                  steps + in-CTA stable top-`keep` prune (tasks.py:131-136)
+//   k_beam_stage2  one thread per survivor: remaining LM steps, segmented
+//                  warp-shuffle argmin, FP64 pose errors (tasks.py:137-161)
+//   k_lane_*       the IkLaneProblem API (beam.py:133-240), one thread/lane
+//   k_fk_tree      full-tree FK, reference op order (robot.py:404-448)
+//   k_link_pose    FK of one link + canonicalisation (benchmark targets)
+//   k_philox       numpy Philox4x64-10 uniform draws, bit-exact
+//
+// Mapping: the workload is compute/latency bound (FP32 FMA + MUFU), so lanes
+// map to threads with the whole LM state in registers; model constants are
+// kernel parameters (constant bank).  Blocks are 256 threads (4 targets x 64
+// seeds) in stage 1; the only shared memory is the per-lane cost history and
+// the prune's cost vector.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kop_kernels.cuh"
+
+namespace kop {
+
+// ---------------------------------------------------------------------------
+// IK-Beam stage 1
+// ---------------------------------------------------------------------------
+template <typename T, int NQ, int K, bool ID>
+__global__ void __launch_bounds__(256)
+k_beam_stage1(const ChainParams<T, K> C, const CostParams<T, NQ> W, const double* __restrict__ targets,
+              int64_t B, const double* __restrict__ seeds, int S, int P, int steps1, int keep,
+              T* __restrict__ surv, int rec) {
+  extern __shared__ unsigned char smem_raw[];
+  T* hist = reinterpret_cast<T*>(smem_raw);           // [(steps1+1) * bd]
+  T* costs = hist + (size_t)(steps1 + 1) * blockDim.x;  // [bd]
+  const int tid = threadIdx.x, bd = blockDim.x;
+  const int64_t tgt = (int64_t)blockIdx.x * (bd / P) + tid / P;
+  const int s = tid % P;
+  const bool active = (tgt < B) && (s < S);
+  const int64_t tc = tgt < B ? tgt : B - 1;
+  double tinv[7];
+  target_inverse(targets + tc * 7, tinv);
+  const TargetInv<T> tg = to_target<T>(tinv);
+
+  LaneState<T, NQ> st;
+  const double* sd = seeds + (size_t)(s < S ? s : 0) * NQ;
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) st.q[i] = T(sd[i]);
+  st.cost = lane_normal<T, NQ, K, ID>(C, W, tg, st.q, st.A, st.g);
+  st.lam = T(BeamConsts::damping_init);
+  hist[tid] = st.cost;
+  for (int it = 0; it < steps1; ++it) {
+    lm_step<T, NQ, K, ID>(C, W, tg, st);
+    hist[(size_t)(it + 1) * bd + tid] = st.cost;
+  }
+  costs[tid] = active ? st.cost : T(NAN);
+  __syncthreads();
+  if (!active) return;
+  const int base = tid - s;
+  int rank = 0;
+  for (int j = 0; j < S; ++j) rank += rank_less(costs[base + j], j, st.cost, s) ? 1 : 0;
+  if (rank >= keep) return;
+  T* out = surv + (size_t)(tgt * keep + rank) * rec;
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) out[i] = st.q[i];
+  out[NQ] = st.lam;
+  out[NQ + 1] = st.cost;
+  for (int h = 0; h <= steps1; ++h) out[NQ + 2 + h] = hist[(size_t)h * bd + tid];
+}
+
+// ---------------------------------------------------------------------------
+// IK-Beam stage 2 + winner + pose errors
+// ---------------------------------------------------------------------------
+template <int K>
+__device__ __forceinline__ void chain_pose_f64(const ChainParams<double, K>& C, const double* q,
+                                               quat<double>& eq, vec3<double>& ep) {
+  quat<double> pq{1.0, 0.0, 0.0, 0.0};
+  vec3<double> pp{0.0, 0.0, 0.0};
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    if (k < C.k) {
+      const quat<double> tq{C.tq[k][0], C.tq[k][1], C.tq[k][2], C.tq[k][3]};
+      const vec3<double> tp{C.tp[k][0], C.tp[k][1], C.tp[k][2]};
+      const quat<double> fq = qmul(pq, tq);
+      const vec3<double> o = qrot(pq, tp);
+      const vec3<double> fp{pp.x + o.x, pp.y + o.y, pp.z + o.z};
+      const double th = q[C.qcol[k]] * C.mult[k] + C.offset[k];
+      if (C.prismatic[k]) {
+        const vec3<double> z = qzaxis(fq);
+        pq = fq;
+        pp = {fp.x + th * z.x, fp.y + th * z.y, fp.z + th * z.z};
+      } else {
+        double sn, cs;
+        sincos(0.5 * th, &sn, &cs);
+        pq = qmul_z(fq, cs, sn);
+        pp = fp;
+      }
+    }
+  }
+  eq = qmul(pq, quat<double>{C.eq[0], C.eq[1], C.eq[2], C.eq[3]});
+  const vec3<double> eo = qrot(pq, vec3<double>{C.ep[0], C.ep[1], C.ep[2]});
+  ep = {pp.x + eo.x, pp.y + eo.y, pp.z + eo.z};
+}
+
+// tasks.py:109-116: |t(T_t^-1 T)| and |log R(T_t^-1 T)| in double.
+template <int K>
+__device__ __forceinline__ void pose_errors_f64(const ChainParams<double, K>& C, const double* q,
+                                                const double tinv[7], double& pe, double& re) {
+  quat<double> eq;
+  vec3<double> ep;
+  chain_pose_f64<K>(C, q, eq, ep);
+  const double n = sqrt(eq.w * eq.w + eq.x * eq.x + eq.y * eq.y + eq.z * eq.z);
+  eq = {eq.w / n, eq.x / n, eq.y / n, eq.z / n};
+  const quat<double> iq{tinv[0], tinv[1], tinv[2], tinv[3]};
+  const quat<double> rq = qmul(iq, eq);
+  const vec3<double> rt = qrot(iq, ep);
+  const vec3<double> t{tinv[4] + rt.x, tinv[5] + rt.y, tinv[6] + rt.z};
+  pe = sqrt(t.x * t.x + t.y * t.y + t.z * t.z);
+  const vec3<double> w = qlog(rq);
+  re = sqrt(w.x * w.x + w.y * w.y + w.z * w.z);
+}
+
+template <typename T, int NQ, int K, bool ID>
+__global__ void __launch_bounds__(128)
+k_beam_stage2(const ChainParams<T, K> C, const CostParams<T, NQ> W, const ChainParams<double, K> Cd,
+              const double* __restrict__ targets, int64_t B, const T* __restrict__ surv, int rec,
+              int steps1, int steps2, int keep, int G, double pos_tol, double rot_tol,
+              double* __restrict__ q_out, double* __restrict__ cost_out, double* __restrict__ hist_out,
+              double* __restrict__ pos_err, double* __restrict__ rot_err, uint8_t* __restrict__ success) {
+  extern __shared__ unsigned char smem_raw[];
+  T* hist = reinterpret_cast<T*>(smem_raw);  // [steps2 * bd]
+  const int tid = threadIdx.x, bd = blockDim.x;
+  const int64_t lane = (int64_t)blockIdx.x * bd + tid;
+  const int64_t tgt = lane / G;
+  const int r = (int)(lane % G);
+  const bool active = (tgt < B) && (r < keep);
+  const int64_t tc = tgt < B ? tgt : B - 1;
+  const int rc = r < keep ? r : 0;
+  double tinv[7];
+  target_inverse(targets + tc * 7, tinv);
+  const TargetInv<T> tg = to_target<T>(tinv);
+  const T* rin = surv + (size_t)(tc * keep + rc) * rec;
+
+  LaneState<T, NQ> st;
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) st.q[i] = rin[i];
+  st.lam = rin[NQ];
+  // the carried cost is the stage-1 state cost (LaneState.select, beam.py:60-68);
+  // A/g are re-derived at q, as the reference re-derives r and J (beam.py:202)
+  lane_normal<T, NQ, K, ID>(C, W, tg, st.q, st.A, st.g);
+  st.cost = rin[NQ + 1];
+  for (int it = 0; it < steps2; ++it) {
+    lm_step<T, NQ, K, ID>(C, W, tg, st);
+    hist[(size_t)it * bd + tid] = st.cost;
+  }
+  // winner = argmin over the keep survivors, ties -> lower stage-1 rank (tasks.py:139)
+  T best = active ? st.cost : T(NAN);
+  int bidx = active ? r : (1 << 30);
+  for (int off = G >> 1; off > 0; off >>= 1) {
+    const T oc = __shfl_xor_sync(0xffffffffu, best, off);
+    const int oi = __shfl_xor_sync(0xffffffffu, bidx, off);
+    if (rank_less(oc, oi, best, bidx)) {
+      best = oc;
+      bidx = oi;
+    }
+  }
+  if (!active || bidx != r) return;
+  double qd[NQ];
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) {
+    qd[i] = double(st.q[i]);
+    q_out[tgt * NQ + i] = qd[i];
+  }
+  cost_out[tgt] = double(st.cost);
+  if (hist_out) {
+    double* h = hist_out + tgt * (steps1 + 1 + steps2);
+    for (int i = 0; i <= steps1; ++i) h[i] = double(rin[NQ + 2 + i]);
+    for (int i = 0; i < steps2; ++i) h[steps1 + 1 + i] = double(hist[(size_t)i * bd + tid]);
+  }
+  double pe, re;
+  pose_errors_f64<K>(Cd, qd, tinv, pe, re);
+  pos_err[tgt] = pe;
+  rot_err[tgt] = re;
+  success[tgt] = (pe < pos_tol && re < rot_tol) ? 1 : 0;
+}
+
+// ---------------------------------------------------------------------------
+// Lane API kernels (IkLaneProblem with one target per lane)
+// ---------------------------------------------------------------------------
+template <typename T, int NQ, int K, bool ID>
+__global__ void __launch_bounds__(128)
+k_lane_resjac(const ChainParams<T, K> C, const CostParams<T, NQ> W, const double* __restrict__ tinv,
+              const int32_t* __restrict__ lane_target, const double* __restrict__ q_in, int64_t lanes,
+              double* __restrict__ res, double* __restrict__ jac) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= lanes) return;
+  const TargetInv<T> tg = load_target_inv<T>(tinv + (int64_t)lane_target[l] * 7);
+  T q[NQ];
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) q[i] = T(q_in[l * NQ + i]);
+  T r[6], J[6][NQ];
+  pose_rows<T, NQ, K, ID, true>(C, W, tg, q, r, J);
+  T rl[NQ], gl[NQ], rr[NQ];
+  diag_rows(W, q, rl, gl, rr);
+  constexpr int M = 6 + 2 * NQ;
+  double* ro = res + l * M;
+  double* jo = jac + l * M * NQ;
+#pragma unroll
+  for (int m = 0; m < 6; ++m) {
+    ro[m] = double(r[m]);
+#pragma unroll
+    for (int c = 0; c < NQ; ++c) jo[m * NQ + c] = double(J[m][c]);
+  }
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) {
+    ro[6 + i] = double(rl[i]);
+    ro[6 + NQ + i] = double(rr[i]);
+#pragma unroll
+    for (int c = 0; c < NQ; ++c) {
+      jo[(6 + i) * NQ + c] = c == i ? double(gl[i]) : 0.0;
+      jo[(6 + NQ + i) * NQ + c] = c == i ? double(W.w_rest) : 0.0;
+    }
+  }
+}
+
+template <typename T, int NQ, int K, bool ID>
+__global__ void __launch_bounds__(128)
+k_lane_start(const ChainParams<T, K> C, const CostParams<T, NQ> W, const double* __restrict__ tinv,
+             const int32_t* __restrict__ lane_target, const double* __restrict__ q_in, int64_t lanes,
+             double* __restrict__ lam, double* __restrict__ cost) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= lanes) return;
+  const TargetInv<T> tg = load_target_inv<T>(tinv + (int64_t)lane_target[l] * 7);
+  T q[NQ];
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) q[i] = T(q_in[l * NQ + i]);
+  cost[l] = double(lane_cost<T, NQ, K, ID>(C, W, tg, q));
+  lam[l] = BeamConsts::damping_init;
+}
+
+template <typename T, int NQ, int K, bool ID>
+__global__ void __launch_bounds__(128)
+k_lane_run(const ChainParams<T, K> C, const CostParams<T, NQ> W, const double* __restrict__ tinv,
+           const int32_t* __restrict__ lane_target, int64_t lanes, int steps, double* __restrict__ q_io,
+           double* __restrict__ lam_io, double* __restrict__ cost_io, double* __restrict__ hist) {
+  const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (l >= lanes) return;
+  const TargetInv<T> tg = load_target_inv<T>(tinv + (int64_t)lane_target[l] * 7);
+  LaneState<T, NQ> st;
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) st.q[i] = T(q_io[l * NQ + i]);
+  st.lam = T(lam_io[l]);
+  lane_normal<T, NQ, K, ID>(C, W, tg, st.q, st.A, st.g);
+  st.cost = T(cost_io[l]);
+  for (int it = 0; it < steps; ++it) {
+    lm_step<T, NQ, K, ID>(C, W, tg, st);
+    if (hist) hist[l * steps + it] = double(st.cost);
+  }
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) q_io[l * NQ + i] = double(st.q[i]);
+  lam_io[l] = double(st.lam);
+  cost_io[l] = double(st.cost);
+}
+
+// Two-pass (reference-structured) stage-1 variant for A/B measurement.
+template <typename T, int NQ, int K, bool ID>
+__global__ void __launch_bounds__(256)
+k_beam_stage1_twopass(const ChainParams<T, K> C, const CostParams<T, NQ> W,
+                      const double* __restrict__ targets, int64_t B, const double* __restrict__ seeds,
+                      int S, int P, int steps1, int keep, T* __restrict__ surv, int rec) {
+  extern __shared__ unsigned char smem_raw[];
+  T* hist = reinterpret_cast<T*>(smem_raw);
+  T* costs = hist + (size_t)(steps1 + 1) * blockDim.x;
+  const int tid = threadIdx.x, bd = blockDim.x;
+  const int64_t tgt = (int64_t)blockIdx.x * (bd / P) + tid / P;
+  const int s = tid % P;
+  const bool active = (tgt < B) && (s < S);
+  const int64_t tc = tgt < B ? tgt : B - 1;
+  double tinv[7];
+  target_inverse(targets + tc * 7, tinv);
+  const TargetInv<T> tg = to_target<T>(tinv);
+  LaneState<T, NQ> st;
+  const double* sd = seeds + (size_t)(s < S ? s : 0) * NQ;
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) st.q[i] = T(sd[i]);
+  st.cost = lane_cost<T, NQ, K, ID>(C, W, tg, st.q);
+  st.lam = T(BeamConsts::damping_init);
+  hist[tid] = st.cost;
+  for (int it = 0; it < steps1; ++it) {
+    lm_step_twopass<T, NQ, K, ID>(C, W, tg, st);
+    hist[(size_t)(it + 1) * bd + tid] = st.cost;
+  }
+  costs[tid] = active ? st.cost : T(NAN);
+  __syncthreads();
+  if (!active) return;
+  const int base = tid - s;
+  int rank = 0;
+  for (int j = 0; j < S; ++j) rank += rank_less(costs[base + j], j, st.cost, s) ? 1 : 0;
+  if (rank >= keep) return;
+  T* out = surv + (size_t)(tgt * keep + rank) * rec;
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) out[i] = st.q[i];
+  out[NQ] = st.lam;
+  out[NQ + 1] = st.cost;
+  for (int h = 0; h <= steps1; ++h) out[NQ + 2 + h] = hist[(size_t)h * bd + tid];
+}
+
+// ---------------------------------------------------------------------------
+// Launchers (instantiated per supported shape)
+// ---------------------------------------------------------------------------
+template <typename T, int NQ, int K, bool ID>
+cudaError_t launch_beam(const ChainParams<T, K>& C, const CostParams<T, NQ>& W,
+                        const ChainParams<double, K>& Cd, const BeamLaunch& L, cudaStream_t st) {
+  const int rec = NQ + 2 + L.steps1 + 1;
+  T* surv = reinterpret_cast<T*>(L.workspace);
+  // stage 1: P lanes per target (power of two >= S), 256-thread blocks
+  const int tpb = L.P >= 256 ? L.P : 256;
+  const int per_block = tpb / L.P;
+  const int64_t blocks1 = (L.B + per_block - 1) / per_block;
+  const size_t smem1 = sizeof(T) * ((size_t)(L.steps1 + 1) * tpb + tpb);
+  if (L.twopass) {
+    k_beam_stage1_twopass<T, NQ, K, ID><<<(unsigned)blocks1, tpb, smem1, st>>>(
+        C, W, L.targets, L.B, L.seeds, L.S, L.P, L.steps1, L.keep, surv, rec);
+  } else {
+    k_beam_stage1<T, NQ, K, ID><<<(unsigned)blocks1, tpb, smem1, st>>>(
+        C, W, L.targets, L.B, L.seeds, L.S, L.P, L.steps1, L.keep, surv, rec);
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  const int tpb2 = 128;
+  const int64_t lanes2 = L.B * L.G;
+  const int64_t blocks2 = (lanes2 + tpb2 - 1) / tpb2;
+  const size_t smem2 = sizeof(T) * (size_t)(L.steps2 > 0 ? L.steps2 : 1) * tpb2;
+  k_beam_stage2<T, NQ, K, ID><<<(unsigned)blocks2, tpb2, smem2, st>>>(
+      C, W, Cd, L.targets, L.B, surv, rec, L.steps1, L.steps2, L.keep, L.G, L.pos_tol, L.rot_tol,
+      L.q_out, L.cost_out, L.hist_out, L.pos_err, L.rot_err, L.success);
+  return cudaGetLastError();
+}
+
+template <typename T, int NQ, int K, bool ID>
+cudaError_t launch_lane(const ChainParams<T, K>& C, const CostParams<T, NQ>& W, const LaneLaunch& L,
+                        cudaStream_t st) {
+  const int tpb = 128;
+  const unsigned blocks = (unsigned)((L.lanes + tpb - 1) / tpb);
+  if (L.lanes == 0) return cudaSuccess;
+  switch (L.op) {
+    case LaneOp::kResJac:
+      k_lane_resjac<T, NQ, K, ID><<<blocks, tpb, 0, st>>>(C, W, L.tinv, L.lane_target, L.q_in, L.lanes,
+                                                          L.res, L.jac);
+      break;
+    case LaneOp::kStart:
+      k_lane_start<T, NQ, K, ID><<<blocks, tpb, 0, st>>>(C, W, L.tinv, L.lane_target, L.q_in, L.lanes,
+                                                         L.lam, L.cost);
+      break;
+    case LaneOp::kRun:
+      k_lane_run<T, NQ, K, ID><<<blocks, tpb, 0, st>>>(C, W, L.tinv, L.lane_target, L.lanes, L.steps,
+                                                       L.q_io, L.lam, L.cost, L.hist);
+      break;
+  }
+  return cudaGetLastError();
+}
+
+#define KOP_INSTANTIATE(T, NQ, K, ID)                                                              \
+  template cudaError_t launch_beam<T, NQ, K, ID>(const ChainParams<T, K>&, const CostParams<T, NQ>&, \
+                                                 const ChainParams<double, K>&, const BeamLaunch&,   \
+                                                 cudaStream_t);                                      \
+  template cudaError_t launch_lane<T, NQ, K, ID>(const ChainParams<T, K>&, const CostParams<T, NQ>&, \
+                                                 const LaneLaunch&, cudaStream_t);
+
+KOP_FOR_EACH_SHAPE(KOP_INSTANTIATE)
+
+}  // namespace kop

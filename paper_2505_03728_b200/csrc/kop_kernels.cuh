@@ -1,0 +1,68 @@
+// Internal launch interface between the C ABI (kop_capi.cu) and the kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kop_chain.h"
+#include "kop_lane.cuh"
+
+namespace kop {
+
+// Compiled (NQ actuated, K chain joints, identity column map) shapes.  ID
+// shapes serve serial chains whose moving joints are exactly the actuated
+// joints (Panda, planar 2R, UR-class); the generic shape serves trees, mimic
+// joints and sub-chains with K <= NQ <= 8.
+#define KOP_FOR_EACH_SHAPE(X) \
+  X(float, 2, 2, true)        \
+  X(double, 2, 2, true)       \
+  X(float, 6, 6, true)        \
+  X(double, 6, 6, true)       \
+  X(float, 7, 7, true)        \
+  X(double, 7, 7, true)       \
+  X(float, 8, 8, false)       \
+  X(double, 8, 8, false)
+
+struct BeamLaunch {
+  const double* targets;
+  int64_t B;
+  const double* seeds;
+  int S, P, G;  // seeds, lanes per target (pow2 >= S), survivor group (pow2 >= keep)
+  int steps1, steps2, keep;
+  double pos_tol, rot_tol;
+  void* workspace;
+  double *q_out, *cost_out, *hist_out, *pos_err, *rot_err;
+  uint8_t* success;
+  bool twopass;
+};
+
+enum class LaneOp { kResJac, kStart, kRun };
+
+struct LaneLaunch {
+  LaneOp op;
+  const double* tinv;
+  const int32_t* lane_target;
+  const double* q_in;
+  int64_t lanes;
+  int steps;
+  double *q_io, *lam, *cost, *hist, *res, *jac;
+};
+
+template <typename T, int NQ, int K, bool ID>
+cudaError_t launch_beam(const ChainParams<T, K>& C, const CostParams<T, NQ>& W,
+                        const ChainParams<double, K>& Cd, const BeamLaunch& L, cudaStream_t st);
+
+template <typename T, int NQ, int K, bool ID>
+cudaError_t launch_lane(const ChainParams<T, K>& C, const CostParams<T, NQ>& W, const LaneLaunch& L,
+                        cudaStream_t st);
+
+// kop_aux.cu
+cudaError_t launch_fk_tree(const TreeParams& P, int precision, const double* q, int64_t B,
+                           double* lq, double* lp, double* jp, double* ja, cudaStream_t st);
+cudaError_t launch_link_pose(const TreeParams& path, const double* q, int64_t B, double* poses,
+                             cudaStream_t st);
+cudaError_t launch_philox(uint64_t key0, uint64_t key1_base, int64_t count, int n, const double* lo,
+                          const double* range, const uint8_t* negate, double* out, cudaStream_t st);
+cudaError_t launch_fma_peak(int blocks, int threads, int iters, float* sink, cudaStream_t st);
+
+}  // namespace kop

@@ -1,0 +1,280 @@
+// Device Lie-group kernels (SO(3)/SE(3)), templated on float / double.
+//
+// Conventions follow liegroups.py:1-13: quaternions (w,x,y,z), twists
+// translation-first, right-multiplicative retraction.  The functions are
+// register-only __device__ code meant to be inlined into the fused LM kernel.
+//
+// FP32 hazard: the reference's closed forms for the SO(3)/SE(3)
+// Jacobian coefficients (liegroups.py:176-191, :210-235) cancel
+// catastrophically in float well above its 1e-7 series threshold.  Here every
+// coefficient switches to its Taylor series (exact rational coefficients,
+// derived independently of the reference's -- whose c2/c3 series carry a sign
+// slip) below kSeriesBelow<T>, which keeps float relative error at
+// ~1e-7 across [0, pi].
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+namespace kop {
+
+template <typename T>
+struct quat {
+  T w, x, y, z;
+};
+template <typename T>
+struct vec3 {
+  T x, y, z;
+};
+
+// ---- scalar helpers ------------------------------------------------------
+__device__ __forceinline__ void sincos_t(float a, float* s, float* c) { sincosf(a, s, c); }
+__device__ __forceinline__ void sincos_t(double a, double* s, double* c) { sincos(a, s, c); }
+__device__ __forceinline__ float sqrt_t(float a) { return sqrtf(a); }
+__device__ __forceinline__ double sqrt_t(double a) { return sqrt(a); }
+__device__ __forceinline__ float rsqrt_t(float a) { return rsqrtf(a); }
+__device__ __forceinline__ double rsqrt_t(double a) { return 1.0 / sqrt(a); }
+__device__ __forceinline__ float atan2_t(float y, float x) { return atan2f(y, x); }
+__device__ __forceinline__ double atan2_t(double y, double x) { return atan2(y, x); }
+__device__ __forceinline__ float tan_t(float a) { return tanf(a); }
+__device__ __forceinline__ double tan_t(double a) { return tan(a); }
+__device__ __forceinline__ bool finite_t(float a) { return isfinite(a); }
+__device__ __forceinline__ bool finite_t(double a) { return isfinite(a); }
+
+template <typename T>
+__device__ __forceinline__ T tmax(T a, T b) { return a > b ? a : b; }
+template <typename T>
+__device__ __forceinline__ T tmin(T a, T b) { return a < b ? a : b; }
+
+// Below this angle the Jacobian coefficients use their Taylor series.  In
+// float the closed forms lose ~180*eps/theta^4 relative accuracy (k3), so
+// the series (6 terms, truncation < 1e-9 at theta = 1) covers [0, 1).
+template <typename T>
+struct LieConst;
+template <>
+struct LieConst<float> {
+  static constexpr float series_below = 1.0f;
+  static constexpr float log_series_below = 1e-7f;  // liegroups.py:23,139-140
+};
+template <>
+struct LieConst<double> {
+  static constexpr double series_below = 0.03;
+  static constexpr double log_series_below = 1e-7;
+};
+
+// ---- quaternion kernels (liegroups.py:48-85) ------------------------------
+template <typename T>
+__device__ __forceinline__ vec3<T> cross(const vec3<T>& a, const vec3<T>& b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+template <typename T>
+__device__ __forceinline__ T dot(const vec3<T>& a, const vec3<T>& b) {
+  return a.x * b.x + a.y * b.y + a.z * b.z;
+}
+
+// Hamilton product a*b.
+template <typename T>
+__device__ __forceinline__ quat<T> qmul(const quat<T>& a, const quat<T>& b) {
+  return {a.w * b.w - (a.x * b.x + a.y * b.y + a.z * b.z),
+          a.w * b.x + b.w * a.x + (a.y * b.z - a.z * b.y),
+          a.w * b.y + b.w * a.y + (a.z * b.x - a.x * b.z),
+          a.w * b.z + b.w * a.z + (a.x * b.y - a.y * b.x)};
+}
+
+// a * (c, 0, 0, s): composition with a rotation about the local z axis.
+template <typename T>
+__device__ __forceinline__ quat<T> qmul_z(const quat<T>& a, T c, T s) {
+  return {a.w * c - a.z * s, a.x * c + a.y * s, a.y * c - a.x * s, a.z * c + a.w * s};
+}
+
+// Rotate p by unit q: p + w t + v x t with t = 2 v x p.
+template <typename T>
+__device__ __forceinline__ vec3<T> qrot(const quat<T>& q, const vec3<T>& p) {
+  const vec3<T> v{q.x, q.y, q.z};
+  vec3<T> t = cross(v, p);
+  t = {T(2) * t.x, T(2) * t.y, T(2) * t.z};
+  const vec3<T> u = cross(v, t);
+  return {p.x + q.w * t.x + u.x, p.y + q.w * t.y + u.y, p.z + q.w * t.z + u.z};
+}
+
+// Third column of R(q) = q * e_z (the world direction of a local z axis).
+template <typename T>
+__device__ __forceinline__ vec3<T> qzaxis(const quat<T>& q) {
+  return {T(2) * (q.x * q.z + q.w * q.y), T(2) * (q.y * q.z - q.w * q.x),
+          T(1) - T(2) * (q.x * q.x + q.y * q.y)};
+}
+
+template <typename T>
+struct mat3 {
+  T m[3][3];
+};
+
+template <typename T>
+__device__ __forceinline__ mat3<T> qmat(const quat<T>& q) {
+  const T xx = q.x * q.x, yy = q.y * q.y, zz = q.z * q.z;
+  const T xy = q.x * q.y, xz = q.x * q.z, yz = q.y * q.z;
+  const T wx = q.w * q.x, wy = q.w * q.y, wz = q.w * q.z;
+  mat3<T> r;
+  r.m[0][0] = T(1) - T(2) * (yy + zz);
+  r.m[0][1] = T(2) * (xy - wz);
+  r.m[0][2] = T(2) * (xz + wy);
+  r.m[1][0] = T(2) * (xy + wz);
+  r.m[1][1] = T(1) - T(2) * (xx + zz);
+  r.m[1][2] = T(2) * (yz - wx);
+  r.m[2][0] = T(2) * (xz - wy);
+  r.m[2][1] = T(2) * (yz + wx);
+  r.m[2][2] = T(1) - T(2) * (xx + yy);
+  return r;
+}
+
+template <typename T>
+__device__ __forceinline__ vec3<T> mulT(const mat3<T>& r, const vec3<T>& v) {  // R^T v
+  return {r.m[0][0] * v.x + r.m[1][0] * v.y + r.m[2][0] * v.z,
+          r.m[0][1] * v.x + r.m[1][1] * v.y + r.m[2][1] * v.z,
+          r.m[0][2] * v.x + r.m[1][2] * v.y + r.m[2][2] * v.z};
+}
+template <typename T>
+__device__ __forceinline__ vec3<T> mul(const mat3<T>& r, const vec3<T>& v) {  // R v
+  return {r.m[0][0] * v.x + r.m[0][1] * v.y + r.m[0][2] * v.z,
+          r.m[1][0] * v.x + r.m[1][1] * v.y + r.m[1][2] * v.z,
+          r.m[2][0] * v.x + r.m[2][1] * v.y + r.m[2][2] * v.z};
+}
+
+// ---- so(3) log (liegroups.py:130-141) -------------------------------------
+template <typename T>
+__device__ __forceinline__ vec3<T> qlog(quat<T> q) {
+  if (q.w < T(0)) q = {-q.w, -q.x, -q.y, -q.z};
+  const T s = sqrt_t(q.x * q.x + q.y * q.y + q.z * q.z);
+  T scale;
+  if (s < LieConst<T>::log_series_below) {
+    scale = T(2) / tmax(q.w, T(0.5)) * (T(1) - s * s / T(3));
+  } else {
+    scale = T(2) * atan2_t(s, q.w) / s;
+  }
+  return {scale * q.x, scale * q.y, scale * q.z};
+}
+
+// ---- Jacobian coefficients, Horner in t = theta^2 -------------------------
+// c1 = (th - sin th)/th^3;  k2 = (th^2/2 + cos th - 1)/th^4;
+// k3 = (2 th - 3 sin th + th cos th)/(2 th^5);  b = (1 - (th/2)cot(th/2))/th^2.
+template <typename T>
+struct JacCoef {
+  T c1, k2, k3, b;
+};
+
+template <typename T>
+__device__ __forceinline__ JacCoef<T> jac_coefs(T th) {
+  const T t = th * th;
+  JacCoef<T> k;
+  if (th < LieConst<T>::series_below) {
+    k.c1 = T(1.0 / 6.0) + t * (T(-1.0 / 120.0) + t * (T(1.0 / 5040.0) + t * (T(-1.0 / 362880.0) +
+           t * (T(1.0 / 39916800.0) + t * T(-1.0 / 6227020800.0)))));
+    k.k2 = T(1.0 / 24.0) + t * (T(-1.0 / 720.0) + t * (T(1.0 / 40320.0) + t * (T(-1.0 / 3628800.0) +
+           t * (T(1.0 / 479001600.0) + t * T(-1.0 / 87178291200.0)))));
+    k.k3 = T(1.0 / 120.0) + t * (T(-1.0 / 2520.0) + t * (T(1.0 / 120960.0) + t * (T(-1.0 / 9979200.0) +
+           t * (T(1.0 / 1245404160.0) + t * T(-1.0 / 217945728000.0)))));
+    k.b = T(1.0 / 12.0) + t * (T(1.0 / 720.0) + t * (T(1.0 / 30240.0) + t * (T(1.0 / 1209600.0) +
+          t * (T(1.0 / 47900160.0) + t * T(691.0 / 1307674368000.0)))));
+  } else {
+    T sn, cs;
+    sincos_t(th, &sn, &cs);
+    const T t2 = t * t;
+    k.c1 = (th - sn) / (t * th);
+    k.k2 = (T(0.5) * t + cs - T(1)) / t2;
+    k.k3 = (T(2) * th - T(3) * sn + th * cs) / (T(2) * t2 * th);
+    const T h = T(0.5) * th;
+    k.b = (T(1) - h / tan_t(h)) / t;
+  }
+  return k;
+}
+
+// ---- SE(3) log as a translation-first twist (liegroups.py:203-207) -------
+// v = Jl^-1(phi) t = t - phi x t / 2 + b phi x (phi x t).
+template <typename T>
+struct Twist {
+  vec3<T> v, phi;
+  T theta;
+  JacCoef<T> k;
+};
+
+template <typename T>
+__device__ __forceinline__ Twist<T> se3_log(const quat<T>& q, const vec3<T>& t) {
+  Twist<T> xi;
+  xi.phi = qlog(q);
+  xi.theta = sqrt_t(dot(xi.phi, xi.phi));
+  xi.k = jac_coefs(xi.theta);
+  const vec3<T> a = cross(xi.phi, t);
+  const vec3<T> b2 = cross(xi.phi, a);
+  xi.v = {t.x - T(0.5) * a.x + xi.k.b * b2.x, t.y - T(0.5) * a.y + xi.k.b * b2.y,
+          t.z - T(0.5) * a.z + xi.k.b * b2.z};
+  return xi;
+}
+
+// ---- Jr^-1(xi) = Jl^-1(-xi) = [[A, Bm], [0, A]] (liegroups.py:238-252) ----
+// With rho = -v, ph = -phi, d = ph.rho:
+//   A  = (1 - b th^2) I - [ph]x / 2 + b ph ph^T           (so3 Jl^-1)
+//   Q  = [s]x + c1 (rho ph^T + ph rho^T) - 2 k3 d ph ph^T + (2 k3 d th^2 - 2 c1 d) I,
+//        s = (1/2 - k2 th^2) rho + (2 k2 - c1) d ph        (Barfoot's Q, expanded
+//        with [a]x[b]x = b a^T - (a.b) I; equals liegroups.py:230-235)
+//   Bm = -A Q A.
+template <typename T>
+struct JrInv {
+  mat3<T> A, B;
+};
+
+template <typename T>
+__device__ __forceinline__ JrInv<T> se3_jr_inv(const Twist<T>& xi) {
+  const vec3<T> rho{-xi.v.x, -xi.v.y, -xi.v.z};
+  const vec3<T> ph{-xi.phi.x, -xi.phi.y, -xi.phi.z};
+  const T t = xi.theta * xi.theta;
+  const T b = xi.k.b, c1 = xi.k.c1, k2 = xi.k.k2, k3 = xi.k.k3;
+  const T d = dot(ph, rho);
+  JrInv<T> J;
+  const T diag = T(1) - b * t;
+  const T px[3] = {ph.x, ph.y, ph.z};
+  const T rx[3] = {rho.x, rho.y, rho.z};
+  // A
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) J.A.m[i][j] = b * px[i] * px[j] + (i == j ? diag : T(0));
+  J.A.m[0][1] += T(0.5) * ph.z;
+  J.A.m[0][2] -= T(0.5) * ph.y;
+  J.A.m[1][0] -= T(0.5) * ph.z;
+  J.A.m[1][2] += T(0.5) * ph.x;
+  J.A.m[2][0] += T(0.5) * ph.y;
+  J.A.m[2][1] -= T(0.5) * ph.x;
+  // Q
+  const T a1 = T(0.5) - k2 * t, a2 = (T(2) * k2 - c1) * d;
+  const vec3<T> s{a1 * rho.x + a2 * ph.x, a1 * rho.y + a2 * ph.y, a1 * rho.z + a2 * ph.z};
+  const T e = T(-2) * k3 * d;
+  const T qd = T(2) * k3 * d * t - T(2) * c1 * d;
+  mat3<T> Q;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      Q.m[i][j] = c1 * (rx[i] * px[j] + px[i] * rx[j]) + e * px[i] * px[j] + (i == j ? qd : T(0));
+  Q.m[0][1] -= s.z;
+  Q.m[0][2] += s.y;
+  Q.m[1][0] += s.z;
+  Q.m[1][2] -= s.x;
+  Q.m[2][0] -= s.y;
+  Q.m[2][1] += s.x;
+  // B = -A Q A
+  mat3<T> QA;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      QA.m[i][j] = Q.m[i][0] * J.A.m[0][j] + Q.m[i][1] * J.A.m[1][j] + Q.m[i][2] * J.A.m[2][j];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j)
+      J.B.m[i][j] = -(J.A.m[i][0] * QA.m[0][j] + J.A.m[i][1] * QA.m[1][j] + J.A.m[i][2] * QA.m[2][j]);
+  return J;
+}
+
+}  // namespace kop

@@ -1,0 +1,226 @@
+"""Task drivers: IK-Beam on the device (tasks.py:40-180 of the reference).
+
+``solve_ik_beam(IkRequest) -> IkResult`` keeps the reference signature;
+``solve_ik_beam_batch`` / ``IkBeamSolver`` are the batched entry the
+reference lacks (it loops targets one by one, benchmark.py:136-151): B
+targets x S seeds run as B*S device lanes in one launch sequence.
+
+IK-Beam (tasks.py:119-161): all seeds run ``prune_after`` LM steps, the
+``keep`` lowest-cost lanes (stable order) survive, run the remaining steps,
+and the lowest-cost survivor wins.  Seeds are Philox-keyed by (rng_seed, i),
+shared by every target, and drawn bit-identically to numpy on the device.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _device as dv
+from . import costs as ck
+from ._lib import KopIkParams, check, lib
+from .errors import UnsupportedFeatureError
+from .liegroups import Transform2, Transform3
+from .robot import RobotModel, _precision
+from .solver import SolveReport, VariableSet
+
+BASE_PINNED = 1e12
+ANCHOR_WEIGHT = 1e3
+
+
+@dataclass
+class IkRequest:
+    model: RobotModel
+    target_link: str
+    target_pose: Transform3
+    weights: ck.CostWeights = field(default_factory=ck.CostWeights)
+    seeds: int = 64
+    total_steps: int = 16
+    prune_after: int = 6
+    keep: int = 4
+    success_pos_tol: float = 0.005
+    success_rot_tol: float = 0.05
+    rng_seed: int = 0
+    optimize_base: bool = False
+    base_reg_weight: float = 0.0
+    precision: str = "fp32"
+
+    def __post_init__(self):
+        if not 0 < self.prune_after < self.total_steps:
+            raise ValueError("need 0 < prune_after < total_steps")
+        if not 1 <= self.keep <= self.seeds:
+            raise ValueError("need 1 <= keep <= seeds")
+
+
+@dataclass
+class IkResult:
+    q: np.ndarray
+    base: Transform2 | None
+    pos_error: float
+    rot_error: float
+    success: bool
+    report: SolveReport
+
+    def to_json(self, include_timing: bool = False) -> dict:
+        out = {"q": self.q.tolist(), "pos_error": self.pos_error, "rot_error": self.rot_error,
+               "success": self.success, "report": self.report.to_json(include_timing=include_timing)}
+        if self.base is not None:
+            out["base"] = {"angle": self.base.angle, "xy": self.base.translation.tolist()}
+        return out
+
+
+def _seed_bounds(model: RobotModel):
+    fin_lo, fin_hi = np.isfinite(model.lower_limits), np.isfinite(model.upper_limits)
+    lo = np.where(fin_lo, model.lower_limits, -math.pi)
+    hi = np.where(fin_hi, model.upper_limits, math.pi)
+    return lo, hi, ~(fin_lo & fin_hi)
+
+
+def philox_uniform_device(key0: int, key1_base: int, count: int, lo, hi, negate=None):
+    """Row i = Generator(Philox(key=[key0, key1_base+i])).uniform(lo, hi) (device, bit-exact)."""
+    lo = np.ascontiguousarray(lo, dtype=float)
+    hi = np.ascontiguousarray(hi, dtype=float)
+    n = lo.size
+    neg = np.ascontiguousarray(np.zeros(n, np.uint8) if negate is None else np.asarray(negate, np.uint8))
+    out = dv.empty((count, n))
+    check(lib().kop_sample_uniform(C.c_uint64(int(key0) & (2**64 - 1)), C.c_uint64(int(key1_base) & (2**64 - 1)),
+                                   count, n, lo.ctypes.data, hi.ctypes.data, neg.ctypes.data, dv.ptr(out),
+                                   dv.stream_handle()), "kop_sample_uniform")
+    return out
+
+
+def sample_seed_configurations_device(model: RobotModel, count: int, rng_seed: int):
+    lo, hi, unbounded = _seed_bounds(model)
+    return philox_uniform_device(rng_seed, 0, count, lo, hi, unbounded)
+
+
+def sample_seed_configurations(model: RobotModel, count: int, rng_seed: int) -> np.ndarray:
+    """tasks.py:88-106: seed i ~ U(lo, hi) from Philox key (rng_seed, i); (-pi, pi] for continuous."""
+    return sample_seed_configurations_device(model, count, rng_seed).cpu().numpy()
+
+
+def targets_to_array(targets) -> np.ndarray:
+    """Transform3 / list of Transform3 / (B,7) array -> (B,7) float64 (w,x,y,z,px,py,pz)."""
+    if isinstance(targets, Transform3):
+        return targets.as_array()[None]
+    if isinstance(targets, (list, tuple)) and targets and isinstance(targets[0], Transform3):
+        return np.stack([t.as_array() for t in targets])
+    arr = np.asarray(targets, dtype=float)
+    if arr.ndim != 2 or arr.shape[1] != 7:
+        raise ValueError(f"targets must have shape (B, 7), got {arr.shape}")
+    return arr
+
+
+@dataclass
+class BeamBatch:
+    """Per-target IK-Beam outputs (device tensors or host arrays)."""
+
+    q: object
+    cost: object
+    history: object
+    pos_error: object
+    rot_error: object
+    success: object
+
+    def cpu(self) -> "BeamBatch":
+        f = lambda x: x.cpu().numpy() if hasattr(x, "cpu") else x
+        return BeamBatch(*(f(getattr(self, k)) for k in ("q", "cost", "history", "pos_error", "rot_error", "success")))
+
+
+class IkBeamSolver:
+    """Reusable batched IK-Beam for one (robot, link, request shape).
+
+    Holds the seeds on the device and a grow-only workspace; ``solve_device``
+    only enqueues kernels on the current stream (CUDA-graph capturable once
+    the workspace has been sized).
+    """
+
+    def __init__(self, model: RobotModel, link: str, weights: ck.CostWeights | None = None, seeds: int = 64,
+                 total_steps: int = 16, prune_after: int = 6, keep: int = 4, rng_seed: int = 0,
+                 success_pos_tol: float = 0.005, success_rot_tol: float = 0.05, precision="fp32",
+                 seed_configurations=None):
+        if not 0 < prune_after < total_steps:
+            raise ValueError("need 0 < prune_after < total_steps")
+        if not 1 <= keep <= seeds:
+            raise ValueError("need 1 <= keep <= seeds")
+        self.model, self.link = model, link
+        self.link_idx = model.link_index(link)
+        w = (weights or ck.CostWeights()).ik_row_weights()
+        self.total_steps = total_steps
+        self.params = KopIkParams(w[0], w[1], w[2], w[3], seeds, total_steps, prune_after, keep,
+                                  success_pos_tol, success_rot_tol, _precision(precision))
+        if seed_configurations is not None:
+            self.seeds = dv.to_dev(np.asarray(seed_configurations, dtype=float).reshape(seeds, model.actuated_count))
+        else:
+            self.seeds = sample_seed_configurations_device(model, seeds, rng_seed)
+        self._ws = None
+
+    def workspace(self, batch: int):
+        need = int(lib().kop_ik_beam_workspace_bytes(self.model._handle, self.link_idx, C.byref(self.params), batch))
+        if need < 0:
+            check(need, "kop_ik_beam_workspace_bytes")
+        if self._ws is None or self._ws.numel() < need:
+            t = dv.require_cuda()
+            self._ws = t.empty(need, dtype=t.uint8, device="cuda")
+        return self._ws
+
+    def alloc_outputs(self, batch: int) -> BeamBatch:
+        t = dv.require_cuda()
+        n = self.model.actuated_count
+        return BeamBatch(dv.empty((batch, n)), dv.empty(batch), dv.empty((batch, self.total_steps + 1)),
+                         dv.empty(batch), dv.empty(batch), t.empty(batch, dtype=t.uint8, device="cuda"))
+
+    def solve_device(self, targets, out: BeamBatch | None = None, history: bool = True) -> BeamBatch:
+        """targets: device (B,7) float64 tensor.  Enqueues the solve; returns device outputs."""
+        targets = dv.to_dev(targets)
+        b = targets.shape[0]
+        out = out or self.alloc_outputs(b)
+        ws = self.workspace(b)
+        check(lib().kop_ik_beam(self.model._handle, self.link_idx, C.byref(self.params), dv.ptr(targets), b,
+                                dv.ptr(self.seeds), dv.ptr(ws), ws.numel(), dv.ptr(out.q), dv.ptr(out.cost),
+                                dv.ptr(out.history) if history else None, dv.ptr(out.pos_error),
+                                dv.ptr(out.rot_error), dv.ptr(out.success), dv.stream_handle()), "kop_ik_beam")
+        return out
+
+    def solve(self, targets) -> BeamBatch:
+        """Host in, host out (synchronous)."""
+        arr = targets_to_array(targets)
+        return self.solve_device(dv.to_dev(arr)).cpu()
+
+
+def solve_ik_beam_batch(model: RobotModel, link: str, targets, weights: ck.CostWeights | None = None,
+                        seeds: int = 64, total_steps: int = 16, prune_after: int = 6, keep: int = 4,
+                        rng_seed: int = 0, precision="fp32", success_pos_tol: float = 0.005,
+                        success_rot_tol: float = 0.05) -> BeamBatch:
+    """IK-Beam over B targets at once (host arrays in and out)."""
+    solver = IkBeamSolver(model, link, weights, seeds, total_steps, prune_after, keep, rng_seed,
+                          success_pos_tol, success_rot_tol, precision)
+    return solver.solve(targets)
+
+
+def solve_ik_beam(req: IkRequest) -> IkResult:
+    """Multi-seed IK with mid-optimisation pruning; never raises on unreachable targets."""
+    if req.optimize_base:
+        return solve_ik_mobile(req)
+    res = solve_ik_beam_batch(req.model, req.target_link, req.target_pose, req.weights, req.seeds,
+                              req.total_steps, req.prune_after, req.keep, req.rng_seed, req.precision,
+                              req.success_pos_tol, req.success_rot_tol)
+    q = res.q[0].copy()
+    hist = [float(h) for h in res.history[0]]
+    report = SolveReport(final_values=VariableSet.of(q=q), initial_cost=hist[0], final_cost=float(res.cost[0]),
+                         iterations_run=req.total_steps, termination="max_iterations", cost_history=hist)
+    return IkResult(q=q, base=None, pos_error=float(res.pos_error[0]), rot_error=float(res.rot_error[0]),
+                    success=bool(res.success[0]), report=report)
+
+
+def solve_ik_mobile(req: IkRequest) -> IkResult:
+    """Mobile-base IK (tasks.py:169-180).  A pinned base reduces to arm-only IK."""
+    if req.base_reg_weight >= BASE_PINNED:
+        import dataclasses
+        res = solve_ik_beam(dataclasses.replace(req, optimize_base=False))
+        res.base = Transform2.identity()
+        return res
+    raise UnsupportedFeatureError("mobile-base lanes (SE(2) variable) are not compiled in this build yet")

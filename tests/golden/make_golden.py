@@ -1,0 +1,117 @@
+"""Generate golden vectors by running the REFERENCE implementation (read-only).
+
+Run in the build container only (``/root/reference`` does not exist on the GPU
+box); the resulting ``reference_golden.npz`` is committed and is what the
+oracle and the CUDA parity tests are pinned against.
+
+    python tests/golden/make_golden.py
+
+Every array below comes from calling the reference's own public functions:
+``robot.fk_arrays`` (robot.py:404), ``liegroups.se3_log_arrays`` /
+``se3_right_jacobian_inv`` (liegroups.py:203-252), ``beam.IkLaneProblem``
+(beam.py:71-240), ``tasks.sample_seed_configurations`` (tasks.py:88),
+``tasks.solve_ik_beam`` (tasks.py:164) and
+``benchmark.generate_reachable_targets`` (benchmark.py:83).
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+
+from kinoptik import beam, liegroups, robot, tasks  # noqa: E402
+from kinoptik.benchmark import generate_reachable_targets  # noqa: E402
+from kinoptik.liegroups import Transform3  # noqa: E402
+
+ROBOTS = os.path.join(REF, "kinoptik", "robots")
+OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "reference_golden.npz")
+
+
+def main():
+    arm7 = robot.load_robot(os.path.join(ROBOTS, "arm7.urdf"), os.path.join(ROBOTS, "arm7.sidecar.json"))
+    p2r = robot.load_robot(os.path.join(ROBOTS, "planar_2r.urdf"), os.path.join(ROBOTS, "planar_2r.sidecar.json"))
+    grip = robot.load_robot(os.path.join(ROBOTS, "arm7_gripper.urdf"))
+    g = {}
+    rng = np.random.default_rng(1234)
+
+    # --- FK on random in-limit configurations (three fixtures) -------------
+    for name, m in (("arm7", arm7), ("planar_2r", p2r), ("arm7_gripper", grip)):
+        qs = np.stack([m.sample_configuration(rng) for _ in range(32)])
+        quat, pos, jp, ja = robot.fk_arrays(m, qs)
+        g[f"fk_{name}_q"], g[f"fk_{name}_quat"], g[f"fk_{name}_pos"] = qs, quat, pos
+        g[f"fk_{name}_jpos"], g[f"fk_{name}_jaxis"] = jp, ja
+        g[f"tables_{name}_lower"], g[f"tables_{name}_upper"] = m.lower_limits, m.upper_limits
+        g[f"tables_{name}_rest"] = m.rest_pose
+        g[f"tables_{name}_origin_quat"] = m._origin_quat
+
+    # --- SE(3) log and Jr^-1 on twists spanning small to large angles -------
+    xi = rng.normal(size=(64, 6))
+    xi[:, 3:] *= np.geomspace(1e-9, 3.0, 64)[:, None] / np.linalg.norm(xi[:, 3:], axis=1, keepdims=True)
+    quats, trans = [], []
+    for x in xi:
+        t = Transform3.exp(x)
+        quats.append(t.rotation.wxyz)
+        trans.append(t.translation)
+    quats, trans = np.array(quats), np.array(trans)
+    g["lie_q"], g["lie_t"] = quats, trans
+    g["lie_log"] = liegroups.se3_log_arrays(quats, trans)
+    g["lie_xi"] = xi
+    g["lie_jrinv"] = liegroups.se3_right_jacobian_inv(xi)
+
+    # --- seeds and targets ---------------------------------------------------
+    g["seeds_arm7_77"] = tasks.sample_seed_configurations(arm7, 64, 77)
+    g["seeds_arm7_3"] = tasks.sample_seed_configurations(arm7, 16, 3)
+    g["seeds_p2r_5"] = tasks.sample_seed_configurations(p2r, 64, 5)
+    targets = generate_reachable_targets(arm7, "flange", 40, 77)
+    g["targets_arm7_77_wxyz"] = np.array([t.rotation.wxyz for t in targets])
+    g["targets_arm7_77_pos"] = np.array([t.translation for t in targets])
+
+    # --- lane engine: per-step cost of all 64 seeds on target 0 ------------
+    t0 = targets[0]
+    w = tasks.IkRequest(model=arm7, target_link="flange", target_pose=t0).weights
+    prob = beam.IkLaneProblem(arm7, "flange", t0, w.pose_position, w.pose_orientation, w.limit, w.rest)
+    st = prob.start_state(g["seeds_arm7_77"])
+    st = prob.run(st, 16)
+    g["lane_t0_hist"] = np.stack(st.history, axis=1)
+    g["lane_t0_q"], g["lane_t0_damping"] = st.q, st.damping
+    r, jac = prob.residuals_and_jacobian(g["seeds_arm7_77"][:8])
+    g["lane_t0_r"], g["lane_t0_jac"] = r, jac
+
+    # --- full IK-Beam on the first 40 benchmark targets (rng 77) ----------
+    rows = {k: [] for k in ("q", "cost", "hist", "pos", "rot", "succ")}
+    for t in targets:
+        res = tasks.solve_ik_beam(tasks.IkRequest(model=arm7, target_link="flange", target_pose=t, rng_seed=77))
+        rows["q"].append(res.q)
+        rows["cost"].append(res.report.final_cost)
+        rows["hist"].append(res.report.cost_history)
+        rows["pos"].append(res.pos_error)
+        rows["rot"].append(res.rot_error)
+        rows["succ"].append(res.success)
+    for k, v in rows.items():
+        g[f"beam_arm7_77_{k}"] = np.array(v)
+
+    # --- unreachable target and planar 2R beam ----------------------------
+    far = Transform3.from_parts([1, 0, 0, 0], [10.0, 0.0, 0.5])
+    res = tasks.solve_ik_beam(tasks.IkRequest(model=arm7, target_link="flange", target_pose=far, rng_seed=0))
+    g["beam_far_q"], g["beam_far_pos"], g["beam_far_hist"] = res.q, res.pos_error, np.array(res.report.cost_history)
+    p_targets = generate_reachable_targets(p2r, "ee", 8, 5)
+    g["targets_p2r_5_wxyz"] = np.array([t.rotation.wxyz for t in p_targets])
+    g["targets_p2r_5_pos"] = np.array([t.translation for t in p_targets])
+    ph, pp = [], []
+    for t in p_targets:
+        res = tasks.solve_ik_beam(tasks.IkRequest(model=p2r, target_link="ee", target_pose=t, rng_seed=5))
+        ph.append(res.report.cost_history)
+        pp.append(res.q)
+    g["beam_p2r_5_hist"], g["beam_p2r_5_q"] = np.array(ph), np.array(pp)
+
+    np.savez_compressed(OUT, **g)
+    print(f"wrote {OUT}: {len(g)} arrays")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,71 @@
+"""The CPU oracle is pinned to the reference: every check here compares the
+oracle (oracle/ik_oracle.py) with golden vectors produced by running the
+reference itself (tests/golden/make_golden.py).  Exact equality wherever the
+restatement follows the reference's operation order."""
+
+import numpy as np
+import pytest
+
+from oracle import ik_oracle as o
+
+
+@pytest.mark.parametrize("name", ["arm7", "planar_2r", "arm7_gripper"])
+def test_fk_matches_reference_bitwise(chains, golden, name):
+    ch = chains[name]
+    out = o.fk(ch, golden[f"fk_{name}_q"])
+    for arr, key in zip(out, ("quat", "pos", "jpos", "jaxis")):
+        assert np.array_equal(arr, golden[f"fk_{name}_{key}"]), key
+    assert np.array_equal(ch.oq, golden[f"tables_{name}_origin_quat"])
+    assert np.array_equal(ch.rest, golden[f"tables_{name}_rest"])
+    assert np.array_equal(ch.lower, golden[f"tables_{name}_lower"])
+
+
+def test_se3_log_and_jr_inv(golden):
+    assert np.array_equal(o.se3_log(golden["lie_q"], golden["lie_t"]), golden["lie_log"])
+    assert np.array_equal(o.se3_jr_inv(golden["lie_xi"]), golden["lie_jrinv"])
+
+
+def test_seeds_bitwise(chains, golden):
+    assert np.array_equal(o.sample_seeds(chains["arm7"], 64, 77), golden["seeds_arm7_77"])
+    assert np.array_equal(o.sample_seeds(chains["arm7"], 16, 3), golden["seeds_arm7_3"])
+    assert np.array_equal(o.sample_seeds(chains["planar_2r"], 64, 5), golden["seeds_p2r_5"])
+
+
+def test_targets_bitwise(chains, golden):
+    tq, tt, _ = o.reachable_targets(chains["arm7"], 8, 40, 77)
+    assert np.array_equal(tq, golden["targets_arm7_77_wxyz"])
+    assert np.array_equal(tt, golden["targets_arm7_77_pos"])
+
+
+def test_lane_engine_bitwise(chains, golden):
+    ch = chains["arm7"]
+    iq, it = o.target_inverse(golden["targets_arm7_77_wxyz"][:1], golden["targets_arm7_77_pos"][:1])
+    eng = o.LaneEngine(ch, 8, np.repeat(iq, 8, 0), np.repeat(it, 8, 0), o.DEFAULT_WEIGHTS)
+    r, j = eng.residuals_and_jacobian(golden["seeds_arm7_77"][:8])
+    assert np.array_equal(r, golden["lane_t0_r"]) and np.array_equal(j, golden["lane_t0_jac"])
+    eng = o.LaneEngine(ch, 8, np.repeat(iq, 64, 0), np.repeat(it, 64, 0), o.DEFAULT_WEIGHTS)
+    st = eng.run(eng.start(golden["seeds_arm7_77"]), 16)
+    assert np.array_equal(np.stack(st.hist, 1), golden["lane_t0_hist"])
+    assert np.array_equal(st.q, golden["lane_t0_q"])
+    assert np.array_equal(st.lam, golden["lane_t0_damping"])
+
+
+def test_ik_beam_bitwise_40_targets(chains, golden):
+    ch = chains["arm7"]
+    res = o.ik_beam(ch, 8, golden["targets_arm7_77_wxyz"], golden["targets_arm7_77_pos"], golden["seeds_arm7_77"])
+    assert np.array_equal(res.hist, golden["beam_arm7_77_hist"])
+    assert np.array_equal(res.q, golden["beam_arm7_77_q"])
+    assert np.allclose(res.pos_err, golden["beam_arm7_77_pos"], rtol=1e-12, atol=1e-15)
+    assert np.array_equal(res.success, golden["beam_arm7_77_succ"])
+
+
+def test_ik_beam_unreachable_and_planar(chains, golden):
+    ch = chains["arm7"]
+    seeds = o.sample_seeds(ch, 64, 0)
+    res = o.ik_beam(ch, 8, np.array([[1.0, 0, 0, 0]]), np.array([[10.0, 0.0, 0.5]]), seeds)
+    assert np.array_equal(res.hist[0], golden["beam_far_hist"])
+    assert not res.success[0] and 8.0 < res.pos_err[0] < 10.0
+    p = chains["planar_2r"]
+    res = o.ik_beam(p, p.link("ee"), golden["targets_p2r_5_wxyz"], golden["targets_p2r_5_pos"],
+                    o.sample_seeds(p, 64, 5))
+    assert np.array_equal(res.hist, golden["beam_p2r_5_hist"])
