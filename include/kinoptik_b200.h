@@ -135,6 +135,14 @@ int kop_ik_beam(const KopModel* model, int32_t link, const KopIkParams* params,
                 int64_t workspace_bytes, double* q_out, double* cost_out, double* history_out,
                 double* pos_err, double* rot_err, uint8_t* success, void* stream);
 
+/* The two launches of kop_ik_beam issued separately (stages: 1 = seeds +
+ * prune into the workspace, 2 = survivors + winner + errors, 3 = both), so a
+ * caller can bracket each kernel with CUDA events.  Same arguments. */
+int kop_ik_beam_stage(const KopModel* model, int32_t link, const KopIkParams* params, int32_t stages,
+                      const double* targets, int64_t batch, const double* seeds, void* workspace,
+                      int64_t workspace_bytes, double* q_out, double* cost_out, double* history_out,
+                      double* pos_err, double* rot_err, uint8_t* success, void* stream);
+
 /* --- counter-based sampling ---------------------------------------------
  * replaces: tasks.sample_seed_configurations (tasks.py:88-106) and the draws
  * of benchmark.generate_reachable_targets (benchmark.py:83-93): row i is

@@ -51,6 +51,8 @@ SIGNATURES = {
     "kop_ik_beam_workspace_bytes": (_i64, [_p, _i32, C.POINTER(KopIkParams), _i64]),
     "kop_ik_beam": (C.c_int, [_p, _i32, C.POINTER(KopIkParams), _p, _i64, _p, _p, _i64,
                               _p, _p, _p, _p, _p, _p, _p]),
+    "kop_ik_beam_stage": (C.c_int, [_p, _i32, C.POINTER(KopIkParams), _i32, _p, _i64, _p, _p, _i64,
+                                    _p, _p, _p, _p, _p, _p, _p]),
     "kop_sample_uniform": (C.c_int, [_u64, _u64, _i64, _i32, _p, _p, _p, _p, _p]),
     "kop_link_poses": (C.c_int, [_p, _i32, _p, _i64, _p, _p]),
     "kop_fma_peak_kernel": (C.c_int, [_i32, _i32, _i32, _p, C.POINTER(_f64), _p]),

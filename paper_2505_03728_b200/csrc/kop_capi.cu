@@ -50,6 +50,13 @@ void hrot(const HQ& q, const double p[3], double out[3]) {
   out[1] = p[1] + q.w * t1 + (q.z * t0 - q.x * t2);
   out[2] = p[2] + q.w * t2 + (q.x * t1 - q.y * t0);
 }
+void hmat(const HQ& q, double r[3][3]) {
+  const double xx = q.x * q.x, yy = q.y * q.y, zz = q.z * q.z, xy = q.x * q.y, xz = q.x * q.z,
+               yz = q.y * q.z, wx = q.w * q.x, wy = q.w * q.y, wz = q.w * q.z;
+  r[0][0] = 1 - 2 * (yy + zz); r[0][1] = 2 * (xy - wz); r[0][2] = 2 * (xz + wy);
+  r[1][0] = 2 * (xy + wz); r[1][1] = 1 - 2 * (xx + zz); r[1][2] = 2 * (yz - wx);
+  r[2][0] = 2 * (xz - wy); r[2][1] = 2 * (yz + wx); r[2][2] = 1 - 2 * (xx + yy);
+}
 // Rotation taking +z onto the unit vector a.
 HQ align_z(const double a[3]) {
   if (a[2] < -1.0 + 1e-12) return {0.0, 1.0, 0.0, 0.0};
@@ -88,6 +95,7 @@ int compile_chain(const KopModel& m, int link, ChainParams<double, kChainMax>& C
     const HQ tq = hmul(hmul(pend, oq), al);
     C.tq[k][0] = tq.w; C.tq[k][1] = tq.x; C.tq[k][2] = tq.y; C.tq[k][3] = tq.z;
     memcpy(C.tp[k], tp, sizeof(tp));
+    hmat(tq, C.tr[k]);
     C.mult[k] = P.mult[j];
     C.offset[k] = P.offset[j];
     C.qcol[k] = P.qcol[j];
@@ -112,6 +120,8 @@ ChainParams<T, K> cast_chain(const ChainParams<double, kChainMax>& D) {
   for (int k = 0; k < K && k < kChainMax; ++k) {
     for (int i = 0; i < 4; ++i) C.tq[k][i] = T(D.tq[k][i]);
     for (int i = 0; i < 3; ++i) C.tp[k][i] = T(D.tp[k][i]);
+    for (int i = 0; i < 3; ++i)
+      for (int j = 0; j < 3; ++j) C.tr[k][i][j] = T(D.tr[k][i][j]);
     C.mult[k] = T(D.mult[k]);
     C.offset[k] = T(D.offset[k]);
     C.qcol[k] = D.qcol[k];
@@ -387,9 +397,11 @@ cudaError_t restride(const double* src, int64_t rows, int sn, int dn, double* ds
 
 extern "C" {
 
-int kop_ik_beam(const KopModel* m, int32_t link, const KopIkParams* p, const double* targets, int64_t batch,
-                const double* seeds, void* workspace, int64_t workspace_bytes, double* q_out, double* cost_out,
-                double* history_out, double* pos_err, double* rot_err, uint8_t* success, void* stream) {
+int kop_ik_beam_stage(const KopModel* m, int32_t link, const KopIkParams* p, int32_t stages, const double* targets,
+                      int64_t batch, const double* seeds, void* workspace, int64_t workspace_bytes, double* q_out,
+                      double* cost_out, double* history_out, double* pos_err, double* rot_err, uint8_t* success,
+                      void* stream) {
+  if (stages < 1 || stages > 3) return fail(KOP_EINVAL, "stages must be 1, 2 or 3");
   if (!p) return fail(KOP_EINVAL, "null params");
   ChainParams<double, kChainMax> C;
   Shape sh;
@@ -442,12 +454,22 @@ int kop_ik_beam(const KopModel* m, int32_t link, const KopIkParams* p, const dou
   L.success = success;
   const char* tp = getenv("KOP_TWOPASS");
   L.twopass = tp && tp[0] == '1';
+  L.stages = stages;
+  if (sh == Shape::kGen8 && n != 8 && stages != 3)
+    return fail(KOP_EUNSUPPORTED, "split-stage launches need n == 8 or an identity-chain shape");
   const double w[4] = {p->w_position, p->w_orientation, p->w_limit, p->w_rest};
   cudaError_t e = p->precision == KOP_FP32 ? dispatch_beam<float>(sh, *m, C, w, L, st)
                                            : dispatch_beam<double>(sh, *m, C, w, L, st);
   if (e == cudaSuccess && q_k != q_out) e = restride(q_k, batch, 8, n, q_out, st);
   if (seeds_pad.ptr) cudaStreamSynchronize(st);  // scratch freed at return
   return cuda_status(e);
+}
+
+int kop_ik_beam(const KopModel* m, int32_t link, const KopIkParams* p, const double* targets, int64_t batch,
+                const double* seeds, void* workspace, int64_t workspace_bytes, double* q_out, double* cost_out,
+                double* history_out, double* pos_err, double* rot_err, uint8_t* success, void* stream) {
+  return kop_ik_beam_stage(m, link, p, 3, targets, batch, seeds, workspace, workspace_bytes, q_out, cost_out,
+                           history_out, pos_err, rot_err, success, stream);
 }
 
 static int lane_call(const KopModel* m, int32_t link, int32_t precision, const double* weights,

@@ -11,6 +11,11 @@
 //    8-FMA product q * (cos, 0, 0, sin) and the world axis is one column of
 //    R(q) -- the same transform as robot.py:437-447, fewer flops.
 // Mathematically identical to fk_arrays; differences are rounding only.
+//
+// The device evaluates the chain BACKWARD (end effector -> root): with
+// S_k = child_k -> EE, the body-frame Jacobian column of joint k is read off
+// S_k directly (axis = +z there), so no per-joint world anchors/axes are kept
+// live and the pass ends with the world EE pose S_0 for the residual.
 #pragma once
 
 #include <stdint.h>
@@ -24,6 +29,7 @@ template <typename T, int K>
 struct ChainParams {
   T tq[K][4];    // joint-frame rotation relative to the previous moving child frame
   T tp[K][3];    // joint anchor translation relative to the previous moving child frame
+  T tr[K][3][3]; // R(tq): the backward pass rotates positions with 9 constant-operand FMAs
   T mult[K];     // mimic multiplier (robot.py:93-97)
   T offset[K];   // mimic offset
   int32_t qcol[K];

@@ -25,13 +25,14 @@ namespace kop {
 // IK-Beam stage 1
 // ---------------------------------------------------------------------------
 template <typename T, int NQ, int K, bool ID>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
 k_beam_stage1(const ChainParams<T, K> C, const CostParams<T, NQ> W, const double* __restrict__ targets,
               int64_t B, const double* __restrict__ seeds, int S, int P, int steps1, int keep,
               T* __restrict__ surv, int rec) {
   extern __shared__ unsigned char smem_raw[];
   T* hist = reinterpret_cast<T*>(smem_raw);           // [(steps1+1) * bd]
   T* costs = hist + (size_t)(steps1 + 1) * blockDim.x;  // [bd]
+  T* Ag = costs + blockDim.x;                           // [(Tri + NQ) * bd]
   const int tid = threadIdx.x, bd = blockDim.x;
   const int64_t tgt = (int64_t)blockIdx.x * (bd / P) + tid / P;
   const int s = tid % P;
@@ -42,10 +43,12 @@ k_beam_stage1(const ChainParams<T, K> C, const CostParams<T, NQ> W, const double
   const TargetInv<T> tg = to_target<T>(tinv);
 
   LaneState<T, NQ> st;
+  st.Ag = Ag + tid;
+  st.stride = bd;
   const double* sd = seeds + (size_t)(s < S ? s : 0) * NQ;
 #pragma unroll
   for (int i = 0; i < NQ; ++i) st.q[i] = T(sd[i]);
-  st.cost = lane_normal<T, NQ, K, ID>(C, W, tg, st.q, st.A, st.g);
+  lane_init<T, NQ, K, ID>(C, W, tg, st);
   st.lam = T(BeamConsts::damping_init);
   hist[tid] = st.cost;
   for (int it = 0; it < steps1; ++it) {
@@ -120,7 +123,7 @@ __device__ __forceinline__ void pose_errors_f64(const ChainParams<double, K>& C,
 }
 
 template <typename T, int NQ, int K, bool ID>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 4)
 k_beam_stage2(const ChainParams<T, K> C, const CostParams<T, NQ> W, const ChainParams<double, K> Cd,
               const double* __restrict__ targets, int64_t B, const T* __restrict__ surv, int rec,
               int steps1, int steps2, int keep, int G, double pos_tol, double rot_tol,
@@ -129,6 +132,7 @@ k_beam_stage2(const ChainParams<T, K> C, const CostParams<T, NQ> W, const ChainP
   extern __shared__ unsigned char smem_raw[];
   T* hist = reinterpret_cast<T*>(smem_raw);  // [steps2 * bd]
   const int tid = threadIdx.x, bd = blockDim.x;
+  T* Ag = hist + (size_t)(steps2 > 0 ? steps2 : 1) * bd;  // [(Tri + NQ) * bd]
   const int64_t lane = (int64_t)blockIdx.x * bd + tid;
   const int64_t tgt = lane / G;
   const int r = (int)(lane % G);
@@ -141,12 +145,14 @@ k_beam_stage2(const ChainParams<T, K> C, const CostParams<T, NQ> W, const ChainP
   const T* rin = surv + (size_t)(tc * keep + rc) * rec;
 
   LaneState<T, NQ> st;
+  st.Ag = Ag + tid;
+  st.stride = bd;
 #pragma unroll
   for (int i = 0; i < NQ; ++i) st.q[i] = rin[i];
   st.lam = rin[NQ];
   // the carried cost is the stage-1 state cost (LaneState.select, beam.py:60-68);
   // A/g are re-derived at q, as the reference re-derives r and J (beam.py:202)
-  lane_normal<T, NQ, K, ID>(C, W, tg, st.q, st.A, st.g);
+  lane_init<T, NQ, K, ID>(C, W, tg, st);
   st.cost = rin[NQ + 1];
   for (int it = 0; it < steps2; ++it) {
     lm_step<T, NQ, K, ID>(C, W, tg, st);
@@ -238,18 +244,21 @@ k_lane_start(const ChainParams<T, K> C, const CostParams<T, NQ> W, const double*
 }
 
 template <typename T, int NQ, int K, bool ID>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 4)
 k_lane_run(const ChainParams<T, K> C, const CostParams<T, NQ> W, const double* __restrict__ tinv,
            const int32_t* __restrict__ lane_target, int64_t lanes, int steps, double* __restrict__ q_io,
            double* __restrict__ lam_io, double* __restrict__ cost_io, double* __restrict__ hist) {
   const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= lanes) return;
+  extern __shared__ unsigned char smem_raw[];
   const TargetInv<T> tg = load_target_inv<T>(tinv + (int64_t)lane_target[l] * 7);
   LaneState<T, NQ> st;
+  st.Ag = reinterpret_cast<T*>(smem_raw) + threadIdx.x;
+  st.stride = blockDim.x;
 #pragma unroll
   for (int i = 0; i < NQ; ++i) st.q[i] = T(q_io[l * NQ + i]);
   st.lam = T(lam_io[l]);
-  lane_normal<T, NQ, K, ID>(C, W, tg, st.q, st.A, st.g);
+  lane_init<T, NQ, K, ID>(C, W, tg, st);
   st.cost = T(cost_io[l]);
   for (int it = 0; it < steps; ++it) {
     lm_step<T, NQ, K, ID>(C, W, tg, st);
@@ -263,7 +272,7 @@ k_lane_run(const ChainParams<T, K> C, const CostParams<T, NQ> W, const double* _
 
 // Two-pass (reference-structured) stage-1 variant for A/B measurement.
 template <typename T, int NQ, int K, bool ID>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 2)
 k_beam_stage1_twopass(const ChainParams<T, K> C, const CostParams<T, NQ> W,
                       const double* __restrict__ targets, int64_t B, const double* __restrict__ seeds,
                       int S, int P, int steps1, int keep, T* __restrict__ surv, int rec) {
@@ -316,20 +325,33 @@ cudaError_t launch_beam(const ChainParams<T, K>& C, const CostParams<T, NQ>& W,
   const int tpb = L.P >= 256 ? L.P : 256;
   const int per_block = tpb / L.P;
   const int64_t blocks1 = (L.B + per_block - 1) / per_block;
-  const size_t smem1 = sizeof(T) * ((size_t)(L.steps1 + 1) * tpb + tpb);
-  if (L.twopass) {
-    k_beam_stage1_twopass<T, NQ, K, ID><<<(unsigned)blocks1, tpb, smem1, st>>>(
-        C, W, L.targets, L.B, L.seeds, L.S, L.P, L.steps1, L.keep, surv, rec);
-  } else {
-    k_beam_stage1<T, NQ, K, ID><<<(unsigned)blocks1, tpb, smem1, st>>>(
-        C, W, L.targets, L.B, L.seeds, L.S, L.P, L.steps1, L.keep, surv, rec);
+  constexpr int kAg = Tri<NQ>::size + NQ;
+  const size_t smem1 = sizeof(T) * ((size_t)(L.steps1 + 1) * tpb + tpb + (size_t)kAg * tpb);
+  cudaError_t e = cudaSuccess;
+  if (L.stages & 1) {
+    if (L.twopass) {
+      if (smem1 > 48 * 1024)
+        cudaFuncSetAttribute(k_beam_stage1_twopass<T, NQ, K, ID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem1);
+      k_beam_stage1_twopass<T, NQ, K, ID><<<(unsigned)blocks1, tpb, smem1, st>>>(
+          C, W, L.targets, L.B, L.seeds, L.S, L.P, L.steps1, L.keep, surv, rec);
+    } else {
+      if (smem1 > 48 * 1024)
+        cudaFuncSetAttribute(k_beam_stage1<T, NQ, K, ID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem1);
+      k_beam_stage1<T, NQ, K, ID><<<(unsigned)blocks1, tpb, smem1, st>>>(
+          C, W, L.targets, L.B, L.seeds, L.S, L.P, L.steps1, L.keep, surv, rec);
+    }
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
   }
-  cudaError_t e = cudaGetLastError();
-  if (e != cudaSuccess) return e;
+  if (!(L.stages & 2)) return cudaSuccess;
   const int tpb2 = 128;
   const int64_t lanes2 = L.B * L.G;
   const int64_t blocks2 = (lanes2 + tpb2 - 1) / tpb2;
-  const size_t smem2 = sizeof(T) * (size_t)(L.steps2 > 0 ? L.steps2 : 1) * tpb2;
+  const size_t smem2 = sizeof(T) * ((size_t)(L.steps2 > 0 ? L.steps2 : 1) * tpb2 + (size_t)kAg * tpb2);
+  if (smem2 > 48 * 1024)
+    cudaFuncSetAttribute(k_beam_stage2<T, NQ, K, ID>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
   k_beam_stage2<T, NQ, K, ID><<<(unsigned)blocks2, tpb2, smem2, st>>>(
       C, W, Cd, L.targets, L.B, surv, rec, L.steps1, L.steps2, L.keep, L.G, L.pos_tol, L.rot_tol,
       L.q_out, L.cost_out, L.hist_out, L.pos_err, L.rot_err, L.success);
@@ -352,7 +374,7 @@ cudaError_t launch_lane(const ChainParams<T, K>& C, const CostParams<T, NQ>& W, 
                                                          L.lam, L.cost);
       break;
     case LaneOp::kRun:
-      k_lane_run<T, NQ, K, ID><<<blocks, tpb, 0, st>>>(C, W, L.tinv, L.lane_target, L.lanes, L.steps,
+      k_lane_run<T, NQ, K, ID><<<blocks, tpb, sizeof(T) * (Tri<NQ>::size + NQ) * tpb, st>>>(C, W, L.tinv, L.lane_target, L.lanes, L.steps,
                                                        L.q_io, L.lam, L.cost, L.hist);
       break;
   }

@@ -34,6 +34,7 @@ struct BeamLaunch {
   double *q_out, *cost_out, *hist_out, *pos_err, *rot_err;
   uint8_t* success;
   bool twopass;
+  int stages;  // bit 0: stage 1 (seeds + prune), bit 1: stage 2 (survivors + winner)
 };
 
 enum class LaneOp { kResJac, kStart, kRun };

@@ -69,53 +69,66 @@ __device__ __forceinline__ T pick(const T (&q)[NQ], int idx) {
 // Pose residual (6 weighted rows) and, if JAC, its weighted Jacobian rows.
 // ID: the chain's moving joints are exactly the actuated joints in order with
 // unit multipliers (qcol[k] == k), so columns need no scatter.
+//
+// Backward pass (kop_chain.h): S = child_k -> EE starts at the EE offset and
+// is pre-multiplied by M_k = Rz(theta_k) (or Tz) and the joint frame O_k for
+// k = K-1 .. 0, ending at the world EE pose.  Before composing joint k, S is
+// child_k -> EE, where joint k's axis is +z through the origin, so its body
+// (EE-frame) Jacobian column is  ang = R_S^T z = row 2 of R_S,
+// lin = R_S^T (z x p_S) = -p_y row0 + p_x row1  -- the same columns as
+// beam.py:142-146 (R^T J_geom) without any per-joint world state.
 // ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ quat<T> zmul_left(T c, T s, const quat<T>& b) {  // (c,0,0,s) * b
+  return {c * b.w - s * b.z, c * b.x - s * b.y, c * b.y + s * b.x, c * b.z + s * b.w};
+}
+
 template <typename T, int NQ, int K, bool ID, bool JAC>
 __device__ __forceinline__ void pose_rows(const ChainParams<T, K>& C, const CostParams<T, NQ>& W,
                                           const TargetInv<T>& tg, const T (&q)[NQ], T (&r)[6],
                                           T (&J)[6][NQ]) {
-  quat<T> pq{T(1), T(0), T(0), T(0)};
-  vec3<T> pp{T(0), T(0), T(0)};
-  vec3<T> anc[K], ax[K];
+  quat<T> sq{C.eq[0], C.eq[1], C.eq[2], C.eq[3]};
+  vec3<T> sp{C.ep[0], C.ep[1], C.ep[2]};
+  T col[K][6];
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
+  for (int k = K - 1; k >= 0; --k) {
     if (ID || k < C.k) {
-      const quat<T> tq{C.tq[k][0], C.tq[k][1], C.tq[k][2], C.tq[k][3]};
-      const vec3<T> tp{C.tp[k][0], C.tp[k][1], C.tp[k][2]};
-      quat<T> fq;
-      vec3<T> fp;
-      if (k == 0) {  // the root frame is the identity (robot.py:418-419)
-        fq = tq;
-        fp = tp;
-      } else {
-        fq = qmul(pq, tq);
-        const vec3<T> o = qrot(pq, tp);
-        fp = {pp.x + o.x, pp.y + o.y, pp.z + o.z};
-      }
-      const vec3<T> z = qzaxis(fq);
+      const bool pri = !ID && C.prismatic[k];
       if (JAC) {
-        anc[k] = fp;
-        ax[k] = z;
+        const T x2 = sq.x + sq.x, y2 = sq.y + sq.y, z2 = sq.z + sq.z;
+        // rows of R(sq)
+        const T r20 = sq.x * z2 - sq.w * y2, r21 = sq.y * z2 + sq.w * x2, r22 = T(1) - (sq.x * x2 + sq.y * y2);
+        if (pri) {
+          col[k][0] = r20; col[k][1] = r21; col[k][2] = r22;
+          col[k][3] = T(0); col[k][4] = T(0); col[k][5] = T(0);
+        } else {
+          const T r00 = T(1) - (sq.y * y2 + sq.z * z2), r01 = sq.x * y2 - sq.w * z2, r02 = sq.x * z2 + sq.w * y2;
+          const T r10 = sq.x * y2 + sq.w * z2, r11 = T(1) - (sq.x * x2 + sq.z * z2), r12 = sq.y * z2 - sq.w * x2;
+          col[k][0] = sp.x * r10 - sp.y * r00;
+          col[k][1] = sp.x * r11 - sp.y * r01;
+          col[k][2] = sp.x * r12 - sp.y * r02;
+          col[k][3] = r20; col[k][4] = r21; col[k][5] = r22;
+        }
       }
       const T th = ID ? q[k] : pick(q, C.qcol[k]) * C.mult[k] + C.offset[k];
-      if (C.prismatic[k]) {
-        pq = fq;
-        pp = {fp.x + th * z.x, fp.y + th * z.y, fp.z + th * z.z};
+      if (pri) {
+        sp.z += th;
       } else {
         T s, c;
         sincos_t(T(0.5) * th, &s, &c);
-        pq = qmul_z(fq, c, s);
-        pp = fp;
+        sq = zmul_left(c, s, sq);
+        const T c2 = c * c - s * s, s2 = T(2) * c * s;
+        sp = {c2 * sp.x - s2 * sp.y, s2 * sp.x + c2 * sp.y, sp.z};
       }
+      sq = qmul(quat<T>{C.tq[k][0], C.tq[k][1], C.tq[k][2], C.tq[k][3]}, sq);
+      sp = {C.tp[k][0] + (C.tr[k][0][0] * sp.x + C.tr[k][0][1] * sp.y + C.tr[k][0][2] * sp.z),
+            C.tp[k][1] + (C.tr[k][1][0] * sp.x + C.tr[k][1][1] * sp.y + C.tr[k][1][2] * sp.z),
+            C.tp[k][2] + (C.tr[k][2][0] * sp.x + C.tr[k][2][1] * sp.y + C.tr[k][2][2] * sp.z)};
     }
   }
-  // end-effector frame
-  const quat<T> eq = qmul(pq, quat<T>{C.eq[0], C.eq[1], C.eq[2], C.eq[3]});
-  const vec3<T> eo = qrot(pq, vec3<T>{C.ep[0], C.ep[1], C.ep[2]});
-  const vec3<T> ep{pp.x + eo.x, pp.y + eo.y, pp.z + eo.z};
-  // pose error T_t^-1 * FK  (beam.py:119-121)
-  const quat<T> e_q = qmul(tg.q, eq);
-  const vec3<T> et = qrot(tg.q, ep);
+  // pose error T_t^-1 * FK  (beam.py:119-121); sq, sp = world EE pose
+  const quat<T> e_q = qmul(tg.q, sq);
+  const vec3<T> et = qrot(tg.q, sp);
   const vec3<T> e_t{tg.t.x + et.x, tg.t.y + et.y, tg.t.z + et.z};
   const Twist<T> xi = se3_log(e_q, e_t);
   r[0] = W.w_pos * xi.v.x;
@@ -126,23 +139,17 @@ __device__ __forceinline__ void pose_rows(const ChainParams<T, K>& C, const Cost
   r[5] = W.w_ori * xi.phi.z;
   if (!JAC) return;
 
-  // J_pose = diag(w) Jr^-1(xi) [R^T J_lin; R^T J_ang]   (beam.py:142-156)
-  JrInv<T> jr = se3_jr_inv(xi);
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      jr.B.m[i][j] *= W.w_pos;
-    }
-  mat3<T> At, Ab;
+  // J_pose = diag(w) Jr^-1(xi) [lin; ang]   (beam.py:142-156)
+  const JrInv<T> jr = se3_jr_inv(xi);
+  mat3<T> At, Bt, Ab;
 #pragma unroll
   for (int i = 0; i < 3; ++i)
 #pragma unroll
     for (int j = 0; j < 3; ++j) {
       At.m[i][j] = W.w_pos * jr.A.m[i][j];
+      Bt.m[i][j] = W.w_pos * jr.B.m[i][j];
       Ab.m[i][j] = W.w_ori * jr.A.m[i][j];
     }
-  const mat3<T> R = qmat(eq);
   if (!ID) {
 #pragma unroll
     for (int m = 0; m < 6; ++m)
@@ -152,21 +159,12 @@ __device__ __forceinline__ void pose_rows(const ChainParams<T, K>& C, const Cost
 #pragma unroll
   for (int k = 0; k < K; ++k) {
     if (ID || k < C.k) {
-      const vec3<T> ab = mulT(R, ax[k]);
-      vec3<T> lin, ang;
-      if (C.prismatic[k]) {
-        lin = ab;
-        ang = {T(0), T(0), T(0)};
-      } else {
-        const vec3<T> db = mulT(R, vec3<T>{ep.x - anc[k].x, ep.y - anc[k].y, ep.z - anc[k].z});
-        lin = cross(ab, db);
-        ang = ab;
-      }
-      const vec3<T> t1 = mul(At, lin), t2 = mul(jr.B, ang), b1 = mul(Ab, ang);
-      const T col[6] = {t1.x + t2.x, t1.y + t2.y, t1.z + t2.z, b1.x, b1.y, b1.z};
+      const vec3<T> lin{col[k][0], col[k][1], col[k][2]}, ang{col[k][3], col[k][4], col[k][5]};
+      const vec3<T> t1 = mul(At, lin), t2 = mul(Bt, ang), b1 = mul(Ab, ang);
+      const T cj[6] = {t1.x + t2.x, t1.y + t2.y, t1.z + t2.z, b1.x, b1.y, b1.z};
       if (ID) {
 #pragma unroll
-        for (int m = 0; m < 6; ++m) J[m][k] = col[m];
+        for (int m = 0; m < 6; ++m) J[m][k] = cj[m];
       } else {
         const int qc = C.qcol[k];
         const T mu = C.mult[k];
@@ -174,7 +172,7 @@ __device__ __forceinline__ void pose_rows(const ChainParams<T, K>& C, const Cost
         for (int c = 0; c < NQ; ++c)
           if (qc == c) {
 #pragma unroll
-            for (int m = 0; m < 6; ++m) J[m][c] += mu * col[m];
+            for (int m = 0; m < 6; ++m) J[m][c] += mu * cj[m];
           }
       }
     }
@@ -296,18 +294,47 @@ __device__ __forceinline__ bool damped_solve(const T (&A)[Tri<NQ>::size], const 
   return ok;
 }
 
-// Per-lane LM state.  A/g are the normal equations AT q (fused mode keeps
-// them from the accepted candidate's evaluation instead of recomputing FK).
+// Per-lane LM state.  The normal equations AT q (packed lower A, then g)
+// live in shared memory, element e of this lane at Ag[e * stride]: the fused
+// step keeps them from the accepted candidate's evaluation instead of
+// recomputing FK, and holding them outside the register file keeps the lane
+// at <= 128 registers (2 CTAs of 256 threads per SM).
 template <typename T, int NQ>
 struct LaneState {
   T q[NQ];
-  T A[Tri<NQ>::size];
-  T g[NQ];
   T lam, cost;
+  T* Ag;
+  int stride;
 };
+
+template <typename T, int NQ>
+__device__ __forceinline__ void store_normal(const LaneState<T, NQ>& s, const T (&A)[Tri<NQ>::size],
+                                             const T (&g)[NQ]) {
+#pragma unroll
+  for (int i = 0; i < Tri<NQ>::size; ++i) s.Ag[i * s.stride] = A[i];
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) s.Ag[(Tri<NQ>::size + i) * s.stride] = g[i];
+}
+
+template <typename T, int NQ>
+__device__ __forceinline__ void load_normal(const LaneState<T, NQ>& s, T (&A)[Tri<NQ>::size], T (&g)[NQ]) {
+#pragma unroll
+  for (int i = 0; i < Tri<NQ>::size; ++i) A[i] = s.Ag[i * s.stride];
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) g[i] = s.Ag[(Tri<NQ>::size + i) * s.stride];
+}
 
 template <typename T>
 __device__ __forceinline__ T inf_t() { return T(INFINITY); }
+
+// Start a lane at q: cost and normal equations (beam.py:182-196 + :202-204).
+template <typename T, int NQ, int K, bool ID>
+__device__ __forceinline__ void lane_init(const ChainParams<T, K>& C, const CostParams<T, NQ>& W,
+                                          const TargetInv<T>& tg, LaneState<T, NQ>& s) {
+  T A[Tri<NQ>::size], g[NQ];
+  s.cost = lane_normal<T, NQ, K, ID>(C, W, tg, s.q, A, g);
+  store_normal(s, A, g);
+}
 
 // One LM proposal (beam.py:201-239), fused form: the candidate's evaluation
 // also produces its normal equations, so an accepted step needs no second FK
@@ -317,7 +344,12 @@ template <typename T, int NQ, int K, bool ID>
 __device__ __forceinline__ void lm_step(const ChainParams<T, K>& C, const CostParams<T, NQ>& W,
                                         const TargetInv<T>& tg, LaneState<T, NQ>& s) {
   T d[NQ];
-  const bool ok = damped_solve<T, NQ>(s.A, s.g, s.lam, d);
+  bool ok;
+  {
+    T A[Tri<NQ>::size], g[NQ];
+    load_normal(s, A, g);
+    ok = damped_solve<T, NQ>(A, g, s.lam, d);
+  }
   T qn[NQ];
 #pragma unroll
   for (int i = 0; i < NQ; ++i) qn[i] = s.q[i] + (ok ? d[i] : T(0));
@@ -328,10 +360,7 @@ __device__ __forceinline__ void lm_step(const ChainParams<T, K>& C, const CostPa
   if (acc) {
 #pragma unroll
     for (int i = 0; i < NQ; ++i) s.q[i] = qn[i];
-#pragma unroll
-    for (int i = 0; i < Tri<NQ>::size; ++i) s.A[i] = An[i];
-#pragma unroll
-    for (int i = 0; i < NQ; ++i) s.g[i] = gn[i];
+    store_normal(s, An, gn);
     s.cost = cn;
     s.lam = tmax(s.lam * T(BeamConsts::damping_down), T(BeamConsts::damping_min));
   } else {

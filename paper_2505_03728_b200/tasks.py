@@ -173,16 +173,20 @@ class IkBeamSolver:
         return BeamBatch(dv.empty((batch, n)), dv.empty(batch), dv.empty((batch, self.total_steps + 1)),
                          dv.empty(batch), dv.empty(batch), t.empty(batch, dtype=t.uint8, device="cuda"))
 
-    def solve_device(self, targets, out: BeamBatch | None = None, history: bool = True) -> BeamBatch:
-        """targets: device (B,7) float64 tensor.  Enqueues the solve; returns device outputs."""
+    def solve_device(self, targets, out: BeamBatch | None = None, history: bool = True,
+                     stages: int = 3) -> BeamBatch:
+        """targets: device (B,7) float64 tensor.  Enqueues the solve on the current
+        stream and returns the device outputs.  ``stages`` 1 / 2 issue only the
+        seed+prune or the survivor+winner kernel (for per-kernel timing)."""
         targets = dv.to_dev(targets)
         b = targets.shape[0]
         out = out or self.alloc_outputs(b)
         ws = self.workspace(b)
-        check(lib().kop_ik_beam(self.model._handle, self.link_idx, C.byref(self.params), dv.ptr(targets), b,
-                                dv.ptr(self.seeds), dv.ptr(ws), ws.numel(), dv.ptr(out.q), dv.ptr(out.cost),
-                                dv.ptr(out.history) if history else None, dv.ptr(out.pos_error),
-                                dv.ptr(out.rot_error), dv.ptr(out.success), dv.stream_handle()), "kop_ik_beam")
+        check(lib().kop_ik_beam_stage(self.model._handle, self.link_idx, C.byref(self.params), int(stages),
+                                      dv.ptr(targets), b, dv.ptr(self.seeds), dv.ptr(ws), ws.numel(),
+                                      dv.ptr(out.q), dv.ptr(out.cost), dv.ptr(out.history) if history else None,
+                                      dv.ptr(out.pos_error), dv.ptr(out.rot_error), dv.ptr(out.success),
+                                      dv.stream_handle()), "kop_ik_beam")
         return out
 
     def solve(self, targets) -> BeamBatch:
