@@ -48,12 +48,10 @@ k_beam_stage1(const ChainParams<T, K> C, const CostParams<T, NQ> W, const double
   const double* sd = seeds + (size_t)(s < S ? s : 0) * NQ;
 #pragma unroll
   for (int i = 0; i < NQ; ++i) st.q[i] = T(sd[i]);
-  lane_init<T, NQ, K, ID>(C, W, tg, st);
   st.lam = T(BeamConsts::damping_init);
-  hist[tid] = st.cost;
-  for (int it = 0; it < steps1; ++it) {
-    lm_step<T, NQ, K, ID>(C, W, tg, st);
-    hist[(size_t)(it + 1) * bd + tid] = st.cost;
+  for (int it = 0; it <= steps1; ++it) {  // it == 0: start_state
+    lm_iter<T, NQ, K, ID>(C, W, tg, st, it == 0 ? 1 : 0);
+    hist[(size_t)it * bd + tid] = st.cost;
   }
   costs[tid] = active ? st.cost : T(NAN);
   __syncthreads();
@@ -152,11 +150,10 @@ k_beam_stage2(const ChainParams<T, K> C, const CostParams<T, NQ> W, const ChainP
   st.lam = rin[NQ];
   // the carried cost is the stage-1 state cost (LaneState.select, beam.py:60-68);
   // A/g are re-derived at q, as the reference re-derives r and J (beam.py:202)
-  lane_init<T, NQ, K, ID>(C, W, tg, st);
   st.cost = rin[NQ + 1];
-  for (int it = 0; it < steps2; ++it) {
-    lm_step<T, NQ, K, ID>(C, W, tg, st);
-    hist[(size_t)it * bd + tid] = st.cost;
+  for (int it = -1; it < steps2; ++it) {  // it == -1: re-derive A, g at the survivor's q
+    lm_iter<T, NQ, K, ID>(C, W, tg, st, it < 0 ? 2 : 0);
+    if (it >= 0) hist[(size_t)it * bd + tid] = st.cost;
   }
   // winner = argmin over the keep survivors, ties -> lower stage-1 rank (tasks.py:139)
   T best = active ? st.cost : T(NAN);
@@ -258,11 +255,10 @@ k_lane_run(const ChainParams<T, K> C, const CostParams<T, NQ> W, const double* _
 #pragma unroll
   for (int i = 0; i < NQ; ++i) st.q[i] = T(q_io[l * NQ + i]);
   st.lam = T(lam_io[l]);
-  lane_init<T, NQ, K, ID>(C, W, tg, st);
   st.cost = T(cost_io[l]);
-  for (int it = 0; it < steps; ++it) {
-    lm_step<T, NQ, K, ID>(C, W, tg, st);
-    if (hist) hist[l * steps + it] = double(st.cost);
+  for (int it = -1; it < steps; ++it) {
+    lm_iter<T, NQ, K, ID>(C, W, tg, st, it < 0 ? 2 : 0);
+    if (hist && it >= 0) hist[l * steps + it] = double(st.cost);
   }
 #pragma unroll
   for (int i = 0; i < NQ; ++i) q_io[l * NQ + i] = double(st.q[i]);

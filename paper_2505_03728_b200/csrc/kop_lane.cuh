@@ -327,37 +327,43 @@ __device__ __forceinline__ void load_normal(const LaneState<T, NQ>& s, T (&A)[Tr
 template <typename T>
 __device__ __forceinline__ T inf_t() { return T(INFINITY); }
 
-// Start a lane at q: cost and normal equations (beam.py:182-196 + :202-204).
+// One LM iteration of a lane, or its start (beam.py:182-196) when mode != 0.
+//   mode 0  one proposal (beam.py:201-239), fused form: the candidate's
+//           evaluation also produces its normal equations, so an accepted step
+//           needs no second FK at the start of the next step.  Same accept /
+//           reject semantics: accept iff finite and cost' < cost; lam /3
+//           (>= 1e-12) or x10 (<= 1e10).
+//   mode 1  start at q: cost and normal equations from one evaluation.
+//   mode 2  restart at q keeping the carried cost (survivors after the prune:
+//           LaneState.select keeps cost, beam.py:60-68, while r and J are
+//           re-derived at q, beam.py:202).
+// A single inlined evaluation serves all three (one copy of the ~2K-instruction
+// body per kernel keeps the hot loop inside the instruction cache).
 template <typename T, int NQ, int K, bool ID>
-__device__ __forceinline__ void lane_init(const ChainParams<T, K>& C, const CostParams<T, NQ>& W,
-                                          const TargetInv<T>& tg, LaneState<T, NQ>& s) {
-  T A[Tri<NQ>::size], g[NQ];
-  s.cost = lane_normal<T, NQ, K, ID>(C, W, tg, s.q, A, g);
-  store_normal(s, A, g);
-}
-
-// One LM proposal (beam.py:201-239), fused form: the candidate's evaluation
-// also produces its normal equations, so an accepted step needs no second FK
-// at the start of the next step.  Identical accept/reject semantics:
-// accept iff finite and cost' < cost; lam /3 (>= 1e-12) or x10 (<= 1e10).
-template <typename T, int NQ, int K, bool ID>
-__device__ __forceinline__ void lm_step(const ChainParams<T, K>& C, const CostParams<T, NQ>& W,
-                                        const TargetInv<T>& tg, LaneState<T, NQ>& s) {
+__device__ __forceinline__ void lm_iter(const ChainParams<T, K>& C, const CostParams<T, NQ>& W,
+                                        const TargetInv<T>& tg, LaneState<T, NQ>& s, int mode) {
   T d[NQ];
-  bool ok;
-  {
+  bool ok = true;
+  if (mode == 0) {
     T A[Tri<NQ>::size], g[NQ];
     load_normal(s, A, g);
     ok = damped_solve<T, NQ>(A, g, s.lam, d);
+  } else {
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) d[i] = T(0);
   }
   T qn[NQ];
 #pragma unroll
   for (int i = 0; i < NQ; ++i) qn[i] = s.q[i] + (ok ? d[i] : T(0));
   T An[Tri<NQ>::size], gn[NQ];
-  T cn = lane_normal<T, NQ, K, ID>(C, W, tg, qn, An, gn);
-  if (!finite_t(cn)) cn = inf_t<T>();
-  const bool acc = ok && (cn < s.cost);
-  if (acc) {
+  const T raw = lane_normal<T, NQ, K, ID>(C, W, tg, qn, An, gn);
+  if (mode != 0) {
+    store_normal(s, An, gn);
+    if (mode == 1) s.cost = raw;  // start_state keeps a non-finite cost as is
+    return;
+  }
+  const T cn = finite_t(raw) ? raw : inf_t<T>();
+  if (ok && (cn < s.cost)) {
 #pragma unroll
     for (int i = 0; i < NQ; ++i) s.q[i] = qn[i];
     store_normal(s, An, gn);

@@ -6,11 +6,11 @@
 //
 // FP32 hazard: the reference's closed forms for the SO(3)/SE(3)
 // Jacobian coefficients (liegroups.py:176-191, :210-235) cancel
-// catastrophically in float well above its 1e-7 series threshold.  Here every
-// coefficient switches to its Taylor series (exact rational coefficients,
+// catastrophically in float well above its 1e-7 series threshold.  In float
+// every coefficient is a Taylor polynomial (exact rational coefficients,
 // derived independently of the reference's -- whose c2/c3 series carry a sign
-// slip) below kSeriesBelow<T>, which keeps float relative error at
-// ~1e-7 across [0, pi].
+// slip) over the whole [0, pi], relative error <= 1.4e-7; double
+// uses the series below 0.03 rad and the closed forms above.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -40,6 +40,9 @@ __device__ __forceinline__ double atan2_t(double y, double x) { return atan2(y, 
 __device__ __forceinline__ float tan_t(float a) { return tanf(a); }
 __device__ __forceinline__ double tan_t(double a) { return tan(a); }
 __device__ __forceinline__ bool finite_t(float a) { return isfinite(a); }
+// float: MUFU.RCP-based quotient (<= 2 ulp); double: IEEE division
+__device__ __forceinline__ float div_t(float a, float b) { return __fdividef(a, b); }
+__device__ __forceinline__ double div_t(double a, double b) { return a / b; }
 __device__ __forceinline__ bool finite_t(double a) { return isfinite(a); }
 
 template <typename T>
@@ -47,9 +50,7 @@ __device__ __forceinline__ T tmax(T a, T b) { return a > b ? a : b; }
 template <typename T>
 __device__ __forceinline__ T tmin(T a, T b) { return a < b ? a : b; }
 
-// Below this angle the Jacobian coefficients use their Taylor series.  In
-// float the closed forms lose ~180*eps/theta^4 relative accuracy (k3), so
-// the series (6 terms, truncation < 1e-9 at theta = 1) covers [0, 1).
+// Series thresholds (double Jacobian coefficients; so(3) log in both types).
 template <typename T>
 struct LieConst;
 template <>
@@ -150,7 +151,7 @@ __device__ __forceinline__ vec3<T> qlog(quat<T> q) {
   if (s < LieConst<T>::log_series_below) {
     scale = T(2) / tmax(q.w, T(0.5)) * (T(1) - s * s / T(3));
   } else {
-    scale = T(2) * atan2_t(s, q.w) / s;
+    scale = div_t(T(2) * atan2_t(s, q.w), s);
   }
   return {scale * q.x, scale * q.y, scale * q.z};
 }
@@ -163,28 +164,52 @@ struct JacCoef {
   T c1, k2, k3, b;
 };
 
-template <typename T>
-__device__ __forceinline__ JacCoef<T> jac_coefs(T th) {
-  const T t = th * th;
-  JacCoef<T> k;
-  if (th < LieConst<T>::series_below) {
-    k.c1 = T(1.0 / 6.0) + t * (T(-1.0 / 120.0) + t * (T(1.0 / 5040.0) + t * (T(-1.0 / 362880.0) +
-           t * (T(1.0 / 39916800.0) + t * T(-1.0 / 6227020800.0)))));
-    k.k2 = T(1.0 / 24.0) + t * (T(-1.0 / 720.0) + t * (T(1.0 / 40320.0) + t * (T(-1.0 / 3628800.0) +
-           t * (T(1.0 / 479001600.0) + t * T(-1.0 / 87178291200.0)))));
-    k.k3 = T(1.0 / 120.0) + t * (T(-1.0 / 2520.0) + t * (T(1.0 / 120960.0) + t * (T(-1.0 / 9979200.0) +
-           t * (T(1.0 / 1245404160.0) + t * T(-1.0 / 217945728000.0)))));
-    k.b = T(1.0 / 12.0) + t * (T(1.0 / 720.0) + t * (T(1.0 / 30240.0) + t * (T(1.0 / 1209600.0) +
-          t * (T(1.0 / 47900160.0) + t * T(691.0 / 1307674368000.0)))));
+// float: one branch-free Horner polynomial per coefficient in t = theta^2,
+// valid on the whole range theta in [0, pi] that qlog produces (truncation
+// < 1.4e-7 relative at theta = pi, checked against 40-digit arithmetic);
+// no divisions, no sin/cos, and no warp divergence between small- and
+// large-angle lanes.  b has radius of convergence 2 pi, hence 13 terms.
+__device__ __forceinline__ JacCoef<float> jac_coefs_t(float t) {
+  JacCoef<float> k;
+  k.c1 = 0.16666666666666666f + t * (-0.0083333333333333332f + t * (0.00019841269841269841f +
+         t * (-2.7557319223985893e-06f + t * (2.505210838544172e-08f + t * (-1.6059043836821613e-10f +
+         t * (7.6471637318198164e-13f + t * (-2.8114572543455206e-15f + t * 8.2206352466243295e-18f)))))));
+  k.k2 = 0.041666666666666664f + t * (-0.0013888888888888889f + t * (2.4801587301587302e-05f +
+         t * (-2.7557319223985888e-07f + t * (2.08767569878681e-09f + t * (-1.1470745597729725e-11f +
+         t * (4.7794773323873853e-14f + t * (-1.5619206968586225e-16f + t * 4.1103176233121648e-19f)))))));
+  k.k3 = 0.0083333333333333332f + t * (-0.00039682539682539683f + t * (8.2671957671957678e-06f +
+         t * (-1.0020843354176688e-07f + t * (8.0295219184108074e-10f + t * (-4.5882982390918896e-12f +
+         t * (1.9680200780418645e-14f + t * (-6.5765081972994636e-17f + t * 1.7615646957052136e-19f)))))));
+  k.b = 0.083333333333333329f + t * (0.0013888888888888889f + t * (3.3068783068783071e-05f +
+        t * (8.2671957671957675e-07f + t * (2.08767569878681e-08f + t * (5.2841901386874932e-10f +
+        t * (1.3382536530684679e-11f + t * (3.3896802963225827e-13f + t * (8.5860620562778452e-15f +
+        t * (2.1748686985580619e-16f + t * (5.5090028283602295e-18f + t * (1.3954464685812522e-19f +
+        t * 3.5347070396294673e-21f)))))))))));
+  return k;
+}
+
+// double: 6-term series below 0.03 rad (truncation < 1e-20), closed forms above.
+__device__ __forceinline__ JacCoef<double> jac_coefs_t(double t) {
+  const double th = sqrt(t);
+  JacCoef<double> k;
+  if (th < LieConst<double>::series_below) {
+    k.c1 = 1.0 / 6.0 + t * (-1.0 / 120.0 + t * (1.0 / 5040.0 + t * (-1.0 / 362880.0 +
+           t * (1.0 / 39916800.0 + t * (-1.0 / 6227020800.0)))));
+    k.k2 = 1.0 / 24.0 + t * (-1.0 / 720.0 + t * (1.0 / 40320.0 + t * (-1.0 / 3628800.0 +
+           t * (1.0 / 479001600.0 + t * (-1.0 / 87178291200.0)))));
+    k.k3 = 1.0 / 120.0 + t * (-1.0 / 2520.0 + t * (1.0 / 120960.0 + t * (-1.0 / 9979200.0 +
+           t * (1.0 / 1245404160.0 + t * (-1.0 / 217945728000.0)))));
+    k.b = 1.0 / 12.0 + t * (1.0 / 720.0 + t * (1.0 / 30240.0 + t * (1.0 / 1209600.0 +
+          t * (1.0 / 47900160.0 + t * (691.0 / 1307674368000.0)))));
   } else {
-    T sn, cs;
-    sincos_t(th, &sn, &cs);
-    const T t2 = t * t;
+    double sn, cs;
+    sincos(th, &sn, &cs);
+    const double t2 = t * t;
     k.c1 = (th - sn) / (t * th);
-    k.k2 = (T(0.5) * t + cs - T(1)) / t2;
-    k.k3 = (T(2) * th - T(3) * sn + th * cs) / (T(2) * t2 * th);
-    const T h = T(0.5) * th;
-    k.b = (T(1) - h / tan_t(h)) / t;
+    k.k2 = (0.5 * t + cs - 1.0) / t2;
+    k.k3 = (2.0 * th - 3.0 * sn + th * cs) / (2.0 * t2 * th);
+    const double h = 0.5 * th;
+    k.b = (1.0 - h / tan(h)) / t;
   }
   return k;
 }
@@ -194,7 +219,7 @@ __device__ __forceinline__ JacCoef<T> jac_coefs(T th) {
 template <typename T>
 struct Twist {
   vec3<T> v, phi;
-  T theta;
+  T theta2;  // |phi|^2
   JacCoef<T> k;
 };
 
@@ -202,8 +227,8 @@ template <typename T>
 __device__ __forceinline__ Twist<T> se3_log(const quat<T>& q, const vec3<T>& t) {
   Twist<T> xi;
   xi.phi = qlog(q);
-  xi.theta = sqrt_t(dot(xi.phi, xi.phi));
-  xi.k = jac_coefs(xi.theta);
+  xi.theta2 = dot(xi.phi, xi.phi);
+  xi.k = jac_coefs_t(xi.theta2);
   const vec3<T> a = cross(xi.phi, t);
   const vec3<T> b2 = cross(xi.phi, a);
   xi.v = {t.x - T(0.5) * a.x + xi.k.b * b2.x, t.y - T(0.5) * a.y + xi.k.b * b2.y,
@@ -227,7 +252,7 @@ template <typename T>
 __device__ __forceinline__ JrInv<T> se3_jr_inv(const Twist<T>& xi) {
   const vec3<T> rho{-xi.v.x, -xi.v.y, -xi.v.z};
   const vec3<T> ph{-xi.phi.x, -xi.phi.y, -xi.phi.z};
-  const T t = xi.theta * xi.theta;
+  const T t = xi.theta2;
   const T b = xi.k.b, c1 = xi.k.c1, k2 = xi.k.k2, k3 = xi.k.k3;
   const T d = dot(ph, rho);
   JrInv<T> J;
