@@ -86,6 +86,13 @@ int kop_model_create(const KopModelDesc* desc, KopModel** out);
 void kop_model_destroy(KopModel* model);
 /* Moving joints on the root->link chain (fixed joints folded); -1 on error. */
 int kop_model_chain_length(const KopModel* model, int32_t link);
+/* The compiled root->link chain the IK kernels evaluate (kop_chain.h): per
+ * moving joint k < K (K = return value, <= 8) the joint frame relative to the
+ * previous moving child frame with its axis rotated onto +z: tq [K*4],
+ * tp [K*3]; qcol/mult/offset/prismatic [K]; ee [7] the link offset after the
+ * last moving joint.  Host arrays, any may be NULL.  For tests and tooling. */
+int kop_model_chain_export(const KopModel* model, int32_t link, double* tq, double* tp, int32_t* qcol,
+                           double* mult, double* offset, int32_t* prismatic, double* ee);
 const char* kop_last_error(void);
 const char* kop_build_info(void);
 

@@ -42,6 +42,7 @@ SIGNATURES = {
     "kop_model_create": (C.c_int, [C.POINTER(KopModelDesc), C.POINTER(_p)]),
     "kop_model_destroy": (None, [_p]),
     "kop_model_chain_length": (C.c_int, [_p, _i32]),
+    "kop_model_chain_export": (C.c_int, [_p, _i32, _p, _p, _p, _p, _p, _p, _p]),
     "kop_last_error": (C.c_char_p, []),
     "kop_build_info": (C.c_char_p, []),
     "kop_fk": (C.c_int, [_p, _i32, _p, _i64, _p, _p, _p, _p, _p]),

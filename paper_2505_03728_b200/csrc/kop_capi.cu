@@ -253,6 +253,28 @@ int kop_model_chain_length(const KopModel* m, int32_t link) {
   return k;
 }
 
+int kop_model_chain_export(const KopModel* m, int32_t link, double* tq, double* tp, int32_t* qcol, double* mult,
+                           double* offset, int32_t* prismatic, double* ee) {
+  if (!m) return fail(KOP_EINVAL, "null model");
+  ChainParams<double, kChainMax> C;
+  bool id;
+  const int k = compile_chain(*m, link, C, id);
+  if (k < 0) return k;
+  for (int i = 0; i < k; ++i) {
+    if (tq) memcpy(tq + 4 * i, C.tq[i], sizeof(C.tq[i]));
+    if (tp) memcpy(tp + 3 * i, C.tp[i], sizeof(C.tp[i]));
+    if (qcol) qcol[i] = C.qcol[i];
+    if (mult) mult[i] = C.mult[i];
+    if (offset) offset[i] = C.offset[i];
+    if (prismatic) prismatic[i] = C.prismatic[i];
+  }
+  if (ee) {
+    memcpy(ee, C.eq, sizeof(C.eq));
+    memcpy(ee + 4, C.ep, sizeof(C.ep));
+  }
+  return k;
+}
+
 int kop_fk(const KopModel* m, int32_t precision, const double* q, int64_t batch, double* lq, double* lp,
            double* jp, double* ja, void* stream) {
   if (!m || batch < 0 || (batch > 0 && !q)) return fail(KOP_EINVAL, "invalid FK arguments");
