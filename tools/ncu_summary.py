@@ -16,20 +16,23 @@ RAW = ["dram__bytes_read.sum", "dram__bytes_write.sum", "sm__inst_executed_pipe_
        "launch__registers_per_thread", "sm__warps_active.avg.pct_of_peak_sustained_active"]
 
 
-def run(rep):
+def run(rep, index=0):
     det = subprocess.run(["ncu", "-i", rep, "--page", "details", "--csv"], capture_output=True, text=True).stdout
     out = {}
     rows = list(csv.reader(io.StringIO(det)))
     ci = rows[0].index("Metric Name")
+    ids = sorted({r[0] for r in rows[1:]}, key=int)
+    kid = ids[index]
     for row in rows[1:]:
-        if len(row) <= ci + 2:
+        if len(row) <= ci + 2 or row[0] != kid:
             continue
+        out.setdefault("kernel", row[rows[0].index("Kernel Name")].split("(")[0])
         name, unit, val = row[ci], row[ci + 1], row[ci + 2]
         if name in KEYS and name not in out:
             out[name] = f"{val} {unit}".strip()
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    hdr, units, vals = rows[0], rows[1], rows[2]
+    hdr, units, vals = rows[0], rows[1], rows[2 + index]
     stalls = {}
     for h, u, v in zip(hdr, units, vals):
         if h in RAW:
@@ -45,4 +48,4 @@ def run(rep):
 
 
 if __name__ == "__main__":
-    print(json.dumps(run(sys.argv[1]), indent=1))
+    print(json.dumps(run(sys.argv[1], int(sys.argv[2]) if len(sys.argv) > 2 else 0), indent=1))
