@@ -30,17 +30,16 @@ k_beam_stage1(const ChainParams<T, K> C, const CostParams<T, NQ> W, const double
               int64_t B, const double* __restrict__ seeds, int S, int P, int steps1, int keep,
               T* __restrict__ surv, int rec) {
   extern __shared__ unsigned char smem_raw[];
-  T* hist = reinterpret_cast<T*>(smem_raw);           // [(steps1+1) * bd]
-  T* costs = hist + (size_t)(steps1 + 1) * blockDim.x;  // [bd]
-  T* Ag = costs + blockDim.x;                           // [(Tri + NQ) * bd]
+  T* hist = reinterpret_cast<T*>(smem_raw);  // [(steps1+1) * bd]
+  unsigned long long* keys =                  // [bd] 8-byte prune keys (or double costs)
+      reinterpret_cast<unsigned long long*>(hist + (size_t)(steps1 + 1) * blockDim.x);
+  T* Ag = reinterpret_cast<T*>(keys + blockDim.x);  // [(Tri + NQ) * bd]
   const int tid = threadIdx.x, bd = blockDim.x;
   const int64_t tgt = (int64_t)blockIdx.x * (bd / P) + tid / P;
   const int s = tid % P;
   const bool active = (tgt < B) && (s < S);
   const int64_t tc = tgt < B ? tgt : B - 1;
-  double tinv[7];
-  target_inverse(targets + tc * 7, tinv);
-  const TargetInv<T> tg = to_target<T>(tinv);
+  const TargetInv<T> tg = target_inverse_t<T>(targets + tc * 7);
 
   LaneState<T, NQ> st;
   st.Ag = Ag + tid;
@@ -53,12 +52,30 @@ k_beam_stage1(const ChainParams<T, K> C, const CostParams<T, NQ> W, const double
     lm_iter<T, NQ, K, ID>(C, W, tg, st, it == 0 ? 1 : 0);
     hist[(size_t)it * bd + tid] = st.cost;
   }
-  costs[tid] = active ? st.cost : T(NAN);
-  __syncthreads();
-  if (!active) return;
+  // stable top-`keep` of the target's S lanes (tasks.py:135): rank = number of
+  // lanes ordered before this one by (cost, seed index), NaN last
   const int base = tid - s;
   int rank = 0;
-  for (int j = 0; j < S; ++j) rank += rank_less(costs[base + j], j, st.cost, s) ? 1 : 0;
+  if constexpr (sizeof(T) == 4) {
+    keys[tid] = active ? prune_key(st.cost, s) : ~0ull;  // padding lanes sort last
+    __syncthreads();
+    if (!active) return;
+    const unsigned long long me = keys[tid];
+    if (P >= 2) {
+      const ulonglong2* kv = reinterpret_cast<const ulonglong2*>(keys + base);
+#pragma unroll 8
+      for (int j = 0; j < P / 2; ++j) {
+        const ulonglong2 v = kv[j];
+        rank += (v.x < me ? 1 : 0) + (v.y < me ? 1 : 0);
+      }
+    }
+  } else {
+    T* costs = reinterpret_cast<T*>(keys);
+    costs[tid] = active ? st.cost : T(NAN);
+    __syncthreads();
+    if (!active) return;
+    for (int j = 0; j < S; ++j) rank += rank_less(costs[base + j], j, st.cost, s) ? 1 : 0;
+  }
   if (rank >= keep) return;
   T* out = surv + (size_t)(tgt * keep + rank) * rec;
 #pragma unroll
@@ -137,9 +154,7 @@ k_beam_stage2(const ChainParams<T, K> C, const CostParams<T, NQ> W, const ChainP
   const bool active = (tgt < B) && (r < keep);
   const int64_t tc = tgt < B ? tgt : B - 1;
   const int rc = r < keep ? r : 0;
-  double tinv[7];
-  target_inverse(targets + tc * 7, tinv);
-  const TargetInv<T> tg = to_target<T>(tinv);
+  const TargetInv<T> tg = target_inverse_t<T>(targets + tc * 7);
   const T* rin = surv + (size_t)(tc * keep + rc) * rec;
 
   LaneState<T, NQ> st;
@@ -179,6 +194,8 @@ k_beam_stage2(const ChainParams<T, K> C, const CostParams<T, NQ> W, const ChainP
     for (int i = 0; i <= steps1; ++i) h[i] = double(rin[NQ + 2 + i]);
     for (int i = 0; i < steps2; ++i) h[steps1 + 1 + i] = double(hist[(size_t)i * bd + tid]);
   }
+  double tinv[7];
+  target_inverse(targets + tgt * 7, tinv);
   double pe, re;
   pose_errors_f64<K>(Cd, qd, tinv, pe, re);
   pos_err[tgt] = pe;
@@ -322,7 +339,7 @@ cudaError_t launch_beam(const ChainParams<T, K>& C, const CostParams<T, NQ>& W,
   const int per_block = tpb / L.P;
   const int64_t blocks1 = (L.B + per_block - 1) / per_block;
   constexpr int kAg = Tri<NQ>::size + NQ;
-  const size_t smem1 = sizeof(T) * ((size_t)(L.steps1 + 1) * tpb + tpb + (size_t)kAg * tpb);
+  const size_t smem1 = sizeof(T) * ((size_t)(L.steps1 + 1) * tpb + (size_t)kAg * tpb) + 8 * (size_t)tpb;
   cudaError_t e = cudaSuccess;
   if (L.stages & 1) {
     if (L.twopass) {

@@ -46,6 +46,36 @@ __device__ __forceinline__ void target_inverse(const double* __restrict__ pose, 
   out[4] = -t.x; out[5] = -t.y; out[6] = -t.z;
 }
 
+// Per-lane target inverse.  double: the exact canonical inverse above.
+// float: q^-1 = conj(q) renormalised with rsqrtf and t^-1 = -R(q^-1) t, all in
+// float (the target is already canonical, so the canonical sign flip is the
+// identity except at w == 0, handled by the same lead-component rule).
+template <typename T>
+__device__ __forceinline__ TargetInv<T> target_inverse_t(const double* __restrict__ pose);
+
+template <>
+__device__ __forceinline__ TargetInv<double> target_inverse_t<double>(const double* __restrict__ pose) {
+  double v[7];
+  target_inverse(pose, v);
+  return {{v[0], v[1], v[2], v[3]}, {v[4], v[5], v[6]}};
+}
+
+template <>
+__device__ __forceinline__ TargetInv<float> target_inverse_t<float>(const double* __restrict__ pose) {
+  float w = float(pose[0]), x = -float(pose[1]), y = -float(pose[2]), z = -float(pose[3]);
+  const float rn = rsqrtf(w * w + x * x + y * y + z * z);
+  w *= rn; x *= rn; y *= rn; z *= rn;
+  float sign = w < 0.f ? -1.f : 1.f;
+  if (w == 0.f) {
+    const float ax = fabsf(x), ay = fabsf(y), az = fabsf(z);
+    const float lead = (ax >= ay && ax >= az) ? x : (ay >= az ? y : z);
+    sign = lead < 0.f ? -1.f : 1.f;
+  }
+  const quat<float> q{w * sign, x * sign, y * sign, z * sign};
+  const vec3<float> t = qrot(q, vec3<float>{float(pose[4]), float(pose[5]), float(pose[6])});
+  return {q, {-t.x, -t.y, -t.z}};
+}
+
 template <typename T>
 __device__ __forceinline__ TargetInv<T> to_target(const double v[7]) {
   return {{T(v[0]), T(v[1]), T(v[2]), T(v[3])}, {T(v[4]), T(v[5]), T(v[6])}};
@@ -400,6 +430,15 @@ __device__ __forceinline__ void lm_step_twopass(const ChainParams<T, K>& C,
   }
 }
 
+// Sort key of a lane for the stable top-k prune: (cost bits, lane index) as
+// one uint64.  Costs are sums of squares, so their IEEE bits (sign cleared)
+// order like the values, +inf above every finite cost and NaN (0x7fffffff)
+// above +inf -- np.argsort(kind="stable") order with NaN last.
+__device__ __forceinline__ unsigned long long prune_key(float c, int idx) {
+  uint32_t b = __float_as_uint(c) & 0x7fffffffu;
+  if (c != c) b = 0x7fffffffu;
+  return ((unsigned long long)b << 32) | (uint32_t)idx;
+}
 // (cost, index) ordering of np.argsort(kind="stable") with NaN last.
 template <typename T>
 __device__ __forceinline__ bool rank_less(T a, int ia, T b, int ib) {
