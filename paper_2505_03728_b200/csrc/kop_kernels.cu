@@ -24,17 +24,18 @@ namespace kop {
 // ---------------------------------------------------------------------------
 // IK-Beam stage 1
 // ---------------------------------------------------------------------------
-template <typename T, int NQ, int K, bool ID>
-__global__ void __launch_bounds__(256, 2)
+template <typename T, int NQ, int K, bool ID, int TPB>
+__global__ void __launch_bounds__(TPB, (TPB <= 256 ? 2 : 1))
 k_beam_stage1(const ChainParams<T, K> C, const CostParams<T, NQ> W, const double* __restrict__ targets,
               int64_t B, const double* __restrict__ seeds, int S, int P, int steps1, int keep,
               T* __restrict__ surv, int rec) {
   extern __shared__ unsigned char smem_raw[];
   T* hist = reinterpret_cast<T*>(smem_raw);  // [(steps1+1) * bd]
   unsigned long long* keys =                  // [bd] 8-byte prune keys (or double costs)
-      reinterpret_cast<unsigned long long*>(hist + (size_t)(steps1 + 1) * blockDim.x);
-  T* Ag = reinterpret_cast<T*>(keys + blockDim.x);  // [(Tri + NQ) * bd]
-  const int tid = threadIdx.x, bd = blockDim.x;
+      reinterpret_cast<unsigned long long*>(hist + (size_t)(steps1 + 1) * TPB);
+  T* Ag = reinterpret_cast<T*>(keys + TPB);  // [(Tri + NQ) * bd]
+  const int tid = threadIdx.x;
+  constexpr int bd = TPB;
   const int64_t tgt = (int64_t)blockIdx.x * (bd / P) + tid / P;
   const int s = tid % P;
   const bool active = (tgt < B) && (s < S);
@@ -49,7 +50,7 @@ k_beam_stage1(const ChainParams<T, K> C, const CostParams<T, NQ> W, const double
   for (int i = 0; i < NQ; ++i) st.q[i] = T(sd[i]);
   st.lam = T(BeamConsts::damping_init);
   for (int it = 0; it <= steps1; ++it) {  // it == 0: start_state
-    lm_iter<T, NQ, K, ID>(C, W, tg, st, it == 0 ? 1 : 0);
+    lm_iter<T, NQ, K, ID, TPB>(C, W, tg, st, it == 0 ? 1 : 0);
     hist[(size_t)it * bd + tid] = st.cost;
   }
   // stable top-`keep` of the target's S lanes (tasks.py:135): rank = number of
@@ -146,7 +147,8 @@ k_beam_stage2(const ChainParams<T, K> C, const CostParams<T, NQ> W, const ChainP
               double* __restrict__ pos_err, double* __restrict__ rot_err, uint8_t* __restrict__ success) {
   extern __shared__ unsigned char smem_raw[];
   T* hist = reinterpret_cast<T*>(smem_raw);  // [steps2 * bd]
-  const int tid = threadIdx.x, bd = blockDim.x;
+  const int tid = threadIdx.x;
+  constexpr int bd = 128;  // launch_beam launches stage 2 with 128 threads
   T* Ag = hist + (size_t)(steps2 > 0 ? steps2 : 1) * bd;  // [(Tri + NQ) * bd]
   const int64_t lane = (int64_t)blockIdx.x * bd + tid;
   const int64_t tgt = lane / G;
@@ -167,7 +169,7 @@ k_beam_stage2(const ChainParams<T, K> C, const CostParams<T, NQ> W, const ChainP
   // A/g are re-derived at q, as the reference re-derives r and J (beam.py:202)
   st.cost = rin[NQ + 1];
   for (int it = -1; it < steps2; ++it) {  // it == -1: re-derive A, g at the survivor's q
-    lm_iter<T, NQ, K, ID>(C, W, tg, st, it < 0 ? 2 : 0);
+    lm_iter<T, NQ, K, ID, 128>(C, W, tg, st, it < 0 ? 2 : 0);
     if (it >= 0) hist[(size_t)it * bd + tid] = st.cost;
   }
   // winner = argmin over the keep survivors, ties -> lower stage-1 rank (tasks.py:139)
@@ -274,7 +276,7 @@ k_lane_run(const ChainParams<T, K> C, const CostParams<T, NQ> W, const double* _
   st.lam = T(lam_io[l]);
   st.cost = T(cost_io[l]);
   for (int it = -1; it < steps; ++it) {
-    lm_iter<T, NQ, K, ID>(C, W, tg, st, it < 0 ? 2 : 0);
+    lm_iter<T, NQ, K, ID, 128>(C, W, tg, st, it < 0 ? 2 : 0);
     if (hist && it >= 0) hist[l * steps + it] = double(st.cost);
   }
 #pragma unroll
@@ -335,7 +337,7 @@ cudaError_t launch_beam(const ChainParams<T, K>& C, const CostParams<T, NQ>& W,
   const int rec = NQ + 2 + L.steps1 + 1;
   T* surv = reinterpret_cast<T*>(L.workspace);
   // stage 1: P lanes per target (power of two >= S), 256-thread blocks
-  const int tpb = L.P >= 256 ? L.P : 256;
+  const int tpb = L.P <= 256 ? 256 : 1024;  // P <= 1024 (seeds <= 1024)
   const int per_block = tpb / L.P;
   const int64_t blocks1 = (L.B + per_block - 1) / per_block;
   constexpr int kAg = Tri<NQ>::size + NQ;
@@ -349,11 +351,19 @@ cudaError_t launch_beam(const ChainParams<T, K>& C, const CostParams<T, NQ>& W,
       k_beam_stage1_twopass<T, NQ, K, ID><<<(unsigned)blocks1, tpb, smem1, st>>>(
           C, W, L.targets, L.B, L.seeds, L.S, L.P, L.steps1, L.keep, surv, rec);
     } else {
-      if (smem1 > 48 * 1024)
-        cudaFuncSetAttribute(k_beam_stage1<T, NQ, K, ID>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem1);
-      k_beam_stage1<T, NQ, K, ID><<<(unsigned)blocks1, tpb, smem1, st>>>(
-          C, W, L.targets, L.B, L.seeds, L.S, L.P, L.steps1, L.keep, surv, rec);
+      if (tpb == 256) {
+        if (smem1 > 48 * 1024)
+          cudaFuncSetAttribute(k_beam_stage1<T, NQ, K, ID, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem1);
+        k_beam_stage1<T, NQ, K, ID, 256><<<(unsigned)blocks1, tpb, smem1, st>>>(
+            C, W, L.targets, L.B, L.seeds, L.S, L.P, L.steps1, L.keep, surv, rec);
+      } else {
+        if (smem1 > 48 * 1024)
+          cudaFuncSetAttribute(k_beam_stage1<T, NQ, K, ID, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)smem1);
+        k_beam_stage1<T, NQ, K, ID, 1024><<<(unsigned)blocks1, 1024, smem1, st>>>(
+            C, W, L.targets, L.B, L.seeds, L.S, L.P, L.steps1, L.keep, surv, rec);
+      }
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;

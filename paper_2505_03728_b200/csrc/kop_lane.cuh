@@ -259,11 +259,13 @@ __device__ __forceinline__ T lane_normal(const ChainParams<T, K>& C, const CostP
 #pragma unroll
   for (int i = 0; i < NQ; ++i) {
 #pragma unroll
-    for (int j = 0; j <= i; ++j) {
-      T a = T(0);
+    for (int j = 0; j < NQ; ++j) {
+      if (j <= i) {
+        T a = T(0);
 #pragma unroll
-      for (int m = 0; m < 6; ++m) a += J[m][i] * J[m][j];
-      A[Tri<NQ>::at(i, j)] = a;
+        for (int m = 0; m < 6; ++m) a += J[m][i] * J[m][j];
+        A[Tri<NQ>::at(i, j)] = a;
+      }
     }
     A[Tri<NQ>::at(i, i)] += gl[i] * gl[i] + W.w_rest * W.w_rest;
     T s = T(0);
@@ -280,6 +282,9 @@ __device__ __forceinline__ T lane_normal(const ChainParams<T, K>& C, const CostP
 template <typename T, int NQ>
 __device__ __forceinline__ bool damped_solve(const T (&A)[Tri<NQ>::size], const T (&g)[NQ], T lam,
                                              T (&delta)[NQ]) {
+  // All loops have constant trip counts with the triangular bounds as
+  // predicates, so they unroll completely and L stays in registers (nested
+  // loops with j-dependent bounds were left rolled and put L in local memory).
   T L[Tri<NQ>::size];
   T dinv[NQ];
   bool ok = true;
@@ -294,16 +299,20 @@ __device__ __forceinline__ bool damped_solve(const T (&A)[Tri<NQ>::size], const 
   for (int j = 0; j < NQ; ++j) {
     T s = L[Tri<NQ>::at(j, j)];
 #pragma unroll
-    for (int k = 0; k < j; ++k) s -= L[Tri<NQ>::at(j, k)] * L[Tri<NQ>::at(j, k)];
+    for (int k = 0; k < NQ; ++k)
+      if (k < j) s -= L[Tri<NQ>::at(j, k)] * L[Tri<NQ>::at(j, k)];
     ok = ok && (s > T(0)) && finite_t(s);
     const T inv = rsqrt_t(s);
     dinv[j] = inv;
 #pragma unroll
-    for (int i = j + 1; i < NQ; ++i) {
-      T v = L[Tri<NQ>::at(i, j)];
+    for (int i = 0; i < NQ; ++i) {
+      if (i > j) {
+        T v = L[Tri<NQ>::at(i, j)];
 #pragma unroll
-      for (int k = 0; k < j; ++k) v -= L[Tri<NQ>::at(i, k)] * L[Tri<NQ>::at(j, k)];
-      L[Tri<NQ>::at(i, j)] = v * inv;
+        for (int k = 0; k < NQ; ++k)
+          if (k < j) v -= L[Tri<NQ>::at(i, k)] * L[Tri<NQ>::at(j, k)];
+        L[Tri<NQ>::at(i, j)] = v * inv;
+      }
     }
   }
   T y[NQ];
@@ -311,14 +320,17 @@ __device__ __forceinline__ bool damped_solve(const T (&A)[Tri<NQ>::size], const 
   for (int i = 0; i < NQ; ++i) {
     T v = -g[i];
 #pragma unroll
-    for (int k = 0; k < i; ++k) v -= L[Tri<NQ>::at(i, k)] * y[k];
+    for (int k = 0; k < NQ; ++k)
+      if (k < i) v -= L[Tri<NQ>::at(i, k)] * y[k];
     y[i] = v * dinv[i];
   }
 #pragma unroll
-  for (int i = NQ - 1; i >= 0; --i) {
+  for (int ii = 0; ii < NQ; ++ii) {
+    const int i = NQ - 1 - ii;
     T v = y[i];
 #pragma unroll
-    for (int k = i + 1; k < NQ; ++k) v -= L[Tri<NQ>::at(k, i)] * delta[k];
+    for (int k = 0; k < NQ; ++k)
+      if (k > i) v -= L[Tri<NQ>::at(k, i)] * delta[k];
     delta[i] = v * dinv[i];
   }
   return ok;
@@ -337,21 +349,25 @@ struct LaneState {
   int stride;
 };
 
-template <typename T, int NQ>
+// STRIDE: the block size when it is a compile-time constant (then every
+// shared-memory access is base + immediate), 0 = use s.stride.
+template <int STRIDE, typename T, int NQ>
 __device__ __forceinline__ void store_normal(const LaneState<T, NQ>& s, const T (&A)[Tri<NQ>::size],
                                              const T (&g)[NQ]) {
+  const int st = STRIDE ? STRIDE : s.stride;
 #pragma unroll
-  for (int i = 0; i < Tri<NQ>::size; ++i) s.Ag[i * s.stride] = A[i];
+  for (int i = 0; i < Tri<NQ>::size; ++i) s.Ag[i * st] = A[i];
 #pragma unroll
-  for (int i = 0; i < NQ; ++i) s.Ag[(Tri<NQ>::size + i) * s.stride] = g[i];
+  for (int i = 0; i < NQ; ++i) s.Ag[(Tri<NQ>::size + i) * st] = g[i];
 }
 
-template <typename T, int NQ>
+template <int STRIDE, typename T, int NQ>
 __device__ __forceinline__ void load_normal(const LaneState<T, NQ>& s, T (&A)[Tri<NQ>::size], T (&g)[NQ]) {
+  const int st = STRIDE ? STRIDE : s.stride;
 #pragma unroll
-  for (int i = 0; i < Tri<NQ>::size; ++i) A[i] = s.Ag[i * s.stride];
+  for (int i = 0; i < Tri<NQ>::size; ++i) A[i] = s.Ag[i * st];
 #pragma unroll
-  for (int i = 0; i < NQ; ++i) g[i] = s.Ag[(Tri<NQ>::size + i) * s.stride];
+  for (int i = 0; i < NQ; ++i) g[i] = s.Ag[(Tri<NQ>::size + i) * st];
 }
 
 template <typename T>
@@ -369,14 +385,14 @@ __device__ __forceinline__ T inf_t() { return T(INFINITY); }
 //           re-derived at q, beam.py:202).
 // A single inlined evaluation serves all three (one copy of the ~2K-instruction
 // body per kernel keeps the hot loop inside the instruction cache).
-template <typename T, int NQ, int K, bool ID>
+template <typename T, int NQ, int K, bool ID, int STRIDE = 0>
 __device__ __forceinline__ void lm_iter(const ChainParams<T, K>& C, const CostParams<T, NQ>& W,
                                         const TargetInv<T>& tg, LaneState<T, NQ>& s, int mode) {
   T d[NQ];
   bool ok = true;
   if (mode == 0) {
     T A[Tri<NQ>::size], g[NQ];
-    load_normal(s, A, g);
+    load_normal<STRIDE>(s, A, g);
     ok = damped_solve<T, NQ>(A, g, s.lam, d);
   } else {
 #pragma unroll
@@ -387,16 +403,16 @@ __device__ __forceinline__ void lm_iter(const ChainParams<T, K>& C, const CostPa
   for (int i = 0; i < NQ; ++i) qn[i] = s.q[i] + (ok ? d[i] : T(0));
   T An[Tri<NQ>::size], gn[NQ];
   const T raw = lane_normal<T, NQ, K, ID>(C, W, tg, qn, An, gn);
+  const T cn = finite_t(raw) ? raw : inf_t<T>();
+  const bool acc = mode != 0 || (ok && (cn < s.cost));
+  if (acc) store_normal<STRIDE>(s, An, gn);  // one store site for start and accept
   if (mode != 0) {
-    store_normal(s, An, gn);
     if (mode == 1) s.cost = raw;  // start_state keeps a non-finite cost as is
     return;
   }
-  const T cn = finite_t(raw) ? raw : inf_t<T>();
-  if (ok && (cn < s.cost)) {
+  if (acc) {
 #pragma unroll
     for (int i = 0; i < NQ; ++i) s.q[i] = qn[i];
-    store_normal(s, An, gn);
     s.cost = cn;
     s.lam = tmax(s.lam * T(BeamConsts::damping_down), T(BeamConsts::damping_min));
   } else {
