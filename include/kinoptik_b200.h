@@ -76,7 +76,9 @@ typedef struct {
   double w_position, w_orientation, w_limit, w_rest;
   int32_t seeds, total_steps, prune_after, keep;
   double success_pos_tol, success_rot_tol;
-  int32_t precision; /* KOP_FP32 | KOP_FP64 */
+  int32_t precision;     /* KOP_FP32 | KOP_FP64 */
+  int32_t optimize_base; /* 1: SE(2) mobile base as 3 extra variables (beam.py:98-112) */
+  double w_base;         /* base regularisation weight (IkRequest.base_reg_weight) */
 } KopIkParams;
 
 /* --- model ----------------------------------------------------------------
@@ -106,49 +108,55 @@ int kop_fk(const KopModel* model, int32_t precision, const double* q, int64_t ba
            void* stream);
 
 /* --- lane engine ----------------------------------------------------------
- * replaces: beam.IkLaneProblem(model, link, target, weights...) with
- * .residuals_and_jacobian (beam.py:133-180), .start_state (beam.py:182-196)
- * and .run(state, steps) (beam.py:198-240), generalised to one target per
- * lane.  target_inv: device [T*7] double, the INVERSE target pose per target
- * (beam.py:89-91); lane_target: device [B] int32 target index per lane.
- * State arrays (device, double): q [B*n] in/out, damping [B] in/out,
- * cost [B] in/out; history: device [B*steps] double (may be NULL).
- * weights: host [4] (position, orientation, limit, rest). */
+ * replaces: beam.IkLaneProblem(model, link, target, weights..., use_base,
+ * base_reg_weight) with .residuals_and_jacobian (beam.py:133-180),
+ * .start_state (beam.py:182-196) and .run(state, steps) (beam.py:198-240),
+ * generalised to one target per lane.  target_inv: device [T*7] double, the
+ * INVERSE target pose per target (beam.py:89-91); lane_target: device [B]
+ * int32 target index per lane.  State arrays (device, double): q [B*n]
+ * in/out, base_state [B*3] (x, y, angle) in/out or NULL for a fixed base
+ * (NULL = use_base False), damping [B] in/out, cost [B] in/out; history:
+ * device [B*steps] double (may be NULL).  weights: host [5] (position,
+ * orientation, limit, rest, base).  Residual rows: 6 pose, n limit, n rest,
+ * (3 base); Jacobian columns: n joints (+3 base tangent vx, vy, w). */
 int kop_lane_residuals_jacobian(const KopModel* model, int32_t link, int32_t precision,
                                 const double* weights, const double* target_inv,
-                                const int32_t* lane_target, const double* q, int64_t lanes,
-                                double* residual, double* jacobian, void* stream);
+                                const int32_t* lane_target, const double* q, const double* base_state,
+                                int64_t lanes, double* residual, double* jacobian, void* stream);
 int kop_lane_start(const KopModel* model, int32_t link, int32_t precision, const double* weights,
                    const double* target_inv, const int32_t* lane_target, const double* q,
-                   int64_t lanes, double* damping, double* cost, void* stream);
+                   const double* base_state, int64_t lanes, double* damping, double* cost, void* stream);
 int kop_lane_run(const KopModel* model, int32_t link, int32_t precision, const double* weights,
                  const double* target_inv, const int32_t* lane_target, int64_t lanes,
-                 int32_t steps, double* q, double* damping, double* cost, double* history,
-                 void* stream);
+                 int32_t steps, double* q, double* base_state, double* damping, double* cost,
+                 double* history, void* stream);
 
 /* --- IK-Beam ----------------------------------------------------------------
- * replaces: tasks.solve_ik_beam(IkRequest) -> IkResult (tasks.py:119-166),
+ * replaces: tasks.solve_ik_beam / solve_ik_mobile(IkRequest) -> IkResult
+ * (tasks.py:119-180),
  * batched over B independent targets (the reference loops targets one by one,
  * benchmark.py:136-151).  targets: device [B*7] double (w,x,y,z,px,py,pz);
  * seeds: device [S*n] double, shared by every target (tasks.py:131).
- * Outputs (device): q [B*n] double, cost [B] double, history
- * [B*(total_steps+1)] double (NULL ok), pos_err [B], rot_err [B] double
- * (tasks.py:109-116, evaluated in double), success [B] uint8.
+ * Outputs (device): q [B*n] double, base [B*3] (x, y, angle; NULL ok, only
+ * written with optimize_base), cost [B] double, history [B*(total_steps+1)]
+ * double (NULL ok), pos_err [B], rot_err [B] double (tasks.py:109-116,
+ * evaluated in double, base included), success [B] uint8.
  * workspace: device scratch of kop_ik_beam_workspace_bytes() bytes. */
 int64_t kop_ik_beam_workspace_bytes(const KopModel* model, int32_t link, const KopIkParams* params,
                                     int64_t batch);
 int kop_ik_beam(const KopModel* model, int32_t link, const KopIkParams* params,
                 const double* targets, int64_t batch, const double* seeds, void* workspace,
-                int64_t workspace_bytes, double* q_out, double* cost_out, double* history_out,
-                double* pos_err, double* rot_err, uint8_t* success, void* stream);
+                int64_t workspace_bytes, double* q_out, double* base_out, double* cost_out,
+                double* history_out, double* pos_err, double* rot_err, uint8_t* success, void* stream);
 
 /* The two launches of kop_ik_beam issued separately (stages: 1 = seeds +
  * prune into the workspace, 2 = survivors + winner + errors, 3 = both), so a
  * caller can bracket each kernel with CUDA events.  Same arguments. */
 int kop_ik_beam_stage(const KopModel* model, int32_t link, const KopIkParams* params, int32_t stages,
                       const double* targets, int64_t batch, const double* seeds, void* workspace,
-                      int64_t workspace_bytes, double* q_out, double* cost_out, double* history_out,
-                      double* pos_err, double* rot_err, uint8_t* success, void* stream);
+                      int64_t workspace_bytes, double* q_out, double* base_out, double* cost_out,
+                      double* history_out, double* pos_err, double* rot_err, uint8_t* success,
+                      void* stream);
 
 /* --- counter-based sampling ---------------------------------------------
  * replaces: tasks.sample_seed_configurations (tasks.py:88-106) and the draws

@@ -181,6 +181,44 @@ def se3_jr_inv(xi):
     return out
 
 
+def se3_adjoint(q, t):
+    """Adjoint on translation-first twists -- liegroups.py:255-262."""
+    r = qmat(q)
+    out = np.zeros(r.shape[:-2] + (6, 6), dtype=r.dtype)
+    out[..., :3, :3] = r
+    out[..., 3:, 3:] = r
+    out[..., :3, 3:] = hat(t) @ r
+    return out
+
+
+def wrap_angle(a):
+    """(-pi, pi] -- liegroups.py:270-273."""
+    w = np.mod(np.asarray(a, dtype=float) + math.pi, 2.0 * math.pi) - math.pi
+    return np.where(w == -math.pi, math.pi, w)
+
+
+def se2_exp(delta):
+    """se(2) (vx, vy, w) -> (angle, translation) -- liegroups.py:276-287."""
+    v, w = delta[..., :2], delta[..., 2]
+    small = np.abs(w) < SERIES_BELOW
+    safe = np.where(w == 0.0, 1.0, w)
+    w2 = w * w
+    s = np.where(small, 1.0 - w2 / 6.0, np.sin(safe) / safe)
+    c = np.where(small, 0.5 * w - w * w2 / 24.0, (1.0 - np.cos(safe)) / safe)
+    return wrap_angle(w), np.stack([s * v[..., 0] - c * v[..., 1], c * v[..., 0] + s * v[..., 1]], axis=-1)
+
+
+def rot2(a):
+    c, s = np.cos(a), np.sin(a)
+    out = np.empty(np.shape(a) + (2, 2))
+    out[..., 0, 0], out[..., 0, 1], out[..., 1, 0], out[..., 1, 1] = c, -s, s, c
+    return out
+
+
+SE2_EMBED = np.zeros((6, 3))  # costs.py:88-92
+SE2_EMBED[0, 0] = SE2_EMBED[1, 1] = SE2_EMBED[5, 2] = 1.0
+
+
 # ---------------------------------------------------------------------------
 # robot tables (robot.py)
 # ---------------------------------------------------------------------------
@@ -366,16 +404,19 @@ def point_jacobian(ch: Chain, point, jp, ja, link, rotational=True):
 
 @dataclass
 class Lanes:
-    """beam.py:45-68 LaneState (no mobile base)."""
+    """beam.py:45-68 LaneState; ``ba``/``bxy`` = base angle / xy (None: fixed base)."""
 
     q: np.ndarray
     lam: np.ndarray
     cost: np.ndarray
     hist: list
+    ba: np.ndarray | None = None
+    bxy: np.ndarray | None = None
 
     def take(self, idx):
         return Lanes(self.q[idx].copy(), self.lam[idx].copy(), self.cost[idx].copy(),
-                     [h[idx].copy() for h in self.hist])
+                     [h[idx].copy() for h in self.hist], None if self.ba is None else self.ba[idx].copy(),
+                     None if self.bxy is None else self.bxy[idx].copy())
 
 
 class LaneEngine:
@@ -388,53 +429,84 @@ class LaneEngine:
     when it solves one target at a time.
     """
 
-    def __init__(self, ch: Chain, link: int, tinv_q, tinv_t, weights, group=None, dtype=np.float64):
+    def __init__(self, ch: Chain, link: int, tinv_q, tinv_t, weights, group=None, dtype=np.float64,
+                 use_base=False, base_weight=0.0):
         self.ch, self.link, self.dt = ch, link, np.dtype(dtype)
         self.tq = np.asarray(tinv_q, dtype=self.dt)
         self.tt = np.asarray(tinv_t, dtype=self.dt)
         wp, wo, wl, wr = weights
         n = ch.n
-        self.w = np.concatenate([np.full(3, wp), np.full(3, wo), np.full(n, wl), np.full(n, wr)]).astype(self.dt)
+        rows = [np.full(3, wp), np.full(3, wo), np.full(n, wl), np.full(n, wr)]
+        if use_base:
+            rows.append(np.full(3, base_weight))
+        self.w = np.concatenate(rows).astype(self.dt)
         self.lo, self.hi = ch.lower.astype(self.dt), ch.upper.astype(self.dt)
         self.rest = ch.rest.astype(self.dt)
         self.group = group
+        self.use_base = use_base
+        self.dim = n + (3 if use_base else 0)
 
-    def _pose(self, lq, lp):
+    def _compose(self, fq, fp, ba, bxy):
+        """beam.py:104-112."""
+        if not self.use_base:
+            return fq, fp
+        bq = np.zeros(ba.shape + (4,))
+        bq[..., 0], bq[..., 3] = np.cos(0.5 * ba), np.sin(0.5 * ba)
+        bp = np.concatenate([bxy, np.zeros(ba.shape + (1,))], axis=-1)
+        return qmul(bq, fq), qrot(bq, fp) + bp
+
+    def _pose(self, lq, lp, ba=None, bxy=None):
         fq, fpos = lq[..., self.link, :], lp[..., self.link, :]
-        eq = qmul(self.tq, fq)
-        et = self.tt + qrot(self.tq, fpos)
+        cq, cp = self._compose(fq, fpos, ba, bxy)
+        eq = qmul(self.tq, cq)
+        et = self.tt + qrot(self.tq, cp)
         return se3_log(eq, et), fq, fpos
 
-    def residuals(self, q, kin=None):
+    def residuals(self, q, kin=None, ba=None, bxy=None):
         """beam.py:114-131."""
         lq, lp, _, _ = kin if kin is not None else fk(self.ch, q)
-        pose, _, _ = self._pose(lq, lp)
+        pose, _, _ = self._pose(lq, lp, ba, bxy)
         lim = np.maximum(0.0, q - self.hi) + np.maximum(0.0, self.lo - q)
-        return np.concatenate([pose, lim, q - self.rest], axis=-1) * self.w
+        parts = [pose, lim, q - self.rest]
+        if self.use_base:
+            parts.append(np.concatenate([bxy, ba[..., None]], axis=-1))
+        return np.concatenate(parts, axis=-1) * self.w
 
-    def residuals_and_jacobian(self, q):
+    def residuals_and_jacobian(self, q, ba=None, bxy=None):
         """beam.py:133-180."""
         kin = fk(self.ch, q)
         lq, lp, jp, ja = kin
-        r = self.residuals(q, kin)
+        r = self.residuals(q, kin, ba, bxy)
         n = self.ch.n
-        pose, fq, fpos = self._pose(lq, lp)
+        pose, fq, fpos = self._pose(lq, lp, ba, bxy)
         jg = point_jacobian(self.ch, fpos, jp, ja, self.link)
         rt = np.swapaxes(qmat(fq), -1, -2)
         body = np.concatenate([rt @ jg[..., :3, :], rt @ jg[..., 3:, :]], axis=-2)
-        jac = np.zeros(q.shape[:-1] + (6 + 2 * n, n), dtype=self.dt)
-        jac[..., :6, :] = se3_jr_inv(pose) @ body
+        jri = se3_jr_inv(pose)
+        jac = np.zeros(q.shape[:-1] + (self.w.size, self.dim), dtype=self.dt)
+        jac[..., :6, :n] = jri @ body
         i = np.arange(n)
         jac[..., 6 + i, i] = np.where(q > self.hi, 1.0, 0.0) + np.where(q < self.lo, -1.0, 0.0)
         jac[..., 6 + n + i, i] = 1.0
+        if self.use_base:
+            iq = qconj(fq)
+            jac[..., :6, n:] = jri @ se3_adjoint(iq, -qrot(iq, fpos)) @ SE2_EMBED
+            rb = 6 + 2 * n
+            ca, sa = np.cos(ba), np.sin(ba)
+            jac[..., rb, n], jac[..., rb, n + 1] = ca, -sa
+            jac[..., rb + 1, n], jac[..., rb + 1, n + 1] = sa, ca
+            jac[..., rb + 2, n + 2] = 1.0
         return r, jac * self.w[:, None]
 
     def start(self, q0) -> Lanes:
         """beam.py:182-196."""
         q0 = np.asarray(q0, dtype=self.dt)
-        r = self.residuals(q0)
+        b = q0.shape[0]
+        ba = np.zeros(b) if self.use_base else None
+        bxy = np.zeros((b, 2)) if self.use_base else None
+        r = self.residuals(q0, None, ba, bxy)
         c = np.einsum("bm,bm->b", r, r)
-        return Lanes(q0.copy(), np.full(q0.shape[0], LAMBDA0, dtype=self.dt), c, [c.copy()])
+        return Lanes(q0.copy(), np.full(b, LAMBDA0, dtype=self.dt), c, [c.copy()], ba, bxy)
 
     def _solve(self, h, g):
         try:
@@ -458,18 +530,26 @@ class LaneEngine:
         """beam.py:198-240: one proposal per step, per-lane accept and damping."""
         n = self.ch.n
         for _ in range(steps):
-            r, jac = self.residuals_and_jacobian(st.q)
+            r, jac = self.residuals_and_jacobian(st.q, st.ba, st.bxy)
             jtj = np.einsum("bmi,bmj->bij", jac, jac)
             g = np.einsum("bmi,bm->bi", jac, r)
             d = np.maximum(np.einsum("bii->bi", jtj), self.dt.type(DIAG_FLOOR))
-            h = jtj + st.lam[:, None, None] * d[:, :, None] * np.eye(n, dtype=self.dt)
+            h = jtj + st.lam[:, None, None] * d[:, :, None] * np.eye(self.dim, dtype=self.dt)
             delta, ok = self._solve(h, g)
-            qn = st.q + delta
-            rn = self.residuals(qn)
+            qn = st.q + delta[:, :n]
+            ban = bxyn = None
+            if self.use_base:
+                ang, xy = se2_exp(delta[:, n:])
+                ban = wrap_angle(st.ba + ang)
+                bxyn = st.bxy + (rot2(st.ba) @ xy[..., None])[..., 0]
+            rn = self.residuals(qn, None, ban, bxyn)
             cn = np.einsum("bm,bm->b", rn, rn)
             cn = np.where(np.isfinite(cn), cn, np.inf)
             acc = (cn < st.cost) & ok
             st.q = np.where(acc[:, None], qn, st.q)
+            if self.use_base:
+                st.ba = np.where(acc, ban, st.ba)
+                st.bxy = np.where(acc[:, None], bxyn, st.bxy)
             st.cost = np.where(acc, cn, st.cost)
             st.lam = np.where(acc, np.maximum(st.lam * LAMBDA_DOWN, LAMBDA_MIN),
                               np.minimum(st.lam * LAMBDA_UP, LAMBDA_MAX)).astype(self.dt)
@@ -523,11 +603,15 @@ def target_inverse(tq, tt):
     return iq, -qrot(iq, tt)
 
 
-def pose_errors(ch: Chain, link: int, tq, tt, q):
-    """tasks.py:109-116 (no base): |t(T_t^-1 T)|, |log R(T_t^-1 T)|."""
+def pose_errors(ch: Chain, link: int, tq, tt, q, ba=None, bxy=None):
+    """tasks.py:109-116: |t(T_t^-1 (B) T)|, |log R(T_t^-1 (B) T)|."""
     lq, lp, _, _ = fk(ch, np.asarray(q, dtype=float))
     cq = qcanon(lq[..., link, :])
     cp = lp[..., link, :]
+    if ba is not None:  # Transform2.to_transform3().compose(current), liegroups.py:449-453
+        bq = qexp(np.stack([np.zeros_like(ba), np.zeros_like(ba), ba], axis=-1))
+        cp = np.concatenate([bxy, np.zeros_like(ba)[..., None]], axis=-1) + qrot(bq, cp)
+        cq = qcanon(qmul(bq, cq))
     iq, it = target_inverse(tq, tt)
     rq = qcanon(qmul(iq, cq))
     rt = it + qrot(iq, cp)
@@ -542,13 +626,15 @@ class BeamResult:
     pos_err: np.ndarray
     rot_err: np.ndarray
     success: np.ndarray
+    base: np.ndarray | None = None  # (B, 3) x, y, angle
 
 
 DEFAULT_WEIGHTS = (50.0, 10.0, 100.0, 0.01)  # costs.py:52-62 (pos, ori, limit, rest)
 
 
 def ik_beam(ch: Chain, link: int, tq, tt, seeds, weights=DEFAULT_WEIGHTS, total_steps=16,
-            prune_after=6, keep=4, pos_tol=0.005, rot_tol=0.05, dtype=np.float64) -> BeamResult:
+            prune_after=6, keep=4, pos_tol=0.005, rot_tol=0.05, dtype=np.float64, use_base=False,
+            base_weight=0.0) -> BeamResult:
     """tasks.py:119-161 over B targets at once (lanes = B x S seeds).
 
     Each target's lanes are independent, so batching targets reproduces the
@@ -558,21 +644,27 @@ def ik_beam(ch: Chain, link: int, tq, tt, seeds, weights=DEFAULT_WEIGHTS, total_
     b, s = tq.shape[0], seeds.shape[0]
     iq, it = target_inverse(tq, tt)
     lane_t = np.repeat(np.arange(b), s)
-    eng = LaneEngine(ch, link, iq[lane_t], it[lane_t], weights, group=lane_t, dtype=dtype)
+    kw = dict(dtype=dtype, use_base=use_base, base_weight=base_weight)
+    eng = LaneEngine(ch, link, iq[lane_t], it[lane_t], weights, group=lane_t, **kw)
     st = eng.start(np.tile(seeds, (b, 1)))
     st = eng.run(st, prune_after)
     cost = st.cost.reshape(b, s)
     order = np.argsort(cost, axis=1, kind="stable")[:, :keep]
     pick = (order + np.arange(b)[:, None] * s).reshape(-1)
     st2 = st.take(pick)
-    eng2 = LaneEngine(ch, link, iq[lane_t[pick]], it[lane_t[pick]], weights,
-                      group=lane_t[pick], dtype=dtype)
+    eng2 = LaneEngine(ch, link, iq[lane_t[pick]], it[lane_t[pick]], weights, group=lane_t[pick], **kw)
     st2 = eng2.run(st2, total_steps - prune_after)
     c2 = st2.cost.reshape(b, keep)
     win = np.argmin(c2, axis=1)
     sel = np.arange(b) * keep + win
     q = st2.q[sel].astype(np.float64)
     hist = np.stack([h[sel] for h in st2.hist], axis=1)
-    pe, re = pose_errors(ch, link, tq, tt, q)
+    base = None
+    if use_base:
+        ba = wrap_angle(st2.ba[sel])  # Transform2 wraps the angle
+        base = np.concatenate([st2.bxy[sel], ba[:, None]], axis=1)
+        pe, re = pose_errors(ch, link, tq, tt, q, ba, st2.bxy[sel])
+    else:
+        pe, re = pose_errors(ch, link, tq, tt, q)
     return BeamResult(q=q, cost=st2.cost[sel], hist=hist, pos_err=pe, rot_err=re,
-                      success=(pe < pos_tol) & (re < rot_tol))
+                      success=(pe < pos_tol) & (re < rot_tol), base=base)

@@ -34,6 +34,7 @@ class KopIkParams(C.Structure):
         ("w_position", _f64), ("w_orientation", _f64), ("w_limit", _f64), ("w_rest", _f64),
         ("seeds", _i32), ("total_steps", _i32), ("prune_after", _i32), ("keep", _i32),
         ("success_pos_tol", _f64), ("success_rot_tol", _f64), ("precision", _i32),
+        ("optimize_base", _i32), ("w_base", _f64),
     ]
 
 
@@ -46,14 +47,14 @@ SIGNATURES = {
     "kop_last_error": (C.c_char_p, []),
     "kop_build_info": (C.c_char_p, []),
     "kop_fk": (C.c_int, [_p, _i32, _p, _i64, _p, _p, _p, _p, _p]),
-    "kop_lane_residuals_jacobian": (C.c_int, [_p, _i32, _i32, _p, _p, _p, _p, _i64, _p, _p, _p]),
-    "kop_lane_start": (C.c_int, [_p, _i32, _i32, _p, _p, _p, _p, _i64, _p, _p, _p]),
-    "kop_lane_run": (C.c_int, [_p, _i32, _i32, _p, _p, _p, _i64, _i32, _p, _p, _p, _p, _p]),
+    "kop_lane_residuals_jacobian": (C.c_int, [_p, _i32, _i32, _p, _p, _p, _p, _p, _i64, _p, _p, _p]),
+    "kop_lane_start": (C.c_int, [_p, _i32, _i32, _p, _p, _p, _p, _p, _i64, _p, _p, _p]),
+    "kop_lane_run": (C.c_int, [_p, _i32, _i32, _p, _p, _p, _i64, _i32, _p, _p, _p, _p, _p, _p]),
     "kop_ik_beam_workspace_bytes": (_i64, [_p, _i32, C.POINTER(KopIkParams), _i64]),
     "kop_ik_beam": (C.c_int, [_p, _i32, C.POINTER(KopIkParams), _p, _i64, _p, _p, _i64,
-                              _p, _p, _p, _p, _p, _p, _p]),
+                              _p, _p, _p, _p, _p, _p, _p, _p]),
     "kop_ik_beam_stage": (C.c_int, [_p, _i32, C.POINTER(KopIkParams), _i32, _p, _i64, _p, _p, _i64,
-                                    _p, _p, _p, _p, _p, _p, _p]),
+                                    _p, _p, _p, _p, _p, _p, _p, _p]),
     "kop_sample_uniform": (C.c_int, [_u64, _u64, _i64, _i32, _p, _p, _p, _p, _p]),
     "kop_link_poses": (C.c_int, [_p, _i32, _p, _i64, _p, _p]),
     "kop_fma_peak_kernel": (C.c_int, [_i32, _i32, _i32, _p, C.POINTER(_f64), _p]),

@@ -136,8 +136,9 @@ ChainParams<T, K> cast_chain(const ChainParams<double, kChainMax>& D) {
 // Cost parameters; dimensions beyond the robot's n are padded with an
 // unlimited, zero-rest, Jacobian-free joint: its normal-equation row is
 // decoupled (A_ii = w_rest^2, g_i = 0), so the padded solve is exact.
+// w: (position, orientation, limit, rest, base) row weights.
 template <typename T, int NQ>
-CostParams<T, NQ> make_costs(const KopModel& m, const double w[4]) {
+CostParams<T, NQ> make_costs(const KopModel& m, const double w[5]) {
   CostParams<T, NQ> W;
   const int n = m.tree.n;
   for (int i = 0; i < NQ; ++i) {
@@ -149,6 +150,7 @@ CostParams<T, NQ> make_costs(const KopModel& m, const double w[4]) {
   W.w_ori = T(w[1]);
   W.w_lim = T(w[2]);
   W.w_rest = T(w[3]);
+  W.w_base = T(w[4]);
   return W;
 }
 
@@ -161,23 +163,25 @@ int next_pow2(int v) {
 // Shape selection shared by every chain-based entry point.
 enum class Shape { kId2, kId6, kId7, kGen8, kNone };
 
-Shape pick_shape(int n, int k, bool identity) {
+Shape pick_shape(int n, int k, bool identity, bool base) {
   if (identity && n == 7) return Shape::kId7;
-  if (identity && n == 2) return Shape::kId2;
-  if (identity && n == 6) return Shape::kId6;
+  if (!base && identity && n == 2) return Shape::kId2;
+  if (!base && identity && n == 6) return Shape::kId6;
   if (n <= 8 && k <= 8) return Shape::kGen8;
   return Shape::kNone;
 }
 
 // Padded-configuration helpers: the generic shape works on NQ = 8 internally;
-// the API arrays have stride n.  Lane kernels need stride n == NQ, so for
-// the generic shape the host pads through device scratch allocated here.
+// the API arrays have stride n, so for n < 8 the host pads through device
+// scratch allocated here (not on the Panda path, which is an ID shape).
 struct PadBuf {
   double* ptr = nullptr;
   ~PadBuf() {
     if (ptr) cudaFree(ptr);
   }
 };
+
+int kernel_nq(Shape sh, int n) { return sh == Shape::kGen8 ? 8 : n; }
 
 }  // namespace
 
@@ -186,7 +190,7 @@ extern "C" {
 const char* kop_last_error(void) { return g_err.c_str(); }
 
 const char* kop_build_info(void) {
-  return "kinoptik_b200 sm_100a; fp32/fp64 x shapes {id2, id6, id7, gen8}";
+  return "kinoptik_b200 sm_100a; fp32/fp64 x shapes {id2, id6, id7, gen8} + SE(2) base {id7, gen8}";
 }
 
 int kop_model_create(const KopModelDesc* d, KopModel** out) {
@@ -335,11 +339,11 @@ int64_t kop_ik_beam_workspace_bytes(const KopModel* m, int32_t link, const KopIk
   bool id;
   const int k = compile_chain(*m, link, C, id);
   if (k < 0) return k;
-  const Shape sh = pick_shape(m->tree.n, k, id);
+  const Shape sh = pick_shape(m->tree.n, k, id, p->optimize_base != 0);
   if (sh == Shape::kNone) return fail(KOP_EUNSUPPORTED, "robot shape not compiled in");
-  const int nq = sh == Shape::kGen8 ? 8 : m->tree.n;
+  const int nq = kernel_nq(sh, m->tree.n);
   const size_t el = p->precision == KOP_FP64 ? 8 : 4;
-  const int64_t rec = nq + 2 + p->prune_after + 1;
+  const int64_t rec = nq + (p->optimize_base ? 3 : 0) + 2 + p->prune_after + 1;
   return batch * (int64_t)p->keep * rec * (int64_t)el + 256;
 }
 
@@ -347,51 +351,67 @@ int64_t kop_ik_beam_workspace_bytes(const KopModel* m, int32_t link, const KopIk
 
 namespace {
 
-template <typename T, int NQ, int K, bool ID>
-cudaError_t run_beam(const KopModel& m, const ChainParams<double, kChainMax>& D, const double w[4],
+template <class G>
+cudaError_t run_beam(const KopModel& m, const ChainParams<double, kChainMax>& D, const double w[5],
                      const BeamLaunch& L, cudaStream_t st) {
-  return launch_beam<T, NQ, K, ID>(cast_chain<T, K>(D), make_costs<T, NQ>(m, w), cast_chain<double, K>(D), L,
-                                   st);
+  return launch_beam<G>(cast_chain<typename G::T, G::K>(D), make_costs<typename G::T, G::NQ>(m, w),
+                        cast_chain<double, G::K>(D), L, st);
 }
 
-template <typename T>
+template <typename T, bool BASE>
 cudaError_t dispatch_beam(Shape sh, const KopModel& m, const ChainParams<double, kChainMax>& D,
-                          const double w[4], const BeamLaunch& L, cudaStream_t st) {
-  switch (sh) {
-    case Shape::kId7: return run_beam<T, 7, 7, true>(m, D, w, L, st);
-    case Shape::kId2: return run_beam<T, 2, 2, true>(m, D, w, L, st);
-    case Shape::kId6: return run_beam<T, 6, 6, true>(m, D, w, L, st);
-    case Shape::kGen8: return run_beam<T, 8, 8, false>(m, D, w, L, st);
-    default: return cudaErrorInvalidValue;
+                          const double w[5], const BeamLaunch& L, cudaStream_t st) {
+  if constexpr (BASE) {
+    switch (sh) {
+      case Shape::kId7: return run_beam<Cfg<T, 7, 7, true, true>>(m, D, w, L, st);
+      case Shape::kGen8: return run_beam<Cfg<T, 8, 8, false, true>>(m, D, w, L, st);
+      default: return cudaErrorInvalidValue;
+    }
+  } else {
+    switch (sh) {
+      case Shape::kId7: return run_beam<Cfg<T, 7, 7, true, false>>(m, D, w, L, st);
+      case Shape::kId2: return run_beam<Cfg<T, 2, 2, true, false>>(m, D, w, L, st);
+      case Shape::kId6: return run_beam<Cfg<T, 6, 6, true, false>>(m, D, w, L, st);
+      case Shape::kGen8: return run_beam<Cfg<T, 8, 8, false, false>>(m, D, w, L, st);
+      default: return cudaErrorInvalidValue;
+    }
   }
 }
 
-template <typename T, int NQ, int K, bool ID>
-cudaError_t run_lane(const KopModel& m, const ChainParams<double, kChainMax>& D, const double w[4],
+template <class G>
+cudaError_t run_lane(const KopModel& m, const ChainParams<double, kChainMax>& D, const double w[5],
                      const LaneLaunch& L, cudaStream_t st) {
-  return launch_lane<T, NQ, K, ID>(cast_chain<T, K>(D), make_costs<T, NQ>(m, w), L, st);
+  return launch_lane<G>(cast_chain<typename G::T, G::K>(D), make_costs<typename G::T, G::NQ>(m, w), L, st);
 }
 
-template <typename T>
+template <typename T, bool BASE>
 cudaError_t dispatch_lane(Shape sh, const KopModel& m, const ChainParams<double, kChainMax>& D,
-                          const double w[4], const LaneLaunch& L, cudaStream_t st) {
-  switch (sh) {
-    case Shape::kId7: return run_lane<T, 7, 7, true>(m, D, w, L, st);
-    case Shape::kId2: return run_lane<T, 2, 2, true>(m, D, w, L, st);
-    case Shape::kId6: return run_lane<T, 6, 6, true>(m, D, w, L, st);
-    case Shape::kGen8: return run_lane<T, 8, 8, false>(m, D, w, L, st);
-    default: return cudaErrorInvalidValue;
+                          const double w[5], const LaneLaunch& L, cudaStream_t st) {
+  if constexpr (BASE) {
+    switch (sh) {
+      case Shape::kId7: return run_lane<Cfg<T, 7, 7, true, true>>(m, D, w, L, st);
+      case Shape::kGen8: return run_lane<Cfg<T, 8, 8, false, true>>(m, D, w, L, st);
+      default: return cudaErrorInvalidValue;
+    }
+  } else {
+    switch (sh) {
+      case Shape::kId7: return run_lane<Cfg<T, 7, 7, true, false>>(m, D, w, L, st);
+      case Shape::kId2: return run_lane<Cfg<T, 2, 2, true, false>>(m, D, w, L, st);
+      case Shape::kId6: return run_lane<Cfg<T, 6, 6, true, false>>(m, D, w, L, st);
+      case Shape::kGen8: return run_lane<Cfg<T, 8, 8, false, false>>(m, D, w, L, st);
+      default: return cudaErrorInvalidValue;
+    }
   }
 }
 
 // Resolve the chain + shape for a lane / beam call.
-int prepare(const KopModel* m, int link, int precision, ChainParams<double, kChainMax>& C, Shape& sh) {
+int prepare(const KopModel* m, int link, int precision, bool base, ChainParams<double, kChainMax>& C, Shape& sh) {
   if (!m) return fail(KOP_EINVAL, "null model");
   if (precision != KOP_FP32 && precision != KOP_FP64) return fail(KOP_EINVAL, "bad precision");
   bool id = false;
   const int k = compile_chain(*m, link, C, id);
   if (k < 0) return k;
-  sh = pick_shape(m->tree.n, k, id);
+  sh = pick_shape(m->tree.n, k, id, base);
   if (sh == Shape::kNone)
     return fail(KOP_EUNSUPPORTED, "robot with " + std::to_string(m->tree.n) +
                                       " actuated joints is not compiled in (max 8)");
@@ -421,13 +441,14 @@ extern "C" {
 
 int kop_ik_beam_stage(const KopModel* m, int32_t link, const KopIkParams* p, int32_t stages, const double* targets,
                       int64_t batch, const double* seeds, void* workspace, int64_t workspace_bytes, double* q_out,
-                      double* cost_out, double* history_out, double* pos_err, double* rot_err, uint8_t* success,
-                      void* stream) {
+                      double* base_out, double* cost_out, double* history_out, double* pos_err, double* rot_err,
+                      uint8_t* success, void* stream) {
   if (stages < 1 || stages > 3) return fail(KOP_EINVAL, "stages must be 1, 2 or 3");
   if (!p) return fail(KOP_EINVAL, "null params");
+  const bool base = p->optimize_base != 0;
   ChainParams<double, kChainMax> C;
   Shape sh;
-  int rc = prepare(m, link, p->precision, C, sh);
+  int rc = prepare(m, link, p->precision, base, C, sh);
   if (rc != KOP_OK) return rc;
   // IkRequest.__post_init__ (tasks.py:56-60)
   if (!(0 < p->prune_after && p->prune_after < p->total_steps))
@@ -443,14 +464,17 @@ int kop_ik_beam_stage(const KopModel* m, int32_t link, const KopIkParams* p, int
   if (workspace_bytes < need) return fail(KOP_EINVAL, "workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
   const int n = m->tree.n;
+  const int nq = kernel_nq(sh, n);
+  if (nq != n && stages != 3)
+    return fail(KOP_EUNSUPPORTED, "split-stage launches need n == 8 or an identity-chain shape");
   PadBuf seeds_pad, q_pad;
   const double* seeds_k = seeds;
   double* q_k = q_out;
-  if (sh == Shape::kGen8 && n != 8) {
-    if (cudaMalloc(&seeds_pad.ptr, sizeof(double) * 8 * p->seeds) != cudaSuccess ||
-        cudaMalloc(&q_pad.ptr, sizeof(double) * 8 * batch) != cudaSuccess)
+  if (nq != n) {
+    if (cudaMalloc(&seeds_pad.ptr, sizeof(double) * nq * p->seeds) != cudaSuccess ||
+        cudaMalloc(&q_pad.ptr, sizeof(double) * nq * batch) != cudaSuccess)
       return cuda_status(cudaGetLastError());
-    rc = cuda_status(restride(seeds, p->seeds, n, 8, seeds_pad.ptr, st));
+    rc = cuda_status(restride(seeds, p->seeds, n, nq, seeds_pad.ptr, st));
     if (rc) return rc;
     seeds_k = seeds_pad.ptr;
     q_k = q_pad.ptr;
@@ -469,46 +493,48 @@ int kop_ik_beam_stage(const KopModel* m, int32_t link, const KopIkParams* p, int
   L.rot_tol = p->success_rot_tol;
   L.workspace = workspace;
   L.q_out = q_k;
+  L.base_out = base_out;
   L.cost_out = cost_out;
   L.hist_out = history_out;
   L.pos_err = pos_err;
   L.rot_err = rot_err;
   L.success = success;
-  const char* tp = getenv("KOP_TWOPASS");
-  L.twopass = tp && tp[0] == '1';
   L.stages = stages;
-  if (sh == Shape::kGen8 && n != 8 && stages != 3)
-    return fail(KOP_EUNSUPPORTED, "split-stage launches need n == 8 or an identity-chain shape");
-  const double w[4] = {p->w_position, p->w_orientation, p->w_limit, p->w_rest};
-  cudaError_t e = p->precision == KOP_FP32 ? dispatch_beam<float>(sh, *m, C, w, L, st)
-                                           : dispatch_beam<double>(sh, *m, C, w, L, st);
-  if (e == cudaSuccess && q_k != q_out) e = restride(q_k, batch, 8, n, q_out, st);
+  const double w[5] = {p->w_position, p->w_orientation, p->w_limit, p->w_rest, p->w_base};
+  cudaError_t e;
+  if (p->precision == KOP_FP32)
+    e = base ? dispatch_beam<float, true>(sh, *m, C, w, L, st) : dispatch_beam<float, false>(sh, *m, C, w, L, st);
+  else
+    e = base ? dispatch_beam<double, true>(sh, *m, C, w, L, st) : dispatch_beam<double, false>(sh, *m, C, w, L, st);
+  if (e == cudaSuccess && q_k != q_out) e = restride(q_k, batch, nq, n, q_out, st);
   if (seeds_pad.ptr) cudaStreamSynchronize(st);  // scratch freed at return
   return cuda_status(e);
 }
 
 int kop_ik_beam(const KopModel* m, int32_t link, const KopIkParams* p, const double* targets, int64_t batch,
-                const double* seeds, void* workspace, int64_t workspace_bytes, double* q_out, double* cost_out,
-                double* history_out, double* pos_err, double* rot_err, uint8_t* success, void* stream) {
-  return kop_ik_beam_stage(m, link, p, 3, targets, batch, seeds, workspace, workspace_bytes, q_out, cost_out,
-                           history_out, pos_err, rot_err, success, stream);
+                const double* seeds, void* workspace, int64_t workspace_bytes, double* q_out, double* base_out,
+                double* cost_out, double* history_out, double* pos_err, double* rot_err, uint8_t* success,
+                void* stream) {
+  return kop_ik_beam_stage(m, link, p, 3, targets, batch, seeds, workspace, workspace_bytes, q_out, base_out,
+                           cost_out, history_out, pos_err, rot_err, success, stream);
 }
 
-static int lane_call(const KopModel* m, int32_t link, int32_t precision, const double* weights,
-                     LaneLaunch L, int64_t lanes, void* stream) {
+static int lane_call(const KopModel* m, int32_t link, int32_t precision, const double* weights, LaneLaunch L,
+                     int64_t lanes, void* stream) {
+  const bool base = L.base_in != nullptr || L.base_io != nullptr;
   ChainParams<double, kChainMax> C;
   Shape sh;
-  int rc = prepare(m, link, precision, C, sh);
+  int rc = prepare(m, link, precision, base, C, sh);
   if (rc != KOP_OK) return rc;
   if (!weights) return fail(KOP_EINVAL, "null weights");
   if (lanes < 0) return fail(KOP_EINVAL, "negative lane count");
   if (lanes == 0) return KOP_OK;
   cudaStream_t st = (cudaStream_t)stream;
   const int n = m->tree.n;
-  const int nq = sh == Shape::kGen8 ? 8 : n;
+  const int nq = kernel_nq(sh, n);
+  const int nd = nq + (base ? 3 : 0), ndu = n + (base ? 3 : 0);
   L.lanes = lanes;
   PadBuf qin, qio, res, jac;
-  const double* user_qin = L.q_in;
   double* user_qio = L.q_io;
   double* user_res = L.res;
   double* user_jac = L.jac;
@@ -524,44 +550,55 @@ static int lane_call(const KopModel* m, int32_t link, int32_t precision, const d
       L.q_io = qio.ptr;
     }
     if (L.res) {
-      const int M = 6 + 2 * nq;
+      const int M = 6 + 2 * nq + (base ? 3 : 0);
       if (cudaMalloc(&res.ptr, sizeof(double) * M * lanes) != cudaSuccess ||
-          cudaMalloc(&jac.ptr, sizeof(double) * M * nq * lanes) != cudaSuccess)
+          cudaMalloc(&jac.ptr, sizeof(double) * M * nd * lanes) != cudaSuccess)
         return cuda_status(cudaGetLastError());
       L.res = res.ptr;
       L.jac = jac.ptr;
     }
   }
-  cudaError_t e = precision == KOP_FP32 ? dispatch_lane<float>(sh, *m, C, weights, L, st)
-                                        : dispatch_lane<double>(sh, *m, C, weights, L, st);
+  cudaError_t e;
+  if (precision == KOP_FP32)
+    e = base ? dispatch_lane<float, true>(sh, *m, C, weights, L, st)
+             : dispatch_lane<float, false>(sh, *m, C, weights, L, st);
+  else
+    e = base ? dispatch_lane<double, true>(sh, *m, C, weights, L, st)
+             : dispatch_lane<double, false>(sh, *m, C, weights, L, st);
   if (e == cudaSuccess && nq != n) {
     if (user_qio) e = restride(L.q_io, lanes, nq, n, user_qio, st);
     if (e == cudaSuccess && user_res) {
-      // rows: pose 6 | limit nq | rest nq  ->  pose 6 | limit n | rest n; cols nq -> n
-      const int Mk = 6 + 2 * nq, Mu = 6 + 2 * n;
+      // rows: pose 6 | limit nq | rest nq | base 3  ->  pose 6 | limit n | rest n | base 3;
+      // cols: q nq | base 3  ->  q n | base 3
+      const int Mk = 6 + 2 * nq + (base ? 3 : 0), Mu = 6 + 2 * n + (base ? 3 : 0);
       std::vector<int> rowmap;
       for (int r = 0; r < 6; ++r) rowmap.push_back(r);
       for (int r = 0; r < n; ++r) rowmap.push_back(6 + r);
       for (int r = 0; r < n; ++r) rowmap.push_back(6 + nq + r);
-      // small: do it with per-row strided copies
+      if (base)
+        for (int r = 0; r < 3; ++r) rowmap.push_back(6 + 2 * nq + r);
       for (int r = 0; r < Mu && e == cudaSuccess; ++r) {
         e = cudaMemcpy2DAsync(user_res + r, sizeof(double) * Mu, L.res + rowmap[r], sizeof(double) * Mk,
                               sizeof(double), lanes, cudaMemcpyDeviceToDevice, st);
         if (e == cudaSuccess)
-          e = cudaMemcpy2DAsync(user_jac + (size_t)r * n, sizeof(double) * Mu * n,
-                                L.jac + (size_t)rowmap[r] * nq, sizeof(double) * Mk * nq, sizeof(double) * n,
+          e = cudaMemcpy2DAsync(user_jac + (size_t)r * ndu, sizeof(double) * Mu * ndu,
+                                L.jac + (size_t)rowmap[r] * nd, sizeof(double) * Mk * nd, sizeof(double) * n,
+                                lanes, cudaMemcpyDeviceToDevice, st);
+        if (e == cudaSuccess && base)
+          e = cudaMemcpy2DAsync(user_jac + (size_t)r * ndu + n, sizeof(double) * Mu * ndu,
+                                L.jac + (size_t)rowmap[r] * nd + nq, sizeof(double) * Mk * nd, sizeof(double) * 3,
                                 lanes, cudaMemcpyDeviceToDevice, st);
       }
     }
-    (void)user_qin;
     cudaStreamSynchronize(st);  // scratch freed at return
   }
   return cuda_status(e);
 }
 
 int kop_lane_residuals_jacobian(const KopModel* m, int32_t link, int32_t precision, const double* weights,
-                                const double* tinv, const int32_t* lane_target, const double* q, int64_t lanes,
-                                double* residual, double* jacobian, void* stream) {
+                                const double* tinv, const int32_t* lane_target, const double* q,
+                                const double* base_state, int64_t lanes, double* residual, double* jacobian,
+                                void* stream) {
   if (lanes > 0 && (!tinv || !lane_target || !q || !residual || !jacobian))
     return fail(KOP_EINVAL, "null array argument");
   LaneLaunch L{};
@@ -569,14 +606,15 @@ int kop_lane_residuals_jacobian(const KopModel* m, int32_t link, int32_t precisi
   L.tinv = tinv;
   L.lane_target = lane_target;
   L.q_in = q;
+  L.base_in = base_state;
   L.res = residual;
   L.jac = jacobian;
   return lane_call(m, link, precision, weights, L, lanes, stream);
 }
 
 int kop_lane_start(const KopModel* m, int32_t link, int32_t precision, const double* weights,
-                   const double* tinv, const int32_t* lane_target, const double* q, int64_t lanes,
-                   double* damping, double* cost, void* stream) {
+                   const double* tinv, const int32_t* lane_target, const double* q, const double* base_state,
+                   int64_t lanes, double* damping, double* cost, void* stream) {
   if (lanes > 0 && (!tinv || !lane_target || !q || !damping || !cost))
     return fail(KOP_EINVAL, "null array argument");
   LaneLaunch L{};
@@ -584,14 +622,15 @@ int kop_lane_start(const KopModel* m, int32_t link, int32_t precision, const dou
   L.tinv = tinv;
   L.lane_target = lane_target;
   L.q_in = q;
+  L.base_in = base_state;
   L.lam = damping;
   L.cost = cost;
   return lane_call(m, link, precision, weights, L, lanes, stream);
 }
 
 int kop_lane_run(const KopModel* m, int32_t link, int32_t precision, const double* weights, const double* tinv,
-                 const int32_t* lane_target, int64_t lanes, int32_t steps, double* q, double* damping,
-                 double* cost, double* history, void* stream) {
+                 const int32_t* lane_target, int64_t lanes, int32_t steps, double* q, double* base_state,
+                 double* damping, double* cost, double* history, void* stream) {
   if (steps < 0) return fail(KOP_EINVAL, "negative step count");
   if (lanes > 0 && (!tinv || !lane_target || !q || !damping || !cost))
     return fail(KOP_EINVAL, "null array argument");
@@ -601,6 +640,7 @@ int kop_lane_run(const KopModel* m, int32_t link, int32_t precision, const doubl
   L.lane_target = lane_target;
   L.steps = steps;
   L.q_io = q;
+  L.base_io = base_state;
   L.lam = damping;
   L.cost = cost;
   L.hist = history;

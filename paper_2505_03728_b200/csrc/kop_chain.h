@@ -43,6 +43,7 @@ template <typename T, int NQ>
 struct CostParams {
   T lower[NQ], upper[NQ], rest[NQ];
   T w_pos, w_ori, w_lim, w_rest;  // beam.py:95-100 row weights
+  T w_base;                       // base regularisation rows (beam.py:98-99)
 };
 
 // Full-tree tables for the generic FK kernel (robot.py:404-448 semantics,

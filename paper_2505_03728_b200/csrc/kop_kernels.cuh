@@ -9,19 +9,24 @@
 
 namespace kop {
 
-// Compiled (NQ actuated, K chain joints, identity column map) shapes.  ID
-// shapes serve serial chains whose moving joints are exactly the actuated
-// joints (Panda, planar 2R, UR-class); the generic shape serves trees, mimic
-// joints and sub-chains with K <= NQ <= 8.
-#define KOP_FOR_EACH_SHAPE(X) \
-  X(float, 2, 2, true)        \
-  X(double, 2, 2, true)       \
-  X(float, 6, 6, true)        \
-  X(double, 6, 6, true)       \
-  X(float, 7, 7, true)        \
-  X(double, 7, 7, true)       \
-  X(float, 8, 8, false)       \
-  X(double, 8, 8, false)
+// Compiled (T, NQ actuated, K chain joints, identity column map, SE(2) base)
+// shapes.  ID shapes serve serial chains whose moving joints are exactly the
+// actuated joints (Panda, planar 2R, UR-class); the generic shape serves
+// trees, mimic joints and sub-chains with K <= NQ <= 8 (smaller robots are
+// padded to NQ = 8 exactly, see kop_capi.cu:make_costs).
+#define KOP_FOR_EACH_SHAPE(X)   \
+  X(float, 2, 2, true, false)   \
+  X(double, 2, 2, true, false)  \
+  X(float, 6, 6, true, false)   \
+  X(double, 6, 6, true, false)  \
+  X(float, 7, 7, true, false)   \
+  X(double, 7, 7, true, false)  \
+  X(float, 8, 8, false, false)  \
+  X(double, 8, 8, false, false) \
+  X(float, 7, 7, true, true)    \
+  X(double, 7, 7, true, true)   \
+  X(float, 8, 8, false, true)   \
+  X(double, 8, 8, false, true)
 
 struct BeamLaunch {
   const double* targets;
@@ -31,9 +36,8 @@ struct BeamLaunch {
   int steps1, steps2, keep;
   double pos_tol, rot_tol;
   void* workspace;
-  double *q_out, *cost_out, *hist_out, *pos_err, *rot_err;
+  double *q_out, *base_out, *cost_out, *hist_out, *pos_err, *rot_err;
   uint8_t* success;
-  bool twopass;
   int stages;  // bit 0: stage 1 (seeds + prune), bit 1: stage 2 (survivors + winner)
 };
 
@@ -44,18 +48,19 @@ struct LaneLaunch {
   const double* tinv;
   const int32_t* lane_target;
   const double* q_in;
+  const double* base_in;  // [lanes*3] (x, y, angle) when the base is optimised
   int64_t lanes;
   int steps;
-  double *q_io, *lam, *cost, *hist, *res, *jac;
+  double *q_io, *base_io, *lam, *cost, *hist, *res, *jac;
 };
 
-template <typename T, int NQ, int K, bool ID>
-cudaError_t launch_beam(const ChainParams<T, K>& C, const CostParams<T, NQ>& W,
-                        const ChainParams<double, K>& Cd, const BeamLaunch& L, cudaStream_t st);
+template <class G>
+cudaError_t launch_beam(const ChainParams<typename G::T, G::K>& C, const CostParams<typename G::T, G::NQ>& W,
+                        const ChainParams<double, G::K>& Cd, const BeamLaunch& L, cudaStream_t st);
 
-template <typename T, int NQ, int K, bool ID>
-cudaError_t launch_lane(const ChainParams<T, K>& C, const CostParams<T, NQ>& W, const LaneLaunch& L,
-                        cudaStream_t st);
+template <class G>
+cudaError_t launch_lane(const ChainParams<typename G::T, G::K>& C, const CostParams<typename G::T, G::NQ>& W,
+                        const LaneLaunch& L, cudaStream_t st);
 
 // kop_aux.cu
 cudaError_t launch_fk_tree(const TreeParams& P, int precision, const double* q, int64_t B,

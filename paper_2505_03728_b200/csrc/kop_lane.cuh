@@ -95,8 +95,19 @@ __device__ __forceinline__ T pick(const T (&q)[NQ], int idx) {
   return v;
 }
 
+// Compile-time lane configuration: scalar type, actuated joints NQ, chain
+// joints K, identity column map, and the optional SE(2) mobile base (three
+// extra tangent dimensions after the joints, beam.py:98-102).
+template <typename T_, int NQ_, int K_, bool ID_, bool BASE_>
+struct Cfg {
+  using T = T_;
+  static constexpr int NQ = NQ_, K = K_, ND = NQ_ + (BASE_ ? 3 : 0);
+  static constexpr bool ID = ID_, BASE = BASE_;
+};
+
 // ---------------------------------------------------------------------------
-// Pose residual (6 weighted rows) and, if JAC, its weighted Jacobian rows.
+// Pose residual (6 weighted rows) and, if JAC, its weighted Jacobian rows
+// over the ND tangent columns.
 // ID: the chain's moving joints are exactly the actuated joints in order with
 // unit multipliers (qcol[k] == k), so columns need no scatter.
 //
@@ -107,37 +118,59 @@ __device__ __forceinline__ T pick(const T (&q)[NQ], int idx) {
 // (EE-frame) Jacobian column is  ang = R_S^T z = row 2 of R_S,
 // lin = R_S^T (z x p_S) = -p_y row0 + p_x row1  -- the same columns as
 // beam.py:142-146 (R^T J_geom) without any per-joint world state.
+//
+// Mobile base (beam.py:104-112, 167-179): the SE(2) base B = (Rz(a), (x,y,0))
+// left-multiplies the arm; its right-multiplicative tangent (vx, vy, w) acts
+// like a prismatic-x, prismatic-y and revolute-z joint at the arm root, so its
+// columns Jr^-1 Ad(FK^-1) E_se2 are read off S_0 exactly like joint columns.
 // ---------------------------------------------------------------------------
 template <typename T>
 __device__ __forceinline__ quat<T> zmul_left(T c, T s, const quat<T>& b) {  // (c,0,0,s) * b
   return {c * b.w - s * b.z, c * b.x - s * b.y, c * b.y + s * b.x, c * b.z + s * b.w};
 }
 
-template <typename T, int NQ, int K, bool ID, bool JAC>
-__device__ __forceinline__ void pose_rows(const ChainParams<T, K>& C, const CostParams<T, NQ>& W,
-                                          const TargetInv<T>& tg, const T (&q)[NQ], T (&r)[6],
-                                          T (&J)[6][NQ]) {
+// body columns of S = (sq, sp) for a revolute-z / prismatic-z joint at S's origin
+template <typename T>
+__device__ __forceinline__ void s_columns(const quat<T>& sq, const vec3<T>& sp, T (&rev)[6], T (&px)[3],
+                                          T (&py)[3], T (&pz)[3]) {
+  const T x2 = sq.x + sq.x, y2 = sq.y + sq.y, z2 = sq.z + sq.z;
+  const T r00 = T(1) - (sq.y * y2 + sq.z * z2), r01 = sq.x * y2 - sq.w * z2, r02 = sq.x * z2 + sq.w * y2;
+  const T r10 = sq.x * y2 + sq.w * z2, r11 = T(1) - (sq.x * x2 + sq.z * z2), r12 = sq.y * z2 - sq.w * x2;
+  const T r20 = sq.x * z2 - sq.w * y2, r21 = sq.y * z2 + sq.w * x2, r22 = T(1) - (sq.x * x2 + sq.y * y2);
+  rev[0] = sp.x * r10 - sp.y * r00;
+  rev[1] = sp.x * r11 - sp.y * r01;
+  rev[2] = sp.x * r12 - sp.y * r02;
+  rev[3] = r20; rev[4] = r21; rev[5] = r22;
+  px[0] = r00; px[1] = r01; px[2] = r02;
+  py[0] = r10; py[1] = r11; py[2] = r12;
+  pz[0] = r20; pz[1] = r21; pz[2] = r22;
+}
+
+template <class G, bool JAC>
+__device__ __forceinline__ void pose_rows(const ChainParams<typename G::T, G::K>& C,
+                                          const CostParams<typename G::T, G::NQ>& W,
+                                          const TargetInv<typename G::T>& tg, const typename G::T (&q)[G::NQ],
+                                          const typename G::T (&base)[3], typename G::T (&r)[6],
+                                          typename G::T (&J)[6][G::ND]) {
+  using T = typename G::T;
+  constexpr int K = G::K, NQ = G::NQ, ND = G::ND;
+  constexpr bool ID = G::ID;
   quat<T> sq{C.eq[0], C.eq[1], C.eq[2], C.eq[3]};
   vec3<T> sp{C.ep[0], C.ep[1], C.ep[2]};
-  T col[K][6];
+  T col[K + (G::BASE ? 3 : 0)][6];
 #pragma unroll
   for (int k = K - 1; k >= 0; --k) {
     if (ID || k < C.k) {
       const bool pri = !ID && C.prismatic[k];
       if (JAC) {
-        const T x2 = sq.x + sq.x, y2 = sq.y + sq.y, z2 = sq.z + sq.z;
-        // rows of R(sq)
-        const T r20 = sq.x * z2 - sq.w * y2, r21 = sq.y * z2 + sq.w * x2, r22 = T(1) - (sq.x * x2 + sq.y * y2);
+        T rev[6], px[3], py[3], pz[3];
+        s_columns(sq, sp, rev, px, py, pz);
         if (pri) {
-          col[k][0] = r20; col[k][1] = r21; col[k][2] = r22;
+          col[k][0] = pz[0]; col[k][1] = pz[1]; col[k][2] = pz[2];
           col[k][3] = T(0); col[k][4] = T(0); col[k][5] = T(0);
         } else {
-          const T r00 = T(1) - (sq.y * y2 + sq.z * z2), r01 = sq.x * y2 - sq.w * z2, r02 = sq.x * z2 + sq.w * y2;
-          const T r10 = sq.x * y2 + sq.w * z2, r11 = T(1) - (sq.x * x2 + sq.z * z2), r12 = sq.y * z2 - sq.w * x2;
-          col[k][0] = sp.x * r10 - sp.y * r00;
-          col[k][1] = sp.x * r11 - sp.y * r01;
-          col[k][2] = sp.x * r12 - sp.y * r02;
-          col[k][3] = r20; col[k][4] = r21; col[k][5] = r22;
+#pragma unroll
+          for (int m = 0; m < 6; ++m) col[k][m] = rev[m];
         }
       }
       const T th = ID ? q[k] : pick(q, C.qcol[k]) * C.mult[k] + C.offset[k];
@@ -156,7 +189,25 @@ __device__ __forceinline__ void pose_rows(const ChainParams<T, K>& C, const Cost
             C.tp[k][2] + (C.tr[k][2][0] * sp.x + C.tr[k][2][1] * sp.y + C.tr[k][2][2] * sp.z)};
     }
   }
-  // pose error T_t^-1 * FK  (beam.py:119-121); sq, sp = world EE pose
+  if (G::BASE) {
+    if (JAC) {  // base tangent (vx, vy, w): prismatic x, prismatic y, revolute z at the arm root
+      T rev[6], px[3], py[3], pz[3];
+      s_columns(sq, sp, rev, px, py, pz);
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        col[K][m] = px[m]; col[K][3 + m] = T(0);
+        col[K + 1][m] = py[m]; col[K + 1][3 + m] = T(0);
+      }
+#pragma unroll
+      for (int m = 0; m < 6; ++m) col[K + 2][m] = rev[m];
+    }
+    T s, c;  // compose the base: B * S_0 (beam.py:104-112)
+    sincos_t(T(0.5) * base[2], &s, &c);
+    sq = zmul_left(c, s, sq);
+    const T c2 = c * c - s * s, s2 = T(2) * c * s;
+    sp = {c2 * sp.x - s2 * sp.y + base[0], s2 * sp.x + c2 * sp.y + base[1], sp.z};
+  }
+  // pose error T_t^-1 * (B) * FK  (beam.py:119-121)
   const quat<T> e_q = qmul(tg.q, sq);
   const vec3<T> et = qrot(tg.q, sp);
   const vec3<T> e_t{tg.t.x + et.x, tg.t.y + et.y, tg.t.z + et.z};
@@ -169,7 +220,7 @@ __device__ __forceinline__ void pose_rows(const ChainParams<T, K>& C, const Cost
   r[5] = W.w_ori * xi.phi.z;
   if (!JAC) return;
 
-  // J_pose = diag(w) Jr^-1(xi) [lin; ang]   (beam.py:142-156)
+  // J_pose = diag(w) Jr^-1(xi) [lin; ang]   (beam.py:142-156, 170)
   const JrInv<T> jr = se3_jr_inv(xi);
   mat3<T> At, Bt, Ab;
 #pragma unroll
@@ -187,14 +238,15 @@ __device__ __forceinline__ void pose_rows(const ChainParams<T, K>& C, const Cost
       for (int c = 0; c < NQ; ++c) J[m][c] = T(0);
   }
 #pragma unroll
-  for (int k = 0; k < K; ++k) {
-    if (ID || k < C.k) {
+  for (int k = 0; k < K + (G::BASE ? 3 : 0); ++k) {
+    if (ID || k >= K || k < C.k) {
       const vec3<T> lin{col[k][0], col[k][1], col[k][2]}, ang{col[k][3], col[k][4], col[k][5]};
       const vec3<T> t1 = mul(At, lin), t2 = mul(Bt, ang), b1 = mul(Ab, ang);
       const T cj[6] = {t1.x + t2.x, t1.y + t2.y, t1.z + t2.z, b1.x, b1.y, b1.z};
-      if (ID) {
+      if (ID || k >= K) {
+        const int c = k >= K ? NQ + (k - K) : k;
 #pragma unroll
-        for (int m = 0; m < 6; ++m) J[m][k] = cj[m];
+        for (int m = 0; m < 6; ++m) J[m][c] = cj[m];
       } else {
         const int qc = C.qcol[k];
         const T mu = C.mult[k];
@@ -222,14 +274,30 @@ __device__ __forceinline__ void diag_rows(const CostParams<T, NQ>& W, const T (&
   }
 }
 
-// Cost only (candidate evaluation in the reference-structured step).
-template <typename T, int NQ, int K, bool ID>
-__device__ __forceinline__ T lane_cost(const ChainParams<T, K>& C, const CostParams<T, NQ>& W,
-                                       const TargetInv<T>& tg, const T (&q)[NQ]) {
-  T r[6], J[6][NQ];
-  pose_rows<T, NQ, K, ID, false>(C, W, tg, q, r, J);
+// Weighted residual stack, its cost and (JAC) the normal equations
+// A = J^T J (packed lower, ND x ND), g = J^T r.  Rows: pose (6, dense), limit
+// and rest (diagonal), base regularisation (x, y, a) * w_base whose Jacobian
+// [[R(a), 0], [0, 1]] (beam.py:171-178) is orthogonal, so it adds w_base^2 I
+// to A and w_base R^T-rotated residuals to g.
+template <class G, bool JAC>
+__device__ __forceinline__ typename G::T lane_eval(const ChainParams<typename G::T, G::K>& C,
+                                                   const CostParams<typename G::T, G::NQ>& W,
+                                                   const TargetInv<typename G::T>& tg,
+                                                   const typename G::T (&q)[G::NQ], const typename G::T (&base)[3],
+                                                   typename G::T (&A)[Tri<G::ND>::size],
+                                                   typename G::T (&g)[G::ND]) {
+  using T = typename G::T;
+  constexpr int NQ = G::NQ, ND = G::ND;
+  T r[6], J[6][ND];
+  pose_rows<G, JAC>(C, W, tg, q, base, r, J);
   T rl[NQ], gl[NQ], rr[NQ];
   diag_rows(W, q, rl, gl, rr);
+  T rb[3] = {T(0), T(0), T(0)};
+  if (G::BASE) {
+    rb[0] = W.w_base * base[0];
+    rb[1] = W.w_base * base[1];
+    rb[2] = W.w_base * base[2];
+  }
   T c = T(0);
 #pragma unroll
   for (int m = 0; m < 6; ++m) c += r[m] * r[m];
@@ -237,41 +305,39 @@ __device__ __forceinline__ T lane_cost(const ChainParams<T, K>& C, const CostPar
   for (int i = 0; i < NQ; ++i) c += rl[i] * rl[i];
 #pragma unroll
   for (int i = 0; i < NQ; ++i) c += rr[i] * rr[i];
-  return c;
-}
-
-// Cost plus normal equations A = J^T J (packed lower), g = J^T r.
-template <typename T, int NQ, int K, bool ID>
-__device__ __forceinline__ T lane_normal(const ChainParams<T, K>& C, const CostParams<T, NQ>& W,
-                                         const TargetInv<T>& tg, const T (&q)[NQ],
-                                         T (&A)[Tri<NQ>::size], T (&g)[NQ]) {
-  T r[6], J[6][NQ];
-  pose_rows<T, NQ, K, ID, true>(C, W, tg, q, r, J);
-  T rl[NQ], gl[NQ], rr[NQ];
-  diag_rows(W, q, rl, gl, rr);
-  T c = T(0);
+  if (G::BASE) c += rb[0] * rb[0] + rb[1] * rb[1] + rb[2] * rb[2];
+  if (!JAC) return c;
 #pragma unroll
-  for (int m = 0; m < 6; ++m) c += r[m] * r[m];
+  for (int i = 0; i < ND; ++i) {
 #pragma unroll
-  for (int i = 0; i < NQ; ++i) c += rl[i] * rl[i];
-#pragma unroll
-  for (int i = 0; i < NQ; ++i) c += rr[i] * rr[i];
-#pragma unroll
-  for (int i = 0; i < NQ; ++i) {
-#pragma unroll
-    for (int j = 0; j < NQ; ++j) {
+    for (int j = 0; j < ND; ++j) {
       if (j <= i) {
         T a = T(0);
 #pragma unroll
         for (int m = 0; m < 6; ++m) a += J[m][i] * J[m][j];
-        A[Tri<NQ>::at(i, j)] = a;
+        A[Tri<ND>::at(i, j)] = a;
       }
     }
-    A[Tri<NQ>::at(i, i)] += gl[i] * gl[i] + W.w_rest * W.w_rest;
     T s = T(0);
 #pragma unroll
     for (int m = 0; m < 6; ++m) s += J[m][i] * r[m];
-    g[i] = s + gl[i] * rl[i] + W.w_rest * rr[i];
+    g[i] = s;
+  }
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) {
+    A[Tri<ND>::at(i, i)] += gl[i] * gl[i] + W.w_rest * W.w_rest;
+    g[i] += gl[i] * rl[i] + W.w_rest * rr[i];
+  }
+  if (G::BASE) {
+    const T wb2 = W.w_base * W.w_base;
+    T sa, ca;
+    sincos_t(T(0.5) * base[2], &sa, &ca);
+    const T cs = ca * ca - sa * sa, sn = T(2) * ca * sa;  // cos a, sin a
+#pragma unroll
+    for (int i = NQ; i < ND; ++i) A[Tri<ND>::at(i, i)] += wb2;
+    g[NQ] += W.w_base * (cs * rb[0] + sn * rb[1]);
+    g[NQ + 1] += W.w_base * (-sn * rb[0] + cs * rb[1]);
+    g[NQ + 2] += W.w_base * rb[2];
   }
   return c;
 }
@@ -336,42 +402,83 @@ __device__ __forceinline__ bool damped_solve(const T (&A)[Tri<NQ>::size], const 
   return ok;
 }
 
-// Per-lane LM state.  The normal equations AT q (packed lower A, then g)
-// live in shared memory, element e of this lane at Ag[e * stride]: the fused
-// step keeps them from the accepted candidate's evaluation instead of
-// recomputing FK, and holding them outside the register file keeps the lane
-// at <= 128 registers (2 CTAs of 256 threads per SM).
-template <typename T, int NQ>
+// Per-lane LM state.  The normal equations AT the current iterate (packed
+// lower A, then g) live in shared memory, element e of this lane at
+// Ag[e * stride]: the fused step keeps them from the accepted candidate's
+// evaluation instead of recomputing FK, and holding them outside the register
+// file keeps the lane at <= 128 registers (2 CTAs of 256 threads per SM).
+template <class G>
 struct LaneState {
-  T q[NQ];
-  T lam, cost;
-  T* Ag;
+  typename G::T q[G::NQ];
+  typename G::T base[3];  // (x, y, angle) of the SE(2) base when G::BASE
+  typename G::T lam, cost;
+  typename G::T* Ag;
   int stride;
 };
 
 // STRIDE: the block size when it is a compile-time constant (then every
 // shared-memory access is base + immediate), 0 = use s.stride.
-template <int STRIDE, typename T, int NQ>
-__device__ __forceinline__ void store_normal(const LaneState<T, NQ>& s, const T (&A)[Tri<NQ>::size],
-                                             const T (&g)[NQ]) {
+template <int STRIDE, class G>
+__device__ __forceinline__ void store_normal(const LaneState<G>& s, const typename G::T (&A)[Tri<G::ND>::size],
+                                             const typename G::T (&g)[G::ND]) {
   const int st = STRIDE ? STRIDE : s.stride;
 #pragma unroll
-  for (int i = 0; i < Tri<NQ>::size; ++i) s.Ag[i * st] = A[i];
+  for (int i = 0; i < Tri<G::ND>::size; ++i) s.Ag[i * st] = A[i];
 #pragma unroll
-  for (int i = 0; i < NQ; ++i) s.Ag[(Tri<NQ>::size + i) * st] = g[i];
+  for (int i = 0; i < G::ND; ++i) s.Ag[(Tri<G::ND>::size + i) * st] = g[i];
 }
 
-template <int STRIDE, typename T, int NQ>
-__device__ __forceinline__ void load_normal(const LaneState<T, NQ>& s, T (&A)[Tri<NQ>::size], T (&g)[NQ]) {
+template <int STRIDE, class G>
+__device__ __forceinline__ void load_normal(const LaneState<G>& s, typename G::T (&A)[Tri<G::ND>::size],
+                                            typename G::T (&g)[G::ND]) {
   const int st = STRIDE ? STRIDE : s.stride;
 #pragma unroll
-  for (int i = 0; i < Tri<NQ>::size; ++i) A[i] = s.Ag[i * st];
+  for (int i = 0; i < Tri<G::ND>::size; ++i) A[i] = s.Ag[i * st];
 #pragma unroll
-  for (int i = 0; i < NQ; ++i) g[i] = s.Ag[(Tri<NQ>::size + i) * st];
+  for (int i = 0; i < G::ND; ++i) g[i] = s.Ag[(Tri<G::ND>::size + i) * st];
 }
 
 template <typename T>
 __device__ __forceinline__ T inf_t() { return T(INFINITY); }
+
+// wrap to (-pi, pi] (liegroups.py:270-273, np.mod semantics)
+template <typename T>
+__device__ __forceinline__ T wrap_angle_t(T a) {
+  const T two_pi = T(6.283185307179586476925286766559);
+  const T x = a + T(3.1415926535897932384626433832795);
+  T w = x - two_pi * floor(x / two_pi) - T(3.1415926535897932384626433832795);
+  return w == -T(3.1415926535897932384626433832795) ? T(3.1415926535897932384626433832795) : w;
+}
+
+// SE(2) retraction of the base (beam.py:216-221, liegroups.py:276-287):
+// angle' = wrap(a + wrap(w)); xy' = xy + R(a) V(w) v.  float evaluates
+// (1 - cos w)/w as 2 sin^2(w/2)/w (the reference form cancels in float).
+template <typename T>
+__device__ __forceinline__ void base_retract(const T (&b)[3], T vx, T vy, T w, T (&out)[3]) {
+  T s, c;
+  if (fabs(w) < T(1e-7)) {
+    s = T(1) - w * w / T(6);
+    c = T(0.5) * w - w * w * w / T(24);
+  } else {
+    T sw, cw;
+    sincos_t(w, &sw, &cw);
+    s = sw / w;
+    if (sizeof(T) == 4) {
+      T sh, ch;
+      sincos_t(T(0.5) * w, &sh, &ch);
+      c = T(2) * sh * sh / w;
+    } else {
+      c = (T(1) - cw) / w;
+    }
+  }
+  const T tx = s * vx - c * vy, ty = c * vx + s * vy;
+  T sa, ca;
+  sincos_t(T(0.5) * b[2], &sa, &ca);
+  const T cs = ca * ca - sa * sa, sn = T(2) * ca * sa;
+  out[0] = b[0] + (cs * tx - sn * ty);
+  out[1] = b[1] + (sn * tx + cs * ty);
+  out[2] = wrap_angle_t(b[2] + wrap_angle_t(w));
+}
 
 // One LM iteration of a lane, or its start (beam.py:182-196) when mode != 0.
 //   mode 0  one proposal (beam.py:201-239), fused form: the candidate's
@@ -385,24 +492,34 @@ __device__ __forceinline__ T inf_t() { return T(INFINITY); }
 //           re-derived at q, beam.py:202).
 // A single inlined evaluation serves all three (one copy of the ~2K-instruction
 // body per kernel keeps the hot loop inside the instruction cache).
-template <typename T, int NQ, int K, bool ID, int STRIDE = 0>
-__device__ __forceinline__ void lm_iter(const ChainParams<T, K>& C, const CostParams<T, NQ>& W,
-                                        const TargetInv<T>& tg, LaneState<T, NQ>& s, int mode) {
-  T d[NQ];
+template <class G, int STRIDE = 0>
+__device__ __forceinline__ void lm_iter(const ChainParams<typename G::T, G::K>& C,
+                                        const CostParams<typename G::T, G::NQ>& W,
+                                        const TargetInv<typename G::T>& tg, LaneState<G>& s, int mode) {
+  using T = typename G::T;
+  constexpr int NQ = G::NQ, ND = G::ND;
+  T d[ND];
   bool ok = true;
   if (mode == 0) {
-    T A[Tri<NQ>::size], g[NQ];
+    T A[Tri<ND>::size], g[ND];
     load_normal<STRIDE>(s, A, g);
-    ok = damped_solve<T, NQ>(A, g, s.lam, d);
+    ok = damped_solve<T, ND>(A, g, s.lam, d);
   } else {
 #pragma unroll
-    for (int i = 0; i < NQ; ++i) d[i] = T(0);
+    for (int i = 0; i < ND; ++i) d[i] = T(0);
   }
-  T qn[NQ];
+  T qn[NQ], bn[3];
 #pragma unroll
   for (int i = 0; i < NQ; ++i) qn[i] = s.q[i] + (ok ? d[i] : T(0));
-  T An[Tri<NQ>::size], gn[NQ];
-  const T raw = lane_normal<T, NQ, K, ID>(C, W, tg, qn, An, gn);
+  if (G::BASE) {
+    if (mode == 0 && ok) {
+      base_retract(s.base, d[NQ], d[NQ + 1], d[NQ + 2], bn);
+    } else {
+      bn[0] = s.base[0]; bn[1] = s.base[1]; bn[2] = s.base[2];
+    }
+  }
+  T An[Tri<ND>::size], gn[ND];
+  const T raw = lane_eval<G, true>(C, W, tg, qn, bn, An, gn);
   const T cn = finite_t(raw) ? raw : inf_t<T>();
   const bool acc = mode != 0 || (ok && (cn < s.cost));
   if (acc) store_normal<STRIDE>(s, An, gn);  // one store site for start and accept
@@ -413,32 +530,9 @@ __device__ __forceinline__ void lm_iter(const ChainParams<T, K>& C, const CostPa
   if (acc) {
 #pragma unroll
     for (int i = 0; i < NQ; ++i) s.q[i] = qn[i];
-    s.cost = cn;
-    s.lam = tmax(s.lam * T(BeamConsts::damping_down), T(BeamConsts::damping_min));
-  } else {
-    s.lam = tmin(s.lam * T(BeamConsts::damping_up), T(BeamConsts::damping_max));
-  }
-}
-
-// Reference-structured step (two FK per step, beam.py:202 + :224): kept for
-// A/B measurement of the fused form.
-template <typename T, int NQ, int K, bool ID>
-__device__ __forceinline__ void lm_step_twopass(const ChainParams<T, K>& C,
-                                                const CostParams<T, NQ>& W,
-                                                const TargetInv<T>& tg, LaneState<T, NQ>& s) {
-  T A[Tri<NQ>::size], g[NQ];
-  lane_normal<T, NQ, K, ID>(C, W, tg, s.q, A, g);
-  T d[NQ];
-  const bool ok = damped_solve<T, NQ>(A, g, s.lam, d);
-  T qn[NQ];
-#pragma unroll
-  for (int i = 0; i < NQ; ++i) qn[i] = s.q[i] + (ok ? d[i] : T(0));
-  T cn = lane_cost<T, NQ, K, ID>(C, W, tg, qn);
-  if (!finite_t(cn)) cn = inf_t<T>();
-  const bool acc = ok && (cn < s.cost);
-  if (acc) {
-#pragma unroll
-    for (int i = 0; i < NQ; ++i) s.q[i] = qn[i];
+    if (G::BASE) {
+      s.base[0] = bn[0]; s.base[1] = bn[1]; s.base[2] = bn[2];
+    }
     s.cost = cn;
     s.lam = tmax(s.lam * T(BeamConsts::damping_down), T(BeamConsts::damping_min));
   } else {

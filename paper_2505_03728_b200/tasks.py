@@ -22,7 +22,6 @@ import numpy as np
 from . import _device as dv
 from . import costs as ck
 from ._lib import KopIkParams, check, lib
-from .errors import UnsupportedFeatureError
 from .liegroups import Transform2, Transform3
 from .robot import RobotModel, _precision
 from .solver import SolveReport, VariableSet
@@ -116,7 +115,8 @@ def targets_to_array(targets) -> np.ndarray:
 
 @dataclass
 class BeamBatch:
-    """Per-target IK-Beam outputs (device tensors or host arrays)."""
+    """Per-target IK-Beam outputs (device tensors or host arrays).  ``base`` is
+    (B, 3) (x, y, angle) with an optimised mobile base, else None."""
 
     q: object
     cost: object
@@ -124,10 +124,13 @@ class BeamBatch:
     pos_error: object
     rot_error: object
     success: object
+    base: object = None
+
+    FIELDS = ("q", "cost", "history", "pos_error", "rot_error", "success", "base")
 
     def cpu(self) -> "BeamBatch":
         f = lambda x: x.cpu().numpy() if hasattr(x, "cpu") else x
-        return BeamBatch(*(f(getattr(self, k)) for k in ("q", "cost", "history", "pos_error", "rot_error", "success")))
+        return BeamBatch(*(f(getattr(self, k)) for k in self.FIELDS))
 
 
 class IkBeamSolver:
@@ -141,7 +144,7 @@ class IkBeamSolver:
     def __init__(self, model: RobotModel, link: str, weights: ck.CostWeights | None = None, seeds: int = 64,
                  total_steps: int = 16, prune_after: int = 6, keep: int = 4, rng_seed: int = 0,
                  success_pos_tol: float = 0.005, success_rot_tol: float = 0.05, precision="fp32",
-                 seed_configurations=None):
+                 seed_configurations=None, optimize_base: bool = False, base_reg_weight: float = 0.0):
         if not 0 < prune_after < total_steps:
             raise ValueError("need 0 < prune_after < total_steps")
         if not 1 <= keep <= seeds:
@@ -150,8 +153,10 @@ class IkBeamSolver:
         self.link_idx = model.link_index(link)
         w = (weights or ck.CostWeights()).ik_row_weights()
         self.total_steps = total_steps
+        self.optimize_base = bool(optimize_base)
         self.params = KopIkParams(w[0], w[1], w[2], w[3], seeds, total_steps, prune_after, keep,
-                                  success_pos_tol, success_rot_tol, _precision(precision))
+                                  success_pos_tol, success_rot_tol, _precision(precision),
+                                  1 if self.optimize_base else 0, float(base_reg_weight))
         if seed_configurations is not None:
             self.seeds = dv.to_dev(np.asarray(seed_configurations, dtype=float).reshape(seeds, model.actuated_count))
         else:
@@ -171,7 +176,8 @@ class IkBeamSolver:
         t = dv.require_cuda()
         n = self.model.actuated_count
         return BeamBatch(dv.empty((batch, n)), dv.empty(batch), dv.empty((batch, self.total_steps + 1)),
-                         dv.empty(batch), dv.empty(batch), t.empty(batch, dtype=t.uint8, device="cuda"))
+                         dv.empty(batch), dv.empty(batch), t.empty(batch, dtype=t.uint8, device="cuda"),
+                         dv.empty((batch, 3)) if self.optimize_base else None)
 
     def solve_device(self, targets, out: BeamBatch | None = None, history: bool = True,
                      stages: int = 3) -> BeamBatch:
@@ -184,7 +190,8 @@ class IkBeamSolver:
         ws = self.workspace(b)
         check(lib().kop_ik_beam_stage(self.model._handle, self.link_idx, C.byref(self.params), int(stages),
                                       dv.ptr(targets), b, dv.ptr(self.seeds), dv.ptr(ws), ws.numel(),
-                                      dv.ptr(out.q), dv.ptr(out.cost), dv.ptr(out.history) if history else None,
+                                      dv.ptr(out.q), dv.ptr(out.base), dv.ptr(out.cost),
+                                      dv.ptr(out.history) if history else None,
                                       dv.ptr(out.pos_error), dv.ptr(out.rot_error), dv.ptr(out.success),
                                       dv.stream_handle()), "kop_ik_beam")
         return out
@@ -198,33 +205,48 @@ class IkBeamSolver:
 def solve_ik_beam_batch(model: RobotModel, link: str, targets, weights: ck.CostWeights | None = None,
                         seeds: int = 64, total_steps: int = 16, prune_after: int = 6, keep: int = 4,
                         rng_seed: int = 0, precision="fp32", success_pos_tol: float = 0.005,
-                        success_rot_tol: float = 0.05) -> BeamBatch:
+                        success_rot_tol: float = 0.05, optimize_base: bool = False,
+                        base_reg_weight: float = 0.0) -> BeamBatch:
     """IK-Beam over B targets at once (host arrays in and out)."""
     solver = IkBeamSolver(model, link, weights, seeds, total_steps, prune_after, keep, rng_seed,
-                          success_pos_tol, success_rot_tol, precision)
+                          success_pos_tol, success_rot_tol, precision, optimize_base=optimize_base,
+                          base_reg_weight=base_reg_weight)
     return solver.solve(targets)
 
 
-def solve_ik_beam(req: IkRequest) -> IkResult:
-    """Multi-seed IK with mid-optimisation pruning; never raises on unreachable targets."""
-    if req.optimize_base:
-        return solve_ik_mobile(req)
+def _result(req: IkRequest, res: BeamBatch, i: int = 0) -> IkResult:
+    q = res.q[i].copy()
+    hist = [float(h) for h in res.history[i]]
+    base = None
+    if res.base is not None:
+        base = Transform2(float(res.base[i, 2]), res.base[i, :2].copy())
+    values = VariableSet.of(q=q) if base is None else VariableSet.of(q=q, base=base)
+    report = SolveReport(final_values=values, initial_cost=hist[0], final_cost=float(res.cost[i]),
+                         iterations_run=req.total_steps, termination="max_iterations", cost_history=hist)
+    return IkResult(q=q, base=base, pos_error=float(res.pos_error[i]), rot_error=float(res.rot_error[i]),
+                    success=bool(res.success[i]), report=report)
+
+
+def _solve(req: IkRequest, use_base: bool) -> IkResult:
     res = solve_ik_beam_batch(req.model, req.target_link, req.target_pose, req.weights, req.seeds,
                               req.total_steps, req.prune_after, req.keep, req.rng_seed, req.precision,
-                              req.success_pos_tol, req.success_rot_tol)
-    q = res.q[0].copy()
-    hist = [float(h) for h in res.history[0]]
-    report = SolveReport(final_values=VariableSet.of(q=q), initial_cost=hist[0], final_cost=float(res.cost[0]),
-                         iterations_run=req.total_steps, termination="max_iterations", cost_history=hist)
-    return IkResult(q=q, base=None, pos_error=float(res.pos_error[0]), rot_error=float(res.rot_error[0]),
-                    success=bool(res.success[0]), report=report)
+                              req.success_pos_tol, req.success_rot_tol, optimize_base=use_base,
+                              base_reg_weight=req.base_reg_weight if use_base else 0.0)
+    return _result(req, res)
+
+
+def solve_ik_beam(req: IkRequest) -> IkResult:
+    """Multi-seed IK with mid-optimisation pruning (tasks.py:164-166); never raises
+    on unreachable targets.  Like the reference, the base is never optimised here."""
+    return _solve(req, use_base=False)
 
 
 def solve_ik_mobile(req: IkRequest) -> IkResult:
-    """Mobile-base IK (tasks.py:169-180).  A pinned base reduces to arm-only IK."""
+    """IK with the SE(2) base pose as an extra variable (tasks.py:169-180).  Each
+    seed starts with the base at identity; base_reg_weight >= BASE_PINNED drops
+    the base variable, reproducing solve_ik_beam exactly."""
     if req.base_reg_weight >= BASE_PINNED:
-        import dataclasses
-        res = solve_ik_beam(dataclasses.replace(req, optimize_base=False))
-        res.base = Transform2.identity()
-        return res
-    raise UnsupportedFeatureError("mobile-base lanes (SE(2) variable) are not compiled in this build yet")
+        result = _solve(req, use_base=False)
+        result.base = Transform2.identity()
+        return result
+    return _solve(req, use_base=True)

@@ -109,6 +109,39 @@ def main():
         pp.append(res.q)
     g["beam_p2r_5_hist"], g["beam_p2r_5_q"] = np.array(ph), np.array(pp)
 
+    # --- mobile base (beam.py:98-112, 167-179, 216-221; tasks.py:169-180) ----
+    from kinoptik.benchmark import disk_translations
+
+    shifts = disk_translations(12, 2.0, 2024)
+    g["mobile_shifts_2024"] = disk_translations(50, 2.0, 2024)
+    mtargets = generate_reachable_targets(arm7, "flange", 12, 2024)
+    g["mobile_targets_wxyz"] = np.array([t.rotation.wxyz for t in mtargets])
+    g["mobile_targets_pos"] = np.array([t.translation for t in mtargets]) + shifts
+    mq, mh, mp, mr, mb, ms = [], [], [], [], [], []
+    for i, t in enumerate(mtargets):
+        sh = Transform3(t.rotation, t.translation + shifts[i])
+        res = tasks.solve_ik_mobile(tasks.IkRequest(model=arm7, target_link="flange", target_pose=sh,
+                                                    rng_seed=2024, optimize_base=True))
+        mq.append(res.q)
+        mh.append(res.report.cost_history)
+        mp.append(res.pos_error)
+        mr.append(res.rot_error)
+        mb.append([res.base.translation[0], res.base.translation[1], res.base.angle])
+        ms.append(res.success)
+    for k, v in (("q", mq), ("hist", mh), ("pos", mp), ("rot", mr), ("base", mb), ("succ", ms)):
+        g[f"mobile_{k}"] = np.array(v)
+    sh0 = Transform3(mtargets[0].rotation, mtargets[0].translation + shifts[0])
+    mprob = beam.IkLaneProblem(arm7, "flange", sh0, w.pose_position, w.pose_orientation, w.limit, w.rest,
+                               use_base=True, base_reg_weight=0.3)
+    seeds24 = tasks.sample_seed_configurations(arm7, 64, 2024)
+    ba = np.linspace(-3.0, 3.0, 8)
+    bxy = np.stack([np.linspace(-1, 1, 8), np.linspace(0.5, -0.5, 8)], axis=1)
+    r, jac = mprob.residuals_and_jacobian(seeds24[:8], ba, bxy)
+    g["mobile_lane_ba"], g["mobile_lane_bxy"], g["mobile_lane_r"], g["mobile_lane_jac"] = ba, bxy, r, jac
+    st = mprob.run(mprob.start_state(seeds24), 16)
+    g["mobile_lane_hist"] = np.stack(st.history, axis=1)
+    g["mobile_lane_q"], g["mobile_lane_base_angle"], g["mobile_lane_base_xy"] = st.q, st.base_angle, st.base_xy
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT}: {len(g)} arrays")
 

@@ -291,3 +291,69 @@ def test_invalid_requests_raise(models):
         IkBeamSolver(models["arm7"], "flange", keep=100)
     with pytest.raises(ValueError):
         IkBeamSolver(models["arm7"], "nope")
+
+
+# ---------------------------------------------------------------------------
+# Mobile base (SE(2) variable; beam.py:98-112, 167-179, 216-221)
+# ---------------------------------------------------------------------------
+def _mobile_problem(models, golden, precision, w_base=0.3):
+    t0 = k.Transform3.from_parts(golden["mobile_targets_wxyz"][0], golden["mobile_targets_pos"][0])
+    return IkLaneProblem(models["arm7"], "flange", t0, 50.0, 10.0, 100.0, 0.01, use_base=True,
+                         base_reg_weight=w_base, precision=precision)
+
+
+def test_mobile_lane_residuals_jacobian(models, golden):
+    seeds = sample_seed_configurations(models["arm7"], 64, 2024)
+    for prec, tol in (("fp64", 1e-9), ("fp32", 2e-4)):
+        p = _mobile_problem(models, golden, prec)
+        r, j = p.residuals_and_jacobian(seeds[:8], golden["mobile_lane_ba"], golden["mobile_lane_bxy"])
+        assert np.abs(r - golden["mobile_lane_r"]).max() <= tol * np.abs(golden["mobile_lane_r"]).max()
+        assert np.abs(j - golden["mobile_lane_jac"]).max() <= tol * np.abs(golden["mobile_lane_jac"]).max()
+
+
+def test_mobile_lane_run_fp64_tracks_reference(models, golden):
+    seeds = sample_seed_configurations(models["arm7"], 64, 2024)
+    p = _mobile_problem(models, golden, "fp64")
+    st = p.run(p.start_state(seeds), 16)
+    rel = np.abs(np.stack(st.history, 1) - golden["mobile_lane_hist"]) / golden["mobile_lane_hist"]
+    assert np.mean(rel < 1e-6) >= 0.98, np.percentile(rel, [50, 99, 100])
+
+
+def test_solve_ik_mobile_vs_reference(models, golden):
+    tg = np.concatenate([golden["mobile_targets_wxyz"], golden["mobile_targets_pos"]], 1)
+    r64 = k.solve_ik_beam_batch(models["arm7"], "flange", tg, rng_seed=2024, precision="fp64", optimize_base=True)
+    assert np.array_equal(r64.success.astype(bool), golden["mobile_succ"])
+    rel = np.abs(r64.history - golden["mobile_hist"]) / golden["mobile_hist"]
+    assert np.mean(rel.max(axis=1) < 1e-6) >= 0.75
+    r32 = k.solve_ik_beam_batch(models["arm7"], "flange", tg, rng_seed=2024, optimize_base=True)
+    assert r32.success.mean() >= golden["mobile_succ"].mean()
+    assert np.all(np.diff(r32.history, axis=1) <= 0)
+    t = k.Transform3.from_parts(tg[0, :4], tg[0, 4:])
+    res = k.solve_ik_mobile(k.IkRequest(model=models["arm7"], target_link="flange", target_pose=t, rng_seed=2024,
+                                        optimize_base=True))
+    assert res.success and res.base is not None and -np.pi < res.base.angle <= np.pi
+    assert "base" in res.to_json()
+
+
+def test_mobile_pinned_base_reduces_to_arm_only(models):
+    t = k.Transform3.from_parts(*np.split(reachable_target_array(models["arm7"], "flange", 1, 14).cpu().numpy()[0], [4]))
+    req = dict(model=models["arm7"], target_link="flange", target_pose=t, rng_seed=5)
+    arm = k.solve_ik_beam(k.IkRequest(**req))
+    pinned = k.solve_ik_mobile(k.IkRequest(base_reg_weight=1e15, **req))
+    assert np.array_equal(arm.q, pinned.q) and arm.report.cost_history == pinned.report.cost_history
+    assert pinned.base.angle == 0.0 and np.allclose(pinned.base.translation, 0.0)
+
+
+def test_mobile_benchmark_acceptance(models):
+    """test_acceptance.py:40-69 criterion on the device: optimised >= 99% success,
+    mean errors < 1e-4 m / 1e-3 rad; static base <= 60%."""
+    from paper_2505_03728_b200.benchmark import BenchmarkSpec, disk_translations, run_mobile_benchmark
+
+    assert np.array_equal(disk_translations(50, 2.0, 2024), np.load(
+        __import__("conftest").GOLDEN)["mobile_shifts_2024"])
+    spec = BenchmarkSpec(urdf=k.robot_path("arm7.urdf"), sidecar=k.robot_path("arm7.sidecar.json"), task="ik_mobile",
+                         num_targets=100, rng_seed=2024, target_link="flange", translation_radius=2.0)
+    out = run_mobile_benchmark(spec, model=models["arm7"])
+    opt, static = out["results"]["optimized"], out["results"]["static"]
+    assert opt["success_rate"] >= 0.99 and opt["pos_mean"] < 1e-4 and opt["rot_mean"] < 1e-3, opt
+    assert static["success_rate"] <= 0.60, static

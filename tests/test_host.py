@@ -110,7 +110,7 @@ def test_workspace_and_argument_validation(models):
     assert b >= 1000 * 4 * (7 + 2 + 7) * 4
     bad = _lib.KopIkParams(50, 10, 100, 0.01, 64, 16, 16, 4, 0.005, 0.05, 0)
     rc = lib.kop_ik_beam(models["arm7"]._handle, 8, C.byref(bad), None, 10, None, None, 0, None, None, None,
-                         None, None, None, None)
+                         None, None, None, None, None)
     assert rc == _lib.KOP_EINVAL and b"prune_after" in lib.kop_last_error()
     assert lib.kop_model_chain_length(models["arm7"]._handle, 99) == _lib.KOP_EINVAL
 

@@ -69,3 +69,24 @@ def test_ik_beam_unreachable_and_planar(chains, golden):
     res = o.ik_beam(p, p.link("ee"), golden["targets_p2r_5_wxyz"], golden["targets_p2r_5_pos"],
                     o.sample_seeds(p, 64, 5))
     assert np.array_equal(res.hist, golden["beam_p2r_5_hist"])
+
+
+def test_mobile_lane_and_beam_bitwise(chains, golden):
+    """Mobile-base lanes (beam.py:98-112, 167-179, 216-221) and solve_ik_mobile."""
+    ch = chains["arm7"]
+    tq, tt = golden["mobile_targets_wxyz"], golden["mobile_targets_pos"]
+    iq, it = o.target_inverse(tq[:1], tt[:1])
+    seeds = o.sample_seeds(ch, 64, 2024)
+    eng = o.LaneEngine(ch, 8, np.repeat(iq, 8, 0), np.repeat(it, 8, 0), o.DEFAULT_WEIGHTS, use_base=True,
+                       base_weight=0.3)
+    r, j = eng.residuals_and_jacobian(seeds[:8], golden["mobile_lane_ba"], golden["mobile_lane_bxy"])
+    assert np.array_equal(r, golden["mobile_lane_r"]) and np.array_equal(j, golden["mobile_lane_jac"])
+    eng = o.LaneEngine(ch, 8, np.repeat(iq, 64, 0), np.repeat(it, 64, 0), o.DEFAULT_WEIGHTS, use_base=True,
+                       base_weight=0.3)
+    st = eng.run(eng.start(seeds), 16)
+    assert np.array_equal(np.stack(st.hist, 1), golden["mobile_lane_hist"])
+    assert np.array_equal(st.ba, golden["mobile_lane_base_angle"])
+    res = o.ik_beam(ch, 8, tq, tt, seeds, use_base=True, base_weight=0.0)
+    assert np.array_equal(res.hist, golden["mobile_hist"])
+    assert np.array_equal(res.base, golden["mobile_base"])
+    assert np.array_equal(res.success, golden["mobile_succ"])
