@@ -176,7 +176,8 @@ def accuracy(pos, rot, succ):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled every 100 ms from the start of the
+    warm-up to the end of the timed region (all of it under load)."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -188,7 +189,7 @@ class ClockSampler:
     def start(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+                                          "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
         except OSError:
             self.proc = None
             return
@@ -276,14 +277,14 @@ def run_ours(args, rank, world, local_rank):
             torch.distributed.barrier()
         torch.cuda.synchronize()
 
+    clocks = ClockSampler() if rank == 0 else None
+    if clocks:
+        clocks.start()
     for _ in range(args.warmup):
         solver.solve_device(targets, out)
     barrier()
 
     # ---- device-timed region: K steps, L2 flushed (untimed) between steps ----
-    clocks = ClockSampler() if rank == 0 else None
-    if clocks:
-        clocks.start()
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     barrier()
     for s in range(args.steps):

@@ -68,6 +68,15 @@ typedef struct {
   const double* lower;          /* [n] (-inf where absent, robot.py:114-126)   */
   const double* upper;          /* [n] (+inf where absent)                     */
   const double* rest;           /* [n] rest pose (robot.py:128-141)            */
+  /* collision spheres (URDF <collision><sphere> or sidecar, robot.py:209-218,
+   * 355-361) in model link order, and self-collision link pairs
+   * (RobotModel.self_collision_pairs, robot.py:174-190); counts may be 0 */
+  int32_t num_spheres;          /* S <= 32                                     */
+  const int32_t* sphere_link;   /* [S] link index                              */
+  const double* sphere_center;  /* [S*3] centre in the link frame              */
+  const double* sphere_radius;  /* [S]                                         */
+  int32_t num_self_pairs;       /* P <= 64                                     */
+  const int32_t* self_pair_links; /* [P*2] link index pairs                    */
 } KopModelDesc;
 
 /* IK-Beam request scalars: IkRequest (tasks.py:40-60) + CostWeights
@@ -157,6 +166,69 @@ int kop_ik_beam_stage(const KopModel* model, int32_t link, const KopIkParams* pa
                       int64_t workspace_bytes, double* q_out, double* base_out, double* cost_out,
                       double* history_out, double* pos_err, double* rot_err, uint8_t* success,
                       void* stream);
+
+/* --- collision IK (config 4) and the generic LM solve -------------------
+ * Cost stack (the viewer's, server.py:60-97): pose (w_position,
+ * w_orientation) | limit (w_limit) | rest (w_rest) | world collision, one
+ * row per (sphere link, obstacle) (costs.py:499-551; w_world, eta_world) |
+ * self collision, one row per model self pair (costs.py:435-496; w_self,
+ * eta_self); soft minimum with `sharpness` (1/m) unless hard_min.
+ * Spheres must lie on links of the root->link chain. */
+#define KOP_OBSTACLE_SPHERE 0    /* a = centre, radius                  */
+#define KOP_OBSTACLE_CAPSULE 1   /* a, b = endpoints, radius            */
+#define KOP_OBSTACLE_HALFSPACE 2 /* a = normal, radius = offset         */
+
+typedef struct {
+  int32_t kind;
+  double a[3], b[3];
+  double radius;
+} KopObstacle;
+
+typedef struct {
+  double w_position, w_orientation, w_limit, w_rest;
+  double w_world, eta_world, w_self, eta_self, sharpness;
+  int32_t hard_min;
+  int32_t num_obstacles;        /* <= 16 */
+  const KopObstacle* obstacles; /* host */
+} KopCollisionCosts;
+
+/* solver.SolveOptions (solver.py:179-198) */
+typedef struct {
+  int32_t max_iterations;
+  double initial_damping, damping_increase, damping_decrease;
+  double gradient_tolerance, step_tolerance;
+  int32_t max_rejections;
+  int32_t precision;
+} KopLmOptions;
+
+/* Residual rows of the stack for `link` (6 + 2n + links*obstacles + pairs), or < 0. */
+int kop_collision_rows(const KopModel* model, int32_t link, const KopCollisionCosts* costs);
+/* replaces: the costs' raw_residual * weight and jacobian (solver.py:289-324)
+ * for one target per lane: residual [lanes*R], jacobian [lanes*R*n] (device). */
+int kop_collision_residuals_jacobian(const KopModel* model, int32_t link, int32_t precision,
+                                     const KopCollisionCosts* costs, const double* target_inv,
+                                     const int32_t* lane_target, const double* q, int64_t lanes,
+                                     double* residual, double* jacobian, void* stream);
+/* IK-Beam (tasks.py:119-161) over the collision stack; same outputs as kop_ik_beam. */
+int64_t kop_ik_beam_collision_workspace_bytes(const KopModel* model, int32_t link, const KopIkParams* params,
+                                              const KopCollisionCosts* costs, int64_t batch);
+int kop_ik_beam_collision(const KopModel* model, int32_t link, const KopIkParams* params,
+                          const KopCollisionCosts* costs, const double* targets, int64_t batch,
+                          const double* seeds, void* workspace, int64_t workspace_bytes, double* q_out,
+                          double* cost_out, double* history_out, double* pos_err, double* rot_err,
+                          uint8_t* success, void* stream);
+/* replaces: solver.solve / solve_batch (solver.py:364-460) for problems of
+ * this cost stack: one problem per target, q0 [B*n] start configurations.
+ * Outputs (device): q [B*n], cost [B], initial cost [B], history
+ * [B*(max_iterations+1)] (NaN-padded, NULL ok), iterations [B] int32,
+ * termination [B] int32: 0 max_iterations, 1 gradient_converged,
+ * 2 step_converged (step tolerance), 3 numerical_failure (damping > 1e10),
+ * 4 step_converged (rejection budget exhausted), 5 numerical_failure
+ * (non-finite residual, the CostEvaluationError solve_batch isolates). */
+int kop_lm_solve(const KopModel* model, int32_t link, const KopCollisionCosts* costs, const KopLmOptions* options,
+                 const double* targets, const double* q0, int64_t batch, double* q_out, double* cost_out,
+                 double* init_cost_out, double* history_out, int32_t* iterations_out,
+                 int32_t* termination_out, void* stream);
 
 /* --- counter-based sampling ---------------------------------------------
  * replaces: tasks.sample_seed_configurations (tasks.py:88-106) and the draws

@@ -634,7 +634,7 @@ DEFAULT_WEIGHTS = (50.0, 10.0, 100.0, 0.01)  # costs.py:52-62 (pos, ori, limit, 
 
 def ik_beam(ch: Chain, link: int, tq, tt, seeds, weights=DEFAULT_WEIGHTS, total_steps=16,
             prune_after=6, keep=4, pos_tol=0.005, rot_tol=0.05, dtype=np.float64, use_base=False,
-            base_weight=0.0) -> BeamResult:
+            base_weight=0.0, engine=None) -> BeamResult:
     """tasks.py:119-161 over B targets at once (lanes = B x S seeds).
 
     Each target's lanes are independent, so batching targets reproduces the
@@ -645,14 +645,15 @@ def ik_beam(ch: Chain, link: int, tq, tt, seeds, weights=DEFAULT_WEIGHTS, total_
     iq, it = target_inverse(tq, tt)
     lane_t = np.repeat(np.arange(b), s)
     kw = dict(dtype=dtype, use_base=use_base, base_weight=base_weight)
-    eng = LaneEngine(ch, link, iq[lane_t], it[lane_t], weights, group=lane_t, **kw)
+    make = engine or (lambda q_, t_, group: LaneEngine(ch, link, q_, t_, weights, group=group, **kw))
+    eng = make(iq[lane_t], it[lane_t], lane_t)
     st = eng.start(np.tile(seeds, (b, 1)))
     st = eng.run(st, prune_after)
     cost = st.cost.reshape(b, s)
     order = np.argsort(cost, axis=1, kind="stable")[:, :keep]
     pick = (order + np.arange(b)[:, None] * s).reshape(-1)
     st2 = st.take(pick)
-    eng2 = LaneEngine(ch, link, iq[lane_t[pick]], it[lane_t[pick]], weights, group=lane_t[pick], **kw)
+    eng2 = make(iq[lane_t[pick]], it[lane_t[pick]], lane_t[pick])
     st2 = eng2.run(st2, total_steps - prune_after)
     c2 = st2.cost.reshape(b, keep)
     win = np.argmin(c2, axis=1)

@@ -26,6 +26,8 @@ class KopModelDesc(C.Structure):
         ("parent_link", _p), ("child_link", _p), ("kind", _p), ("qcol", _p),
         ("mult", _p), ("offset", _p), ("origin_wxyz", _p), ("origin_xyz", _p), ("axis", _p),
         ("lower", _p), ("upper", _p), ("rest", _p),
+        ("num_spheres", _i32), ("sphere_link", _p), ("sphere_center", _p), ("sphere_radius", _p),
+        ("num_self_pairs", _i32), ("self_pair_links", _p),
     ]
 
 
@@ -36,6 +38,22 @@ class KopIkParams(C.Structure):
         ("success_pos_tol", _f64), ("success_rot_tol", _f64), ("precision", _i32),
         ("optimize_base", _i32), ("w_base", _f64),
     ]
+
+
+class KopObstacle(C.Structure):
+    _fields_ = [("kind", _i32), ("a", _f64 * 3), ("b", _f64 * 3), ("radius", _f64)]
+
+
+class KopCollisionCosts(C.Structure):
+    _fields_ = [(f, _f64) for f in ("w_position", "w_orientation", "w_limit", "w_rest", "w_world", "eta_world",
+                                    "w_self", "eta_self", "sharpness")] + \
+               [("hard_min", _i32), ("num_obstacles", _i32), ("obstacles", C.POINTER(KopObstacle))]
+
+
+class KopLmOptions(C.Structure):
+    _fields_ = [("max_iterations", _i32), ("initial_damping", _f64), ("damping_increase", _f64),
+                ("damping_decrease", _f64), ("gradient_tolerance", _f64), ("step_tolerance", _f64),
+                ("max_rejections", _i32), ("precision", _i32)]
 
 
 # name -> (restype, argtypes); must match include/kinoptik_b200.h exactly
@@ -55,6 +73,15 @@ SIGNATURES = {
                               _p, _p, _p, _p, _p, _p, _p, _p]),
     "kop_ik_beam_stage": (C.c_int, [_p, _i32, C.POINTER(KopIkParams), _i32, _p, _i64, _p, _p, _i64,
                                     _p, _p, _p, _p, _p, _p, _p, _p]),
+    "kop_collision_rows": (C.c_int, [_p, _i32, C.POINTER(KopCollisionCosts)]),
+    "kop_collision_residuals_jacobian": (C.c_int, [_p, _i32, _i32, C.POINTER(KopCollisionCosts), _p, _p, _p, _i64,
+                                                   _p, _p, _p]),
+    "kop_ik_beam_collision_workspace_bytes": (_i64, [_p, _i32, C.POINTER(KopIkParams),
+                                                     C.POINTER(KopCollisionCosts), _i64]),
+    "kop_ik_beam_collision": (C.c_int, [_p, _i32, C.POINTER(KopIkParams), C.POINTER(KopCollisionCosts), _p, _i64,
+                                        _p, _p, _i64, _p, _p, _p, _p, _p, _p, _p]),
+    "kop_lm_solve": (C.c_int, [_p, _i32, C.POINTER(KopCollisionCosts), C.POINTER(KopLmOptions), _p, _p, _i64,
+                               _p, _p, _p, _p, _p, _p, _p]),
     "kop_sample_uniform": (C.c_int, [_u64, _u64, _i64, _i32, _p, _p, _p, _p, _p]),
     "kop_link_poses": (C.c_int, [_p, _i32, _p, _i64, _p, _p]),
     "kop_fma_peak_kernel": (C.c_int, [_i32, _i32, _i32, _p, C.POINTER(_f64), _p]),

@@ -9,6 +9,7 @@
 #include <vector>
 
 #include "../../include/kinoptik_b200.h"
+#include "kop_collision.cuh"
 #include "kop_kernels.cuh"
 
 using namespace kop;
@@ -17,6 +18,10 @@ struct KopModel {
   TreeParams tree;
   std::vector<double> lower, upper, rest;
   std::vector<int32_t> parent_joint;  // per link, -1 for the root
+  // collision spheres (robot.py:66, sidecar) and default self pairs (robot.py:174-190)
+  std::vector<int32_t> sphere_link;
+  std::vector<double> sphere_center, sphere_radius;
+  std::vector<int32_t> pair_links;  // [P*2]
 };
 
 namespace {
@@ -69,7 +74,16 @@ constexpr int kChainMax = 8;
 
 // Root->link moving-joint chain with fixed joints folded and axes aligned to
 // +z (kop_chain.h).  Returns the number of moving joints or a negative status.
-int compile_chain(const KopModel& m, int link, ChainParams<double, kChainMax>& C, bool& identity) {
+// frame of a link on the compiled path: aligned child frame of moving joint
+// `slot` (-1: the root) composed with (q, p)
+struct LinkFrame {
+  int link, slot;
+  HQ q;
+  double p[3];
+};
+
+int compile_chain(const KopModel& m, int link, ChainParams<double, kChainMax>& C, bool& identity,
+                  std::vector<LinkFrame>* frames = nullptr) {
   const TreeParams& P = m.tree;
   if (link < 0 || link >= P.nl) return fail(KOP_EINVAL, "unknown link index " + std::to_string(link));
   std::vector<int> path;
@@ -78,6 +92,10 @@ int compile_chain(const KopModel& m, int link, ChainParams<double, kChainMax>& C
   double pend_p[3] = {0, 0, 0};
   int k = 0;
   memset(&C, 0, sizeof(C));
+  if (frames) {
+    frames->clear();
+    frames->push_back({0, -1, {1, 0, 0, 0}, {0, 0, 0}});
+  }
   for (auto it = path.rbegin(); it != path.rend(); ++it) {
     const int j = *it;
     const HQ oq{P.oq[j][0], P.oq[j][1], P.oq[j][2], P.oq[j][3]};
@@ -87,6 +105,7 @@ int compile_chain(const KopModel& m, int link, ChainParams<double, kChainMax>& C
     if (P.kind[j] == KOP_JOINT_FIXED) {
       pend = hmul(pend, oq);
       memcpy(pend_p, tp, sizeof(tp));
+      if (frames) frames->push_back({P.child[j], k - 1, pend, {pend_p[0], pend_p[1], pend_p[2]}});
       continue;
     }
     if (k >= kChainMax)
@@ -103,6 +122,7 @@ int compile_chain(const KopModel& m, int link, ChainParams<double, kChainMax>& C
     ++k;
     pend = {al.w, -al.x, -al.y, -al.z};
     pend_p[0] = pend_p[1] = pend_p[2] = 0.0;
+    if (frames) frames->push_back({P.child[j], k - 1, pend, {0, 0, 0}});
   }
   C.eq[0] = pend.w; C.eq[1] = pend.x; C.eq[2] = pend.y; C.eq[3] = pend.z;
   memcpy(C.ep, pend_p, sizeof(pend_p));
@@ -183,6 +203,139 @@ struct PadBuf {
 
 int kernel_nq(Shape sh, int n) { return sh == Shape::kGen8 ? 8 : n; }
 
+// Collision parameters for IK on `link` (kop_collision.cuh): every
+// sphere-bearing link must lie on the compiled root->link chain.
+int compile_collision(const KopModel& m, const std::vector<LinkFrame>& frames, const KopCollisionCosts* cc,
+                      CollisionParams<double>& P) {
+  memset(&P, 0, sizeof(P));
+  if (!cc) return fail(KOP_EINVAL, "null collision costs");
+  if (cc->num_obstacles < 0 || cc->num_obstacles > kMaxObstacles)
+    return fail(KOP_EUNSUPPORTED, "more than 16 obstacles (not compiled in)");
+  if ((cc->w_world > 0 && !(cc->eta_world > 0)) || (cc->w_self > 0 && !(cc->eta_self > 0)))
+    return fail(KOP_EINVAL, "buffer distance must be positive");
+  // sphere links in model order (spheres arrive grouped by link)
+  std::vector<int> links, first, count, slot;
+  for (size_t s = 0; s < m.sphere_link.size(); ++s) {
+    const int l = m.sphere_link[s];
+    if (links.empty() || links.back() != l) {
+      int fi = -1;
+      for (size_t f = 0; f < frames.size(); ++f)
+        if (frames[f].link == l) fi = (int)f;
+      if (fi < 0)
+        return fail(KOP_EUNSUPPORTED, "collision spheres on link " + std::to_string(l) +
+                                          ", which is not on the root->IK-link chain (not compiled in)");
+      links.push_back(l);
+      first.push_back((int)s);
+      count.push_back(0);
+      slot.push_back(frames[fi].slot);
+    }
+    count.back()++;
+  }
+  if ((int)links.size() > kMaxSphereLinks) return fail(KOP_EUNSUPPORTED, "more than 16 sphere links");
+  for (size_t i = 1; i < slot.size(); ++i)
+    if (slot[i] < slot[i - 1]) return fail(KOP_EUNSUPPORTED, "sphere links out of chain order");
+  P.ns = (int)m.sphere_link.size();
+  int slot_count[kMaxSlots] = {0};
+  for (size_t li = 0; li < links.size(); ++li) {
+    const LinkFrame* fr = nullptr;
+    for (const auto& f : frames)
+      if (f.link == links[li]) fr = &f;
+    P.lfirst[li] = first[li];
+    P.lcount[li] = count[li];
+    P.lslot[li] = slot[li];
+    slot_count[slot[li] + 1] += count[li];
+    for (int s = first[li]; s < first[li] + count[li]; ++s) {
+      double c[3];
+      hrot(fr->q, &m.sphere_center[3 * s], c);
+      for (int i = 0; i < 3; ++i) P.sc[s][i] = c[i] + fr->p[i];
+      P.sr[s] = m.sphere_radius[s];
+    }
+  }
+  P.slot_first[0] = 0;
+  for (int k = 0; k < kMaxSlots; ++k) P.slot_first[k + 1] = P.slot_first[k] + slot_count[k];
+  P.nl = (int)links.size();
+  P.no = cc->w_world > 0 ? cc->num_obstacles : 0;
+  for (int o = 0; o < P.no; ++o) {
+    const KopObstacle& ob = cc->obstacles[o];
+    if (ob.kind < 0 || ob.kind > 2) return fail(KOP_EINVAL, "unknown obstacle kind");
+    P.okind[o] = ob.kind;
+    double n = 1.0;
+    if (ob.kind == KOP_OBSTACLE_HALFSPACE) {
+      n = sqrt(ob.a[0] * ob.a[0] + ob.a[1] * ob.a[1] + ob.a[2] * ob.a[2]);
+      if (n < 1e-12) return fail(KOP_EINVAL, "half-space normal must be nonzero");
+    }
+    for (int i = 0; i < 3; ++i) {
+      P.oa[o][i] = ob.a[i] / n;
+      P.ob[o][i] = ob.b[i];
+    }
+    P.orad[o] = ob.radius;
+  }
+  P.np = 0;
+  if (cc->w_self > 0) {
+    for (size_t p = 0; p + 1 < m.pair_links.size(); p += 2) {
+      int a = -1, b = -1;
+      for (size_t li = 0; li < links.size(); ++li) {
+        if (links[li] == m.pair_links[p]) a = (int)li;
+        if (links[li] == m.pair_links[p + 1]) b = (int)li;
+      }
+      if (a < 0 || b < 0) return fail(KOP_EUNSUPPORTED, "self pair link without spheres on the chain");
+      P.pa[P.np] = a;
+      P.pb[P.np] = b;
+      P.np++;
+    }
+  }
+  P.w_world = cc->w_world;
+  P.eta_world = cc->eta_world > 0 ? cc->eta_world : 1.0;
+  P.w_self = cc->w_self;
+  P.eta_self = cc->eta_self > 0 ? cc->eta_self : 1.0;
+  P.beta = cc->sharpness > 0 ? cc->sharpness : 100.0;
+  P.hard = cc->hard_min;
+  return KOP_OK;
+}
+
+template <typename T>
+CollisionParams<T> cast_collision(const CollisionParams<double>& D) {
+  CollisionParams<T> P;
+  memset(&P, 0, sizeof(P));
+  P.ns = D.ns;
+  for (int s = 0; s < kMaxSpheres; ++s) {
+    for (int i = 0; i < 3; ++i) P.sc[s][i] = T(D.sc[s][i]);
+    P.sr[s] = T(D.sr[s]);
+  }
+  for (int k = 0; k <= kMaxSlots; ++k) P.slot_first[k] = D.slot_first[k];
+  P.nl = D.nl;
+  for (int l = 0; l < kMaxSphereLinks; ++l) {
+    P.lfirst[l] = D.lfirst[l];
+    P.lcount[l] = D.lcount[l];
+    P.lslot[l] = D.lslot[l];
+  }
+  P.no = D.no;
+  for (int o = 0; o < kMaxObstacles; ++o) {
+    P.okind[o] = D.okind[o];
+    for (int i = 0; i < 3; ++i) {
+      P.oa[o][i] = T(D.oa[o][i]);
+      P.ob[o][i] = T(D.ob[o][i]);
+    }
+    P.orad[o] = T(D.orad[o]);
+  }
+  P.np = D.np;
+  for (int p = 0; p < kMaxSelfPairs; ++p) {
+    P.pa[p] = D.pa[p];
+    P.pb[p] = D.pb[p];
+  }
+  P.w_world = T(D.w_world);
+  P.eta_world = T(D.eta_world);
+  P.w_self = T(D.w_self);
+  P.eta_self = T(D.eta_self);
+  P.beta = T(D.beta);
+  P.hard = D.hard;
+  return P;
+}
+
+int collision_rows(const KopModel& m, const CollisionParams<double>& P) {
+  return 6 + 2 * m.tree.n + P.nl * P.no + P.np;
+}
+
 }  // namespace
 
 extern "C" {
@@ -239,6 +392,28 @@ int kop_model_create(const KopModelDesc* d, KopModel** out) {
       P.axis[j][i] = d->axis[j * 3 + i];
     }
     m->parent_joint[cl] = j;
+  }
+  if (d->num_spheres < 0 || d->num_spheres > kMaxSpheres || d->num_self_pairs < 0 ||
+      d->num_self_pairs > kMaxSelfPairs) {
+    delete m;
+    return fail(KOP_EUNSUPPORTED, "more than 32 collision spheres or 64 self pairs (not compiled in)");
+  }
+  for (int s = 0; s < d->num_spheres; ++s) {
+    const int l = d->sphere_link[s];
+    if (l < 0 || l >= P.nl || !(d->sphere_radius[s] > 0.0)) {
+      delete m;
+      return fail(KOP_EINVAL, "bad collision sphere");
+    }
+    m->sphere_link.push_back(l);
+    for (int i = 0; i < 3; ++i) m->sphere_center.push_back(d->sphere_center[3 * s + i]);
+    m->sphere_radius.push_back(d->sphere_radius[s]);
+  }
+  for (int p = 0; p < 2 * d->num_self_pairs; ++p) {
+    if (d->self_pair_links[p] < 0 || d->self_pair_links[p] >= P.nl) {
+      delete m;
+      return fail(KOP_EINVAL, "bad self-collision pair");
+    }
+    m->pair_links.push_back(d->self_pair_links[p]);
   }
   m->lower.assign(d->lower, d->lower + P.n);
   m->upper.assign(d->upper, d->upper + P.n);
@@ -645,6 +820,249 @@ int kop_lane_run(const KopModel* m, int32_t link, int32_t precision, const doubl
   L.cost = cost;
   L.hist = history;
   return lane_call(m, link, precision, weights, L, lanes, stream);
+}
+
+}  // extern "C"
+
+namespace {
+
+template <class G>
+cudaError_t run_col(const KopModel& m, const ChainParams<double, kChainMax>& D, const CollisionParams<double>& PD,
+                    const double w[5], const ColLaunch& L, cudaStream_t st) {
+  return launch_col<G>(cast_chain<typename G::T, G::K>(D), make_costs<typename G::T, G::NQ>(m, w),
+                       cast_collision<typename G::T>(PD), cast_chain<double, G::K>(D), L, st);
+}
+
+template <typename T>
+cudaError_t dispatch_col(Shape sh, const KopModel& m, const ChainParams<double, kChainMax>& D,
+                         const CollisionParams<double>& PD, const double w[5], const ColLaunch& L, cudaStream_t st) {
+  switch (sh) {
+    case Shape::kId7: return run_col<Cfg<T, 7, 7, true, false>>(m, D, PD, w, L, st);
+    case Shape::kGen8: return run_col<Cfg<T, 8, 8, false, false>>(m, D, PD, w, L, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+// chain + collision params + collision shape (id7 or the padded generic shape)
+int prepare_col(const KopModel* m, int link, int precision, const KopCollisionCosts* cc,
+                ChainParams<double, kChainMax>& C, CollisionParams<double>& PD, Shape& sh) {
+  if (!m) return fail(KOP_EINVAL, "null model");
+  if (precision != KOP_FP32 && precision != KOP_FP64) return fail(KOP_EINVAL, "bad precision");
+  bool id = false;
+  std::vector<LinkFrame> frames;
+  const int k = compile_chain(*m, link, C, id, &frames);
+  if (k < 0) return k;
+  sh = (id && m->tree.n == 7) ? Shape::kId7 : (m->tree.n <= 8 ? Shape::kGen8 : Shape::kNone);
+  if (sh == Shape::kNone) return fail(KOP_EUNSUPPORTED, "collision IK supports up to 8 actuated joints");
+  return compile_collision(*m, frames, cc, PD);
+}
+
+void col_weights(const KopCollisionCosts* cc, double w[5]) {
+  w[0] = cc->w_position;
+  w[1] = cc->w_orientation;
+  w[2] = cc->w_limit;
+  w[3] = cc->w_rest;
+  w[4] = 0.0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int kop_collision_rows(const KopModel* m, int32_t link, const KopCollisionCosts* cc) {
+  ChainParams<double, kChainMax> C;
+  CollisionParams<double> PD;
+  Shape sh;
+  const int rc = prepare_col(m, link, KOP_FP64, cc, C, PD, sh);
+  return rc != KOP_OK ? rc : collision_rows(*m, PD);
+}
+
+int kop_collision_residuals_jacobian(const KopModel* m, int32_t link, int32_t precision, const KopCollisionCosts* cc,
+                                     const double* tinv, const int32_t* lane_target, const double* q,
+                                     int64_t lanes, double* residual, double* jacobian, void* stream) {
+  ChainParams<double, kChainMax> C;
+  CollisionParams<double> PD;
+  Shape sh;
+  int rc = prepare_col(m, link, precision, cc, C, PD, sh);
+  if (rc != KOP_OK) return rc;
+  if (lanes < 0) return fail(KOP_EINVAL, "negative lane count");
+  if (lanes == 0) return KOP_OK;
+  if (!tinv || !lane_target || !q || !residual || !jacobian) return fail(KOP_EINVAL, "null array argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = m->tree.n, nq = kernel_nq(sh, n);
+  const int R = collision_rows(*m, PD), Rk = R + 2 * (nq - n);
+  PadBuf qin, res, jac;
+  ColLaunch L{};
+  L.op = ColOp::kResJac;
+  L.tinv = tinv;
+  L.lane_target = lane_target;
+  L.q_in = q;
+  L.lanes = lanes;
+  L.rows = Rk;
+  L.res = residual;
+  L.jac = jacobian;
+  if (nq != n) {
+    if (cudaMalloc(&qin.ptr, sizeof(double) * nq * lanes) != cudaSuccess ||
+        cudaMalloc(&res.ptr, sizeof(double) * Rk * lanes) != cudaSuccess ||
+        cudaMalloc(&jac.ptr, sizeof(double) * Rk * nq * lanes) != cudaSuccess)
+      return cuda_status(cudaGetLastError());
+    if ((rc = cuda_status(restride(q, lanes, n, nq, qin.ptr, st)))) return rc;
+    L.q_in = qin.ptr;
+    L.res = res.ptr;
+    L.jac = jac.ptr;
+  }
+  double w[5];
+  col_weights(cc, w);
+  cudaError_t e = precision == KOP_FP32 ? dispatch_col<float>(sh, *m, C, PD, w, L, st)
+                                        : dispatch_col<double>(sh, *m, C, PD, w, L, st);
+  if (e == cudaSuccess && nq != n) {
+    std::vector<int> rowmap;
+    for (int r = 0; r < 6; ++r) rowmap.push_back(r);
+    for (int r = 0; r < n; ++r) rowmap.push_back(6 + r);
+    for (int r = 0; r < n; ++r) rowmap.push_back(6 + nq + r);
+    for (int r = 6 + 2 * n; r < R; ++r) rowmap.push_back(r + 2 * (nq - n));
+    for (int r = 0; r < R && e == cudaSuccess; ++r) {
+      e = cudaMemcpy2DAsync(residual + r, sizeof(double) * R, L.res + rowmap[r], sizeof(double) * Rk,
+                            sizeof(double), lanes, cudaMemcpyDeviceToDevice, st);
+      if (e == cudaSuccess)
+        e = cudaMemcpy2DAsync(jacobian + (size_t)r * n, sizeof(double) * R * n, L.jac + (size_t)rowmap[r] * nq,
+                              sizeof(double) * Rk * nq, sizeof(double) * n, lanes, cudaMemcpyDeviceToDevice, st);
+    }
+    cudaStreamSynchronize(st);
+  }
+  return cuda_status(e);
+}
+
+int64_t kop_ik_beam_collision_workspace_bytes(const KopModel* m, int32_t link, const KopIkParams* p,
+                                              const KopCollisionCosts* cc, int64_t batch) {
+  if (!p || batch < 0) return fail(KOP_EINVAL, "invalid arguments");
+  ChainParams<double, kChainMax> C;
+  CollisionParams<double> PD;
+  Shape sh;
+  const int rc = prepare_col(m, link, p->precision, cc, C, PD, sh);
+  if (rc != KOP_OK) return rc;
+  const int64_t rec = kernel_nq(sh, m->tree.n) + 2 + p->prune_after + 1;
+  return batch * (int64_t)p->keep * rec * (p->precision == KOP_FP64 ? 8 : 4) + 256;
+}
+
+int kop_ik_beam_collision(const KopModel* m, int32_t link, const KopIkParams* p, const KopCollisionCosts* cc,
+                          const double* targets, int64_t batch, const double* seeds, void* workspace,
+                          int64_t workspace_bytes, double* q_out, double* cost_out, double* history_out,
+                          double* pos_err, double* rot_err, uint8_t* success, void* stream) {
+  if (!p) return fail(KOP_EINVAL, "null params");
+  ChainParams<double, kChainMax> C;
+  CollisionParams<double> PD;
+  Shape sh;
+  int rc = prepare_col(m, link, p->precision, cc, C, PD, sh);
+  if (rc != KOP_OK) return rc;
+  if (!(0 < p->prune_after && p->prune_after < p->total_steps))
+    return fail(KOP_EINVAL, "need 0 < prune_after < total_steps");
+  if (!(1 <= p->keep && p->keep <= p->seeds)) return fail(KOP_EINVAL, "need 1 <= keep <= seeds");
+  if (p->seeds > 128 || p->keep > 32)
+    return fail(KOP_EUNSUPPORTED, "collision IK-Beam supports seeds <= 128 and keep <= 32");
+  if (batch < 0) return fail(KOP_EINVAL, "negative batch");
+  if (batch == 0) return KOP_OK;
+  if (!targets || !seeds || !workspace || !q_out || !cost_out || !pos_err || !rot_err || !success)
+    return fail(KOP_EINVAL, "null array argument");
+  if (workspace_bytes < kop_ik_beam_collision_workspace_bytes(m, link, p, cc, batch))
+    return fail(KOP_EINVAL, "workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = m->tree.n, nq = kernel_nq(sh, n);
+  PadBuf seeds_pad, q_pad;
+  const double* seeds_k = seeds;
+  double* q_k = q_out;
+  if (nq != n) {
+    if (cudaMalloc(&seeds_pad.ptr, sizeof(double) * nq * p->seeds) != cudaSuccess ||
+        cudaMalloc(&q_pad.ptr, sizeof(double) * nq * batch) != cudaSuccess)
+      return cuda_status(cudaGetLastError());
+    if ((rc = cuda_status(restride(seeds, p->seeds, n, nq, seeds_pad.ptr, st)))) return rc;
+    seeds_k = seeds_pad.ptr;
+    q_k = q_pad.ptr;
+  }
+  ColLaunch L{};
+  L.op = ColOp::kBeam;
+  BeamLaunch& Bm = L.beam;
+  Bm.targets = targets;
+  Bm.B = batch;
+  Bm.seeds = seeds_k;
+  Bm.S = p->seeds;
+  Bm.P = next_pow2(p->seeds);
+  Bm.G = next_pow2(p->keep);
+  Bm.steps1 = p->prune_after;
+  Bm.steps2 = p->total_steps - p->prune_after;
+  Bm.keep = p->keep;
+  Bm.pos_tol = p->success_pos_tol;
+  Bm.rot_tol = p->success_rot_tol;
+  Bm.workspace = workspace;
+  Bm.q_out = q_k;
+  Bm.base_out = nullptr;
+  Bm.cost_out = cost_out;
+  Bm.hist_out = history_out;
+  Bm.pos_err = pos_err;
+  Bm.rot_err = rot_err;
+  Bm.success = success;
+  Bm.stages = 3;
+  double w[5];
+  col_weights(cc, w);
+  cudaError_t e = p->precision == KOP_FP32 ? dispatch_col<float>(sh, *m, C, PD, w, L, st)
+                                           : dispatch_col<double>(sh, *m, C, PD, w, L, st);
+  if (e == cudaSuccess && q_k != q_out) e = restride(q_k, batch, nq, n, q_out, st);
+  if (seeds_pad.ptr) cudaStreamSynchronize(st);
+  return cuda_status(e);
+}
+
+int kop_lm_solve(const KopModel* m, int32_t link, const KopCollisionCosts* cc, const KopLmOptions* o,
+                 const double* targets, const double* q0, int64_t batch, double* q_out, double* cost_out,
+                 double* init_cost_out, double* history_out, int32_t* iterations_out, int32_t* termination_out,
+                 void* stream) {
+  if (!o) return fail(KOP_EINVAL, "null options");
+  ChainParams<double, kChainMax> C;
+  CollisionParams<double> PD;
+  Shape sh;
+  int rc = prepare_col(m, link, o->precision, cc, C, PD, sh);
+  if (rc != KOP_OK) return rc;
+  // SolveOptions.__post_init__ (solver.py:190-198)
+  if (o->max_iterations <= 0 || !(o->initial_damping > 0)) return fail(KOP_EINVAL, "max_iterations and initial_damping must be positive");
+  if (!(o->damping_increase > 1.0)) return fail(KOP_EINVAL, "damping_increase must exceed 1");
+  if (!(o->damping_decrease > 0.0 && o->damping_decrease < 1.0)) return fail(KOP_EINVAL, "damping_decrease must be in (0, 1)");
+  if (o->max_rejections < 1) return fail(KOP_EINVAL, "max_rejections must be positive");
+  if (batch < 0) return fail(KOP_EINVAL, "negative batch");
+  if (batch == 0) return KOP_OK;
+  if (!targets || !q0 || !q_out || !cost_out || !init_cost_out || !iterations_out || !termination_out)
+    return fail(KOP_EINVAL, "null array argument");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = m->tree.n, nq = kernel_nq(sh, n);
+  PadBuf q0p, qop;
+  ColLaunch L{};
+  L.op = ColOp::kSolve;
+  L.targets = targets;
+  L.q_in = q0;
+  L.B = batch;
+  L.q_out = q_out;
+  L.cost_out = cost_out;
+  L.init_cost = init_cost_out;
+  L.hist_out = history_out;
+  L.iters = iterations_out;
+  L.term = termination_out;
+  L.opts = {o->max_iterations, o->max_rejections, o->initial_damping, o->damping_increase, o->damping_decrease,
+            o->gradient_tolerance, o->step_tolerance};
+  if (nq != n) {
+    if (cudaMalloc(&q0p.ptr, sizeof(double) * nq * batch) != cudaSuccess ||
+        cudaMalloc(&qop.ptr, sizeof(double) * nq * batch) != cudaSuccess)
+      return cuda_status(cudaGetLastError());
+    if ((rc = cuda_status(restride(q0, batch, n, nq, q0p.ptr, st)))) return rc;
+    L.q_in = q0p.ptr;
+    L.q_out = qop.ptr;
+  }
+  double w[5];
+  col_weights(cc, w);
+  cudaError_t e = o->precision == KOP_FP32 ? dispatch_col<float>(sh, *m, C, PD, w, L, st)
+                                           : dispatch_col<double>(sh, *m, C, PD, w, L, st);
+  if (e == cudaSuccess && nq != n) {
+    e = restride(qop.ptr, batch, nq, n, q_out, st);
+    cudaStreamSynchronize(st);
+  }
+  return cuda_status(e);
 }
 
 int kop_fma_peak_kernel(int32_t blocks, int32_t threads, int32_t iters, float* sink, double* flops,

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include "kop_chain.h"
+#include "kop_collision.cuh"
 #include "kop_lane.cuh"
 
 namespace kop {
@@ -53,6 +54,46 @@ struct LaneLaunch {
   int steps;
   double *q_io, *base_io, *lam, *cost, *hist, *res, *jac;
 };
+
+// collision-stack shapes (fixed base): the Panda identity chain and the
+// generic padded 8-joint shape
+#define KOP_FOR_EACH_COLLISION_SHAPE(X) \
+  X(float, 7, 7, true)                 \
+  X(double, 7, 7, true)                \
+  X(float, 8, 8, false)                \
+  X(double, 8, 8, false)
+
+// solver.SolveOptions (solver.py:179-198) as the device sees them
+struct LmOptions {
+  int max_iterations, max_rejections;
+  double damping0, up, down, grad_tol, step_tol;
+};
+
+enum class ColOp { kResJac, kBeam, kSolve };
+
+struct ColLaunch {
+  ColOp op;
+  // kResJac
+  const double* tinv;
+  const int32_t* lane_target;
+  const double* q_in;  // also q0 for kSolve
+  int64_t lanes;
+  int rows;
+  double *res, *jac;
+  // kSolve
+  const double* targets;
+  int64_t B;
+  double *q_out, *cost_out, *init_cost, *hist_out;
+  int32_t *iters, *term;
+  LmOptions opts;
+  // kBeam
+  BeamLaunch beam;
+};
+
+template <class G>
+cudaError_t launch_col(const ChainParams<typename G::T, G::K>& C, const CostParams<typename G::T, G::NQ>& W,
+                       const CollisionParams<typename G::T>& P, const ChainParams<double, G::K>& Cd,
+                       const ColLaunch& L, cudaStream_t st);
 
 template <class G>
 cudaError_t launch_beam(const ChainParams<typename G::T, G::K>& C, const CostParams<typename G::T, G::NQ>& W,

@@ -146,6 +146,73 @@ __device__ __forceinline__ void s_columns(const quat<T>& sq, const vec3<T>& sp, 
   pz[0] = r20; pz[1] = r21; pz[2] = r22;
 }
 
+// Pose residual of the (base-composed) world EE pose (sq, sp) and, if JAC,
+// the weighted pose Jacobian J = diag(w) Jr^-1(xi) [lin; ang] from the
+// body-frame columns `col` (chain joints, then the 3 base columns).
+template <class G, bool JAC>
+__device__ __forceinline__ void pose_finish(const ChainParams<typename G::T, G::K>& C,
+                                            const CostParams<typename G::T, G::NQ>& W,
+                                            const TargetInv<typename G::T>& tg, const quat<typename G::T>& sq,
+                                            const vec3<typename G::T>& sp,
+                                            const typename G::T (&col)[G::K + (G::BASE ? 3 : 0)][6],
+                                            typename G::T (&r)[6], typename G::T (&J)[6][G::ND]) {
+  using T = typename G::T;
+  constexpr int K = G::K, NQ = G::NQ;
+  constexpr bool ID = G::ID;
+  // pose error T_t^-1 * (B) * FK  (beam.py:119-121)
+  const quat<T> e_q = qmul(tg.q, sq);
+  const vec3<T> et = qrot(tg.q, sp);
+  const vec3<T> e_t{tg.t.x + et.x, tg.t.y + et.y, tg.t.z + et.z};
+  const Twist<T> xi = se3_log(e_q, e_t);
+  r[0] = W.w_pos * xi.v.x;
+  r[1] = W.w_pos * xi.v.y;
+  r[2] = W.w_pos * xi.v.z;
+  r[3] = W.w_ori * xi.phi.x;
+  r[4] = W.w_ori * xi.phi.y;
+  r[5] = W.w_ori * xi.phi.z;
+  if (!JAC) return;
+
+  // J_pose = diag(w) Jr^-1(xi) [lin; ang]   (beam.py:142-156, 170)
+  const JrInv<T> jr = se3_jr_inv(xi);
+  mat3<T> At, Bt, Ab;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      At.m[i][j] = W.w_pos * jr.A.m[i][j];
+      Bt.m[i][j] = W.w_pos * jr.B.m[i][j];
+      Ab.m[i][j] = W.w_ori * jr.A.m[i][j];
+    }
+  if (!ID) {
+#pragma unroll
+    for (int m = 0; m < 6; ++m)
+#pragma unroll
+      for (int c = 0; c < NQ; ++c) J[m][c] = T(0);
+  }
+#pragma unroll
+  for (int k = 0; k < K + (G::BASE ? 3 : 0); ++k) {
+    if (ID || k >= K || k < C.k) {
+      const vec3<T> lin{col[k][0], col[k][1], col[k][2]}, ang{col[k][3], col[k][4], col[k][5]};
+      const vec3<T> t1 = mul(At, lin), t2 = mul(Bt, ang), b1 = mul(Ab, ang);
+      const T cj[6] = {t1.x + t2.x, t1.y + t2.y, t1.z + t2.z, b1.x, b1.y, b1.z};
+      if (ID || k >= K) {
+        const int c = k >= K ? NQ + (k - K) : k;
+#pragma unroll
+        for (int m = 0; m < 6; ++m) J[m][c] = cj[m];
+      } else {
+        const int qc = C.qcol[k];
+        const T mu = C.mult[k];
+#pragma unroll
+        for (int c = 0; c < NQ; ++c)
+          if (qc == c) {
+#pragma unroll
+            for (int m = 0; m < 6; ++m) J[m][c] += mu * cj[m];
+          }
+      }
+    }
+  }
+}
+
 template <class G, bool JAC>
 __device__ __forceinline__ void pose_rows(const ChainParams<typename G::T, G::K>& C,
                                           const CostParams<typename G::T, G::NQ>& W,
@@ -207,58 +274,7 @@ __device__ __forceinline__ void pose_rows(const ChainParams<typename G::T, G::K>
     const T c2 = c * c - s * s, s2 = T(2) * c * s;
     sp = {c2 * sp.x - s2 * sp.y + base[0], s2 * sp.x + c2 * sp.y + base[1], sp.z};
   }
-  // pose error T_t^-1 * (B) * FK  (beam.py:119-121)
-  const quat<T> e_q = qmul(tg.q, sq);
-  const vec3<T> et = qrot(tg.q, sp);
-  const vec3<T> e_t{tg.t.x + et.x, tg.t.y + et.y, tg.t.z + et.z};
-  const Twist<T> xi = se3_log(e_q, e_t);
-  r[0] = W.w_pos * xi.v.x;
-  r[1] = W.w_pos * xi.v.y;
-  r[2] = W.w_pos * xi.v.z;
-  r[3] = W.w_ori * xi.phi.x;
-  r[4] = W.w_ori * xi.phi.y;
-  r[5] = W.w_ori * xi.phi.z;
-  if (!JAC) return;
-
-  // J_pose = diag(w) Jr^-1(xi) [lin; ang]   (beam.py:142-156, 170)
-  const JrInv<T> jr = se3_jr_inv(xi);
-  mat3<T> At, Bt, Ab;
-#pragma unroll
-  for (int i = 0; i < 3; ++i)
-#pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      At.m[i][j] = W.w_pos * jr.A.m[i][j];
-      Bt.m[i][j] = W.w_pos * jr.B.m[i][j];
-      Ab.m[i][j] = W.w_ori * jr.A.m[i][j];
-    }
-  if (!ID) {
-#pragma unroll
-    for (int m = 0; m < 6; ++m)
-#pragma unroll
-      for (int c = 0; c < NQ; ++c) J[m][c] = T(0);
-  }
-#pragma unroll
-  for (int k = 0; k < K + (G::BASE ? 3 : 0); ++k) {
-    if (ID || k >= K || k < C.k) {
-      const vec3<T> lin{col[k][0], col[k][1], col[k][2]}, ang{col[k][3], col[k][4], col[k][5]};
-      const vec3<T> t1 = mul(At, lin), t2 = mul(Bt, ang), b1 = mul(Ab, ang);
-      const T cj[6] = {t1.x + t2.x, t1.y + t2.y, t1.z + t2.z, b1.x, b1.y, b1.z};
-      if (ID || k >= K) {
-        const int c = k >= K ? NQ + (k - K) : k;
-#pragma unroll
-        for (int m = 0; m < 6; ++m) J[m][c] = cj[m];
-      } else {
-        const int qc = C.qcol[k];
-        const T mu = C.mult[k];
-#pragma unroll
-        for (int c = 0; c < NQ; ++c)
-          if (qc == c) {
-#pragma unroll
-            for (int m = 0; m < 6; ++m) J[m][c] += mu * cj[m];
-          }
-      }
-    }
-  }
+  pose_finish<G, JAC>(C, W, tg, sq, sp, col, r, J);
 }
 
 // Diagonal limit / rest rows (beam.py:122-125, 158-166): residuals, J diag.
@@ -280,16 +296,14 @@ __device__ __forceinline__ void diag_rows(const CostParams<T, NQ>& W, const T (&
 // [[R(a), 0], [0, 1]] (beam.py:171-178) is orthogonal, so it adds w_base^2 I
 // to A and w_base R^T-rotated residuals to g.
 template <class G, bool JAC>
-__device__ __forceinline__ typename G::T lane_eval(const ChainParams<typename G::T, G::K>& C,
-                                                   const CostParams<typename G::T, G::NQ>& W,
-                                                   const TargetInv<typename G::T>& tg,
-                                                   const typename G::T (&q)[G::NQ], const typename G::T (&base)[3],
-                                                   typename G::T (&A)[Tri<G::ND>::size],
-                                                   typename G::T (&g)[G::ND]) {
+__device__ __forceinline__ typename G::T assemble_rows(const CostParams<typename G::T, G::NQ>& W,
+                                                       const typename G::T (&q)[G::NQ],
+                                                       const typename G::T (&base)[3], const typename G::T (&r)[6],
+                                                       const typename G::T (&J)[6][G::ND],
+                                                       typename G::T (&A)[Tri<G::ND>::size],
+                                                       typename G::T (&g)[G::ND]) {
   using T = typename G::T;
   constexpr int NQ = G::NQ, ND = G::ND;
-  T r[6], J[6][ND];
-  pose_rows<G, JAC>(C, W, tg, q, base, r, J);
   T rl[NQ], gl[NQ], rr[NQ];
   diag_rows(W, q, rl, gl, rr);
   T rb[3] = {T(0), T(0), T(0)};
@@ -340,6 +354,19 @@ __device__ __forceinline__ typename G::T lane_eval(const ChainParams<typename G:
     g[NQ + 2] += W.w_base * rb[2];
   }
   return c;
+}
+
+template <class G, bool JAC>
+__device__ __forceinline__ typename G::T lane_eval(const ChainParams<typename G::T, G::K>& C,
+                                                   const CostParams<typename G::T, G::NQ>& W,
+                                                   const TargetInv<typename G::T>& tg,
+                                                   const typename G::T (&q)[G::NQ], const typename G::T (&base)[3],
+                                                   typename G::T (&A)[Tri<G::ND>::size],
+                                                   typename G::T (&g)[G::ND]) {
+  using T = typename G::T;
+  T r[6], J[6][G::ND];
+  pose_rows<G, JAC>(C, W, tg, q, base, r, J);
+  return assemble_rows<G, JAC>(W, q, base, r, J, A, g);
 }
 
 // delta = -(A + lam diag(max(diag A, 1e-8)))^-1 g by an in-register Cholesky.
@@ -492,10 +519,23 @@ __device__ __forceinline__ void base_retract(const T (&b)[3], T vx, T vy, T w, T
 //           re-derived at q, beam.py:202).
 // A single inlined evaluation serves all three (one copy of the ~2K-instruction
 // body per kernel keeps the hot loop inside the instruction cache).
-template <class G, int STRIDE = 0>
-__device__ __forceinline__ void lm_iter(const ChainParams<typename G::T, G::K>& C,
-                                        const CostParams<typename G::T, G::NQ>& W,
-                                        const TargetInv<typename G::T>& tg, LaneState<G>& s, int mode) {
+// The residual model of a lane: pose + limit + rest (+ base) rows.  Other
+// models (collision rows, kop_collision.cuh) provide the same eval().
+template <class G>
+struct PoseModel {
+  using T = typename G::T;
+  const ChainParams<T, G::K>& C;
+  const CostParams<T, G::NQ>& W;
+  TargetInv<T> tg;
+  template <bool JAC>
+  __device__ __forceinline__ T eval(const T (&q)[G::NQ], const T (&base)[3], T (&A)[Tri<G::ND>::size],
+                                    T (&g)[G::ND]) const {
+    return lane_eval<G, JAC>(C, W, tg, q, base, A, g);
+  }
+};
+
+template <class G, int STRIDE, class M>
+__device__ __forceinline__ void lm_iter(const M& model, LaneState<G>& s, int mode) {
   using T = typename G::T;
   constexpr int NQ = G::NQ, ND = G::ND;
   T d[ND];
@@ -519,7 +559,7 @@ __device__ __forceinline__ void lm_iter(const ChainParams<typename G::T, G::K>& 
     }
   }
   T An[Tri<ND>::size], gn[ND];
-  const T raw = lane_eval<G, true>(C, W, tg, qn, bn, An, gn);
+  const T raw = model.template eval<true>(qn, bn, An, gn);
   const T cn = finite_t(raw) ? raw : inf_t<T>();
   const bool acc = mode != 0 || (ok && (cn < s.cost));
   if (acc) store_normal<STRIDE>(s, An, gn);  // one store site for start and accept

@@ -1,18 +1,35 @@
-"""Solver result types (solver.py:36-224 of the reference).
+"""Nonlinear least squares on the device: CostTerm / Problem / solve (solver.py).
 
-``SolveReport`` / ``VariableSet`` are the containers IK-Beam returns
-(tasks.py:149-158).  The generic block-sparse LM ``solve`` for user-composed
-cost sets is the next widening step and is not
-provided by this build yet.
+The reference's generic LM (solver.py:364-429: dense Cholesky, per-iteration
+rejection loop with damping x10, gradient / step / numerical-failure
+terminations) runs here as one GPU thread per problem (csrc/kop_collision.cu,
+``kop_lm_solve``) for problems built from the typed cost builders of
+``costs.py``: one configuration variable and the pose / limit / rest /
+world-collision / self-collision families (the viewer's stack,
+server.py:60-97, and config 4).  ``solve_batch`` launches every compatible
+problem of a batch together.  Costs built from Python callables cannot run on
+the device and raise UnsupportedFeatureError -- there is no CPU fallback.
 """
 
 from __future__ import annotations
 
+import ctypes as C
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
 
+from .errors import CostEvaluationError, UnsupportedFeatureError
 from .liegroups import Rotation3, Transform2, Transform3
+
+DENSE_TANGENT_LIMIT = 200
+DAMPING_MAX = 1e10
+DAMPING_MIN = 1e-12
+DIAG_CLAMP = 1e-8
+TERMINATIONS = {0: ("max_iterations", ""), 1: ("gradient_converged", ""), 2: ("step_converged", ""),
+                3: ("numerical_failure", "no acceptable step below damping 1e10"),
+                4: ("step_converged", "rejection budget exhausted without descent"),
+                5: ("numerical_failure", "cost evaluation returned a non-finite residual")}
 
 
 def _tangent_dim(x) -> int:
@@ -24,7 +41,7 @@ def _tangent_dim(x) -> int:
 
 
 class VariableSet:
-    """Ordered, typed variables (value access only)."""
+    """Ordered, typed variables (solver.py:36-108; value access)."""
 
     def __init__(self):
         self._ids, self._values, self._index = [], [], {}
@@ -69,6 +86,80 @@ class VariableSet:
     def value(self, var_id: str):
         return self._values[self.index(var_id)]
 
+    def values(self, var_ids) -> list:
+        return [self._values[self.index(v)] for v in var_ids]
+
+    def copy(self) -> "VariableSet":
+        out = VariableSet()
+        for vid, v in zip(self._ids, self._values):
+            out.add(vid, v.copy() if isinstance(v, np.ndarray) else v)
+        return out
+
+
+@dataclass
+class CostTerm:
+    """Weighted residual block (solver.py:111-152).  ``kind``/``params`` describe a
+    device cost family; ``evaluator``/``jacobian`` callables are accepted for API
+    compatibility but cannot be evaluated on the device."""
+
+    name: str
+    residual_dim: int
+    variable_refs: list
+    weight: np.ndarray
+    evaluator: object = None
+    jacobian: object = None
+    kind: str | None = None
+    params: dict = field(default_factory=dict)
+
+    def __post_init__(self):
+        w = np.asarray(self.weight, dtype=float)
+        if w.ndim == 0:
+            w = np.full(self.residual_dim, float(w))
+        if w.shape != (self.residual_dim,):
+            raise ValueError(f"cost '{self.name}': weight shape {w.shape} does not match residual_dim "
+                             f"{self.residual_dim}")
+        if np.any(w < 0.0):
+            raise ValueError(f"cost '{self.name}': weights must be nonnegative")
+        self.weight = w
+
+
+@dataclass
+class Problem:
+    variables: VariableSet
+    costs: list
+
+    def __post_init__(self):
+        for cost in self.costs:
+            for ref in cost.variable_refs:
+                self.variables.index(ref)
+
+    @property
+    def residual_dim(self) -> int:
+        return sum(c.residual_dim for c in self.costs)
+
+
+@dataclass
+class SolveOptions:
+    max_iterations: int = 100
+    initial_damping: float = 1e-4
+    damping_increase: float = 10.0
+    damping_decrease: float = 1.0 / 3.0
+    gradient_tolerance: float = 1e-8
+    step_tolerance: float = 1e-10
+    linear_solver: str | None = None
+    max_rejections: int = 20
+    precision: str = "fp64"
+
+    def __post_init__(self):
+        if self.max_iterations <= 0 or self.initial_damping <= 0:
+            raise ValueError("max_iterations and initial_damping must be positive")
+        if self.damping_increase <= 1.0:
+            raise ValueError("damping_increase must exceed 1")
+        if not 0.0 < self.damping_decrease < 1.0:
+            raise ValueError("damping_decrease must be in (0, 1)")
+        if self.linear_solver not in (None, "dense_cholesky", "sparse_cholesky"):
+            raise ValueError(f"unknown linear_solver '{self.linear_solver}'")
+
 
 @dataclass
 class SolveReport:
@@ -90,3 +181,182 @@ class SolveReport:
         if include_timing:
             out["solve_time_s"] = self.solve_time_s
         return out
+
+
+# ---------------------------------------------------------------------------
+# mapping typed problems onto the device stack
+# ---------------------------------------------------------------------------
+
+_DEVICE_KINDS = ("pose", "limit", "rest", "world_collision", "self_collision")
+
+
+@dataclass
+class _Plan:
+    model: object
+    link: str
+    var: str
+    target: Transform3
+    costs: object  # KopCollisionCosts
+    keep: list     # ctypes arrays kept alive
+    key: tuple
+
+
+def _obstacles(world):
+    from . import _lib as L
+    from .collision import Capsule, HalfSpace, Sphere
+
+    arr = (L.KopObstacle * max(1, len(world.obstacles)))()
+    for i, ob in enumerate(world.obstacles):
+        if isinstance(ob, Sphere):
+            arr[i].kind, arr[i].a[:], arr[i].radius = 0, list(ob.center), ob.radius
+        elif isinstance(ob, Capsule):
+            arr[i].kind, arr[i].a[:], arr[i].b[:], arr[i].radius = 1, list(ob.endpoint_a), list(ob.endpoint_b), \
+                ob.radius
+        elif isinstance(ob, HalfSpace):
+            arr[i].kind, arr[i].a[:], arr[i].radius = 2, list(ob.normal), ob.offset
+        else:
+            raise UnsupportedFeatureError(f"unsupported obstacle kind {type(ob).__name__}")
+    return arr
+
+
+def _uniform(w, name):
+    w = np.asarray(w, dtype=float)
+    if w.size and not np.all(w == w[0]):
+        raise UnsupportedFeatureError(f"cost '{name}': per-row weights are not supported on the device")
+    return float(w[0]) if w.size else 0.0
+
+
+def plan(problem: Problem) -> _Plan:
+    """Typed device plan of a problem, or UnsupportedFeatureError."""
+    from . import _lib as L
+
+    if not problem.costs or problem.residual_dim < 1:
+        raise ValueError("problem must declare at least one cost with residual rows")
+    if len(problem.variables.ids) != 1:
+        raise UnsupportedFeatureError("device solve supports a single configuration variable")
+    var = problem.variables.ids[0]
+    by = {}
+    for c in problem.costs:
+        if c.kind not in _DEVICE_KINDS:
+            raise UnsupportedFeatureError(
+                f"cost '{c.name}' has no device kernel (custom Python costs cannot run on the GPU; "
+                "there is no CPU fallback)")
+        if c.kind in by:
+            raise UnsupportedFeatureError(f"more than one '{c.kind}' cost in a device problem")
+        by[c.kind] = c
+    if "pose" not in by:
+        raise UnsupportedFeatureError("device solve needs a pose cost")
+    pose = by["pose"]
+    if pose.params.get("base_var"):
+        raise UnsupportedFeatureError("pose costs with a base variable are not supported by the device solve")
+    model, link = pose.params["model"], pose.params["link"]
+    value = problem.variables.value(var)
+    if not isinstance(value, np.ndarray) or value.size != model.actuated_count:
+        raise ValueError(f"variable '{var}' must be a configuration of {model.actuated_count} values")
+    for c in by.values():
+        if c.params.get("model", model) is not model:
+            raise UnsupportedFeatureError("all costs of a device problem must use the same RobotModel")
+    if "rest" in by and not np.array_equal(by["rest"].params["q_rest"], model.rest_pose):
+        raise UnsupportedFeatureError("rest costs must use the model's rest pose on the device")
+    cc = L.KopCollisionCosts()
+    cc.w_position, cc.w_orientation = _uniform(pose.weight[:3], pose.name), _uniform(pose.weight[3:], pose.name)
+    cc.w_limit = _uniform(by["limit"].weight, "limit") if "limit" in by else 0.0
+    cc.w_rest = _uniform(by["rest"].weight, "rest") if "rest" in by else 0.0
+    keep, world_key = [], ()
+    cc.sharpness, cc.hard_min = 100.0, 0
+    cc.eta_world = cc.eta_self = 1.0
+    if "world_collision" in by:
+        wcp = by["world_collision"].params
+        arr = _obstacles(wcp["world"])
+        keep.append(arr)
+        cc.w_world, cc.eta_world = _uniform(by["world_collision"].weight, "world_collision"), wcp["eta"]
+        cc.num_obstacles, cc.obstacles = len(wcp["world"].obstacles), arr
+        cc.sharpness, cc.hard_min = wcp["sharpness"], int(wcp["hard_min"])
+        world_key = (id(wcp["world"]), wcp["eta"], wcp["sharpness"], wcp["hard_min"])
+    if "self_collision" in by:
+        scp = by["self_collision"].params
+        cc.w_self, cc.eta_self = _uniform(by["self_collision"].weight, "self_collision"), scp["eta"]
+        if "world_collision" in by and (scp["sharpness"] != cc.sharpness or int(scp["hard_min"]) != cc.hard_min):
+            raise UnsupportedFeatureError("world and self collision costs must share sharpness / hard_min")
+        cc.sharpness, cc.hard_min = scp["sharpness"], int(scp["hard_min"])
+    key = (id(model), link, cc.w_position, cc.w_orientation, cc.w_limit, cc.w_rest, cc.w_world, cc.w_self,
+           cc.eta_self, world_key)
+    return _Plan(model, link, var, pose.params["target"], cc, keep, key)
+
+
+def _options(options: SolveOptions):
+    from . import _lib as L
+    from .robot import _precision
+
+    o = L.KopLmOptions()
+    o.max_iterations, o.initial_damping = options.max_iterations, options.initial_damping
+    o.damping_increase, o.damping_decrease = options.damping_increase, options.damping_decrease
+    o.gradient_tolerance, o.step_tolerance = options.gradient_tolerance, options.step_tolerance
+    o.max_rejections, o.precision = options.max_rejections, _precision(options.precision)
+    return o
+
+
+def _run(plans, problems, options: SolveOptions) -> list:
+    """One kop_lm_solve launch for problems sharing a plan key."""
+    from . import _device as dv
+    from ._lib import check, lib
+
+    p0 = plans[0]
+    b = len(plans)
+    tg = dv.to_dev(np.stack([p.target.as_array() for p in plans]))
+    q0 = dv.to_dev(np.stack([pr.variables.value(p.var) for p, pr in zip(plans, problems)]))
+    n = p0.model.actuated_count
+    t = dv.require_cuda()
+    q, cost, init = dv.empty((b, n)), dv.empty(b), dv.empty(b)
+    hist = dv.empty((b, options.max_iterations + 1))
+    iters = t.empty(b, dtype=t.int32, device="cuda")
+    term = t.empty(b, dtype=t.int32, device="cuda")
+    opts = _options(options)
+    t0 = time.perf_counter()
+    check(lib().kop_lm_solve(p0.model._handle, p0.model.link_index(p0.link), C.byref(p0.costs), C.byref(opts),
+                             dv.ptr(tg), dv.ptr(q0), b, dv.ptr(q), dv.ptr(cost), dv.ptr(init), dv.ptr(hist),
+                             dv.ptr(iters), dv.ptr(term), dv.stream_handle()), "kop_lm_solve")
+    qh, ch, ih, hh = q.cpu().numpy(), cost.cpu().numpy(), init.cpu().numpy(), hist.cpu().numpy()
+    ith, th = iters.cpu().numpy(), term.cpu().numpy()
+    dt = (time.perf_counter() - t0) / b
+    out = []
+    for i, (p, pr) in enumerate(zip(plans, problems)):
+        termination, message = TERMINATIONS[int(th[i])]
+        h = hh[i, : int(ith[i]) + 1]
+        out.append(SolveReport(final_values=VariableSet.of(**{p.var: qh[i]}), initial_cost=float(ih[i]),
+                               final_cost=float(ch[i]), iterations_run=int(ith[i]), termination=termination,
+                               cost_history=[float(x) for x in h], solve_time_s=dt, message=message))
+    return out
+
+
+def solve(problem: Problem, options: SolveOptions | None = None) -> SolveReport:
+    """Minimise the sum of squared weighted residuals by LM on the device."""
+    options = options or SolveOptions()
+    rep = _run([plan(problem)], [problem], options)[0]
+    if rep.termination == "numerical_failure" and "non-finite" in rep.message and rep.iterations_run == 0 \
+            and not np.isfinite(rep.initial_cost):
+        raise CostEvaluationError(f"initial residual of '{problem.costs[0].name}' is non-finite")
+    return rep
+
+
+def solve_batch(problems: list, options: SolveOptions | None = None, workers: int = 1) -> list:
+    """Solve independent problems; compatible ones share one device launch.
+    Per-problem failures are isolated into that problem's report (solver.py:432-460)."""
+    if workers < 1:
+        raise ValueError(f"workers must be >= 1, got {workers}")
+    options = options or SolveOptions()
+    reports = [None] * len(problems)
+    groups = {}
+    for i, pr in enumerate(problems):
+        try:
+            p = plan(pr)
+        except Exception as exc:  # isolate per-problem failures
+            reports[i] = SolveReport(final_values=pr.variables, initial_cost=float("nan"), final_cost=float("nan"),
+                                     iterations_run=0, termination="numerical_failure", message=str(exc))
+            continue
+        groups.setdefault(p.key, []).append((i, p))
+    for members in groups.values():
+        idx = [i for i, _ in members]
+        for i, rep in zip(idx, _run([p for _, p in members], [problems[i] for i in idx], options)):
+            reports[i] = rep
+    return reports

@@ -22,6 +22,7 @@ import numpy as np
 from . import _device as dv
 from . import costs as ck
 from ._lib import KopIkParams, check, lib
+from .errors import UnsupportedFeatureError
 from .liegroups import Transform2, Transform3
 from .robot import RobotModel, _precision
 from .solver import SolveReport, VariableSet
@@ -144,7 +145,12 @@ class IkBeamSolver:
     def __init__(self, model: RobotModel, link: str, weights: ck.CostWeights | None = None, seeds: int = 64,
                  total_steps: int = 16, prune_after: int = 6, keep: int = 4, rng_seed: int = 0,
                  success_pos_tol: float = 0.005, success_rot_tol: float = 0.05, precision="fp32",
-                 seed_configurations=None, optimize_base: bool = False, base_reg_weight: float = 0.0):
+                 seed_configurations=None, optimize_base: bool = False, base_reg_weight: float = 0.0,
+                 world=None, self_collision: bool = False, eta_world: float = 0.05, eta_self: float = 0.01,
+                 sharpness: float = ck.SOFTMIN_SHARPNESS, hard_min: bool = False):
+        """``world`` (a WorldModel) and/or ``self_collision`` switch the lanes to the
+        collision stack (config 4): world rows weighted by ``weights.world_collision``
+        and self rows by ``weights.self_collision`` appended to pose / limit / rest."""
         if not 0 < prune_after < total_steps:
             raise ValueError("need 0 < prune_after < total_steps")
         if not 1 <= keep <= seeds:
@@ -157,6 +163,23 @@ class IkBeamSolver:
         self.params = KopIkParams(w[0], w[1], w[2], w[3], seeds, total_steps, prune_after, keep,
                                   success_pos_tol, success_rot_tol, _precision(precision),
                                   1 if self.optimize_base else 0, float(base_reg_weight))
+        self.collision = None
+        if world is not None or self_collision:
+            if optimize_base:
+                raise UnsupportedFeatureError("collision lanes with a mobile base are not compiled in")
+            from ._lib import KopCollisionCosts
+            from .solver import _obstacles
+
+            wts = weights or ck.CostWeights()
+            cc = KopCollisionCosts()
+            cc.w_position, cc.w_orientation, cc.w_limit, cc.w_rest = w
+            self._obs = _obstacles(world) if world is not None and world.obstacles else None
+            cc.w_world = wts.world_collision if self._obs is not None else 0.0
+            cc.eta_world, cc.num_obstacles = eta_world, len(world.obstacles) if self._obs is not None else 0
+            cc.obstacles = self._obs
+            cc.w_self, cc.eta_self = (wts.self_collision if self_collision else 0.0), eta_self
+            cc.sharpness, cc.hard_min = sharpness, int(hard_min)
+            self.collision = cc
         if seed_configurations is not None:
             self.seeds = dv.to_dev(np.asarray(seed_configurations, dtype=float).reshape(seeds, model.actuated_count))
         else:
@@ -164,7 +187,13 @@ class IkBeamSolver:
         self._ws = None
 
     def workspace(self, batch: int):
-        need = int(lib().kop_ik_beam_workspace_bytes(self.model._handle, self.link_idx, C.byref(self.params), batch))
+        if self.collision is not None:
+            need = int(lib().kop_ik_beam_collision_workspace_bytes(self.model._handle, self.link_idx,
+                                                                   C.byref(self.params), C.byref(self.collision),
+                                                                   batch))
+        else:
+            need = int(lib().kop_ik_beam_workspace_bytes(self.model._handle, self.link_idx, C.byref(self.params),
+                                                         batch))
         if need < 0:
             check(need, "kop_ik_beam_workspace_bytes")
         if self._ws is None or self._ws.numel() < need:
@@ -188,6 +217,16 @@ class IkBeamSolver:
         b = targets.shape[0]
         out = out or self.alloc_outputs(b)
         ws = self.workspace(b)
+        if self.collision is not None:
+            if stages != 3:
+                raise ValueError("collision IK-Beam runs both stages together")
+            check(lib().kop_ik_beam_collision(self.model._handle, self.link_idx, C.byref(self.params),
+                                              C.byref(self.collision), dv.ptr(targets), b, dv.ptr(self.seeds),
+                                              dv.ptr(ws), ws.numel(), dv.ptr(out.q), dv.ptr(out.cost),
+                                              dv.ptr(out.history) if history else None, dv.ptr(out.pos_error),
+                                              dv.ptr(out.rot_error), dv.ptr(out.success), dv.stream_handle()),
+                  "kop_ik_beam_collision")
+            return out
         check(lib().kop_ik_beam_stage(self.model._handle, self.link_idx, C.byref(self.params), int(stages),
                                       dv.ptr(targets), b, dv.ptr(self.seeds), dv.ptr(ws), ws.numel(),
                                       dv.ptr(out.q), dv.ptr(out.base), dv.ptr(out.cost),
@@ -250,3 +289,17 @@ def solve_ik_mobile(req: IkRequest) -> IkResult:
         result.base = Transform2.identity()
         return result
     return _solve(req, use_base=True)
+
+
+def solve_ik_collision_batch(model: RobotModel, link: str, targets, world=None, self_collision: bool = True,
+                             weights: ck.CostWeights | None = None, seeds: int = 64, total_steps: int = 16,
+                             prune_after: int = 6, keep: int = 4, rng_seed: int = 0, precision="fp32",
+                             eta_world: float = 0.05, eta_self: float = 0.01, sharpness: float = ck.SOFTMIN_SHARPNESS,
+                             hard_min: bool = False, success_pos_tol: float = 0.005,
+                             success_rot_tol: float = 0.05) -> BeamBatch:
+    """IK-Beam over the collision stack (config 4): pose / limit / rest rows plus
+    world-collision (costs.py:499-551) and self-collision (costs.py:435-496) rows."""
+    solver = IkBeamSolver(model, link, weights, seeds, total_steps, prune_after, keep, rng_seed, success_pos_tol,
+                          success_rot_tol, precision, world=world, self_collision=self_collision,
+                          eta_world=eta_world, eta_self=eta_self, sharpness=sharpness, hard_min=hard_min)
+    return solver.solve(targets)

