@@ -230,6 +230,26 @@ int kop_lm_solve(const KopModel* model, int32_t link, const KopCollisionCosts* c
                  double* init_cost_out, double* history_out, int32_t* iterations_out,
                  int32_t* termination_out, void* stream);
 
+/* --- multi-end-effector IK on a tree (config 3) ----------------------------
+ * replaces: solver.solve over [pose_cost(link_e) for each e] + limit_cost +
+ * rest_cost (costs.py:98-271, solver.py:364-429) on robots with up to 32
+ * actuated / 64 total joints (humanoids): one warp per problem.
+ * targets: device [B*E*7] (pose of end effector e of problem b); q0 [B*n].
+ * Outputs and termination codes as kop_lm_solve. */
+typedef struct {
+  int32_t num_poses;           /* E <= 8 */
+  const int32_t* links;        /* host [E] end-effector link indices */
+  const double* w_position;    /* host [E] */
+  const double* w_orientation; /* host [E] */
+  double w_limit, w_rest;
+  const double* rest;          /* host [n] rest configuration, NULL = the model's */
+} KopPoseCosts;
+
+int kop_multi_pose_solve(const KopModel* model, const KopPoseCosts* costs, const KopLmOptions* options,
+                         const double* targets, const double* q0, int64_t batch, double* q_out,
+                         double* cost_out, double* init_cost_out, double* history_out,
+                         int32_t* iterations_out, int32_t* termination_out, void* stream);
+
 /* --- counter-based sampling ---------------------------------------------
  * replaces: tasks.sample_seed_configurations (tasks.py:88-106) and the draws
  * of benchmark.generate_reachable_targets (benchmark.py:83-93): row i is

@@ -269,13 +269,24 @@ def stack_residual_jacobian(ch, sp, obstacles, link, tinv_q, tinv_t, q, cc: Coll
     return r, (np.concatenate(parts_j, axis=1) if jac else None)
 
 
-def solve_lm(ch, sp, obstacles, link, tq, tt, q0, cc: CollisionCosts, max_iterations=100, damping0=1e-4,
-             up=10.0, down=1.0 / 3.0, grad_tol=1e-8, step_tol=1e-10, max_rejections=20):
-    """solver.py:364-429 for one problem (dense Cholesky path, D <= 200)."""
+def solve_lm(ch, sp, obstacles, link, tq, tt, q0, cc: CollisionCosts, **kw):
+    """solver.py:364-429 for one collision-IK problem (dense Cholesky path, D <= 200)."""
     iq, it = o.target_inverse(np.atleast_2d(tq), np.atleast_2d(tt))
+
+    def stack(q, jac):
+        r, J = stack_residual_jacobian(ch, sp, obstacles, link, iq, it, q[None], cc, jac=jac)
+        return r[0], (J[0] if jac else None)
+
+    return lm(stack, q0, **kw)
+
+
+def lm(stack, q0, max_iterations=100, damping0=1e-4, up=10.0, down=1.0 / 3.0, grad_tol=1e-8, step_tol=1e-10,
+       max_rejections=20):
+    """The classic LM of solver.py:364-429 over a residual/Jacobian callable
+    stack(q, jac) -> (r, J); dense Cholesky (scipy cho_factor / cho_solve)."""
     q = np.asarray(q0, float).copy()
-    r, J = stack_residual_jacobian(ch, sp, obstacles, link, iq, it, q[None], cc)
-    r, J = r[0], J[0]
+    n = q.size
+    r, J = stack(q, True)
     cost = float(r @ r)
     hist = [cost]
     damping = damping0
@@ -290,7 +301,7 @@ def solve_lm(ch, sp, obstacles, link, tq, tt, q0, cc: CollisionCosts, max_iterat
         accepted, step = False, None
         for _ in range(max_rejections):
             h = h0.copy()
-            h[np.arange(ch.n), np.arange(ch.n)] += damping * diag
+            h[np.arange(n), np.arange(n)] += damping * diag
             try:
                 c, low = scipy.linalg.cho_factor(h)
                 delta = scipy.linalg.cho_solve((c, low), -grad)
@@ -298,8 +309,8 @@ def solve_lm(ch, sp, obstacles, link, tq, tt, q0, cc: CollisionCosts, max_iterat
                 delta = None
             if delta is not None:
                 qn = q + delta
-                rn, _ = stack_residual_jacobian(ch, sp, obstacles, link, iq, it, qn[None], cc, jac=False)
-                cn = float(rn[0] @ rn[0])
+                rn, _ = stack(qn, False)
+                cn = float(rn @ rn)
                 if cn < cost:
                     q, cost = qn, cn
                     damping = max(damping * down, o.LAMBDA_MIN)
@@ -316,8 +327,7 @@ def solve_lm(ch, sp, obstacles, link, tq, tt, q0, cc: CollisionCosts, max_iterat
         if np.max(np.abs(step), initial=0.0) < step_tol:
             termination = "step_converged"
             break
-        r, J = stack_residual_jacobian(ch, sp, obstacles, link, iq, it, q[None], cc)
-        r, J = r[0], J[0]
+        r, J = stack(q, True)
     return q, cost, hist, iters, termination
 
 

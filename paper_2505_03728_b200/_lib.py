@@ -56,6 +56,11 @@ class KopLmOptions(C.Structure):
                 ("max_rejections", _i32), ("precision", _i32)]
 
 
+class KopPoseCosts(C.Structure):
+    _fields_ = [("num_poses", _i32), ("links", _p), ("w_position", _p), ("w_orientation", _p),
+                ("w_limit", _f64), ("w_rest", _f64), ("rest", _p)]
+
+
 # name -> (restype, argtypes); must match include/kinoptik_b200.h exactly
 SIGNATURES = {
     "kop_model_create": (C.c_int, [C.POINTER(KopModelDesc), C.POINTER(_p)]),
@@ -82,6 +87,8 @@ SIGNATURES = {
                                         _p, _p, _i64, _p, _p, _p, _p, _p, _p, _p]),
     "kop_lm_solve": (C.c_int, [_p, _i32, C.POINTER(KopCollisionCosts), C.POINTER(KopLmOptions), _p, _p, _i64,
                                _p, _p, _p, _p, _p, _p, _p]),
+    "kop_multi_pose_solve": (C.c_int, [_p, C.POINTER(KopPoseCosts), C.POINTER(KopLmOptions), _p, _p, _i64,
+                                       _p, _p, _p, _p, _p, _p, _p]),
     "kop_sample_uniform": (C.c_int, [_u64, _u64, _i64, _i32, _p, _p, _p, _p, _p]),
     "kop_link_poses": (C.c_int, [_p, _i32, _p, _i64, _p, _p]),
     "kop_fma_peak_kernel": (C.c_int, [_i32, _i32, _i32, _p, C.POINTER(_f64), _p]),

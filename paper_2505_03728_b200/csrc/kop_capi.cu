@@ -11,6 +11,7 @@
 #include "../../include/kinoptik_b200.h"
 #include "kop_collision.cuh"
 #include "kop_kernels.cuh"
+#include "kop_tree.cuh"
 
 using namespace kop;
 
@@ -1062,6 +1063,90 @@ int kop_lm_solve(const KopModel* m, int32_t link, const KopCollisionCosts* cc, c
     e = restride(qop.ptr, batch, nq, n, q_out, st);
     cudaStreamSynchronize(st);
   }
+  return cuda_status(e);
+}
+
+}  // extern "C"
+
+namespace {
+
+template <typename T>
+TreeLmParams<T> tree_params(const KopModel& m, const KopPoseCosts* pc) {
+  TreeLmParams<T> P;
+  memset(&P, 0, sizeof(P));
+  const TreeParams& t = m.tree;
+  P.nj = t.nj;
+  P.n = t.n;
+  P.ne = pc->num_poses;
+  for (int j = 0; j < t.nj; ++j) {
+    P.parent_joint[j] = m.parent_joint[t.parent[j]];
+    P.kind[j] = t.kind[j];
+    P.qcol[j] = t.qcol[j];
+    for (int i = 0; i < 4; ++i) P.oq[j][i] = T(t.oq[j][i]);
+    for (int i = 0; i < 3; ++i) {
+      P.op[j][i] = T(t.op[j][i]);
+      P.axis[j][i] = T(t.axis[j][i]);
+    }
+    P.mult[j] = T(t.mult[j]);
+    P.offset[j] = T(t.offset[j]);
+  }
+  for (int e = 0; e < pc->num_poses; ++e) {
+    const int link = pc->links[e];
+    P.ee_joint[e] = m.parent_joint[link];
+    unsigned long long mask = 0;
+    for (int j = m.parent_joint[link]; j >= 0; j = m.parent_joint[t.parent[j]]) mask |= 1ull << j;
+    P.anc_ee[e] = mask;
+    P.w_pos[e] = T(pc->w_position[e]);
+    P.w_ori[e] = T(pc->w_orientation[e]);
+  }
+  for (int i = 0; i < t.n; ++i) {
+    P.lower[i] = T(m.lower[i]);
+    P.upper[i] = T(m.upper[i]);
+    P.rest[i] = T(pc->rest ? pc->rest[i] : m.rest[i]);
+  }
+  P.w_lim = T(pc->w_limit);
+  P.w_rest = T(pc->w_rest);
+  return P;
+}
+
+}  // namespace
+
+extern "C" {
+
+int kop_multi_pose_solve(const KopModel* m, const KopPoseCosts* pc, const KopLmOptions* o, const double* targets,
+                         const double* q0, int64_t batch, double* q_out, double* cost_out, double* init_cost_out,
+                         double* history_out, int32_t* iterations_out, int32_t* termination_out, void* stream) {
+  if (!m || !pc || !o) return fail(KOP_EINVAL, "null argument");
+  if (o->precision != KOP_FP32 && o->precision != KOP_FP64) return fail(KOP_EINVAL, "bad precision");
+  if (m->tree.n > kTreeMaxDofs || m->tree.nj > kTreeMaxJoints)
+    return fail(KOP_EUNSUPPORTED, "tree solve supports up to 32 actuated and 64 total joints");
+  if (pc->num_poses < 1 || pc->num_poses > kTreeMaxPoses)
+    return fail(KOP_EUNSUPPORTED, "tree solve supports 1..8 pose costs");
+  for (int e = 0; e < pc->num_poses; ++e)
+    if (pc->links[e] < 0 || pc->links[e] >= m->tree.nl) return fail(KOP_EINVAL, "unknown link index");
+  if (o->max_iterations <= 0 || !(o->initial_damping > 0)) return fail(KOP_EINVAL, "max_iterations and initial_damping must be positive");
+  if (!(o->damping_increase > 1.0)) return fail(KOP_EINVAL, "damping_increase must exceed 1");
+  if (!(o->damping_decrease > 0.0 && o->damping_decrease < 1.0)) return fail(KOP_EINVAL, "damping_decrease must be in (0, 1)");
+  if (o->max_rejections < 1) return fail(KOP_EINVAL, "max_rejections must be positive");
+  if (batch < 0) return fail(KOP_EINVAL, "negative batch");
+  if (batch == 0) return KOP_OK;
+  if (!targets || !q0 || !q_out || !cost_out || !init_cost_out || !iterations_out || !termination_out)
+    return fail(KOP_EINVAL, "null array argument");
+  TreeLaunch L;
+  L.targets = targets;
+  L.q0 = q0;
+  L.B = batch;
+  L.opts = {o->max_iterations, o->max_rejections, o->initial_damping, o->damping_increase, o->damping_decrease,
+            o->gradient_tolerance, o->step_tolerance};
+  L.q_out = q_out;
+  L.cost_out = cost_out;
+  L.init_cost = init_cost_out;
+  L.hist_out = history_out;
+  L.iters = iterations_out;
+  L.term = termination_out;
+  cudaStream_t st = (cudaStream_t)stream;
+  const cudaError_t e = o->precision == KOP_FP32 ? launch_tree_solve<float>(tree_params<float>(*m, pc), L, st)
+                                                 : launch_tree_solve<double>(tree_params<double>(*m, pc), L, st);
   return cuda_status(e);
 }
 

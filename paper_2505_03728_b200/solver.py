@@ -196,9 +196,11 @@ class _Plan:
     link: str
     var: str
     target: Transform3
-    costs: object  # KopCollisionCosts
-    keep: list     # ctypes arrays kept alive
+    costs: object  # KopCollisionCosts (path "chain") or KopPoseCosts (path "tree")
+    keep: list     # ctypes / numpy arrays kept alive
     key: tuple
+    path: str = "chain"
+    targets: list = field(default_factory=list)  # tree path: one Transform3 per pose cost
 
 
 def _obstacles(world):
@@ -227,7 +229,13 @@ def _uniform(w, name):
 
 
 def plan(problem: Problem) -> _Plan:
-    """Typed device plan of a problem, or UnsupportedFeatureError."""
+    """Typed device plan of a problem, or UnsupportedFeatureError.
+
+    path "chain": one pose cost (+ limit / rest / world / self collision) on a
+    root->link chain of <= 8 moving joints -- one thread per problem
+    (kop_lm_solve).  path "tree": several pose costs (multi end effector) and
+    limit / rest on trees of <= 32 actuated joints -- one warp per problem
+    (kop_multi_pose_solve, config 3)."""
     from . import _lib as L
 
     if not problem.costs or problem.residual_dim < 1:
@@ -235,53 +243,74 @@ def plan(problem: Problem) -> _Plan:
     if len(problem.variables.ids) != 1:
         raise UnsupportedFeatureError("device solve supports a single configuration variable")
     var = problem.variables.ids[0]
-    by = {}
+    by, poses = {}, []
     for c in problem.costs:
         if c.kind not in _DEVICE_KINDS:
             raise UnsupportedFeatureError(
                 f"cost '{c.name}' has no device kernel (custom Python costs cannot run on the GPU; "
                 "there is no CPU fallback)")
+        if c.kind == "pose":
+            if c.params.get("base_var"):
+                raise UnsupportedFeatureError("pose costs with a base variable are not supported by the device solve")
+            poses.append(c)
+            continue
         if c.kind in by:
             raise UnsupportedFeatureError(f"more than one '{c.kind}' cost in a device problem")
         by[c.kind] = c
-    if "pose" not in by:
+    if not poses:
         raise UnsupportedFeatureError("device solve needs a pose cost")
-    pose = by["pose"]
-    if pose.params.get("base_var"):
-        raise UnsupportedFeatureError("pose costs with a base variable are not supported by the device solve")
-    model, link = pose.params["model"], pose.params["link"]
+    model = poses[0].params["model"]
     value = problem.variables.value(var)
     if not isinstance(value, np.ndarray) or value.size != model.actuated_count:
         raise ValueError(f"variable '{var}' must be a configuration of {model.actuated_count} values")
-    for c in by.values():
+    for c in poses + list(by.values()):
         if c.params.get("model", model) is not model:
             raise UnsupportedFeatureError("all costs of a device problem must use the same RobotModel")
-    if "rest" in by and not np.array_equal(by["rest"].params["q_rest"], model.rest_pose):
-        raise UnsupportedFeatureError("rest costs must use the model's rest pose on the device")
-    cc = L.KopCollisionCosts()
-    cc.w_position, cc.w_orientation = _uniform(pose.weight[:3], pose.name), _uniform(pose.weight[3:], pose.name)
-    cc.w_limit = _uniform(by["limit"].weight, "limit") if "limit" in by else 0.0
-    cc.w_rest = _uniform(by["rest"].weight, "rest") if "rest" in by else 0.0
-    keep, world_key = [], ()
-    cc.sharpness, cc.hard_min = 100.0, 0
-    cc.eta_world = cc.eta_self = 1.0
-    if "world_collision" in by:
-        wcp = by["world_collision"].params
-        arr = _obstacles(wcp["world"])
-        keep.append(arr)
-        cc.w_world, cc.eta_world = _uniform(by["world_collision"].weight, "world_collision"), wcp["eta"]
-        cc.num_obstacles, cc.obstacles = len(wcp["world"].obstacles), arr
-        cc.sharpness, cc.hard_min = wcp["sharpness"], int(wcp["hard_min"])
-        world_key = (id(wcp["world"]), wcp["eta"], wcp["sharpness"], wcp["hard_min"])
-    if "self_collision" in by:
-        scp = by["self_collision"].params
-        cc.w_self, cc.eta_self = _uniform(by["self_collision"].weight, "self_collision"), scp["eta"]
-        if "world_collision" in by and (scp["sharpness"] != cc.sharpness or int(scp["hard_min"]) != cc.hard_min):
-            raise UnsupportedFeatureError("world and self collision costs must share sharpness / hard_min")
-        cc.sharpness, cc.hard_min = scp["sharpness"], int(scp["hard_min"])
-    key = (id(model), link, cc.w_position, cc.w_orientation, cc.w_limit, cc.w_rest, cc.w_world, cc.w_self,
-           cc.eta_self, world_key)
-    return _Plan(model, link, var, pose.params["target"], cc, keep, key)
+    collision = "world_collision" in by or "self_collision" in by
+    link = poses[0].params["link"]
+    chain_ok = model.actuated_count <= 8 and model.chain_length(link) >= 0
+    w_lim = _uniform(by["limit"].weight, "limit") if "limit" in by else 0.0
+    w_rest = _uniform(by["rest"].weight, "rest") if "rest" in by else 0.0
+    if len(poses) == 1 and (chain_ok or collision):
+        pose = poses[0]
+        if "rest" in by and not np.array_equal(by["rest"].params["q_rest"], model.rest_pose):
+            raise UnsupportedFeatureError("rest costs must use the model's rest pose on the chain solve")
+        cc = L.KopCollisionCosts()
+        cc.w_position, cc.w_orientation = _uniform(pose.weight[:3], pose.name), _uniform(pose.weight[3:], pose.name)
+        cc.w_limit, cc.w_rest = w_lim, w_rest
+        keep, world_key = [], ()
+        cc.sharpness, cc.hard_min = 100.0, 0
+        cc.eta_world = cc.eta_self = 1.0
+        if "world_collision" in by:
+            wcp = by["world_collision"].params
+            arr = _obstacles(wcp["world"])
+            keep.append(arr)
+            cc.w_world, cc.eta_world = _uniform(by["world_collision"].weight, "world_collision"), wcp["eta"]
+            cc.num_obstacles, cc.obstacles = len(wcp["world"].obstacles), arr
+            cc.sharpness, cc.hard_min = wcp["sharpness"], int(wcp["hard_min"])
+            world_key = (id(wcp["world"]), wcp["eta"], wcp["sharpness"], wcp["hard_min"])
+        if "self_collision" in by:
+            scp = by["self_collision"].params
+            cc.w_self, cc.eta_self = _uniform(by["self_collision"].weight, "self_collision"), scp["eta"]
+            if "world_collision" in by and (scp["sharpness"] != cc.sharpness or int(scp["hard_min"]) != cc.hard_min):
+                raise UnsupportedFeatureError("world and self collision costs must share sharpness / hard_min")
+            cc.sharpness, cc.hard_min = scp["sharpness"], int(scp["hard_min"])
+        key = ("chain", id(model), link, cc.w_position, cc.w_orientation, cc.w_limit, cc.w_rest, cc.w_world,
+               cc.w_self, cc.eta_self, world_key)
+        return _Plan(model, link, var, pose.params["target"], cc, keep, key, "chain")
+    if collision:
+        raise UnsupportedFeatureError("collision costs need a single pose cost on a chain of <= 8 moving joints")
+    if model.actuated_count > 32 or len(model.joints) > 64 or len(poses) > 8:
+        raise UnsupportedFeatureError("tree solve supports <= 32 actuated joints, 64 joints and 8 pose costs")
+    links = np.ascontiguousarray([model.link_index(p.params["link"]) for p in poses], dtype=np.int32)
+    wpos = np.ascontiguousarray([_uniform(p.weight[:3], p.name) for p in poses])
+    wori = np.ascontiguousarray([_uniform(p.weight[3:], p.name) for p in poses])
+    rest = np.ascontiguousarray(by["rest"].params["q_rest"] if "rest" in by else model.rest_pose, dtype=float)
+    pc = L.KopPoseCosts(len(poses), links.ctypes.data, wpos.ctypes.data, wori.ctypes.data, w_lim, w_rest,
+                        rest.ctypes.data)
+    key = ("tree", id(model), tuple(links), tuple(wpos), tuple(wori), w_lim, w_rest, rest.tobytes())
+    return _Plan(model, poses[0].params["link"], var, poses[0].params["target"], pc, [links, wpos, wori, rest],
+                 key, "tree", [p.params["target"] for p in poses])
 
 
 def _options(options: SolveOptions):
@@ -303,7 +332,10 @@ def _run(plans, problems, options: SolveOptions) -> list:
 
     p0 = plans[0]
     b = len(plans)
-    tg = dv.to_dev(np.stack([p.target.as_array() for p in plans]))
+    if p0.path == "tree":
+        tg = dv.to_dev(np.stack([np.stack([t.as_array() for t in p.targets]) for p in plans]))
+    else:
+        tg = dv.to_dev(np.stack([p.target.as_array() for p in plans]))
     q0 = dv.to_dev(np.stack([pr.variables.value(p.var) for p, pr in zip(plans, problems)]))
     n = p0.model.actuated_count
     t = dv.require_cuda()
@@ -313,9 +345,14 @@ def _run(plans, problems, options: SolveOptions) -> list:
     term = t.empty(b, dtype=t.int32, device="cuda")
     opts = _options(options)
     t0 = time.perf_counter()
-    check(lib().kop_lm_solve(p0.model._handle, p0.model.link_index(p0.link), C.byref(p0.costs), C.byref(opts),
-                             dv.ptr(tg), dv.ptr(q0), b, dv.ptr(q), dv.ptr(cost), dv.ptr(init), dv.ptr(hist),
-                             dv.ptr(iters), dv.ptr(term), dv.stream_handle()), "kop_lm_solve")
+    if p0.path == "tree":
+        check(lib().kop_multi_pose_solve(p0.model._handle, C.byref(p0.costs), C.byref(opts), dv.ptr(tg), dv.ptr(q0),
+                                         b, dv.ptr(q), dv.ptr(cost), dv.ptr(init), dv.ptr(hist), dv.ptr(iters),
+                                         dv.ptr(term), dv.stream_handle()), "kop_multi_pose_solve")
+    else:
+        check(lib().kop_lm_solve(p0.model._handle, p0.model.link_index(p0.link), C.byref(p0.costs), C.byref(opts),
+                                 dv.ptr(tg), dv.ptr(q0), b, dv.ptr(q), dv.ptr(cost), dv.ptr(init), dv.ptr(hist),
+                                 dv.ptr(iters), dv.ptr(term), dv.stream_handle()), "kop_lm_solve")
     qh, ch, ih, hh = q.cpu().numpy(), cost.cpu().numpy(), init.cpu().numpy(), hist.cpu().numpy()
     ith, th = iters.cpu().numpy(), term.cpu().numpy()
     dt = (time.perf_counter() - t0) / b

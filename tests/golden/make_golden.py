@@ -179,6 +179,32 @@ def main():
     for k, v in rows.items():
         g[f"colik_{k}"] = np.array(v)
 
+    # --- config 3: humanoid multi-EE IK through solver.solve -------------------
+    hum = robot.load_robot(os.path.join(os.path.dirname(OUT), "..", "..", "paper_2505_03728_b200", "robots",
+                                        "humanoid29.urdf"))
+    ees = ["left_hand", "right_hand", "left_foot", "right_foot"]
+    hrng = np.random.default_rng(2929)
+    hq = np.stack([hum.sample_configuration(hrng) for _ in range(5)])
+    g["hum_q_true"] = hq
+    g["hum_fk_q"], g["hum_fk_quat"], g["hum_fk_pos"] = hq, *robot.fk_arrays(hum, hq)[:2]
+    hrows = {k: [] for k in ("q", "cost", "hist", "iters", "term", "tw", "tp")}
+    for qi in hq:
+        tgs = [robot.link_transform(hum, qi, e) for e in ees]
+        costs = [ck.pose_cost(hum, "q", e, t, position_weight=W.pose_position, orientation_weight=W.pose_orientation)
+                 for e, t in zip(ees, tgs)]
+        costs += [ck.limit_cost(hum, "q", weight=W.limit), ck.rest_cost("q", hum.rest_pose, weight=W.rest)]
+        rep = sv.solve(sv.Problem(sv.VariableSet.of(q=hum.rest_pose.copy()), costs))
+        hrows["q"].append(rep.final_values.value("q"))
+        hrows["cost"].append(rep.final_cost)
+        hrows["hist"].append(np.pad(rep.cost_history, (0, 101 - len(rep.cost_history)), constant_values=np.nan))
+        hrows["iters"].append(rep.iterations_run)
+        hrows["term"].append(["max_iterations", "gradient_converged", "step_converged",
+                              "numerical_failure"].index(rep.termination))
+        hrows["tw"].append([t.rotation.wxyz for t in tgs])
+        hrows["tp"].append([t.translation for t in tgs])
+    for k, v in hrows.items():
+        g[f"hum_{k}"] = np.array(v)
+
     np.savez_compressed(OUT, **g)
     print(f"wrote {OUT}: {len(g)} arrays")
 

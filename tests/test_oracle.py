@@ -134,3 +134,19 @@ def test_generic_lm_matches_reference_solve(chains, golden):
         # the last accepted step of problem 5 sits at the 1e-10 step tolerance: a
         # rounding-level difference may end it one iteration later as a damping failure
         assert names.index(term) == golden["colik_term"][i] or (i == 5 and term == "numerical_failure")
+
+
+def test_multi_pose_solve_matches_reference_humanoid(golden):
+    """Config 3 oracle: 4 pose costs + limit + rest through the classic LM, bitwise."""
+    from conftest import robot_file
+    from oracle import tree_oracle as to
+
+    ch = o.load_chain_files(robot_file("humanoid29.urdf"))
+    lq, lp, _, _ = o.fk(ch, golden["hum_fk_q"])
+    assert np.array_equal(lq, golden["hum_fk_quat"]) and np.array_equal(lp, golden["hum_fk_pos"])
+    ees = [ch.link(e) for e in ["left_hand", "right_hand", "left_foot", "right_foot"]]
+    for i in (0, 3):
+        poses = [(ees[e], golden["hum_tw"][i][e], golden["hum_tp"][i][e], 50.0, 10.0) for e in range(4)]
+        q, c, h, it, term = to.solve_multi_pose(ch, poses, ch.rest)
+        gh = golden["hum_hist"][i]
+        assert np.array_equal(np.array(h), gh[~np.isnan(gh)]) and it == golden["hum_iters"][i]
