@@ -250,6 +250,56 @@ int kop_multi_pose_solve(const KopModel* model, const KopPoseCosts* costs, const
                          double* cost_out, double* init_cost_out, double* history_out,
                          int32_t* iterations_out, int32_t* termination_out, void* stream);
 
+/* --- trajectory optimisation (config 5) -----------------------------------
+ * replaces: the solve(...) call of plan_trajectory (tasks.py:347-403) over
+ * its cost set -- anchors at q_0 / q_{T-1} (w_anchor), per-pair smoothness
+ * and velocity limit, five-point acceleration / jerk stencils over
+ * t = 2..T-3, per-timestep limit, rest (w_rest), self (w_self, eta_self)
+ * and world (w_world, eta_world) collision, and swept-capsule world rows for
+ * every consecutive pair -- solved by solver.solve (solver.py:364-429), plus
+ * trajectory_signed_distances (tasks.py:251-275) at the solution.
+ * `link` is the chain link (the trajectory's target link) whose root->link
+ * chain carries every collision sphere.  One CTA per trajectory, 5 <= T <= 64.
+ * Device arrays: q_init [B*T*n] (initial trajectories) or NULL,
+ * anchors [B*2*n] (q_start, q_goal), obstacles [B*num_obstacles*8] =
+ * (kind, a[3], b[3], radius|offset) in the robot base frame, unit normals.
+ * q_init NULL = the straight line between the anchors (tasks.py:344-345).
+ * Outputs: q [B*T*n], cost / initial cost [B], history
+ * [B*(max_iterations+1)] (NULL ok), iterations / termination [B] (codes of
+ * kop_lm_solve). */
+typedef struct {
+  int32_t timesteps;
+  double dt;
+  double w_anchor, w_smoothness, w_velocity, w_acceleration, w_jerk, w_limit, w_rest;
+  double w_self, eta_self, w_world, eta_world, sharpness;
+  int32_t hard_min;
+  const double* velocity_limits; /* host [n], +inf where unlimited; NULL = all unlimited */
+  const double* rest;            /* host [n], NULL = the model's rest pose */
+} KopTrajCosts;
+
+int kop_traj_solve(const KopModel* model, int32_t link, const KopTrajCosts* costs, const KopLmOptions* options,
+                   const double* q_init, const double* anchors, const double* obstacles, int32_t num_obstacles,
+                   int64_t batch, double* q_out, double* cost_out, double* init_cost_out, double* history_out,
+                   int32_t* iterations_out, int32_t* termination_out, void* stream);
+/* replaces: solver.assemble + _normal_equation_parts (solver.py:287-343) on
+ * the plan_trajectory Problem: cost r.r [B], gradient J^T r [B*T*n] and
+ * J^T J [B*(T*n)^2] (dense, zero outside the band) at trajectories qs
+ * [B*T*n] -- the parity hook of kop_traj_solve (device arrays). */
+int kop_traj_normal_equations(const KopModel* model, int32_t link, const KopTrajCosts* costs, int32_t precision,
+                              const double* qs, const double* anchors, const double* obstacles,
+                              int32_t num_obstacles, int64_t batch, double* cost_out, double* grad_out,
+                              double* hess_out, void* stream);
+/* replaces: trajectory_signed_distances (tasks.py:251-275) and the endpoint
+ * _pose_errors of plan_trajectory (tasks.py:412-415), FP64, for B
+ * trajectories qs [B*T*n] (device): static [B*T], swept [B*(T-1)], and
+ * their minima [B] (+inf without obstacles); with targets [B*2*7] (start,
+ * goal poses; NULL skips) pos_err / rot_err [B*2].  Output pointers may be
+ * NULL except pos_err / rot_err when targets is given. */
+int kop_traj_report(const KopModel* model, int32_t link, int32_t timesteps, const double* qs,
+                    const double* obstacles, int32_t num_obstacles, const double* targets, int64_t batch,
+                    double* static_out, double* swept_out, double* min_static, double* min_swept,
+                    double* pos_err, double* rot_err, void* stream);
+
 /* --- counter-based sampling ---------------------------------------------
  * replaces: tasks.sample_seed_configurations (tasks.py:88-106) and the draws
  * of benchmark.generate_reachable_targets (benchmark.py:83-93): row i is

@@ -56,6 +56,13 @@ class KopLmOptions(C.Structure):
                 ("max_rejections", _i32), ("precision", _i32)]
 
 
+class KopTrajCosts(C.Structure):
+    _fields_ = [("timesteps", _i32), ("dt", _f64)] + \
+               [(f, _f64) for f in ("w_anchor", "w_smoothness", "w_velocity", "w_acceleration", "w_jerk", "w_limit",
+                                    "w_rest", "w_self", "eta_self", "w_world", "eta_world", "sharpness")] + \
+               [("hard_min", _i32), ("velocity_limits", C.POINTER(_f64)), ("rest", C.POINTER(_f64))]
+
+
 class KopPoseCosts(C.Structure):
     _fields_ = [("num_poses", _i32), ("links", _p), ("w_position", _p), ("w_orientation", _p),
                 ("w_limit", _f64), ("w_rest", _f64), ("rest", _p)]
@@ -89,6 +96,11 @@ SIGNATURES = {
                                _p, _p, _p, _p, _p, _p, _p]),
     "kop_multi_pose_solve": (C.c_int, [_p, C.POINTER(KopPoseCosts), C.POINTER(KopLmOptions), _p, _p, _i64,
                                        _p, _p, _p, _p, _p, _p, _p]),
+    "kop_traj_solve": (C.c_int, [_p, _i32, C.POINTER(KopTrajCosts), C.POINTER(KopLmOptions), _p, _p, _p, _i32,
+                                 _i64, _p, _p, _p, _p, _p, _p, _p]),
+    "kop_traj_normal_equations": (C.c_int, [_p, _i32, C.POINTER(KopTrajCosts), _i32, _p, _p, _p, _i32, _i64, _p,
+                                            _p, _p, _p]),
+    "kop_traj_report": (C.c_int, [_p, _i32, _i32, _p, _p, _i32, _p, _i64, _p, _p, _p, _p, _p, _p, _p]),
     "kop_sample_uniform": (C.c_int, [_u64, _u64, _i64, _i32, _p, _p, _p, _p, _p]),
     "kop_link_poses": (C.c_int, [_p, _i32, _p, _i64, _p, _p]),
     "kop_fma_peak_kernel": (C.c_int, [_i32, _i32, _i32, _p, C.POINTER(_f64), _p]),

@@ -11,6 +11,7 @@
 #include "../../include/kinoptik_b200.h"
 #include "kop_collision.cuh"
 #include "kop_kernels.cuh"
+#include "kop_traj.cuh"
 #include "kop_tree.cuh"
 
 using namespace kop;
@@ -1147,6 +1148,213 @@ int kop_multi_pose_solve(const KopModel* m, const KopPoseCosts* pc, const KopLmO
   cudaStream_t st = (cudaStream_t)stream;
   const cudaError_t e = o->precision == KOP_FP32 ? launch_tree_solve<float>(tree_params<float>(*m, pc), L, st)
                                                  : launch_tree_solve<double>(tree_params<double>(*m, pc), L, st);
+  return cuda_status(e);
+}
+
+}  // extern "C"
+
+namespace {
+
+// plan_trajectory's weights and stencils (tasks.py:347-403, costs.py:198-341)
+template <class G>
+TrajCosts<typename G::T> make_traj_costs(const KopModel& m, const KopTrajCosts* c) {
+  using T = typename G::T;
+  TrajCosts<T> W;
+  memset(&W, 0, sizeof(W));
+  const int n = m.tree.n;
+  W.T_steps = c->timesteps;
+  W.n = n;
+  for (int i = 0; i < 8; ++i) {
+    W.lower[i] = i < n ? T(m.lower[i]) : T(-INFINITY);
+    W.upper[i] = i < n ? T(m.upper[i]) : T(INFINITY);
+    W.rest[i] = i < n ? T(c->rest ? c->rest[i] : m.rest[i]) : T(0);
+    W.vbudget[i] = (i < n && c->velocity_limits) ? T(c->velocity_limits[i] * c->dt) : T(INFINITY);
+  }
+  W.w_lim = T(c->w_limit);
+  W.w_rest = T(c->w_rest);
+  W.anchor = T(c->w_anchor);
+  W.w_smooth = T(c->w_smoothness);
+  W.w_vel = T(c->w_velocity);
+  W.w_acc = T(c->w_acceleration);
+  W.w_jerk = T(c->w_jerk);
+  const double acc[5] = {-1.0, 16.0, -30.0, 16.0, -1.0}, jerk[5] = {-1.0, 2.0, 0.0, -2.0, 1.0};
+  const double dt2 = c->dt * c->dt, dt3 = c->dt * c->dt * c->dt;
+  for (int k = 0; k < 5; ++k) {
+    W.acc_c[k] = T((acc[k] / 12.0) / dt2);
+    W.jerk_c[k] = T((jerk[k] / 2.0) / dt3);
+  }
+  W.w_world = T(c->w_world);
+  W.eta_world = T(c->eta_world > 0 ? c->eta_world : 1.0);
+  return W;
+}
+
+template <class G>
+cudaError_t run_traj(const KopModel& m, const ChainParams<double, kChainMax>& D, const CollisionParams<double>& PD,
+                     const KopTrajCosts* c, const TrajLaunch& L, cudaStream_t st) {
+  return launch_traj<G>(cast_chain<typename G::T, G::K>(D), cast_collision<typename G::T>(PD),
+                        make_traj_costs<G>(m, c), L, st);
+}
+
+template <class G>
+cudaError_t run_traj_normal(const KopModel& m, const ChainParams<double, kChainMax>& D,
+                            const CollisionParams<double>& PD, const KopTrajCosts* c, const TrajLaunch& L,
+                            cudaStream_t st) {
+  return launch_traj_normal<G>(cast_chain<typename G::T, G::K>(D), cast_collision<typename G::T>(PD),
+                               make_traj_costs<G>(m, c), L, st);
+}
+
+template <typename T>
+cudaError_t dispatch_traj(Shape sh, const KopModel& m, const ChainParams<double, kChainMax>& D,
+                          const CollisionParams<double>& PD, const KopTrajCosts* c, const TrajLaunch& L,
+                          cudaStream_t st, bool normal = false) {
+  switch (sh) {
+    case Shape::kId7:
+      return normal ? run_traj_normal<Cfg<T, 7, 7, true, false>>(m, D, PD, c, L, st)
+                    : run_traj<Cfg<T, 7, 7, true, false>>(m, D, PD, c, L, st);
+    case Shape::kGen8:
+      return normal ? run_traj_normal<Cfg<T, 8, 8, false, false>>(m, D, PD, c, L, st)
+                    : run_traj<Cfg<T, 8, 8, false, false>>(m, D, PD, c, L, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+int prepare_traj(const KopModel* m, int link, const KopTrajCosts* c, int precision, int num_obstacles,
+                 ChainParams<double, kChainMax>& C, CollisionParams<double>& PD, Shape& sh) {
+  if (!m || !c) return fail(KOP_EINVAL, "null argument");
+  // TrajRequest.__post_init__ (tasks.py:208-213)
+  if (c->timesteps < 5) return fail(KOP_EINVAL, "trajectory needs at least 5 timesteps for the stencils");
+  if (c->timesteps > kTrajMaxSteps) return fail(KOP_EUNSUPPORTED, "more than 64 timesteps (not compiled in)");
+  if (!(c->dt > 0)) return fail(KOP_EINVAL, "dt must be positive");
+  const double ws[] = {c->w_anchor, c->w_smoothness, c->w_velocity, c->w_acceleration, c->w_jerk,
+                       c->w_limit,  c->w_rest,       c->w_self,     c->w_world};
+  for (double w : ws)
+    if (!(w >= 0)) return fail(KOP_EINVAL, "weights must be nonnegative");
+  if (num_obstacles < 0 || num_obstacles > kMaxObstacles)
+    return fail(KOP_EUNSUPPORTED, "more than 16 obstacles (not compiled in)");
+  KopCollisionCosts cc{};
+  cc.w_self = c->w_self;
+  cc.eta_self = c->eta_self;
+  cc.w_world = c->w_world;
+  cc.eta_world = c->eta_world;
+  cc.sharpness = c->sharpness;
+  cc.hard_min = c->hard_min;
+  cc.num_obstacles = 0;  // per-problem obstacles travel separately
+  return prepare_col(m, link, precision, &cc, C, PD, sh);
+}
+
+}  // namespace
+
+extern "C" {
+
+int kop_traj_solve(const KopModel* m, int32_t link, const KopTrajCosts* c, const KopLmOptions* o,
+                   const double* q_init, const double* anchors, const double* obstacles, int32_t num_obstacles,
+                   int64_t batch, double* q_out, double* cost_out, double* init_cost_out, double* history_out,
+                   int32_t* iterations_out, int32_t* termination_out, void* stream) {
+  if (!o) return fail(KOP_EINVAL, "null argument");
+  ChainParams<double, kChainMax> C;
+  CollisionParams<double> PD;
+  Shape sh;
+  int rc = prepare_traj(m, link, c, o->precision, num_obstacles, C, PD, sh);
+  if (rc != KOP_OK) return rc;
+  if (o->max_iterations <= 0 || !(o->initial_damping > 0)) return fail(KOP_EINVAL, "max_iterations and initial_damping must be positive");
+  if (!(o->damping_increase > 1.0)) return fail(KOP_EINVAL, "damping_increase must exceed 1");
+  if (!(o->damping_decrease > 0.0 && o->damping_decrease < 1.0)) return fail(KOP_EINVAL, "damping_decrease must be in (0, 1)");
+  if (o->max_rejections < 1) return fail(KOP_EINVAL, "max_rejections must be positive");
+  if (batch < 0) return fail(KOP_EINVAL, "negative batch");
+  if (batch == 0) return KOP_OK;
+  if (!anchors || (num_obstacles > 0 && !obstacles) || !q_out || !cost_out || !init_cost_out ||
+      !iterations_out || !termination_out)
+    return fail(KOP_EINVAL, "null array argument");
+  TrajLaunch L{};
+  L.q_init = q_init;
+  L.anchors = anchors;
+  L.obstacles = obstacles;
+  L.n_obs = c->w_world > 0 ? num_obstacles : 0;
+  L.B = batch;
+  L.opts = {o->max_iterations, o->max_rejections, o->initial_damping, o->damping_increase, o->damping_decrease,
+            o->gradient_tolerance, o->step_tolerance};
+  L.q_out = q_out;
+  L.cost_out = cost_out;
+  L.init_cost = init_cost_out;
+  L.hist_out = history_out;
+  L.iters = iterations_out;
+  L.term = termination_out;
+  cudaStream_t st = (cudaStream_t)stream;
+  const cudaError_t e = o->precision == KOP_FP32 ? dispatch_traj<float>(sh, *m, C, PD, c, L, st)
+                                                 : dispatch_traj<double>(sh, *m, C, PD, c, L, st);
+  return cuda_status(e);
+}
+
+int kop_traj_normal_equations(const KopModel* m, int32_t link, const KopTrajCosts* c, int32_t precision,
+                              const double* qs, const double* anchors, const double* obstacles,
+                              int32_t num_obstacles, int64_t batch, double* cost_out, double* grad_out,
+                              double* hess_out, void* stream) {
+  ChainParams<double, kChainMax> C;
+  CollisionParams<double> PD;
+  Shape sh;
+  int rc = prepare_traj(m, link, c, precision, num_obstacles, C, PD, sh);
+  if (rc != KOP_OK) return rc;
+  if (precision != KOP_FP32 && precision != KOP_FP64) return fail(KOP_EINVAL, "bad precision");
+  if (batch < 0) return fail(KOP_EINVAL, "negative batch");
+  if (batch == 0) return KOP_OK;
+  if (!qs || !anchors || (num_obstacles > 0 && !obstacles) || !cost_out || !grad_out || !hess_out)
+    return fail(KOP_EINVAL, "null array argument");
+  const int64_t nr = (int64_t)c->timesteps * m->tree.n;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaMemsetAsync(hess_out, 0, sizeof(double) * batch * nr * nr, st);
+  if (e != cudaSuccess) return cuda_status(e);
+  TrajLaunch L{};
+  L.q_init = qs;
+  L.anchors = anchors;
+  L.obstacles = obstacles;
+  L.n_obs = c->w_world > 0 ? num_obstacles : 0;
+  L.B = batch;
+  L.cost_out = cost_out;
+  L.grad_out = grad_out;
+  L.hess_out = hess_out;
+  e = precision == KOP_FP32 ? dispatch_traj<float>(sh, *m, C, PD, c, L, st, true)
+                            : dispatch_traj<double>(sh, *m, C, PD, c, L, st, true);
+  return cuda_status(e);
+}
+
+int kop_traj_report(const KopModel* m, int32_t link, int32_t timesteps, const double* qs, const double* obstacles,
+                    int32_t num_obstacles, const double* targets, int64_t batch, double* static_out,
+                    double* swept_out, double* min_static, double* min_swept, double* pos_err, double* rot_err,
+                    void* stream) {
+  if (timesteps < 1) return fail(KOP_EINVAL, "need at least one timestep");
+  if (timesteps > kTrajMaxSteps) return fail(KOP_EUNSUPPORTED, "more than 64 timesteps (not compiled in)");
+  if (num_obstacles < 0 || num_obstacles > kMaxObstacles)
+    return fail(KOP_EUNSUPPORTED, "more than 16 obstacles (not compiled in)");
+  if (batch < 0) return fail(KOP_EINVAL, "negative batch");
+  KopCollisionCosts cc{};
+  ChainParams<double, kChainMax> C;
+  CollisionParams<double> PD;
+  Shape sh;
+  int rc = prepare_col(m, link, KOP_FP64, &cc, C, PD, sh);
+  if (rc != KOP_OK) return rc;
+  if (batch == 0) return KOP_OK;
+  if (!qs || (num_obstacles > 0 && !obstacles) || (targets && (!pos_err || !rot_err)))
+    return fail(KOP_EINVAL, "null array argument");
+  TrajReportLaunch L{};
+  L.steps = timesteps;
+  L.n = m->tree.n;
+  L.qs = qs;
+  L.obstacles = obstacles;
+  L.n_obs = num_obstacles;
+  L.targets = targets;
+  L.B = batch;
+  L.static_out = static_out;
+  L.swept_out = swept_out;
+  L.min_static = min_static;
+  L.min_swept = min_swept;
+  L.pos_err = pos_err;
+  L.rot_err = rot_err;
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e;
+  if (sh == Shape::kId7)
+    e = launch_traj_report<Cfg<double, 7, 7, true, false>>(cast_chain<double, 7>(C), PD, L, st);
+  else
+    e = launch_traj_report<Cfg<double, 8, 8, false, false>>(cast_chain<double, 8>(C), PD, L, st);
   return cuda_status(e);
 }
 

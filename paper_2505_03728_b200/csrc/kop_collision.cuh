@@ -70,10 +70,18 @@ __device__ __forceinline__ void activation_t(T d, T eta, T& a, T& da) {
   }
 }
 
-// sphere (centre c, radius r) vs obstacle o: distance and unit gradient (collision.py:192-204)
+// Obstacle tables: CollisionParams (kernel parameter) or a per-problem copy in
+// shared memory (trajectories) -- any type with okind/oa/ob/orad members.
 template <typename T>
-__device__ __forceinline__ T sphere_obstacle_t(const CollisionParams<T>& P, int o, const vec3<T>& c, T r,
-                                               vec3<T>& n) {
+struct ObstacleTable {
+  int32_t no;
+  int32_t okind[kMaxObstacles];
+  T oa[kMaxObstacles][3], ob[kMaxObstacles][3], orad[kMaxObstacles];
+};
+
+// sphere (centre c, radius r) vs obstacle o: distance and unit gradient (collision.py:192-204)
+template <typename T, class OB>
+__device__ __forceinline__ T sphere_obstacle_t(const OB& P, int o, const vec3<T>& c, T r, vec3<T>& n) {
   const int kind = P.okind[o];
   const vec3<T> a{P.oa[o][0], P.oa[o][1], P.oa[o][2]};
   if (kind == kObHalfSpace) {
@@ -159,22 +167,15 @@ __device__ __forceinline__ void col_row_accumulate(const ChainParams<typename G:
   }
 }
 
-// Weighted residual stack [pose 6 | limit n | rest n | world nl*no | self np]
-// of a collision lane: returns the cost; JAC also forms A = J^T J, g = J^T r.
-// row_out (optional, for the parity API) receives every weighted residual and
-// jac_out its Jacobian rows (rows x NQ).
-template <class G, bool JAC>
-__device__ __forceinline__ typename G::T col_eval(const ChainParams<typename G::T, G::K>& C,
-                                                  const CostParams<typename G::T, G::NQ>& W,
-                                                  const CollisionParams<typename G::T>& P,
-                                                  const TargetInv<typename G::T>& tg, const ColLane<G>& L,
-                                                  const typename G::T (&q)[G::NQ],
-                                                  typename G::T (&A)[Tri<G::ND>::size], typename G::T (&g)[G::ND],
-                                                  double* row_out = nullptr, double* jac_out = nullptr) {
+// Forward pass over the compiled chain: Pluecker axes of the moving joints and
+// world sphere centres into the lane scratch; returns the EE world pose.
+template <class G>
+__device__ __forceinline__ void col_forward(const ChainParams<typename G::T, G::K>& C,
+                                            const CollisionParams<typename G::T>& P, const ColLane<G>& L,
+                                            const typename G::T (&q)[G::NQ], quat<typename G::T>& eq_out,
+                                            vec3<typename G::T>& ep_out) {
   using T = typename G::T;
-  constexpr int K = G::K, NQ = G::NQ;
-  static_assert(!G::BASE, "collision lanes have a fixed base");
-  // ---- forward pass: Pluecker axes, sphere centres, EE pose ------------------
+  constexpr int K = G::K;
   for (int s = P.slot_first[0]; s < P.slot_first[1]; ++s)
 #pragma unroll
     for (int i = 0; i < 3; ++i) L.cen(s, i) = P.sc[s][i];
@@ -220,57 +221,35 @@ __device__ __forceinline__ typename G::T col_eval(const ChainParams<typename G::
       }
     }
   }
-  const quat<T> eq = qmul(pq, quat<T>{C.eq[0], C.eq[1], C.eq[2], C.eq[3]});
+  eq_out = qmul(pq, quat<T>{C.eq[0], C.eq[1], C.eq[2], C.eq[3]});
   const vec3<T> eo = qrot(pq, vec3<T>{C.ep[0], C.ep[1], C.ep[2]});
-  const vec3<T> ep{pp.x + eo.x, pp.y + eo.y, pp.z + eo.z};
+  ep_out = {pp.x + eo.x, pp.y + eo.y, pp.z + eo.z};
 
-  // ---- pose rows: body columns from the Pluecker axes -----------------------
-  T col[K][6];
-  if (JAC) {
-    const mat3<T> R = qmat(eq);
-#pragma unroll
-    for (int k = 0; k < K; ++k) {
-      if (G::ID || k < C.k) {
-        const vec3<T> a{L.am(k, 0), L.am(k, 1), L.am(k, 2)};
-        const vec3<T> ang = mulT(R, a);
-        if (!G::ID && C.prismatic[k]) {
-          col[k][0] = ang.x; col[k][1] = ang.y; col[k][2] = ang.z;
-          col[k][3] = T(0); col[k][4] = T(0); col[k][5] = T(0);
-        } else {
-          const vec3<T> m{L.am(k, 3), L.am(k, 4), L.am(k, 5)};
-          const vec3<T> x = cross(a, ep);
-          const vec3<T> lin = mulT(R, vec3<T>{x.x - m.x, x.y - m.y, x.z - m.z});
-          col[k][0] = lin.x; col[k][1] = lin.y; col[k][2] = lin.z;
-          col[k][3] = ang.x; col[k][4] = ang.y; col[k][5] = ang.z;
-        }
-      }
-    }
-  }
-  T r[6], J[6][NQ];
-  const T zb[3] = {T(0), T(0), T(0)};
-  pose_finish<G, JAC>(C, W, tg, eq, ep, col, r, J);
-  T cost = assemble_rows<G, JAC>(W, q, zb, r, J, A, g);
-  if (row_out) {
-#pragma unroll
-    for (int m = 0; m < 6; ++m) {
-      row_out[m] = double(r[m]);
-      if (jac_out)
-#pragma unroll
-        for (int c = 0; c < NQ; ++c) jac_out[m * NQ + c] = double(J[m][c]);
-    }
-  }
-  int row = 6 + 2 * NQ;  // next row index (parity output)
+}
 
+// World (sphere link x obstacle) and self (link pair) activation rows from the
+// lane scratch filled by col_forward: adds their squares to the returned cost
+// and, if JAC, their rank-1 terms to A, g.  row/row_out/jac_out: parity output.
+template <class G, bool JAC, class OB = CollisionParams<typename G::T>>
+__device__ __forceinline__ typename G::T col_rows(const ChainParams<typename G::T, G::K>& C,
+                                                  const CollisionParams<typename G::T>& P, const ColLane<G>& L,
+                                                  typename G::T (&A)[Tri<G::ND>::size], typename G::T (&g)[G::ND],
+                                                  int row = 0, double* row_out = nullptr,
+                                                  double* jac_out = nullptr, const OB* obs = nullptr) {
+  using T = typename G::T;
+  constexpr int NQ = G::NQ;
+  const OB& O = obs ? *obs : reinterpret_cast<const OB&>(P);
+  T cost = T(0);
   // ---- world rows: (sphere link, obstacle), costs.py:499-551 ---------------
   if (P.w_world > T(0)) {
     for (int li = 0; li < P.nl; ++li) {
       const int f = P.lfirst[li], nsph = P.lcount[li];
-      for (int o = 0; o < P.no; ++o, ++row) {
+      for (int o = 0; o < O.no; ++o, ++row) {
         T dmin = inf_t<T>();
         int kmin = 0;
         for (int s = 0; s < nsph; ++s) {
           vec3<T> n;
-          const T d = sphere_obstacle_t(P, o, vec3<T>{L.cen(f + s, 0), L.cen(f + s, 1), L.cen(f + s, 2)},
+          const T d = sphere_obstacle_t<T>(O, o, vec3<T>{L.cen(f + s, 0), L.cen(f + s, 1), L.cen(f + s, 2)},
                                         P.sr[f + s], n);
           if (d < dmin) {
             dmin = d;
@@ -283,7 +262,7 @@ __device__ __forceinline__ typename G::T col_eval(const ChainParams<typename G::
         for (int s = 0; s < nsph; ++s) {
           const vec3<T> c{L.cen(f + s, 0), L.cen(f + s, 1), L.cen(f + s, 2)};
           vec3<T> n;
-          const T d = sphere_obstacle_t(P, o, c, P.sr[f + s], n);
+          const T d = sphere_obstacle_t<T>(O, o, c, P.sr[f + s], n);
           const T z = hard ? (s == kmin ? T(1) : T(0)) : exp_t(-P.beta * (d - dmin));
           sumz += z;
           if (JAC) {
@@ -383,6 +362,65 @@ __device__ __forceinline__ typename G::T col_eval(const ChainParams<typename G::
   }
   return cost;
 }
+
+// Weighted residual stack [pose 6 | limit n | rest n | world nl*no | self np]
+// of a collision lane: returns the cost; JAC also forms A = J^T J, g = J^T r.
+// row_out (optional, for the parity API) receives every weighted residual and
+// jac_out its Jacobian rows (rows x NQ).
+template <class G, bool JAC>
+__device__ __forceinline__ typename G::T col_eval(const ChainParams<typename G::T, G::K>& C,
+                                                  const CostParams<typename G::T, G::NQ>& W,
+                                                  const CollisionParams<typename G::T>& P,
+                                                  const TargetInv<typename G::T>& tg, const ColLane<G>& L,
+                                                  const typename G::T (&q)[G::NQ],
+                                                  typename G::T (&A)[Tri<G::ND>::size], typename G::T (&g)[G::ND],
+                                                  double* row_out = nullptr, double* jac_out = nullptr) {
+  using T = typename G::T;
+  constexpr int K = G::K, NQ = G::NQ;
+  static_assert(!G::BASE, "collision lanes have a fixed base");
+  quat<T> eq;
+  vec3<T> ep;
+  col_forward<G>(C, P, L, q, eq, ep);
+  // ---- pose rows: body columns from the Pluecker axes -----------------------
+  T col[K][6];
+  if (JAC) {
+    const mat3<T> R = qmat(eq);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      if (G::ID || k < C.k) {
+        const vec3<T> a{L.am(k, 0), L.am(k, 1), L.am(k, 2)};
+        const vec3<T> ang = mulT(R, a);
+        if (!G::ID && C.prismatic[k]) {
+          col[k][0] = ang.x; col[k][1] = ang.y; col[k][2] = ang.z;
+          col[k][3] = T(0); col[k][4] = T(0); col[k][5] = T(0);
+        } else {
+          const vec3<T> m{L.am(k, 3), L.am(k, 4), L.am(k, 5)};
+          const vec3<T> x = cross(a, ep);
+          const vec3<T> lin = mulT(R, vec3<T>{x.x - m.x, x.y - m.y, x.z - m.z});
+          col[k][0] = lin.x; col[k][1] = lin.y; col[k][2] = lin.z;
+          col[k][3] = ang.x; col[k][4] = ang.y; col[k][5] = ang.z;
+        }
+      }
+    }
+  }
+  T r[6], J[6][NQ];
+  const T zb[3] = {T(0), T(0), T(0)};
+  pose_finish<G, JAC>(C, W, tg, eq, ep, col, r, J);
+  T cost = assemble_rows<G, JAC>(W, q, zb, r, J, A, g);
+  if (row_out) {
+#pragma unroll
+    for (int m = 0; m < 6; ++m) {
+      row_out[m] = double(r[m]);
+      if (jac_out)
+#pragma unroll
+        for (int c = 0; c < NQ; ++c) jac_out[m * NQ + c] = double(J[m][c]);
+    }
+  }
+  int row = 6 + 2 * NQ;  // next row index (parity output)
+
+  return cost + col_rows<G, JAC>(C, P, L, A, g, row, row_out, jac_out);
+}
+
 
 template <class G>
 struct CollisionModel {

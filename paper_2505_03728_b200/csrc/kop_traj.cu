@@ -1,0 +1,780 @@
+// Batched trajectory optimisation (config 5): the plan_trajectory cost set
+// (tasks.py:347-403) solved by solver.solve's LM (solver.py:364-429), one CTA
+// (128 threads) per trajectory of T <= 64 timesteps.
+//
+// Variables q_0..q_{T-1} (NQ each) are one vector of N = T*NQ unknowns.  The
+// costs couple timestep t with t-1 (smoothness, velocity limit: diagonal;
+// swept capsules: full NQ x NQ blocks) and, through the 5-point acceleration /
+// jerk stencils over t-2..t+2, with t-2, t-3, t-4 (diagonal blocks).  So J^T J
+// is a band matrix of half-bandwidth 4*NQ whose block row t holds a full
+// lower-triangular diagonal block, a full (t, t-1) block and three diagonal
+// blocks; H is stored in that compact form (NT + NQ^2 + 3 NQ per timestep),
+// its Cholesky factor -- which fills the band -- as a band (the reference
+// switches to SuperLU above 200 unknowns, solver.py:327-354; a banded
+// Cholesky is the same linear solve).
+//
+// Per evaluation:
+//   A  thread t: FK forward pass of q_t (Pluecker axes + sphere centres in
+//      shared memory), the timestep-local rows (limit, rest, anchors, world,
+//      self), smoothness / velocity rows of the pair (t-1, t) and the stencil
+//      rows: it owns block row t of the band (rows t*NQ .. t*NQ+NQ-1).
+//   B  thread t: swept-capsule rows of the pair (t-1, t) (costs.py:554-619):
+//      cross block H[t][t-1] written directly, the H[t-1][t-1] part handed to
+//      thread t-1 through a per-pair buffer.
+//   C  thread t adds the handed-over part; block reduction of the cost.
+// LM: gradient test, banded Cholesky of H + lam diag(max(diag H, 1e-8)) with
+// two barriers per column, triangular solves by warp 0, rejection loop,
+// terminations -- the semantics of solver.solve.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "kop_beam.cuh"
+#include "kop_collision.cuh"
+#include "kop_kernels.cuh"
+#include "kop_traj.cuh"
+
+namespace kop {
+
+constexpr int kTrajThreads = 128;
+
+// Shared-memory layout, sized by the trajectory length at launch:
+//   obstacle table | reduction buffer | q, qn, g, y, 1/diag(L)  [N each]
+//   H compact [T x HB]: per timestep D (lower NT) | X = H(t, t-1) (NQ^2, row-major) | E2, E3, E4 (NQ each)
+//   union { L band [N x (BW+1)], L(i, i-d) at [i][d]  |  FK scratch [(6K + 3 ns) x T] + pair buffers }
+// The union is safe: L lives from the factorisation to the end of the
+// triangular solves, the scratch and pair buffers only inside an evaluation.
+template <class G>
+struct TrajView {
+  using T = typename G::T;
+  static constexpr int NQ = G::NQ, BW = 4 * NQ, NT = Tri<NQ>::size, HB = NT + NQ * NQ + 3 * NQ;
+  ObstacleTable<T>* obs;
+  T *red, *anc, *q, *qn, *g, *y, *dinv, *H, *L, *scratch, *pbufA, *pbufg;
+  int steps;
+  __host__ __device__ static size_t bytes(int steps, int ns) {
+    const size_t N = (size_t)steps * NQ;
+    const size_t band = N * (BW + 1);
+    const size_t uni_b = (size_t)(6 * G::K + 3 * ns) * steps + (size_t)steps * (NT + NQ);
+    const size_t head = (sizeof(ObstacleTable<T>) + 15) / 16 * 16;
+    return head + sizeof(T) * (kTrajThreads + 2 * NQ + 5 * N + (size_t)steps * HB + (band > uni_b ? band : uni_b));
+  }
+  __device__ TrajView(unsigned char* base, int steps_, int ns) : steps(steps_) {
+    const int N = steps * NQ;
+    obs = reinterpret_cast<ObstacleTable<T>*>(base);
+    T* p = reinterpret_cast<T*>(base + (sizeof(ObstacleTable<T>) + 15) / 16 * 16);
+    red = p; p += kTrajThreads;
+    anc = p; p += 2 * NQ;
+    q = p; p += N;
+    qn = p; p += N;
+    g = p; p += N;
+    y = p; p += N;
+    dinv = p; p += N;
+    H = p; p += steps * HB;
+    L = p;
+    scratch = p; p += (6 * G::K + 3 * ns) * steps;
+    pbufA = p; p += steps * NT;
+    pbufg = p;
+  }
+  __device__ __forceinline__ T* hd(int t) const { return H + t * HB; }            // D_t
+  __device__ __forceinline__ T* hx(int t) const { return H + t * HB + NT; }       // X_t
+  __device__ __forceinline__ T* he(int t) const { return H + t * HB + NT + NQ * NQ; }  // E2..E4
+  // H(i, i - d) of the band from the compact blocks
+  __device__ __forceinline__ T h(int i, int d) const {
+    const int t = i / NQ, a = i % NQ;
+    if (d <= a) return hd(t)[Tri<NQ>::at(a, a - d)];
+    if (d <= a + NQ) return t >= 1 ? hx(t)[a * NQ + NQ + a - d] : T(0);
+    const int m = d / NQ;
+    return (d % NQ == 0 && t >= m) ? he(t)[(m - 2) * NQ + a] : T(0);
+  }
+  __device__ __forceinline__ T& l(int i, int d) const { return L[i * (BW + 1) + d]; }
+  __device__ __forceinline__ ColLane<G> lane(int t) const { return ColLane<G>{scratch + t, steps}; }
+};
+
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* red) {
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = kTrajThreads / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  const T r = red[0];
+  __syncthreads();
+  return r;
+}
+
+template <typename T>
+__device__ __forceinline__ T block_max(T v, T* red) {
+  red[threadIdx.x] = v;
+  __syncthreads();
+  for (int o = kTrajThreads / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] = tmax(red[threadIdx.x], red[threadIdx.x + o]);
+    __syncthreads();
+  }
+  const T r = red[0];
+  __syncthreads();
+  return r;
+}
+
+template <typename T>
+__device__ __forceinline__ void load_obstacles(ObstacleTable<T>& O, const double* __restrict__ obstacles, int64_t b,
+                                               int n_obs) {
+  if (threadIdx.x == 0) O.no = n_obs;
+  for (int o = threadIdx.x; o < n_obs; o += blockDim.x) {
+    const double* src = obstacles + (b * n_obs + o) * 8;
+    O.okind[o] = int(src[0]);
+    for (int i = 0; i < 3; ++i) {
+      O.oa[o][i] = T(src[1 + i]);
+      O.ob[o][i] = T(src[4 + i]);
+    }
+    O.orad[o] = T(src[7]);
+  }
+}
+
+// capsule (endpoints c0, c1, radius r) vs obstacle o: distance and the
+// gradients at both endpoints (collision.py:207-237 with :115-152)
+template <typename T, class OB>
+__device__ __forceinline__ T capsule_obstacle_t(const OB& O, int o, const vec3<T>& c0, const vec3<T>& c1, T r,
+                                                vec3<T>& ga, vec3<T>& gb) {
+  const int kind = O.okind[o];
+  const vec3<T> a{O.oa[o][0], O.oa[o][1], O.oa[o][2]};
+  if (kind == kObHalfSpace) {
+    const T da = dot(a, c0), db = dot(a, c1);
+    const vec3<T> z{T(0), T(0), T(0)};
+    if (da <= db) {
+      ga = a;
+      gb = z;
+    } else {
+      ga = z;
+      gb = a;
+    }
+    return tmin(da, db) - O.orad[o] - r;
+  }
+  const vec3<T> d1{c1.x - c0.x, c1.y - c0.y, c1.z - c0.z};
+  T s = T(0);
+  vec3<T> qpt = a;
+  if (kind == kObSphere) {
+    const T dd = dot(d1, d1);
+    if (!(dd < T(1e-16))) s = tmin(tmax(dot(vec3<T>{a.x - c0.x, a.y - c0.y, a.z - c0.z}, d1) / dd, T(0)), T(1));
+  } else {  // capsule-capsule: Ericson's clamped quadratic (collision.py:124-152)
+    const vec3<T> b{O.ob[o][0], O.ob[o][1], O.ob[o][2]};
+    const vec3<T> d2{b.x - a.x, b.y - a.y, b.z - a.z};
+    const vec3<T> rr{c0.x - a.x, c0.y - a.y, c0.z - a.z};
+    const T aa = dot(d1, d1), e = dot(d2, d2), f = dot(d2, rr);
+    T t = T(0);
+    if (aa < T(1e-16) && e < T(1e-16)) {
+      s = t = T(0);
+    } else if (aa < T(1e-16)) {
+      s = T(0);
+      t = tmin(tmax(f / e, T(0)), T(1));
+    } else {
+      const T c = dot(d1, rr);
+      if (e < T(1e-16)) {
+        s = tmin(tmax(-c / aa, T(0)), T(1));
+        t = T(0);
+      } else {
+        const T bb = dot(d1, d2);
+        const T den = aa * e - bb * bb;
+        s = den > T(1e-16) ? tmin(tmax((bb * f - c * e) / den, T(0)), T(1)) : T(0);
+        t = (bb * s + f) / e;
+        if (t < T(0)) {
+          t = T(0);
+          s = tmin(tmax(-c / aa, T(0)), T(1));
+        } else if (t > T(1)) {
+          t = T(1);
+          s = tmin(tmax((bb - c) / aa, T(0)), T(1));
+        }
+      }
+    }
+    qpt = {a.x + t * d2.x, a.y + t * d2.y, a.z + t * d2.z};
+  }
+  const vec3<T> p{c0.x + s * d1.x, c0.y + s * d1.y, c0.z + s * d1.z};
+  const vec3<T> v{p.x - qpt.x, p.y - qpt.y, p.z - qpt.z};
+  const T nn = sqrt_t(dot(v, v));
+  vec3<T> dir{T(0), T(0), T(0)};
+  if (!(nn < T(1e-12))) {
+    const T inv = T(1) / nn;
+    dir = {v.x * inv, v.y * inv, v.z * inv};
+  }
+  ga = {(T(1) - s) * dir.x, (T(1) - s) * dir.y, (T(1) - s) * dir.z};
+  gb = {s * dir.x, s * dir.y, s * dir.z};
+  return (nn < T(1e-12) ? T(0) : nn) - r - O.orad[o];
+}
+
+// Jacobian row over the chain joints k <= slot of sum_s w_s g_s . J(c_s):
+// e_k = a_k . M - m_k . G (revolute), a_k . G (prismatic)
+template <class G>
+__device__ __forceinline__ void col_row_entries(const ChainParams<typename G::T, G::K>& C, const ColLane<G>& L,
+                                                int slot, const vec3<typename G::T>& M,
+                                                const vec3<typename G::T>& Gv, typename G::T scale,
+                                                typename G::T (&jr)[G::NQ]) {
+  using T = typename G::T;
+#pragma unroll
+  for (int c = 0; c < G::NQ; ++c) jr[c] = T(0);
+#pragma unroll
+  for (int k = 0; k < G::K; ++k) {
+    if ((G::ID || k < C.k) && k <= slot) {
+      const vec3<T> a{L.am(k, 0), L.am(k, 1), L.am(k, 2)};
+      const vec3<T> m{L.am(k, 3), L.am(k, 4), L.am(k, 5)};
+      const T e = scale * ((!G::ID && C.prismatic[k]) ? dot(a, Gv) : dot(a, M) - dot(m, Gv));
+      if (G::ID) {
+        jr[k] += e;
+      } else {
+#pragma unroll
+        for (int c = 0; c < G::NQ; ++c)
+          if (C.qcol[k] == c) jr[c] += C.mult[k] * e;
+      }
+    }
+  }
+}
+
+// Evaluate the trajectory stack at x (S.q or S.qn); JAC also forms the band
+// H and g.  Returns the cost on every thread.
+template <class G, bool JAC>
+__device__ typename G::T traj_eval(const ChainParams<typename G::T, G::K>& C, const CollisionParams<typename G::T>& P,
+                                   const TrajCosts<typename G::T>& W, const TrajView<G>& S, const typename G::T* x) {
+  using T = typename G::T;
+  constexpr int NQ = G::NQ, NT = Tri<NQ>::size;
+  const int tid = threadIdx.x, Tn = W.T_steps;
+  T cost = T(0);
+  // ---- A: FK + timestep-local rows + smoothness / velocity / stencils --------
+  T Ad[NT], gd[NQ];
+#pragma unroll
+  for (int i = 0; i < NT; ++i) Ad[i] = T(0);
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) gd[i] = T(0);
+  T cross_diag[NQ], off_diag[3][NQ];  // diagonal entries of H(t, t-1) and H(t, t-2..t-4) from diagonal rows
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) cross_diag[i] = off_diag[0][i] = off_diag[1][i] = off_diag[2][i] = T(0);
+  T prevA_diag[NQ], prev_g[NQ];  // diagonal-row contributions to block t-1 (pair (t-1, t))
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) prevA_diag[i] = prev_g[i] = T(0);
+  const int t = tid;
+  if (t < Tn) {
+    T q[NQ];
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) q[i] = x[t * NQ + i];
+    const ColLane<G> L = S.lane(t);
+    quat<T> eq;
+    vec3<T> ep;
+    col_forward<G>(C, P, L, q, eq, ep);
+    // limit (costs.py:174-195), rest (tasks.py:386-389), anchors (tasks.py:352-355)
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) {
+      const T above = q[i] - W.upper[i], below = W.lower[i] - q[i];
+      const T rl = W.w_lim * (tmax(T(0), above) + tmax(T(0), below));
+      const T gl = W.w_lim * ((q[i] > W.upper[i] ? T(1) : T(0)) + (q[i] < W.lower[i] ? T(-1) : T(0)));
+      const T rr = W.w_rest * (q[i] - W.rest[i]);
+      cost += rl * rl + rr * rr;
+      Ad[Tri<NQ>::at(i, i)] += gl * gl + W.w_rest * W.w_rest;
+      gd[i] += gl * rl + W.w_rest * rr;
+      if (t == 0 || t == Tn - 1) {
+        const T ra = W.anchor * (q[i] - S.anc[(t == 0 ? 0 : NQ) + i]);
+        cost += ra * ra;
+        Ad[Tri<NQ>::at(i, i)] += W.anchor * W.anchor;
+        gd[i] += W.anchor * ra;
+      }
+    }
+    // world + self rows (world uses the per-problem obstacle table)
+    cost += col_rows<G, JAC, ObstacleTable<T>>(C, P, L, Ad, gd, 0, nullptr, nullptr, S.obs);
+    // smoothness + velocity of the pair (t-1, t) (costs.py:198-231, 274-290)
+    if (t >= 1) {
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) {
+        const T dq = q[i] - x[(t - 1) * NQ + i];
+        const T rs = W.w_smooth * dq;
+        cost += rs * rs;
+        T jv = T(0), rv = T(0);
+        if (W.w_vel > T(0) && finite_t(W.vbudget[i]) && fabs(dq) > W.vbudget[i]) {
+          rv = W.w_vel * (fabs(dq) - W.vbudget[i]);
+          jv = W.w_vel * (dq > T(0) ? T(1) : (dq < T(0) ? T(-1) : T(0)));
+        }
+        cost += rv * rv;
+        const T h = W.w_smooth * W.w_smooth + jv * jv;
+        Ad[Tri<NQ>::at(i, i)] += h;
+        prevA_diag[i] += h;
+        cross_diag[i] -= h;
+        gd[i] += W.w_smooth * rs + jv * rv;
+        prev_g[i] -= W.w_smooth * rs + jv * rv;
+      }
+    }
+    // 5-point stencils (costs.py:293-341): this thread owns block row t and
+    // adds every stencil centred at s = t-2 .. t+2 that touches it; the cost
+    // of stencil s is added by thread s
+    for (int s = t - 2; s <= t + 2; ++s) {
+      if (s < 2 || s > Tn - 3) continue;
+      const int j = t - s + 2;  // this row's coefficient index
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) {
+        T ra = T(0), rj = T(0);
+#pragma unroll
+        for (int kk = 0; kk < 5; ++kk) {
+          const T xv = x[(s + kk - 2) * NQ + i];
+          ra += W.acc_c[kk] * xv;
+          rj += W.jerk_c[kk] * xv;
+        }
+        ra *= W.w_acc;
+        rj *= W.w_jerk;
+        if (s == t) cost += ra * ra + rj * rj;
+        const T ca = W.w_acc * W.acc_c[j], cj = W.w_jerk * W.jerk_c[j];
+        Ad[Tri<NQ>::at(i, i)] += ca * ca + cj * cj;
+        gd[i] += ca * ra + cj * rj;
+        if (j >= 1) cross_diag[i] += ca * W.w_acc * W.acc_c[j - 1] + cj * W.w_jerk * W.jerk_c[j - 1];
+#pragma unroll
+        for (int m = 2; m <= 4; ++m)
+          if (j >= m) off_diag[m - 2][i] += ca * W.w_acc * W.acc_c[j - m] + cj * W.w_jerk * W.jerk_c[j - m];
+      }
+    }
+  }
+  if (JAC && t < Tn) {  // own band rows: clear, then write the local parts
+    for (int i = 0; i < NQ; ++i)
+      for (int b = 0; b < NQ; ++b) S.hx(t)[i * NQ + b] = T(0);
+  }
+  __syncthreads();
+  // ---- B: swept-capsule rows of the pair (t-1, t) -----------------------------
+  T pA[NT], pg[NQ];  // contribution to block t-1
+#pragma unroll
+  for (int i = 0; i < NT; ++i) pA[i] = T(0);
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) pg[i] = prev_g[i];
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) pA[Tri<NQ>::at(i, i)] = prevA_diag[i];
+  if (t >= 1 && t < Tn && W.w_world > T(0) && S.obs->no > 0) {
+    const ColLane<G> L0 = S.lane(t - 1), L1 = S.lane(t);
+    for (int li = 0; li < P.nl; ++li) {
+      const int f = P.lfirst[li], nsph = P.lcount[li];
+      for (int o = 0; o < S.obs->no; ++o) {
+        T dmin = inf_t<T>();
+        int kmin = 0;
+        for (int s = 0; s < nsph; ++s) {
+          vec3<T> ga, gb;
+          const T d = capsule_obstacle_t<T>(*S.obs, o, vec3<T>{L0.cen(f + s, 0), L0.cen(f + s, 1), L0.cen(f + s, 2)},
+                                            vec3<T>{L1.cen(f + s, 0), L1.cen(f + s, 1), L1.cen(f + s, 2)},
+                                            P.sr[f + s], ga, gb);
+          if (d < dmin) {
+            dmin = d;
+            kmin = s;
+          }
+        }
+        const bool hard = P.hard || nsph == 1;
+        T sumz = T(0);
+        vec3<T> M0{T(0), T(0), T(0)}, G0{T(0), T(0), T(0)}, M1{T(0), T(0), T(0)}, G1{T(0), T(0), T(0)};
+        for (int s = 0; s < nsph; ++s) {
+          const vec3<T> c0{L0.cen(f + s, 0), L0.cen(f + s, 1), L0.cen(f + s, 2)};
+          const vec3<T> c1{L1.cen(f + s, 0), L1.cen(f + s, 1), L1.cen(f + s, 2)};
+          vec3<T> ga, gb;
+          const T d = capsule_obstacle_t<T>(*S.obs, o, c0, c1, P.sr[f + s], ga, gb);
+          const T z = hard ? (s == kmin ? T(1) : T(0)) : exp_t(-P.beta * (d - dmin));
+          sumz += z;
+          if (JAC) {
+            const vec3<T> x0 = cross(c0, ga), x1 = cross(c1, gb);
+            M0 = {M0.x + z * x0.x, M0.y + z * x0.y, M0.z + z * x0.z};
+            G0 = {G0.x + z * ga.x, G0.y + z * ga.y, G0.z + z * ga.z};
+            M1 = {M1.x + z * x1.x, M1.y + z * x1.y, M1.z + z * x1.z};
+            G1 = {G1.x + z * gb.x, G1.y + z * gb.y, G1.z + z * gb.z};
+          }
+        }
+        const T dagg = hard ? dmin : dmin - log_t(sumz) / P.beta;
+        T act, dact;
+        activation_t(dagg, W.eta_world, act, dact);
+        const T res = W.w_world * act;
+        cost += res * res;
+        if (JAC && dact != T(0)) {
+          const T inv = T(1) / sumz;
+          M0 = {M0.x * inv, M0.y * inv, M0.z * inv};
+          G0 = {G0.x * inv, G0.y * inv, G0.z * inv};
+          M1 = {M1.x * inv, M1.y * inv, M1.z * inv};
+          G1 = {G1.x * inv, G1.y * inv, G1.z * inv};
+          T j0[NQ], j1[NQ];
+          col_row_entries<G>(C, L0, P.lslot[li], M0, G0, W.w_world * dact, j0);
+          col_row_entries<G>(C, L1, P.lslot[li], M1, G1, W.w_world * dact, j1);
+#pragma unroll
+          for (int a = 0; a < NQ; ++a) {
+#pragma unroll
+            for (int b = 0; b < NQ; ++b) {
+              if (b <= a) {
+                pA[Tri<NQ>::at(a, b)] += j0[a] * j0[b];
+                Ad[Tri<NQ>::at(a, b)] += j1[a] * j1[b];
+              }
+              S.hx(t)[a * NQ + b] += j1[a] * j0[b];  // H(t, t-1) block, own rows
+            }
+            pg[a] += j0[a] * res;
+            gd[a] += j1[a] * res;
+          }
+        }
+      }
+    }
+  }
+  if (JAC && t >= 1 && t < Tn) {
+#pragma unroll
+    for (int i = 0; i < NT; ++i) S.pbufA[(t) * NT + i] = pA[i];
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) S.pbufg[(t) * NQ + i] = pg[i];
+  }
+  __syncthreads();
+  // ---- C: assemble own block row -------------------------------------------------
+  if (JAC && t < Tn) {
+    if (t + 1 < Tn) {
+#pragma unroll
+      for (int i = 0; i < NT; ++i) Ad[i] += S.pbufA[(t + 1) * NT + i];
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) gd[i] += S.pbufg[(t + 1) * NQ + i];
+    }
+#pragma unroll
+    for (int a = 0; a < NQ; ++a) {
+#pragma unroll
+      for (int b = 0; b < NQ; ++b)
+        if (b <= a) S.hd(t)[Tri<NQ>::at(a, b)] = Ad[Tri<NQ>::at(a, b)];
+      if (t >= 1) S.hx(t)[a * NQ + a] += cross_diag[a];
+#pragma unroll
+      for (int m = 0; m < 3; ++m) S.he(t)[m * NQ + a] = off_diag[m][a];
+      S.g[t * NQ + a] = gd[a];
+    }
+  }
+  return block_sum(cost, S.red);
+}
+
+// Banded damped Cholesky solve: y <- -(H + lam diag(max(diag H, 1e-8)))^-1 g.
+template <class G>
+__device__ bool traj_damped_solve(const TrajView<G>& S, int N, typename G::T lam) {
+  using T = typename G::T;
+  constexpr int BW = TrajView<G>::BW;
+  const int tid = threadIdx.x;
+  for (int i = tid; i < N; i += kTrajThreads) {
+    for (int d = 0; d <= BW; ++d) S.l(i, d) = S.h(i, d);  // zero outside the compact blocks
+    S.l(i, 0) += lam * tmax(S.h(i, 0), T(BeamConsts::diag_clamp));
+    S.y[i] = -S.g[i];
+  }
+  __syncthreads();
+  // trailing-update pairs (di, dj), 1 <= dj <= di <= BW, dealt to the threads once
+  constexpr int NPAIR = BW * (BW + 1) / 2;
+  constexpr int PPT = (NPAIR + kTrajThreads - 1) / kTrajThreads;
+  int pdi[PPT], pdj[PPT];
+#pragma unroll
+  for (int r = 0; r < PPT; ++r) {
+    int rem = tid + r * kTrajThreads, di = 1;
+    while (di <= BW && rem >= di) {
+      rem -= di;
+      ++di;
+    }
+    pdi[r] = di;  // > BW: no pair
+    pdj[r] = rem + 1;
+  }
+  bool ok = true;
+  for (int k = 0; k < N; ++k) {
+    const T piv = S.l(k, 0);
+    ok = ok && piv > T(0) && finite_t(piv);
+    const T inv = rsqrt_t(piv);
+    // L_ik L_jk = raw_ik raw_jk / piv on the unscaled column
+    T upd[PPT];
+#pragma unroll
+    for (int r = 0; r < PPT; ++r)
+      upd[r] = (pdi[r] <= BW && k + pdi[r] < N) ? S.l(k + pdi[r], pdi[r]) * S.l(k + pdj[r], pdj[r]) * (inv * inv)
+                                                : T(0);
+    const bool col = tid >= 1 && tid <= BW && k + tid < N;
+    const T scaled = col ? S.l(k + tid, tid) * inv : T(0);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < PPT; ++r)
+      if (pdi[r] <= BW && k + pdi[r] < N) S.l(k + pdi[r], pdi[r] - pdj[r]) -= upd[r];
+    if (col) S.l(k + tid, tid) = scaled;
+    if (tid == 0) {
+      S.l(k, 0) = piv * inv;
+      S.dinv[k] = inv;
+    }
+    __syncthreads();
+  }
+  ok = __syncthreads_and(ok);
+  // forward / backward substitution by warp 0; lane l handles band offset l + 1 (BW <= 32)
+  static_assert(BW <= 32, "band wider than a warp");
+  if (tid < 32) {
+    const int d = tid + 1;
+    for (int k = 0; k < N; ++k) {
+      const T yk = S.y[k] * S.dinv[k];
+      __syncwarp();
+      if (d <= BW && k + d < N) S.y[k + d] -= S.l(k + d, d) * yk;
+      if (tid == 0) S.y[k] = yk;
+      __syncwarp();
+    }
+    for (int k = N - 1; k >= 0; --k) {
+      T part = (d <= BW && k + d < N) ? S.l(k + d, d) * S.y[k + d] : T(0);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      const T xk = (S.y[k] - part) * S.dinv[k];
+      __syncwarp();
+      if (tid == 0) S.y[k] = xk;
+      __syncwarp();
+    }
+  }
+  __syncthreads();
+  return ok;
+}
+
+template <class G>
+__global__ void __launch_bounds__(kTrajThreads)
+k_traj_solve(const ChainParams<typename G::T, G::K> C, const CollisionParams<typename G::T> P,
+             const TrajCosts<typename G::T> W, const double* __restrict__ q_init, const double* __restrict__ anchors,
+             const double* __restrict__ obstacles, int n_obs, int64_t B, const LmOptions O,
+             double* __restrict__ q_out, double* __restrict__ cost_out, double* __restrict__ init_cost_out,
+             double* __restrict__ hist_out, int32_t* __restrict__ iters_out, int32_t* __restrict__ term_out) {
+  using T = typename G::T;
+  constexpr int NQ = G::NQ;
+  extern __shared__ unsigned char smem_raw[];
+  const TrajView<G> S(smem_raw, W.T_steps, P.ns);
+  const int64_t b = blockIdx.x;
+  const int tid = threadIdx.x, Tn = W.T_steps, N = Tn * NQ, n = W.n;
+  for (int i = tid; i < 2 * NQ; i += kTrajThreads) {
+    const int c = i % NQ;
+    S.anc[i] = c < n ? T(anchors[(b * 2 + i / NQ) * n + c]) : T(0);
+  }
+  load_obstacles(*S.obs, obstacles, b, n_obs);
+  for (int i = tid; i < N; i += kTrajThreads) {
+    const int tt = i / NQ, c = i % NQ;
+    if (q_init) {
+      S.q[i] = c < n ? T(q_init[(b * Tn + tt) * n + c]) : T(0);
+    } else {  // straight line between the anchors (tasks.py:344-345, np.linspace)
+      const double alpha = tt == Tn - 1 ? 1.0 : double(tt) * (1.0 / double(Tn - 1));
+      const double qa = c < n ? anchors[(b * 2) * n + c] : 0.0, qb = c < n ? anchors[(b * 2 + 1) * n + c] : 0.0;
+      S.q[i] = T(__dadd_rn(__dmul_rn(qa, 1.0 - alpha), __dmul_rn(qb, alpha)));  // no FMA: numpy's rounding
+    }
+  }
+  __syncthreads();
+  T cost = traj_eval<G, true>(C, P, W, S, S.q);
+  const int hstride = O.max_iterations + 1;
+  if (tid == 0) {
+    if (hist_out) hist_out[b * hstride] = double(cost);
+    init_cost_out[b] = double(cost);
+  }
+  int term = finite_t(cost) ? 0 : 5, iters = 0;
+  T damping = T(O.damping0);
+  for (int it = 0; it < O.max_iterations && term == 0; ++it) {
+    T gm = T(0);
+    for (int i = tid; i < N; i += kTrajThreads) gm = tmax(gm, fabs(S.g[i]));
+    if (block_max(gm, S.red) < T(O.grad_tol)) {
+      term = 1;
+      break;
+    }
+    bool accepted = false;
+    T smax = T(0);
+    for (int rj = 0; rj < O.max_rejections; ++rj) {
+      const bool ok = traj_damped_solve<G>(S, N, damping);
+      T fin = T(1);
+      for (int i = tid; i < N; i += kTrajThreads) {
+        S.qn[i] = S.q[i] + S.y[i];
+        if (!finite_t(S.y[i])) fin = T(0);
+      }
+      __syncthreads();
+      const bool finite_ok = __syncthreads_and(fin > T(0));
+      if (ok && finite_ok) {
+        const T cn = traj_eval<G, false>(C, P, W, S, S.qn);
+        if (!finite_t(cn)) {
+          term = 5;
+          break;
+        }
+        if (cn < cost) {
+          T sm = T(0);
+          for (int i = tid; i < N; i += kTrajThreads) {
+            sm = tmax(sm, fabs(S.y[i]));
+            S.q[i] = S.qn[i];
+          }
+          smax = block_max(sm, S.red);
+          cost = cn;
+          damping = tmax(damping * T(O.down), T(BeamConsts::damping_min));
+          accepted = true;
+          break;
+        }
+      }
+      damping *= T(O.up);
+      if (damping > T(BeamConsts::damping_max)) break;
+    }
+    if (term != 0) break;
+    if (!accepted) {
+      term = damping > T(BeamConsts::damping_max) ? 3 : 4;
+      break;
+    }
+    ++iters;
+    if (tid == 0 && hist_out) hist_out[b * hstride + iters] = double(cost);
+    if (smax < T(O.step_tol)) {
+      term = 2;
+      break;
+    }
+    traj_eval<G, true>(C, P, W, S, S.q);
+  }
+  // outputs + hard-minimum static / swept signed distances (tasks.py:251-275)
+  if (hist_out)
+    for (int i = iters + 1 + tid; i < hstride; i += kTrajThreads) hist_out[b * hstride + i] = NAN;
+  for (int i = tid; i < N; i += kTrajThreads) {
+    const int tt = i / NQ, c = i % NQ;
+    if (c < n) q_out[(b * Tn + tt) * n + c] = double(S.q[i]);
+  }
+  if (tid == 0) {
+    cost_out[b] = double(cost);
+    iters_out[b] = iters;
+    term_out[b] = term;
+  }
+}
+
+// Normal equations of the trajectory problem at given trajectories (parity
+// hook): cost, gradient J^T r and the band of J^T J, unpadded to T*n dense.
+template <class G>
+__global__ void __launch_bounds__(kTrajThreads)
+k_traj_normal(const ChainParams<typename G::T, G::K> C, const CollisionParams<typename G::T> P,
+              const TrajCosts<typename G::T> W, const double* __restrict__ qs, const double* __restrict__ anchors,
+              const double* __restrict__ obstacles, int n_obs, int64_t B, double* __restrict__ cost_out,
+              double* __restrict__ grad_out, double* __restrict__ hess_out) {
+  using T = typename G::T;
+  constexpr int NQ = G::NQ, BW = TrajView<G>::BW;
+  extern __shared__ unsigned char smem_raw[];
+  const TrajView<G> S(smem_raw, W.T_steps, P.ns);
+  const int64_t b = blockIdx.x;
+  const int tid = threadIdx.x, Tn = W.T_steps, N = Tn * NQ, n = W.n, Nr = Tn * n;
+  for (int i = tid; i < 2 * NQ; i += kTrajThreads) {
+    const int c = i % NQ;
+    S.anc[i] = c < n ? T(anchors[(b * 2 + i / NQ) * n + c]) : T(0);
+  }
+  load_obstacles(*S.obs, obstacles, b, n_obs);
+  for (int i = tid; i < N; i += kTrajThreads) {
+    const int tt = i / NQ, c = i % NQ;
+    S.q[i] = c < n ? T(qs[(b * Tn + tt) * n + c]) : T(0);
+  }
+  __syncthreads();
+  const T cost = traj_eval<G, true>(C, P, W, S, S.q);
+  if (tid == 0) cost_out[b] = double(cost);
+  for (int i = tid; i < N; i += kTrajThreads) {
+    const int a = i % NQ;
+    if (a >= n) continue;
+    const int r1 = (i / NQ) * n + a;
+    grad_out[b * Nr + r1] = double(S.g[i]);
+    for (int d = 0; d <= BW; ++d) {
+      const int pc = i - d;
+      if (pc < 0 || pc % NQ >= n) continue;
+      const int r2 = (pc / NQ) * n + pc % NQ;
+      hess_out[(b * Nr + r1) * Nr + r2] = double(S.h(i, d));
+      hess_out[(b * Nr + r2) * Nr + r1] = double(S.h(i, d));
+    }
+  }
+}
+
+// trajectory_signed_distances (tasks.py:251-275) and the endpoint pose errors
+// of plan_trajectory (tasks.py:412-415) for B finished trajectories, FP64:
+// thread t runs the forward pass of q_t, then the static distances of
+// timestep t and the swept distances of the pair (t-1, t).
+template <class G>
+__global__ void __launch_bounds__(kTrajThreads)
+k_traj_report(const ChainParams<double, G::K> C, const CollisionParams<double> P, int steps, int n,
+              const double* __restrict__ qs, const double* __restrict__ obstacles, int n_obs,
+              const double* __restrict__ targets, int64_t B, double* __restrict__ static_out,
+              double* __restrict__ swept_out, double* __restrict__ min_static, double* __restrict__ min_swept,
+              double* __restrict__ pos_err, double* __restrict__ rot_err) {
+  static_assert(sizeof(typename G::T) == 8, "reports run in FP64");
+  constexpr int NQ = G::NQ;
+  extern __shared__ unsigned char smem_raw[];
+  const TrajView<G> S(smem_raw, steps, P.ns);
+  const int64_t b = blockIdx.x;
+  const int tid = threadIdx.x;
+  load_obstacles(*S.obs, obstacles, b, n_obs);
+  __syncthreads();
+  double q[NQ];
+  if (tid < steps) {
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) q[i] = i < n ? qs[(b * steps + tid) * n + i] : 0.0;
+    quat<double> eq;
+    vec3<double> ep;
+    col_forward<G>(C, P, S.lane(tid), q, eq, ep);
+  }
+  __syncthreads();
+  double ds = INFINITY, dw = INFINITY;
+  if (tid < steps) {
+    const ColLane<G> L1 = S.lane(tid);
+    for (int s = 0; s < P.ns; ++s) {
+      const vec3<double> c1{L1.cen(s, 0), L1.cen(s, 1), L1.cen(s, 2)};
+      for (int o = 0; o < S.obs->no; ++o) {
+        vec3<double> nrm;
+        ds = fmin(ds, sphere_obstacle_t<double>(*S.obs, o, c1, P.sr[s], nrm));
+        if (tid >= 1) {
+          const ColLane<G> L0 = S.lane(tid - 1);
+          vec3<double> ga, gb;
+          dw = fmin(dw, capsule_obstacle_t<double>(*S.obs, o, vec3<double>{L0.cen(s, 0), L0.cen(s, 1), L0.cen(s, 2)},
+                                                   c1, P.sr[s], ga, gb));
+        }
+      }
+    }
+    if (static_out) static_out[b * steps + tid] = ds;
+    if (swept_out && tid >= 1) swept_out[b * (steps - 1) + tid - 1] = dw;
+    if (targets && (tid == 0 || tid == steps - 1)) {
+      const int e = tid == 0 ? 0 : 1;
+      double ti[7], pe, re;
+      target_inverse(targets + (b * 2 + e) * 7, ti);
+      pose_errors_f64<G::K>(C, q, nullptr, ti, pe, re);
+      pos_err[b * 2 + e] = pe;
+      rot_err[b * 2 + e] = re;
+    }
+  }
+  ds = -block_max(-ds, S.red);
+  dw = -block_max(-dw, S.red);
+  if (tid == 0) {
+    if (min_static) min_static[b] = ds;
+    if (min_swept) min_swept[b] = dw;
+  }
+}
+
+template <class G>
+size_t traj_smem_bytes(int steps, int n_spheres) {
+  return TrajView<G>::bytes(steps, n_spheres);
+}
+
+template <class G>
+cudaError_t launch_traj(const ChainParams<typename G::T, G::K>& C, const CollisionParams<typename G::T>& P,
+                        const TrajCosts<typename G::T>& W, const TrajLaunch& L, cudaStream_t st) {
+  if (L.B == 0) return cudaSuccess;
+  const size_t smem = TrajView<G>::bytes(W.T_steps, P.ns);
+  cudaError_t e = cudaFuncSetAttribute(k_traj_solve<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_traj_solve<G><<<(unsigned)L.B, kTrajThreads, smem, st>>>(C, P, W, L.q_init, L.anchors, L.obstacles, L.n_obs,
+                                                             L.B, L.opts, L.q_out, L.cost_out, L.init_cost,
+                                                             L.hist_out, L.iters, L.term);
+  return cudaGetLastError();
+}
+
+template <class G>
+cudaError_t launch_traj_normal(const ChainParams<typename G::T, G::K>& C, const CollisionParams<typename G::T>& P,
+                               const TrajCosts<typename G::T>& W, const TrajLaunch& L, cudaStream_t st) {
+  if (L.B == 0) return cudaSuccess;
+  const size_t smem = TrajView<G>::bytes(W.T_steps, P.ns);
+  cudaError_t e = cudaFuncSetAttribute(k_traj_normal<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_traj_normal<G><<<(unsigned)L.B, kTrajThreads, smem, st>>>(C, P, W, L.q_init, L.anchors, L.obstacles, L.n_obs,
+                                                              L.B, L.cost_out, L.grad_out, L.hess_out);
+  return cudaGetLastError();
+}
+
+template <class G>
+cudaError_t launch_traj_report(const ChainParams<double, G::K>& C, const CollisionParams<double>& P,
+                               const TrajReportLaunch& L, cudaStream_t st) {
+  if (L.B == 0) return cudaSuccess;
+  const size_t smem = TrajView<G>::bytes(L.steps, P.ns);
+  cudaError_t e = cudaFuncSetAttribute(k_traj_report<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_traj_report<G><<<(unsigned)L.B, kTrajThreads, smem, st>>>(C, P, L.steps, L.n, L.qs, L.obstacles, L.n_obs,
+                                                              L.targets, L.B, L.static_out, L.swept_out,
+                                                              L.min_static, L.min_swept, L.pos_err, L.rot_err);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_traj_report<Cfg<double, 7, 7, true, false>>(const ChainParams<double, 7>&,
+                                                                        const CollisionParams<double>&,
+                                                                        const TrajReportLaunch&, cudaStream_t);
+template cudaError_t launch_traj_report<Cfg<double, 8, 8, false, false>>(const ChainParams<double, 8>&,
+                                                                         const CollisionParams<double>&,
+                                                                         const TrajReportLaunch&, cudaStream_t);
+
+#define KOP_TRAJ_INSTANTIATE(T, NQ, K, ID)                                                                   \
+  template size_t traj_smem_bytes<Cfg<T, NQ, K, ID, false>>(int, int);                                      \
+  template cudaError_t launch_traj_normal<Cfg<T, NQ, K, ID, false>>(                                        \
+      const ChainParams<T, K>&, const CollisionParams<T>&, const TrajCosts<T>&, const TrajLaunch&, cudaStream_t); \
+  template cudaError_t launch_traj<Cfg<T, NQ, K, ID, false>>(const ChainParams<T, K>&,                      \
+                                                             const CollisionParams<T>&, const TrajCosts<T>&, \
+                                                             const TrajLaunch&, cudaStream_t);
+
+KOP_FOR_EACH_COLLISION_SHAPE(KOP_TRAJ_INSTANTIATE)
+
+}  // namespace kop

@@ -303,3 +303,8 @@ def solve_ik_collision_batch(model: RobotModel, link: str, targets, world=None, 
                           success_rot_tol, precision, world=world, self_collision=self_collision,
                           eta_world=eta_world, eta_self=eta_self, sharpness=sharpness, hard_min=hard_min)
     return solver.solve(targets)
+
+
+# trajectory optimisation lives in trajectory.py; re-exported here where the reference keeps it (tasks.py:183-424)
+from .trajectory import (TrajectoryPlanner, TrajRequest, TrajResult, plan_trajectory,  # noqa: E402,F401
+                         plan_trajectory_batch, trajectory_signed_distances)

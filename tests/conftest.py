@@ -9,6 +9,7 @@ if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
 GOLDEN = os.path.join(ROOT, "tests", "golden", "reference_golden.npz")
+GOLDEN_TRAJ = os.path.join(ROOT, "tests", "golden", "reference_golden_traj.npz")
 ROBOTS = os.path.join(ROOT, "paper_2505_03728_b200", "robots")
 
 
@@ -23,6 +24,11 @@ def robot_file(name):
 @pytest.fixture(scope="session")
 def golden():
     return np.load(GOLDEN)
+
+
+@pytest.fixture(scope="session")
+def golden_traj():
+    return np.load(GOLDEN_TRAJ)
 
 
 @pytest.fixture(scope="session")

@@ -150,3 +150,80 @@ def test_multi_pose_solve_matches_reference_humanoid(golden):
         q, c, h, it, term = to.solve_multi_pose(ch, poses, ch.rest)
         gh = golden["hum_hist"][i]
         assert np.array_equal(np.array(h), gh[~np.isnan(gh)]) and it == golden["hum_iters"][i]
+
+
+# ---------------------------------------------------------------------------
+# config 5: trajectory optimisation (traj_oracle vs reference plan_trajectory)
+# ---------------------------------------------------------------------------
+from oracle import traj_oracle as to  # noqa: E402
+
+TRAJ_CASES = ["scene0", "scene1", "scene2", "empty"]
+
+
+def traj_case(chains, gt, name):
+    from conftest import robot_file
+
+    ch = chains["arm7"]
+    sp = co.load_spheres_files(ch, robot_file("arm7.urdf"), robot_file("arm7.sidecar.json"))
+    k = lambda s: gt[f"traj_{name}_{s}"]
+    obs = [co.sphere(r[1:4], r[7]) for r in k("obstacles")]
+    return ch, sp, obs, to.TrajCosts(timesteps=int(k("T"))), k
+
+
+def test_traj_velocity_limits(chains, golden_traj):
+    from conftest import robot_file
+
+    with open(robot_file("arm7.urdf")) as f:
+        vl = to.velocity_limits(chains["arm7"], f.read())
+    np.testing.assert_array_equal(vl, golden_traj["velocity_limits"])
+
+
+@pytest.mark.parametrize("name", TRAJ_CASES)
+def test_traj_stack_matches_reference_assemble(chains, golden_traj, name):
+    """Cost, gradient J^T r and J^T J of the plan_trajectory Problem at the straight line."""
+    ch, sp, obs, tc, k = traj_case(chains, golden_traj, name)
+    x0 = to.straight_line(k("q_start"), k("q_goal"), tc.timesteps)
+    r, J = to.traj_stack(ch, sp, obs, x0.reshape(-1), k("q_start"), k("q_goal"), tc, golden_traj["velocity_limits"])
+    np.testing.assert_allclose(r @ r, k("r0") @ k("r0"), rtol=1e-13)
+    np.testing.assert_allclose(J.T @ r, k("grad0"), rtol=0, atol=1e-13 * np.abs(k("grad0")).max())
+    np.testing.assert_allclose(J.T @ J, k("h0"), rtol=0, atol=1e-13 * np.abs(k("h0")).max())
+
+
+@pytest.mark.parametrize("name", TRAJ_CASES)
+def test_traj_solve_matches_reference(chains, golden_traj, name):
+    ch, sp, obs, tc, k = traj_case(chains, golden_traj, name)
+    x0 = to.straight_line(k("q_start"), k("q_goal"), tc.timesteps)
+    qs, cost, hist, iters, term = to.solve_traj(ch, sp, obs, x0, k("q_start"), k("q_goal"), tc,
+                                                golden_traj["velocity_limits"])
+    ref_hist = k("hist")[~np.isnan(k("hist"))]
+    m = min(len(hist), len(ref_hist))
+    np.testing.assert_allclose(hist[:m], ref_hist[:m], rtol=1e-9)
+    # the final iterations sit at roundoff: one accepted step more or less and a
+    # step / damping termination swap are the reference's own run-to-run noise
+    assert abs(iters - int(k("iters"))) <= 1
+    np.testing.assert_allclose(cost, float(k("cost")), rtol=1e-9)
+    np.testing.assert_allclose(qs, k("qs"), atol=1e-6)
+    st, sw = to.signed_distances(ch, sp, obs, qs)
+    if obs:
+        np.testing.assert_allclose(st, k("static"), atol=1e-6)
+        np.testing.assert_allclose(sw, k("swept"), atol=1e-6)
+        st_ref, sw_ref = to.signed_distances(ch, sp, obs, k("qs"))
+        np.testing.assert_allclose(st_ref, k("static"), rtol=0, atol=1e-14)
+        np.testing.assert_allclose(sw_ref, k("swept"), rtol=0, atol=1e-14)
+        assert bool(k("collision_free")) == (min(st.min(), sw.min()) >= 0)
+
+
+def test_capsule_obstacle_kinds():
+    """capsule_obstacle vs collision.py:207-237 on hand-checked cases."""
+    c0, c1 = np.array([[0.0, 0.0, 0.0]]), np.array([[1.0, 0.0, 0.0]])
+    d, ga, gb = to.capsule_obstacle(c0, c1, 0.1, co.sphere([0.5, 0.3, 0.0], 0.1))
+    np.testing.assert_allclose(d, [0.1])
+    np.testing.assert_allclose(ga, [[0, -0.5, 0]])
+    np.testing.assert_allclose(gb, [[0, -0.5, 0]])
+    d, ga, gb = to.capsule_obstacle(c0, c1, 0.1, co.capsule([0.2, 1.0, -1.0], [0.2, 1.0, 1.0], 0.2))
+    np.testing.assert_allclose(d, [0.7])
+    np.testing.assert_allclose(ga, [[0, -0.8, 0]], atol=1e-15)
+    d, ga, gb = to.capsule_obstacle(c0, c1, 0.1, co.halfspace([1.0, 0.0, 0.0], -0.5))
+    np.testing.assert_allclose(d, [0.4])
+    np.testing.assert_allclose(ga, [[1, 0, 0]])
+    np.testing.assert_allclose(gb, [[0, 0, 0]])
