@@ -68,3 +68,55 @@ ms = timeit(lambda: s.solve_device(shd, out))
 print(json.dumps({"workload": "mobile-base IK-Beam (Panda + SE(2) base, disk-shifted targets)", "precision": "fp32",
                   "targets": B, "ms": ms, "solves_per_s": B / ms * 1e3,
                   "success": float(out.success.float().mean())}), flush=True)
+# config 5: trajectory optimisation, T=64, random in-limit anchor pairs, one
+# r=0.07 sphere at the FK of the joint-space midpoint (benchmark.py:250-277
+# without the endpoint IK), plan_trajectory cost set, solver.solve options
+from paper_2505_03728_b200.robot import link_poses_device
+NT = int(os.environ.get("NTRAJ", "10000"))
+TT = int(os.environ.get("TSTEPS", "64"))
+rng = np.random.default_rng(5)
+qa = rng.uniform(m.lower_limits, m.upper_limits, (NT, 7))
+qb = rng.uniform(m.lower_limits, m.upper_limits, (NT, 7))
+mid = link_poses_device(m, dv.to_dev(0.5 * (qa + qb)), "flange").cpu().numpy()[:, 4:7]
+obs = np.zeros((NT, 1, 8)); obs[:, 0, 1:4] = mid; obs[:, 0, 7] = 0.07
+anchors = dv.to_dev(np.stack([qa, qb], axis=1)); obsd = dv.to_dev(obs)
+for prec in ("fp32", "fp64"):
+    pl = k.TrajectoryPlanner(m, "flange", timesteps=TT, precision=prec)
+    res = {}
+    def run():
+        res.update(pl.solve_anchored_device(anchors, obsd, 1, history=False))
+    ms = timeit(run, 2)
+    rep = k.trajectory.trajectory_signed_distances_batch(m, res["qs"], obsd, 1, "flange")
+    free = (torch.minimum(rep["min_static"], rep["min_swept"]) >= 0).float().mean().item()
+    it = res["iterations"].float()
+    print(json.dumps({"workload": f"config5 trajectory optimisation (Panda, T={TT}, 1 sphere at the midpoint)",
+                      "precision": prec, "trajectories": NT, "ms": ms, "trajectories_per_s": NT / ms * 1e3,
+                      "mean_iterations": it.mean().item(), "lm_iterations_per_s": it.sum().item() / ms * 1e3,
+                      "collision_free": free,
+                      "terminations": torch.bincount(res["termination"].long(), minlength=6).tolist()}), flush=True)
+# config 3: humanoid (synthetic G1-class, n=29) multi-EE IK through solver.solve
+# semantics, 4 pose costs (hands, feet) + limit + rest, q0 = rest pose
+hum = k.load_robot(k.robot_path("humanoid29.urdf"))
+EES = ["left_hand", "right_hand", "left_foot", "right_foot"]
+NH = int(os.environ.get("NHUM", "100000"))
+qt = dv.to_dev(np.random.default_rng(29).uniform(hum.lower_limits, hum.upper_limits, (NH, hum.actuated_count)))
+tgh = torch.stack([link_poses_device(hum, qt, e) for e in EES], dim=1).contiguous()
+W0 = k.CostWeights()
+hprob = k.Problem(k.VariableSet.of(q=hum.rest_pose.copy()),
+                  [k.pose_cost(hum, "q", e, k.Transform3.identity(), position_weight=W0.pose_position,
+                               orientation_weight=W0.pose_orientation) for e in EES]
+                  + [k.limit_cost(hum, "q", weight=W0.limit), k.rest_cost("q", hum.rest_pose, weight=W0.rest)])
+hp = plan(hprob)
+for prec in ("fp32", "fp64"):
+    opts = _options(k.SolveOptions(precision=prec))
+    q0 = dv.to_dev(np.tile(hum.rest_pose, (NH, 1)))
+    outs = [dv.empty((NH, hum.actuated_count)), dv.empty(NH), dv.empty(NH), None,
+            torch.empty(NH, dtype=torch.int32, device="cuda"), torch.empty(NH, dtype=torch.int32, device="cuda")]
+    def run():
+        check(lib().kop_multi_pose_solve(hum._handle, C.byref(hp.costs), C.byref(opts), dv.ptr(tgh), dv.ptr(q0), NH,
+                                         *(dv.ptr(x) for x in outs), dv.stream_handle()), "tree")
+    ms = timeit(run, 2)
+    print(json.dumps({"workload": "config3 humanoid multi-EE IK (n=29, 4 pose costs + limit + rest; solver.solve semantics)",
+                      "precision": prec, "problems": NH, "ms": ms, "solves_per_s": NH / ms * 1e3,
+                      "mean_iterations": outs[4].float().mean().item(),
+                      "final_cost_p50": outs[1].median().item()}), flush=True)
