@@ -133,6 +133,10 @@ class BeamBatch:
         f = lambda x: x.cpu().numpy() if hasattr(x, "cpu") else x
         return BeamBatch(*(f(getattr(self, k)) for k in self.FIELDS))
 
+    def rows(self, lo: int, hi: int) -> "BeamBatch":
+        """Row slice [lo, hi) of every field (views)."""
+        return BeamBatch(*((None if getattr(self, k) is None else getattr(self, k)[lo:hi]) for k in self.FIELDS))
+
 
 class IkBeamSolver:
     """Reusable batched IK-Beam for one (robot, link, request shape).
@@ -187,15 +191,7 @@ class IkBeamSolver:
         self._ws = None
 
     def workspace(self, batch: int):
-        if self.collision is not None:
-            need = int(lib().kop_ik_beam_collision_workspace_bytes(self.model._handle, self.link_idx,
-                                                                   C.byref(self.params), C.byref(self.collision),
-                                                                   batch))
-        else:
-            need = int(lib().kop_ik_beam_workspace_bytes(self.model._handle, self.link_idx, C.byref(self.params),
-                                                         batch))
-        if need < 0:
-            check(need, "kop_ik_beam_workspace_bytes")
+        need = self._ws_bytes(batch)
         if self._ws is None or self._ws.numel() < need:
             t = dv.require_cuda()
             self._ws = t.empty(need, dtype=t.uint8, device="cuda")
@@ -209,14 +205,16 @@ class IkBeamSolver:
                          dv.empty((batch, 3)) if self.optimize_base else None)
 
     def solve_device(self, targets, out: BeamBatch | None = None, history: bool = True,
-                     stages: int = 3) -> BeamBatch:
+                     stages: int = 3, workspace=None) -> BeamBatch:
         """targets: device (B,7) float64 tensor.  Enqueues the solve on the current
         stream and returns the device outputs.  ``stages`` 1 / 2 issue only the
-        seed+prune or the survivor+winner kernel (for per-kernel timing)."""
+        seed+prune or the survivor+winner kernel (for per-kernel timing).
+        ``workspace``: a caller-owned uint8 device buffer (for concurrent solves
+        on several streams); default the solver's own."""
         targets = dv.to_dev(targets)
         b = targets.shape[0]
         out = out or self.alloc_outputs(b)
-        ws = self.workspace(b)
+        ws = self.workspace(b) if workspace is None else workspace
         if self.collision is not None:
             if stages != 3:
                 raise ValueError("collision IK-Beam runs both stages together")
@@ -235,10 +233,77 @@ class IkBeamSolver:
                                       dv.stream_handle()), "kop_ik_beam")
         return out
 
+    def alloc_host_outputs(self, batch: int) -> BeamBatch:
+        """Pinned host tensors shaped like ``alloc_outputs``."""
+        dev = self.alloc_outputs(0)
+        mk = lambda x, shape: None if x is None else dv.torch().empty(shape, dtype=x.dtype).pin_memory()
+        n = self.model.actuated_count
+        return BeamBatch(mk(dev.q, (batch, n)), mk(dev.cost, (batch,)), mk(dev.history, (batch, self.total_steps + 1)),
+                         mk(dev.pos_error, (batch,)), mk(dev.rot_error, (batch,)), mk(dev.success, (batch,)),
+                         mk(dev.base, (batch, 3)))
+
+    def solve_pinned(self, host_targets, host_out: BeamBatch | None = None, chunk: int = 131072,
+                     n_streams: int = 3, history: bool = True) -> BeamBatch:
+        """Pinned host (B, 7) targets in, pinned host outputs out.  The batch runs
+        in chunks round-robin over ``n_streams`` CUDA streams, so the host->device
+        copy of one chunk, the kernels of another and the device->host copy of a
+        third overlap (copy engines and SMs are separate).  Enqueued behind and
+        joined back into the current stream; synchronise before reading."""
+        t = dv.require_cuda()
+        b = host_targets.shape[0]
+        host_out = host_out or self.alloc_host_outputs(b)
+        chunk = max(1, min(chunk, b))
+        key = (chunk, n_streams)
+        if getattr(self, "_pipe_key", None) != key:
+            self._pipe = [(t.cuda.Stream(), dv.empty((chunk, 7)), self.alloc_outputs(chunk),
+                           t.empty(self._ws_bytes(chunk), dtype=t.uint8, device="cuda")) for _ in range(n_streams)]
+            self._pipe_key = key
+        cur = t.cuda.current_stream()
+        start = t.cuda.Event()
+        start.record(cur)
+        for i, lo in enumerate(range(0, b, chunk)):
+            hi = min(b, lo + chunk)
+            st, tg, out, ws = self._pipe[i % n_streams]
+            if i < n_streams:
+                st.wait_event(start)
+            with t.cuda.stream(st):
+                tgv = tg[:hi - lo]
+                tgv.copy_(host_targets[lo:hi], non_blocking=True)
+                ov = out.rows(0, hi - lo)
+                self.solve_device(tgv, ov, history=history, workspace=ws)
+                hv = host_out.rows(lo, hi)
+                for kk in BeamBatch.FIELDS:
+                    src = getattr(ov, kk)
+                    if src is not None and (history or kk != "history"):
+                        getattr(hv, kk).copy_(src, non_blocking=True)
+        for st, _, _, _ in self._pipe:
+            ev = t.cuda.Event()
+            ev.record(st)
+            cur.wait_event(ev)
+        return host_out
+
+    def _ws_bytes(self, batch: int) -> int:
+        if self.collision is not None:
+            need = int(lib().kop_ik_beam_collision_workspace_bytes(self.model._handle, self.link_idx,
+                                                                   C.byref(self.params), C.byref(self.collision),
+                                                                   batch))
+        else:
+            need = int(lib().kop_ik_beam_workspace_bytes(self.model._handle, self.link_idx, C.byref(self.params),
+                                                         batch))
+        if need < 0:
+            check(need, "kop_ik_beam_workspace_bytes")
+        return need
+
     def solve(self, targets) -> BeamBatch:
-        """Host in, host out (synchronous)."""
+        """Host in, host out (synchronous); large batches stream through ``solve_pinned``."""
         arr = targets_to_array(targets)
-        return self.solve_device(dv.to_dev(arr)).cpu()
+        if arr.shape[0] <= 131072:
+            return self.solve_device(dv.to_dev(arr)).cpu()
+        t = dv.require_cuda()
+        host = t.from_numpy(np.ascontiguousarray(arr)).pin_memory()
+        res = self.solve_pinned(host)
+        t.cuda.current_stream().synchronize()
+        return res.cpu()
 
 
 def solve_ik_beam_batch(model: RobotModel, link: str, targets, weights: ck.CostWeights | None = None,
