@@ -146,7 +146,8 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * wall / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload_config(per_step, "fp64"),
+        # the same config line as our arm; each reference step is the bounded sample named in cpu_baseline
+        "data": "synthetic", "config": workload_config(args.batch, args.precision),
         "cpu_baseline": {"value": value, "unit": "solves/s", "cores": arm.cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -164,7 +165,7 @@ def workload_config(batch, precision):
                     f"(benchmark.py:83-93, rng {RNG_SEED}); 64 seeds, 6 LM steps, keep 4, 10 more steps",
         "targets_per_gpu": batch, "seeds": SEEDS, "lm_steps": f"{PRUNE}+{TOTAL - PRUNE}", "keep": KEEP,
         "precision": precision, "weights": "CostWeights() defaults (50, 10, 100, 0.01)",
-        "l2": "flushed between timed steps (512 MiB write); inputs 56 MB/GPU",
+        "l2": f"flushed between timed steps (512 MiB write); inputs {batch * 56 / 1e6:.0f} MB/GPU",
         "parallelism": "targets sharded, no collective in the solve",
     }
 
