@@ -53,7 +53,7 @@ __device__ __forceinline__ void sincos_t(double a, double* s, double* c) { sinco
 __device__ __forceinline__ float sqrt_t(float a) { return sqrtf(a); }
 __device__ __forceinline__ double sqrt_t(double a) { return sqrt(a); }
 __device__ __forceinline__ float rsqrt_t(float a) { return rsqrtf(a); }
-__device__ __forceinline__ double rsqrt_t(double a) { return 1.0 / sqrt(a); }
+__device__ __forceinline__ double rsqrt_t(double a) { return ::rsqrt(a); }
 __device__ __forceinline__ float atan2_t(float y, float x) { return atan2f(y, x); }
 __device__ __forceinline__ double atan2_t(double y, double x) { return atan2(y, x); }
 __device__ __forceinline__ float tan_t(float a) { return tanf(a); }

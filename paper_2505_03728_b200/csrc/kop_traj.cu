@@ -434,73 +434,126 @@ __device__ typename G::T traj_eval(const ChainParams<typename G::T, G::K>& C, co
 }
 
 // Banded damped Cholesky solve: y <- -(H + lam diag(max(diag H, 1e-8)))^-1 g.
+//
+// Blocked right-looking factorisation over timestep blocks of NQ columns
+// (three barriers per block instead of two per column), with the forward
+// substitution fused in:
+//   1  warp 0: Cholesky of the NQ x NQ diagonal block, lane a holding row a
+//      in registers (shuffles carry the pivot column), and y_blk <- D^-1 y_blk;
+//   2  threads 0..BW-1: the BW rows below solve x D^T = a (their NQ-wide slice
+//      of the block column) and y_r -= x . y_blk;
+//   3  all threads: trailing update L(r, c) -= x_r . x_c of the BW x BW
+//      lower triangle below the block.
+// Entries of the band beyond half-width BW are structural zeros of the
+// factor (the profile of row t*NQ+a starts at (t-4)*NQ+a), and the recurrences
+// keep them zero, so they are never stored.  The back substitution L^T x = y
+// is a column sweep by warp 0 (lane d updates y[k-d]).
+template <class G>
+__device__ __forceinline__ typename G::T lz(const TrajView<G>& S, int r, int c) {
+  const int d = r - c;
+  return d <= TrajView<G>::BW ? S.l(r, d) : typename G::T(0);
+}
+
 template <class G>
 __device__ bool traj_damped_solve(const TrajView<G>& S, int N, typename G::T lam) {
   using T = typename G::T;
-  constexpr int BW = TrajView<G>::BW;
+  constexpr int NQ = G::NQ, BW = TrajView<G>::BW;
+  static_assert(BW <= 32, "band wider than a warp");
   const int tid = threadIdx.x;
   for (int i = tid; i < N; i += kTrajThreads) {
     for (int d = 0; d <= BW; ++d) S.l(i, d) = S.h(i, d);  // zero outside the compact blocks
     S.l(i, 0) += lam * tmax(S.h(i, 0), T(BeamConsts::diag_clamp));
     S.y[i] = -S.g[i];
   }
-  __syncthreads();
-  // trailing-update pairs (di, dj), 1 <= dj <= di <= BW, dealt to the threads once
+  // trailing-update pairs (ri, ci), 0 <= ci <= ri < BW, dealt to the threads once
   constexpr int NPAIR = BW * (BW + 1) / 2;
   constexpr int PPT = (NPAIR + kTrajThreads - 1) / kTrajThreads;
-  int pdi[PPT], pdj[PPT];
+  int pri[PPT], pci[PPT];
 #pragma unroll
   for (int r = 0; r < PPT; ++r) {
-    int rem = tid + r * kTrajThreads, di = 1;
-    while (di <= BW && rem >= di) {
-      rem -= di;
-      ++di;
+    int rem = tid + r * kTrajThreads, ri = 0;
+    while (ri < BW && rem > ri) {
+      rem -= ri + 1;
+      ++ri;
     }
-    pdi[r] = di;  // > BW: no pair
-    pdj[r] = rem + 1;
+    pri[r] = ri;  // >= BW: no pair
+    pci[r] = rem;
   }
+  __syncthreads();
   bool ok = true;
-  for (int k = 0; k < N; ++k) {
-    const T piv = S.l(k, 0);
-    ok = ok && piv > T(0) && finite_t(piv);
-    const T inv = rsqrt_t(piv);
-    // L_ik L_jk = raw_ik raw_jk / piv on the unscaled column
-    T upd[PPT];
+  const int nblk = N / NQ;
+  for (int jb = 0; jb < nblk; ++jb) {
+    const int c0 = jb * NQ;
+    if (tid < 32) {  // 1: diagonal block + its slice of the forward substitution
+      const int a = tid;
+      T row[NQ];
 #pragma unroll
-    for (int r = 0; r < PPT; ++r)
-      upd[r] = (pdi[r] <= BW && k + pdi[r] < N) ? S.l(k + pdi[r], pdi[r]) * S.l(k + pdj[r], pdj[r]) * (inv * inv)
-                                                : T(0);
-    const bool col = tid >= 1 && tid <= BW && k + tid < N;
-    const T scaled = col ? S.l(k + tid, tid) * inv : T(0);
+      for (int b = 0; b < NQ; ++b) row[b] = (a < NQ && b <= a) ? S.l(c0 + a, a - b) : T(0);
+      T yv = a < NQ ? S.y[c0 + a] : T(0);
+#pragma unroll
+      for (int k = 0; k < NQ; ++k) {
+        const T dk = __shfl_sync(0xffffffffu, row[k], k);
+        ok = ok && dk > T(0) && finite_t(dk);
+        const T inv = rsqrt_t(dk);
+        if (a == k) row[k] = dk * inv;
+        else if (a > k) row[k] *= inv;
+        const T yk = __shfl_sync(0xffffffffu, yv, k) * inv;
+        if (a == k) yv = yk;
+        else if (a > k) yv -= row[k] * yk;
+#pragma unroll
+        for (int j = k + 1; j < NQ; ++j) {
+          const T ljk = __shfl_sync(0xffffffffu, row[k], j);
+          if (a >= j && a < NQ) row[j] -= row[k] * ljk;
+        }
+        if (a == 0) S.dinv[c0 + k] = inv;
+      }
+      if (a < NQ) {
+#pragma unroll
+        for (int b = 0; b < NQ; ++b)
+          if (b <= a) S.l(c0 + a, a - b) = row[b];
+        S.y[c0 + a] = yv;
+      }
+    }
+    __syncthreads();
+    if (tid < BW && c0 + NQ + tid < N) {  // 2: rows below the block
+      const int r = c0 + NQ + tid;
+      T x[NQ];
+      T yu = T(0);
+#pragma unroll
+      for (int b = 0; b < NQ; ++b) {
+        T v = lz(S, r, c0 + b);
+#pragma unroll
+        for (int m = 0; m < NQ; ++m)
+          if (m < b) v -= x[m] * S.l(c0 + b, b - m);
+        x[b] = v * S.dinv[c0 + b];
+        yu += x[b] * S.y[c0 + b];
+      }
+#pragma unroll
+      for (int b = 0; b < NQ; ++b)
+        if (r - (c0 + b) <= BW) S.l(r, r - (c0 + b)) = x[b];
+      S.y[r] -= yu;
+    }
     __syncthreads();
 #pragma unroll
-    for (int r = 0; r < PPT; ++r)
-      if (pdi[r] <= BW && k + pdi[r] < N) S.l(k + pdi[r], pdi[r] - pdj[r]) -= upd[r];
-    if (col) S.l(k + tid, tid) = scaled;
-    if (tid == 0) {
-      S.l(k, 0) = piv * inv;
-      S.dinv[k] = inv;
+    for (int p = 0; p < PPT; ++p) {  // 3: trailing update below the block
+      const int r = c0 + NQ + pri[p], c = c0 + NQ + pci[p];
+      if (pri[p] < BW && r < N) {
+        T acc = T(0);
+#pragma unroll
+        for (int b = 0; b < NQ; ++b) acc += lz(S, r, c0 + b) * lz(S, c, c0 + b);
+        S.l(r, r - c) -= acc;
+      }
     }
     __syncthreads();
   }
   ok = __syncthreads_and(ok);
-  // forward / backward substitution by warp 0; lane l handles band offset l + 1 (BW <= 32)
-  static_assert(BW <= 32, "band wider than a warp");
+  // back substitution L^T x = y, column sweep: x_k final, then y[k-d] -= L(k, k-d) x_k
   if (tid < 32) {
     const int d = tid + 1;
-    for (int k = 0; k < N; ++k) {
-      const T yk = S.y[k] * S.dinv[k];
-      __syncwarp();
-      if (d <= BW && k + d < N) S.y[k + d] -= S.l(k + d, d) * yk;
-      if (tid == 0) S.y[k] = yk;
-      __syncwarp();
-    }
     for (int k = N - 1; k >= 0; --k) {
-      T part = (d <= BW && k + d < N) ? S.l(k + d, d) * S.y[k + d] : T(0);
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      const T xk = (S.y[k] - part) * S.dinv[k];
+      const T xk = S.y[k] * S.dinv[k];
       __syncwarp();
+      if (d <= BW && k - d >= 0) S.y[k - d] -= S.l(k, d) * xk;
       if (tid == 0) S.y[k] = xk;
       __syncwarp();
     }
