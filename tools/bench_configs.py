@@ -1,6 +1,9 @@
 """Device timing of the widened configurations (not the driver's bench line):
 config 4 collision IK-Beam and the generic collision LM solve, config 2 mobile
-IK-Beam.  Prints one JSON line per workload."""
+IK-Beam, config 5 trajectories, config 3 humanoid.  Prints one JSON line per
+workload; with CPU=1 (default) each FP64 line carries a ``cpu_baseline``: the
+oracle port of the reference (test infrastructure, float64 NumPy) timed on one
+host core over a bounded sample of the same workload."""
 import json, os, sys, time
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -11,6 +14,29 @@ from paper_2505_03728_b200.tasks import IkBeamSolver
 DEMO = k.WorldModel([k.Sphere([0.45, 0.1, 0.55], 0.12), k.Capsule([-0.5, -0.4, 0.2], [-0.5, 0.4, 0.6], 0.1),
                      k.HalfSpace([0.0, 0.0, 1.0], -0.3)])
 m = k.load_robot(k.robot_path("arm7.urdf"), k.robot_path("arm7.sidecar.json"))
+
+
+CPU = os.environ.get("CPU", "1") == "1"
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def cpu_time(fn, count, unit, sample):
+    """Single-core wall time of the oracle port over `count` units -> cpu_baseline dict."""
+    if not CPU:
+        return None
+    t0 = time.perf_counter()
+    fn()
+    dt = time.perf_counter() - t0
+    return {"value": count / dt, "unit": unit, "cores": 1, "kind": "port", "sample": sample}
+
+
+if CPU:
+    from oracle import collision_oracle as co, ik_oracle as o, traj_oracle as to, tree_oracle as tro
+    ch7 = o.load_chain_files(k.robot_path("arm7.urdf"), k.robot_path("arm7.sidecar.json"))
+    sp7 = co.load_spheres_files(ch7, k.robot_path("arm7.urdf"), k.robot_path("arm7.sidecar.json"))
+    FL = ch7.link("flange")
+    DEMO_O = [co.sphere([0.45, 0.1, 0.55], 0.12), co.capsule([-0.5, -0.4, 0.2], [-0.5, 0.4, 0.6], 0.1),
+              co.halfspace([0.0, 0.0, 1.0], -0.3)]
 
 
 def timeit(fn, reps=5):
@@ -29,9 +55,16 @@ for prec in ("fp32", "fp64"):
     s = IkBeamSolver(m, "flange", rng_seed=77, precision=prec, world=DEMO, self_collision=True)
     out = s.alloc_outputs(B)
     ms = timeit(lambda: s.solve_device(tg, out))
+    cpu = None
+    if prec == "fp64" and CPU:
+        tgh = tg[:2].cpu().numpy()
+        seeds = o.sample_seeds(ch7, 64, 77)
+        cpu = cpu_time(lambda: co.ik_beam_collision(ch7, sp7, DEMO_O, FL, tgh[:, :4], tgh[:, 4:], seeds,
+                                                    co.CollisionCosts()), 2, "solves/s",
+                       "2 targets of this workload, oracle port (float64 NumPy), 1 core")
     print(json.dumps({"workload": "config4 collision IK-Beam (Panda, demo world: sphere+capsule+half-space, self pairs)",
                       "precision": prec, "targets": B, "ms": ms, "solves_per_s": B / ms * 1e3,
-                      "success": float(out.success.float().mean())}), flush=True)
+                      "success": float(out.success.float().mean()), "cpu_baseline": cpu}), flush=True)
 # generic solve (solver.solve semantics), q0 = rest pose, 100 iterations max
 nb = min(B, 20000)
 probs_t = tg[:nb].cpu().numpy()
@@ -55,9 +88,16 @@ for prec in ("fp32", "fp64"):
                                  *(dv.ptr(x) for x in outs), dv.stream_handle()), "solve")
     ms = timeit(run, 3)
     it = outs[4].float().mean().item()
+    cpu = None
+    if prec == "fp64" and CPU:
+        def cpu_run():
+            for i in range(5):
+                co.solve_lm(ch7, sp7, DEMO_O, FL, probs_t[i, :4], probs_t[i, 4:], m.rest_pose.copy(),
+                            co.CollisionCosts())
+        cpu = cpu_time(cpu_run, 5, "solves/s", "5 problems of this workload, oracle port (float64 NumPy), 1 core")
     print(json.dumps({"workload": "generic LM solve (solver.solve semantics) on the collision stack, q0 = rest pose",
                       "precision": prec, "problems": nb, "ms": ms, "solves_per_s": nb / ms * 1e3,
-                      "mean_iterations": it}), flush=True)
+                      "mean_iterations": it, "cpu_baseline": cpu}), flush=True)
 # mobile
 sh = tg.cpu().numpy().copy()
 sh[:, 4:] += disk_translations(B, 2.0, 2024) if B <= 20000 else np.tile(disk_translations(20000, 2.0, 2024), (B // 20000 + 1, 1))[:B]
@@ -65,9 +105,14 @@ shd = dv.to_dev(sh)
 s = IkBeamSolver(m, "flange", rng_seed=77, optimize_base=True)
 out = s.alloc_outputs(B)
 ms = timeit(lambda: s.solve_device(shd, out))
+cpu = None
+if CPU:
+    seeds = o.sample_seeds(ch7, 64, 77)
+    cpu = cpu_time(lambda: o.ik_beam(ch7, FL, sh[:4, :4], sh[:4, 4:], seeds, use_base=True), 4, "solves/s",
+                   "4 targets of this workload, oracle port (float64 NumPy), 1 core")
 print(json.dumps({"workload": "mobile-base IK-Beam (Panda + SE(2) base, disk-shifted targets)", "precision": "fp32",
                   "targets": B, "ms": ms, "solves_per_s": B / ms * 1e3,
-                  "success": float(out.success.float().mean())}), flush=True)
+                  "success": float(out.success.float().mean()), "cpu_baseline": cpu}), flush=True)
 # config 5: trajectory optimisation, T=64, random in-limit anchor pairs, one
 # r=0.07 sphere at the FK of the joint-space midpoint (benchmark.py:250-277
 # without the endpoint IK), plan_trajectory cost set, solver.solve options
@@ -89,7 +134,13 @@ for prec in ("fp32", "fp64"):
     rep = k.trajectory.trajectory_signed_distances_batch(m, res["qs"], obsd, 1, "flange")
     free = (torch.minimum(rep["min_static"], rep["min_swept"]) >= 0).float().mean().item()
     it = res["iterations"].float()
-    print(json.dumps({"workload": f"config5 trajectory optimisation (Panda, T={TT}, 1 sphere at the midpoint)",
+    cpu = None
+    if prec == "fp64" and CPU:
+        tc = to.TrajCosts(timesteps=TT)
+        cpu = cpu_time(lambda: to.solve_traj(ch7, sp7, [co.sphere(mid[0], 0.07)], to.straight_line(qa[0], qb[0], TT),
+                                             qa[0], qb[0], tc, m.velocity_limits), 1, "trajectories/s",
+                       "trajectory 0 of this workload, oracle port (float64 NumPy, dense normal equations), 1 core")
+    print(json.dumps({"cpu_baseline": cpu, "workload": f"config5 trajectory optimisation (Panda, T={TT}, 1 sphere at the midpoint)",
                       "precision": prec, "trajectories": NT, "ms": ms, "trajectories_per_s": NT / ms * 1e3,
                       "mean_iterations": it.mean().item(), "lm_iterations_per_s": it.sum().item() / ms * 1e3,
                       "collision_free": free,
@@ -116,7 +167,18 @@ for prec in ("fp32", "fp64"):
         check(lib().kop_multi_pose_solve(hum._handle, C.byref(hp.costs), C.byref(opts), dv.ptr(tgh), dv.ptr(q0), NH,
                                          *(dv.ptr(x) for x in outs), dv.stream_handle()), "tree")
     ms = timeit(run, 2)
-    print(json.dumps({"workload": "config3 humanoid multi-EE IK (n=29, 4 pose costs + limit + rest; solver.solve semantics)",
+    cpu = None
+    if prec == "fp64" and CPU:
+        chh = o.load_chain_files(k.robot_path("humanoid29.urdf"))
+        tgc = tgh[:3].cpu().numpy()
+        links = [chh.link(e) for e in EES]
+        def cpu_run():
+            for i in range(3):
+                poses = [(l, tgc[i, j, :4], tgc[i, j, 4:], W0.pose_position, W0.pose_orientation)
+                         for j, l in enumerate(links)]
+                tro.solve_multi_pose(chh, poses, hum.rest_pose.copy())
+        cpu = cpu_time(cpu_run, 3, "solves/s", "3 problems of this workload, oracle port (float64 NumPy), 1 core")
+    print(json.dumps({"cpu_baseline": cpu, "workload": "config3 humanoid multi-EE IK (n=29, 4 pose costs + limit + rest; solver.solve semantics)",
                       "precision": prec, "problems": NH, "ms": ms, "solves_per_s": NH / ms * 1e3,
                       "mean_iterations": outs[4].float().mean().item(),
                       "final_cost_p50": outs[1].median().item()}), flush=True)
