@@ -319,6 +319,10 @@ int kop_link_poses(const KopModel* model, int32_t link, const double* q, int64_t
  * entry exists in MEASURED_PEAKS.json).  Writes flops executed to *flops. */
 int kop_fma_peak_kernel(int32_t blocks, int32_t threads, int32_t iters, float* sink, double* flops,
                         void* stream);
+/* FP64 twin (8 independent DFMA chains per thread) for the FP64 roofline of
+ * the parity-mode / widened kernels. */
+int kop_dfma_peak_kernel(int32_t blocks, int32_t threads, int32_t iters, double* sink, double* flops,
+                         void* stream);
 
 #ifdef __cplusplus
 }

@@ -233,4 +233,24 @@ cudaError_t launch_fma_peak(int blocks, int threads, int iters, float* sink, cud
   return cudaGetLastError();
 }
 
+// FP64 twin: 8 independent DFMA chains per thread
+__global__ void __launch_bounds__(256) k_dfma_peak(double* sink, int iters) {
+  double a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = (double)(threadIdx.x + k) * 1e-3;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fma(a[k], 0.9999, 0.0001);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.678) sink[blockIdx.x] = s;  // never true; defeats DCE
+}
+
+cudaError_t launch_dfma_peak(int blocks, int threads, int iters, double* sink, cudaStream_t st) {
+  k_dfma_peak<<<blocks, threads, 0, st>>>(sink, iters);
+  return cudaGetLastError();
+}
+
 }  // namespace kop

@@ -1358,6 +1358,13 @@ int kop_traj_report(const KopModel* m, int32_t link, int32_t timesteps, const do
   return cuda_status(e);
 }
 
+int kop_dfma_peak_kernel(int32_t blocks, int32_t threads, int32_t iters, double* sink, double* flops,
+                         void* stream) {
+  if (blocks <= 0 || threads <= 0 || iters <= 0 || !sink) return fail(KOP_EINVAL, "invalid arguments");
+  if (flops) *flops = 2.0 * 8.0 * (double)blocks * threads * (double)iters;
+  return cuda_status(launch_dfma_peak(blocks, threads, iters, sink, (cudaStream_t)stream));
+}
+
 int kop_fma_peak_kernel(int32_t blocks, int32_t threads, int32_t iters, float* sink, double* flops,
                         void* stream) {
   if (blocks <= 0 || threads <= 0 || iters <= 0 || !sink) return fail(KOP_EINVAL, "invalid arguments");

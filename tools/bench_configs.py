@@ -39,6 +39,46 @@ if CPU:
               co.halfspace([0.0, 0.0, 1.0], -0.3)]
 
 
+def _peak(fn, dtype, chains):
+    import ctypes as C
+    from paper_2505_03728_b200._lib import lib as _lib
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    sink = torch.zeros(4096, device="cuda", dtype=dtype)
+    fl = C.c_double()
+    st = torch.cuda.current_stream().cuda_stream
+    getattr(_lib(), fn)(sms * 8, 256, 2000, sink.data_ptr(), C.byref(fl), st)
+    torch.cuda.synchronize()
+    best = 0.0
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        getattr(_lib(), fn)(sms * 8, 256, 20000, sink.data_ptr(), C.byref(fl), st)
+        e1.record(); torch.cuda.synchronize()
+        best = max(best, fl.value / (e0.elapsed_time(e1) * 1e-3) / 1e12)
+    return best
+
+
+PEAK = {"fp32": _peak("kop_fma_peak_kernel", torch.float32, 16), "fp64": _peak("kop_dfma_peak_kernel", torch.float64, 8)}
+try:
+    with open(os.path.join(ROOT, "profiles", "r01_widened_flops.json")) as _f:
+        FLOPS = {(w["workload"], w["precision"]): w for w in json.load(_f)["workloads"]}
+except OSError:
+    FLOPS = {}
+
+
+def roofline(key, prec, units_per_s):
+    """Executed-flop roofline of a widened workload against the measured FMA-pipe peak."""
+    w = FLOPS.get((key, prec))
+    if w is None:
+        return None
+    fpu = w["fp32_flops_per_unit"] if prec == "fp32" else w["fp64_flops_per_unit"]
+    ach = fpu * units_per_s / 1e12
+    return {"bound": "latency (serial LM chain per problem); compared with the " + prec.upper() + " FMA pipe",
+            "achieved": ach, "peak": PEAK[prec], "unit": "TFLOP/s", "frac": ach / PEAK[prec],
+            "flops_per_unit": fpu, "basis": "executed flops, ncu SASS counters (profiles/r01_widened_flops.json)",
+            "peak_source": "live " + ("FFMA" if prec == "fp32" else "DFMA") + " microbenchmark"}
+
+
 def timeit(fn, reps=5):
     fn(); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -64,7 +104,8 @@ for prec in ("fp32", "fp64"):
                        "2 targets of this workload, oracle port (float64 NumPy), 1 core")
     print(json.dumps({"workload": "config4 collision IK-Beam (Panda, demo world: sphere+capsule+half-space, self pairs)",
                       "precision": prec, "targets": B, "ms": ms, "solves_per_s": B / ms * 1e3,
-                      "success": float(out.success.float().mean()), "cpu_baseline": cpu}), flush=True)
+                      "success": float(out.success.float().mean()), "cpu_baseline": cpu,
+                      "roofline": roofline("config4 collision IK-Beam", prec, B / ms * 1e3)}), flush=True)
 # generic solve (solver.solve semantics), q0 = rest pose, 100 iterations max
 nb = min(B, 20000)
 probs_t = tg[:nb].cpu().numpy()
@@ -97,7 +138,8 @@ for prec in ("fp32", "fp64"):
         cpu = cpu_time(cpu_run, 5, "solves/s", "5 problems of this workload, oracle port (float64 NumPy), 1 core")
     print(json.dumps({"workload": "generic LM solve (solver.solve semantics) on the collision stack, q0 = rest pose",
                       "precision": prec, "problems": nb, "ms": ms, "solves_per_s": nb / ms * 1e3,
-                      "mean_iterations": it, "cpu_baseline": cpu}), flush=True)
+                      "mean_iterations": it, "cpu_baseline": cpu,
+                      "roofline": roofline("generic LM solve (collision stack)", prec, nb / ms * 1e3)}), flush=True)
 # mobile
 sh = tg.cpu().numpy().copy()
 sh[:, 4:] += disk_translations(B, 2.0, 2024) if B <= 20000 else np.tile(disk_translations(20000, 2.0, 2024), (B // 20000 + 1, 1))[:B]
@@ -112,7 +154,8 @@ if CPU:
                    "4 targets of this workload, oracle port (float64 NumPy), 1 core")
 print(json.dumps({"workload": "mobile-base IK-Beam (Panda + SE(2) base, disk-shifted targets)", "precision": "fp32",
                   "targets": B, "ms": ms, "solves_per_s": B / ms * 1e3,
-                  "success": float(out.success.float().mean()), "cpu_baseline": cpu}), flush=True)
+                  "success": float(out.success.float().mean()), "cpu_baseline": cpu,
+                  "roofline": roofline("mobile-base IK-Beam", "fp32", B / ms * 1e3)}), flush=True)
 # config 5: trajectory optimisation, T=64, random in-limit anchor pairs, one
 # r=0.07 sphere at the FK of the joint-space midpoint (benchmark.py:250-277
 # without the endpoint IK), plan_trajectory cost set, solver.solve options
@@ -144,6 +187,7 @@ for prec in ("fp32", "fp64"):
                       "precision": prec, "trajectories": NT, "ms": ms, "trajectories_per_s": NT / ms * 1e3,
                       "mean_iterations": it.mean().item(), "lm_iterations_per_s": it.sum().item() / ms * 1e3,
                       "collision_free": free,
+                      "roofline": roofline("config5 trajectory optimisation T=64", prec, NT / ms * 1e3) if TT == 64 else None,
                       "terminations": torch.bincount(res["termination"].long(), minlength=6).tolist()}), flush=True)
 # config 3: humanoid (synthetic G1-class, n=29) multi-EE IK through solver.solve
 # semantics, 4 pose costs (hands, feet) + limit + rest, q0 = rest pose
@@ -181,4 +225,5 @@ for prec in ("fp32", "fp64"):
     print(json.dumps({"cpu_baseline": cpu, "workload": "config3 humanoid multi-EE IK (n=29, 4 pose costs + limit + rest; solver.solve semantics)",
                       "precision": prec, "problems": NH, "ms": ms, "solves_per_s": NH / ms * 1e3,
                       "mean_iterations": outs[4].float().mean().item(),
-                      "final_cost_p50": outs[1].median().item()}), flush=True)
+                      "final_cost_p50": outs[1].median().item(),
+                      "roofline": roofline("config3 humanoid multi-EE IK", prec, NH / ms * 1e3)}), flush=True)
