@@ -328,6 +328,19 @@ def run_ours(args, rank, world, local_rank):
         e1.record()
         e1.synchronize()
         e2e_ms += e0.elapsed_time(e1)
+    # PCIe copy rates on their own (report H2D / D2H GB/s separately)
+    def copy_gbs(dst, src, nbytes):
+        dst.copy_(src, non_blocking=True)
+        torch.cuda.synchronize()
+        c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        c0.record()
+        for _ in range(3):
+            dst.copy_(src, non_blocking=True)
+        c1.record()
+        c1.synchronize()
+        return 3 * nbytes / (c0.elapsed_time(c1) * 1e-3) / 1e9
+    h2d_gbs = copy_gbs(torch.empty_like(targets), host_t, h2d)
+    d2h_gbs = copy_gbs(host_out.history, out.history, host_out.history.numel() * 8)
     # the pipelined results must equal the device-resident run's
     e2e_match = bool(np.array_equal(host_out.q.numpy(), res.q) and np.array_equal(host_out.cost.numpy(), res.cost))
     if dist:
@@ -352,7 +365,8 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(d2h * world),
                 "api": "IkBeamSolver.solve_pinned: pinned host targets -> all IkResult fields in pinned host memory; "
                        "131072-target chunks, H2D / kernels / D2H overlapped on 3 streams",
-                "launches_per_step": 2 * -(-B // 131072), "bitwise_equal_to_device_run": e2e_match},
+                "launches_per_step": 2 * -(-B // 131072), "bitwise_equal_to_device_run": e2e_match,
+                "pcie_h2d_gbs": h2d_gbs, "pcie_d2h_gbs": d2h_gbs},
         "gpu_launches": 2 * args.steps,
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,

@@ -107,7 +107,7 @@ for prec in ("fp32", "fp64"):
                       "success": float(out.success.float().mean()), "cpu_baseline": cpu,
                       "roofline": roofline("config4 collision IK-Beam", prec, B / ms * 1e3)}), flush=True)
 # generic solve (solver.solve semantics), q0 = rest pose, 100 iterations max
-nb = min(B, 20000)
+nb = min(B, 100000)
 probs_t = tg[:nb].cpu().numpy()
 from paper_2505_03728_b200.solver import plan, _options
 import ctypes as C
