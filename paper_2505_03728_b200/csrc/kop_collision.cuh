@@ -62,8 +62,9 @@ __device__ __forceinline__ void activation_t(T d, T eta, T& a, T& da) {
     a = -d + T(0.5) * eta;
     da = T(-1);
   } else if (d < eta) {
-    a = (T(0.5) / eta) * (eta - d) * (eta - d);
-    da = -(eta - d) / eta;
+    const T ie = div_t(T(1), eta);
+    a = (T(0.5) * ie) * (eta - d) * (eta - d);
+    da = -(eta - d) * ie;
   } else {
     a = T(0);
     da = T(0);
@@ -94,18 +95,18 @@ __device__ __forceinline__ T sphere_obstacle_t(const OB& P, int o, const vec3<T>
     const T dd = dot(d, d);
     T u = T(0);
     if (!(dd < T(1e-16))) {
-      u = dot(vec3<T>{c.x - a.x, c.y - a.y, c.z - a.z}, d) / dd;
+      u = div_t(dot(vec3<T>{c.x - a.x, c.y - a.y, c.z - a.z}, d), dd);
       u = tmin(tmax(u, T(0)), T(1));
     }
     p = {a.x + u * d.x, a.y + u * d.y, a.z + u * d.z};
   }
   const vec3<T> v{c.x - p.x, c.y - p.y, c.z - p.z};
-  const T nn = sqrt_t(dot(v, v));
+  T nn, inv;
+  norm_inv_t(dot(v, v), nn, inv);
   if (nn < T(1e-12)) {
     n = {T(0), T(0), T(0)};
     return T(0) - r - P.orad[o];
   }
-  const T inv = T(1) / nn;
   n = {v.x * inv, v.y * inv, v.z * inv};
   return nn - r - P.orad[o];
 }
@@ -245,25 +246,32 @@ __device__ __forceinline__ typename G::T col_rows(const ChainParams<typename G::
     for (int li = 0; li < P.nl; ++li) {
       const int f = P.lfirst[li], nsph = P.lcount[li];
       for (int o = 0; o < O.no; ++o, ++row) {
-        T dmin = inf_t<T>();
-        int kmin = 0;
-        for (int s = 0; s < nsph; ++s) {
-          vec3<T> n;
-          const T d = sphere_obstacle_t<T>(O, o, vec3<T>{L.cen(f + s, 0), L.cen(f + s, 1), L.cen(f + s, 2)},
-                                        P.sr[f + s], n);
-          if (d < dmin) {
-            dmin = d;
-            kmin = s;
-          }
-        }
+        // one pass, online soft minimum: rescale the running sums whenever
+        // the minimum drops (same value as costs.py:409-420's two passes)
         const bool hard = P.hard || nsph == 1;
-        T sumz = T(0);
+        T dmin = inf_t<T>(), sumz = T(0);
         vec3<T> M{T(0), T(0), T(0)}, Gv{T(0), T(0), T(0)};
         for (int s = 0; s < nsph; ++s) {
           const vec3<T> c{L.cen(f + s, 0), L.cen(f + s, 1), L.cen(f + s, 2)};
           vec3<T> n;
           const T d = sphere_obstacle_t<T>(O, o, c, P.sr[f + s], n);
-          const T z = hard ? (s == kmin ? T(1) : T(0)) : exp_t(-P.beta * (d - dmin));
+          T z;
+          if (hard) {  // argmin, first on ties
+            if (!(d < dmin)) continue;
+            dmin = d;
+            z = T(1);
+            sumz = T(0);
+            M = Gv = vec3<T>{T(0), T(0), T(0)};
+          } else {
+            if (d < dmin) {
+              const T sc = exp_t(-P.beta * (dmin - d));  // 0 on the first sphere
+              sumz *= sc;
+              M = {M.x * sc, M.y * sc, M.z * sc};
+              Gv = {Gv.x * sc, Gv.y * sc, Gv.z * sc};
+              dmin = d;
+            }
+            z = exp_t(-P.beta * (d - dmin));
+          }
           sumz += z;
           if (JAC) {
             const vec3<T> cn = cross(c, n);
@@ -278,7 +286,7 @@ __device__ __forceinline__ typename G::T col_rows(const ChainParams<typename G::
         cost += res * res;
         if (row_out) row_out[row] = double(res);
         if (JAC && dact != T(0)) {
-          const T inv = T(1) / sumz;
+          const T inv = div_t(T(1), sumz);
           M = {M.x * inv, M.y * inv, M.z * inv};
           Gv = {Gv.x * inv, Gv.y * inv, Gv.z * inv};
           col_row_accumulate<G>(C, L, P.lslot[li], M, -1, M, Gv, P.w_world * dact, res, A, g);
@@ -302,32 +310,37 @@ __device__ __forceinline__ typename G::T col_rows(const ChainParams<typename G::
     for (int pi = 0; pi < P.np; ++pi, ++row) {
       const int la = P.pa[pi], lb = P.pb[pi];
       const int fa = P.lfirst[la], na = P.lcount[la], fb = P.lfirst[lb], nb = P.lcount[lb];
-      T dmin = inf_t<T>();
-      int kmin = 0;
-      for (int i = 0; i < na; ++i)
-        for (int j = 0; j < nb; ++j) {
-          const vec3<T> v{L.cen(fa + i, 0) - L.cen(fb + j, 0), L.cen(fa + i, 1) - L.cen(fb + j, 1),
-                          L.cen(fa + i, 2) - L.cen(fb + j, 2)};
-          const T d = sqrt_t(dot(v, v)) - P.sr[fa + i] - P.sr[fb + j];
-          if (d < dmin) {
-            dmin = d;
-            kmin = i * nb + j;
-          }
-        }
       const bool hard = P.hard || na * nb == 1;
-      T sumz = T(0);
+      T dmin = inf_t<T>(), sumz = T(0);
       vec3<T> Ma{T(0), T(0), T(0)}, Mb{T(0), T(0), T(0)}, Gv{T(0), T(0), T(0)};
       for (int i = 0; i < na; ++i)
         for (int j = 0; j < nb; ++j) {
           const vec3<T> ca{L.cen(fa + i, 0), L.cen(fa + i, 1), L.cen(fa + i, 2)};
           const vec3<T> cb{L.cen(fb + j, 0), L.cen(fb + j, 1), L.cen(fb + j, 2)};
           const vec3<T> v{ca.x - cb.x, ca.y - cb.y, ca.z - cb.z};
-          const T dist = sqrt_t(dot(v, v));
+          T dist, inv;
+          norm_inv_t(dot(v, v), dist, inv);
           const T d = dist - P.sr[fa + i] - P.sr[fb + j];
-          const T z = hard ? ((i * nb + j) == kmin ? T(1) : T(0)) : exp_t(-P.beta * (d - dmin));
+          T z;
+          if (hard) {
+            if (!(d < dmin)) continue;
+            dmin = d;
+            z = T(1);
+            sumz = T(0);
+            Ma = Mb = Gv = vec3<T>{T(0), T(0), T(0)};
+          } else {
+            if (d < dmin) {
+              const T sc = exp_t(-P.beta * (dmin - d));
+              sumz *= sc;
+              Ma = {Ma.x * sc, Ma.y * sc, Ma.z * sc};
+              Mb = {Mb.x * sc, Mb.y * sc, Mb.z * sc};
+              Gv = {Gv.x * sc, Gv.y * sc, Gv.z * sc};
+              dmin = d;
+            }
+            z = exp_t(-P.beta * (d - dmin));
+          }
           sumz += z;
           if (JAC && dist > T(1e-12)) {
-            const T inv = T(1) / dist;
             const vec3<T> n{v.x * inv, v.y * inv, v.z * inv};
             const vec3<T> xa = cross(ca, n), xb = cross(cb, n);
             Ma = {Ma.x + z * xa.x, Ma.y + z * xa.y, Ma.z + z * xa.z};
@@ -342,7 +355,7 @@ __device__ __forceinline__ typename G::T col_rows(const ChainParams<typename G::
       cost += res * res;
       if (row_out) row_out[row] = double(res);
       if (JAC && dact != T(0)) {
-        const T inv = T(1) / sumz;
+        const T inv = div_t(T(1), sumz);
         Ma = {Ma.x * inv, Ma.y * inv, Ma.z * inv};
         Mb = {Mb.x * inv, Mb.y * inv, Mb.z * inv};
         Gv = {Gv.x * inv, Gv.y * inv, Gv.z * inv};

@@ -63,6 +63,18 @@ __device__ __forceinline__ bool finite_t(float a) { return isfinite(a); }
 __device__ __forceinline__ float div_t(float a, float b) { return __fdividef(a, b); }
 __device__ __forceinline__ double div_t(double a, double b) { return a / b; }
 __device__ __forceinline__ bool finite_t(double a) { return isfinite(a); }
+// |v| and 1/|v| from dd = v.v (0 and +inf at dd = 0).  float: one MUFU.RSQ
+// (<= 2 ulp) instead of an IEEE sqrt plus an IEEE division; double: exact.
+__device__ __forceinline__ void norm_inv_t(float dd, float& n, float& inv) {
+  inv = rsqrtf(dd);
+  n = dd > 0.f ? dd * inv : 0.f;
+}
+__device__ __forceinline__ void norm_inv_t(double dd, double& n, double& inv) {
+  n = sqrt(dd);
+  inv = 1.0 / n;
+}
+__device__ __forceinline__ float norm_t(float dd) { return dd > 0.f ? dd * rsqrtf(dd) : 0.f; }
+__device__ __forceinline__ double norm_t(double dd) { return sqrt(dd); }
 
 template <typename T>
 __device__ __forceinline__ T tmax(T a, T b) { return a > b ? a : b; }
