@@ -121,3 +121,87 @@ def self_collision_cost(model, q_var: str, eta: float = 0.01, weight: float = 1.
                     weight=np.full(len(pairs), float(weight)), kind="self_collision",
                     params=dict(model=model, eta=float(eta), weight=float(weight), sharpness=float(sharpness),
                                 hard_min=bool(hard_min)))
+
+
+# ---------------------------------------------------------------------------
+# trajectory families (costs.py:198-341, 554-619); the device solves them as
+# one banded problem when they form a plan_trajectory-shaped Problem
+# ---------------------------------------------------------------------------
+
+ACCEL_COEFFS = np.array([-1.0, 16.0, -30.0, 16.0, -1.0]) / 12.0  # costs.py:295
+JERK_COEFFS = np.array([-1.0, 2.0, 0.0, -2.0, 1.0]) / 2.0  # costs.py:296
+
+
+def velocity_limit_cost(model, prev_var: str, curr_var: str, dt: float, weight: float = 1.0,
+                        name: str | None = None, analytic: bool = True) -> CostTerm:
+    """max(0, |q_t - q_{t-1}| - velocity_limit * dt); unlimited joints 0 (costs.py:198-231)."""
+    if dt <= 0.0:
+        raise ValueError(f"dt must be positive, got {dt}")
+    n = model.actuated_count
+    return CostTerm(name=name or f"velocity[{prev_var}->{curr_var}]", residual_dim=n,
+                    variable_refs=[prev_var, curr_var], weight=np.full(n, float(weight)), kind="velocity",
+                    params=dict(model=model, dt=float(dt), weight=float(weight)))
+
+
+def velocity_limit_cost_direct(model, rate_var: str, weight: float = 1.0, name: str = "velocity_direct") -> CostTerm:
+    """max(0, |qdot| - limit) over an explicit rate variable (costs.py:234-256); no device kernel."""
+    n = model.actuated_count
+    return CostTerm(name=name, residual_dim=n, variable_refs=[rate_var], weight=np.full(n, float(weight)),
+                    kind="velocity_direct", params=dict(model=model, weight=float(weight)))
+
+
+def smoothness_cost(model, prev_var: str, curr_var: str, weight: float = 1.0, name: str | None = None,
+                    analytic: bool = True) -> CostTerm:
+    """q_t - q_{t-1} (costs.py:274-290)."""
+    n = model.actuated_count
+    return CostTerm(name=name or f"smooth[{prev_var}->{curr_var}]", residual_dim=n,
+                    variable_refs=[prev_var, curr_var], weight=np.full(n, float(weight)), kind="smoothness",
+                    params=dict(model=model, weight=float(weight)))
+
+
+def _stencil_cost(model, q_vars, dt, coeffs, scale, weight, name, kind):
+    if len(q_vars) != 5:
+        raise ValueError(f"stencil costs need 5 consecutive timesteps, got {len(q_vars)}")
+    if dt <= 0.0:
+        raise ValueError(f"dt must be positive, got {dt}")
+    n = model.actuated_count
+    return CostTerm(name=name, residual_dim=n, variable_refs=list(q_vars), weight=np.full(n, float(weight)),
+                    kind=kind, params=dict(model=model, dt=float(dt), coeffs=coeffs / scale, weight=float(weight)))
+
+
+def acceleration_cost(model, q_vars, dt: float, weight: float = 1.0, name: str = "acceleration",
+                      analytic: bool = True) -> CostTerm:
+    """Five-point second difference / dt^2 over q_{t-2..t+2} (costs.py:322-330)."""
+    return _stencil_cost(model, q_vars, dt, ACCEL_COEFFS, dt * dt, weight, name, "acceleration")
+
+
+def jerk_cost(model, q_vars, dt: float, weight: float = 1.0, name: str = "jerk", analytic: bool = True) -> CostTerm:
+    """Five-point third difference / dt^3 over q_{t-2..t+2} (costs.py:333-341)."""
+    return _stencil_cost(model, q_vars, dt, JERK_COEFFS, dt ** 3, weight, name, "jerk")
+
+
+def swept_collision_cost(model, prev_var: str, curr_var: str, world, eta: float = 0.05, weight: float = 1.0,
+                         sharpness: float = SOFTMIN_SHARPNESS, hard_min: bool = False, name: str | None = None,
+                         analytic: bool = True) -> CostTerm:
+    """Capsules swept by every sphere between consecutive timesteps vs the world,
+    one row per (sphere link, obstacle) (costs.py:554-619)."""
+    links = [nm for nm in model.link_names if model.collision_spheres.get(nm)]
+    rows = len(links) * len(world.obstacles)
+    if not rows:
+        raise ValueError("no (link, obstacle) pairs: empty world or no collision spheres")
+    if eta <= 0.0:
+        raise ValueError(f"buffer distance must be positive, got {eta}")
+    return CostTerm(name=name or f"swept_collision[{prev_var}->{curr_var}]", residual_dim=rows,
+                    variable_refs=[prev_var, curr_var], weight=np.full(rows, float(weight)),
+                    kind="swept_collision", params=dict(model=model, world=world, eta=float(eta), weight=float(weight),
+                                                        sharpness=float(sharpness), hard_min=bool(hard_min)))
+
+
+def manipulability_cost(model, q_var: str, link: str, weight: float = 1.0, eps: float = MANIP_EPS,
+                        name: str | None = None, analytic: bool = True) -> CostTerm:
+    """1 / (Yoshikawa measure + eps) of the translational Jacobian (costs.py:349-401);
+    no device kernel (no configuration uses it)."""
+    model.link_index(link)
+    return CostTerm(name=name or f"manipulability[{link}]", residual_dim=1, variable_refs=[q_var],
+                    weight=np.array([float(weight)]), kind="manipulability",
+                    params=dict(model=model, link=link, eps=float(eps), weight=float(weight)))

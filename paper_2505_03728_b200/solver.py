@@ -6,8 +6,11 @@ terminations) runs here as one GPU thread per problem (csrc/kop_collision.cu,
 ``kop_lm_solve``) for problems built from the typed cost builders of
 ``costs.py``: one configuration variable and the pose / limit / rest /
 world-collision / self-collision families (the viewer's stack,
-server.py:60-97, and config 4).  ``solve_batch`` launches every compatible
-problem of a batch together.  Costs built from Python callables cannot run on
+server.py:60-97, and config 4), several pose costs on a tree (config 3,
+one warp per problem), and plan_trajectory-shaped problems over T
+configuration variables (config 5, one CTA per problem, banded normal
+equations).  ``solve_batch`` launches every compatible problem of a batch
+together.  Costs built from Python callables cannot run on
 the device and raise UnsupportedFeatureError -- there is no CPU fallback.
 """
 
@@ -201,6 +204,7 @@ class _Plan:
     key: tuple
     path: str = "chain"
     targets: list = field(default_factory=list)  # tree path: one Transform3 per pose cost
+    traj: dict = field(default_factory=dict)     # traj path: var ids, anchors, obstacle table
 
 
 def _obstacles(world):
@@ -240,8 +244,8 @@ def plan(problem: Problem) -> _Plan:
 
     if not problem.costs or problem.residual_dim < 1:
         raise ValueError("problem must declare at least one cost with residual rows")
-    if len(problem.variables.ids) != 1:
-        raise UnsupportedFeatureError("device solve supports a single configuration variable")
+    if len(problem.variables.ids) > 1:
+        return _plan_trajectory(problem)
     var = problem.variables.ids[0]
     by, poses = {}, []
     for c in problem.costs:
@@ -313,6 +317,138 @@ def plan(problem: Problem) -> _Plan:
                  key, "tree", [p.params["target"] for p in poses])
 
 
+_TRAJ_KINDS = ("rest", "limit", "smoothness", "velocity", "acceleration", "jerk", "self_collision",
+               "world_collision", "swept_collision")
+
+
+def _plan_trajectory(problem: Problem) -> _Plan:
+    """Path "traj": variables q_0..q_{T-1} (VariableSet order) under the
+    plan_trajectory cost families (tasks.py:347-403) -- anchors (rest costs on
+    q_0 / q_{T-1}), per-pair smoothness / velocity / swept collision, stencils
+    on every 5-window, per-timestep limit / rest / self / world -- each family
+    present everywhere it applies with one weight, or absent.  Solved by
+    kop_traj_solve (CTA per trajectory, banded normal equations)."""
+    from . import _lib as L
+    from .trajectory import MAX_OBSTACLES, MAX_STEPS, _obstacle_table
+
+    ids = problem.variables.ids
+    T = len(ids)
+    pos = {v: i for i, v in enumerate(ids)}
+    model = None
+    fam = {k: [] for k in _TRAJ_KINDS}
+    for c in problem.costs:
+        if c.kind not in _TRAJ_KINDS:
+            raise UnsupportedFeatureError(
+                f"cost '{c.name}' ({c.kind}) is not a trajectory family the device solve supports")
+        m = c.params.get("model")
+        if m is not None:
+            if model is not None and m is not model:
+                raise UnsupportedFeatureError("all costs of a device problem must use the same RobotModel")
+            model = model or m
+        fam[c.kind].append(c)
+    if model is None:
+        raise UnsupportedFeatureError("trajectory problem needs at least one model-bound cost")
+    n = model.actuated_count
+    for v in ids:
+        val = problem.variables.value(v)
+        if not isinstance(val, np.ndarray) or val.size != n:
+            raise UnsupportedFeatureError(f"variable '{v}' is not a configuration of {n} values")
+    if not 5 <= T <= MAX_STEPS:
+        raise UnsupportedFeatureError(f"trajectory device solve needs 5..{MAX_STEPS} timesteps, got {T}")
+
+    def steps(c):
+        return [pos[r] for r in c.variable_refs]
+
+    def uniform_family(kind, expect, what):
+        """One cost per expected variable tuple, all with one weight (and params); returns the weight or 0."""
+        cs = fam[kind]
+        if not cs:
+            return 0.0, None
+        got = sorted(tuple(steps(c)) for c in cs)
+        if got != sorted(expect):
+            raise UnsupportedFeatureError(f"'{kind}' costs must cover {what}")
+        w = {_uniform(c.weight, c.name) for c in cs}
+        if len(w) != 1:
+            raise UnsupportedFeatureError(f"'{kind}' costs must share one weight")
+        return w.pop(), cs[0]
+
+    pairs = [(t - 1, t) for t in range(1, T)]
+    w_smooth, _ = uniform_family("smoothness", pairs, "every consecutive pair")
+    w_vel, vc = uniform_family("velocity", pairs, "every consecutive pair")
+    win = [tuple(range(t - 2, t + 3)) for t in range(2, T - 2)]
+    w_acc, ac = uniform_family("acceleration", win, "every 5-window t-2..t+2, t = 2..T-3")
+    w_jerk, jc = uniform_family("jerk", win, "every 5-window t-2..t+2, t = 2..T-3")
+    each = [(t,) for t in range(T)]
+    w_lim, _ = uniform_family("limit", each, "every timestep")
+    w_self, sc = uniform_family("self_collision", each, "every timestep")
+    w_world, wc = uniform_family("world_collision", each, "every timestep")
+    w_swept, swc = uniform_family("swept_collision", pairs, "every consecutive pair")
+    dts = {c.params["dt"] for c in fam["velocity"] + fam["acceleration"] + fam["jerk"]}
+    if len(dts) > 1:
+        raise UnsupportedFeatureError("velocity / stencil costs must share one dt")
+    dt = dts.pop() if dts else 0.1
+    if w_world or w_swept:
+        if not (wc and swc) or w_world != w_swept:
+            raise UnsupportedFeatureError("world and swept collision costs must both be present with one weight")
+        worlds = {id(c.params["world"]) for c in fam["world_collision"] + fam["swept_collision"]}
+        keyset = {(c.params["eta"], c.params["sharpness"], c.params["hard_min"])
+                  for c in fam["world_collision"] + fam["swept_collision"]}
+        if len(worlds) != 1 or len(keyset) != 1:
+            raise UnsupportedFeatureError("world / swept collision costs must share one world, eta and softmin")
+    if sc is not None and wc is not None and (sc.params["sharpness"], sc.params["hard_min"]) != (
+            wc.params["sharpness"], wc.params["hard_min"]):
+        raise UnsupportedFeatureError("world and self collision costs must share sharpness / hard_min")
+    # rest costs: anchors on q_0 / q_{T-1}, optionally one rest family on every timestep
+    rests = {t: [c for c in fam["rest"] if steps(c) == [t]] for t in range(T)}
+    if any(len(c.variable_refs) != 1 for c in fam["rest"]):
+        raise UnsupportedFeatureError("rest costs must bind one variable")
+    inner = [rests[t] for t in range(1, T - 1)]
+    w_rest, rest = 0.0, model.rest_pose
+    if any(inner):
+        if any(len(r) != 1 for r in inner):
+            raise UnsupportedFeatureError("rest costs must be on every timestep or only on the endpoints")
+        w_rest = _uniform(inner[0][0].weight, inner[0][0].name)
+        rest = inner[0][0].params["q_rest"]
+        for r in inner:
+            if _uniform(r[0].weight, r[0].name) != w_rest or not np.array_equal(r[0].params["q_rest"], rest):
+                raise UnsupportedFeatureError("per-timestep rest costs must share weight and rest pose")
+    anchors = []
+    for t in (0, T - 1):
+        cand = list(rests[t])
+        if w_rest:
+            fam_c = [c for c in cand if _uniform(c.weight, c.name) == w_rest and np.array_equal(c.params["q_rest"], rest)]
+            if not fam_c:
+                raise UnsupportedFeatureError("the per-timestep rest cost is missing on an endpoint")
+            cand.remove(fam_c[0])
+        if len(cand) != 1:
+            raise UnsupportedFeatureError("each endpoint needs exactly one anchor (rest) cost")
+        anchors.append(cand[0])
+    w_anchor = {_uniform(c.weight, c.name) for c in anchors}
+    if len(w_anchor) != 1:
+        raise UnsupportedFeatureError("the two anchor costs must share one weight")
+    w_anchor = w_anchor.pop()
+    vlim = np.ascontiguousarray(model.velocity_limits, dtype=float)
+    rest = np.ascontiguousarray(rest, dtype=float)
+    cp = (wc or sc).params if (wc or sc) else {"eta": 0.05, "sharpness": SOFTMIN_DEFAULT, "hard_min": False}
+    tc = L.KopTrajCosts(T, dt, w_anchor, w_smooth, w_vel, w_acc, w_jerk, w_lim, w_rest, w_self,
+                        sc.params["eta"] if sc is not None else 0.01, w_world,
+                        wc.params["eta"] if wc is not None else 0.05, cp["sharpness"], int(cp["hard_min"]),
+                        vlim.ctypes.data_as(C.POINTER(C.c_double)), rest.ctypes.data_as(C.POINTER(C.c_double)))
+    world = wc.params["world"] if wc is not None else None
+    if world is not None and len(world.obstacles) > MAX_OBSTACLES:
+        raise UnsupportedFeatureError(f"more than {MAX_OBSTACLES} obstacles are not compiled in")
+    table, n_obs = _obstacle_table([world] if world is not None else [], 1)
+    link = model.link_names[-1]
+    key = ("traj", id(model), T, dt, w_anchor, w_smooth, w_vel, w_acc, w_jerk, w_lim, w_rest, rest.tobytes(),
+           w_self, w_world, n_obs, tc.eta_self, tc.eta_world, tc.sharpness, tc.hard_min)
+    traj = {"vars": ids, "anchors": np.stack([anchors[0].params["q_rest"], anchors[1].params["q_rest"]]),
+            "obstacles": table[0] if n_obs else None, "n_obs": n_obs}
+    return _Plan(model, link, ids[0], Transform3.identity(), tc, [vlim, rest], key, "traj", traj=traj)
+
+
+SOFTMIN_DEFAULT = 100.0
+
+
 def _options(options: SolveOptions):
     from . import _lib as L
     from .robot import _precision
@@ -332,6 +468,8 @@ def _run(plans, problems, options: SolveOptions) -> list:
 
     p0 = plans[0]
     b = len(plans)
+    if p0.path == "traj":
+        return _run_traj(plans, problems, options)
     if p0.path == "tree":
         tg = dv.to_dev(np.stack([np.stack([t.as_array() for t in p.targets]) for p in plans]))
     else:
@@ -363,6 +501,45 @@ def _run(plans, problems, options: SolveOptions) -> list:
         out.append(SolveReport(final_values=VariableSet.of(**{p.var: qh[i]}), initial_cost=float(ih[i]),
                                final_cost=float(ch[i]), iterations_run=int(ith[i]), termination=termination,
                                cost_history=[float(x) for x in h], solve_time_s=dt, message=message))
+    return out
+
+
+def _run_traj(plans, problems, options: SolveOptions) -> list:
+    """One kop_traj_solve launch for trajectory problems sharing a plan key."""
+    from . import _device as dv
+    from ._lib import check, lib
+
+    p0 = plans[0]
+    t = dv.require_cuda()
+    b, T, n = len(plans), p0.costs.timesteps, p0.model.actuated_count
+    qi = dv.to_dev(np.stack([np.stack([pr.variables.value(v) for v in p.traj["vars"]])
+                             for p, pr in zip(plans, problems)]))
+    anchors = dv.to_dev(np.stack([p.traj["anchors"] for p in plans]))
+    n_obs = p0.traj["n_obs"]
+    obs = dv.to_dev(np.stack([p.traj["obstacles"] for p in plans])) if n_obs else None
+    q, cost, init = dv.empty((b, T, n)), dv.empty(b), dv.empty(b)
+    hist = dv.empty((b, options.max_iterations + 1))
+    iters = t.empty(b, dtype=t.int32, device="cuda")
+    term = t.empty(b, dtype=t.int32, device="cuda")
+    opts = _options(options)
+    t0 = time.perf_counter()
+    check(lib().kop_traj_solve(p0.model._handle, p0.model.link_index(p0.link), C.byref(p0.costs), C.byref(opts),
+                               dv.ptr(qi), dv.ptr(anchors), dv.ptr(obs), n_obs, b, dv.ptr(q), dv.ptr(cost),
+                               dv.ptr(init), dv.ptr(hist), dv.ptr(iters), dv.ptr(term), dv.stream_handle()),
+          "kop_traj_solve")
+    qh, ch, ih, hh = q.cpu().numpy(), cost.cpu().numpy(), init.cpu().numpy(), hist.cpu().numpy()
+    ith, th = iters.cpu().numpy(), term.cpu().numpy()
+    dt = (time.perf_counter() - t0) / b
+    out = []
+    for i, p in enumerate(plans):
+        termination, message = TERMINATIONS[int(th[i])]
+        values = VariableSet()
+        for k, v in enumerate(p.traj["vars"]):
+            values.add(v, qh[i, k])
+        out.append(SolveReport(final_values=values, initial_cost=float(ih[i]), final_cost=float(ch[i]),
+                               iterations_run=int(ith[i]), termination=termination,
+                               cost_history=[float(x) for x in hh[i, : int(ith[i]) + 1]], solve_time_s=dt,
+                               message=message))
     return out
 
 

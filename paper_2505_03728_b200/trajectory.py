@@ -144,6 +144,56 @@ def trajectory_signed_distances(model: RobotModel, qs: np.ndarray, world: WorldM
     return out["static"][0].cpu().numpy(), out["swept"][0].cpu().numpy()
 
 
+def trajectory_problem(model: RobotModel, q_start, q_goal, timesteps: int = 20, dt: float = 0.1,
+                       world: WorldModel | None = None, weights: ck.CostWeights | None = None,
+                       eta_world: float = 0.05, eta_self: float = 0.01, anchor_weight: float = ANCHOR_WEIGHT,
+                       init=None):
+    """The Problem plan_trajectory builds (tasks.py:341-403): variables q0..q{T-1}
+    from the straight line (or ``init``), anchors, smoothness / velocity /
+    stencil / limit / rest / self / world / swept costs.  ``solver.solve`` runs
+    it on the device (trajectory path)."""
+    from .solver import Problem
+
+    w = weights or ck.CostWeights(rest=0.0, world_collision=30.0)
+    world = world or WorldModel()
+    q_start, q_goal = np.asarray(q_start, float), np.asarray(q_goal, float)
+    alphas = np.linspace(0.0, 1.0, timesteps)
+    init = (q_start[None, :] * (1 - alphas[:, None]) + q_goal[None, :] * alphas[:, None]) if init is None \
+        else np.asarray(init, float)
+    variables = VariableSet()
+    names = [f"q{t}" for t in range(timesteps)]
+    for t in range(timesteps):
+        variables.add(names[t], init[t])
+    costs = [ck.rest_cost(names[0], q_start, weight=anchor_weight, name="anchor_start"),
+             ck.rest_cost(names[-1], q_goal, weight=anchor_weight, name="anchor_goal")]
+    for t in range(1, timesteps):
+        costs.append(ck.smoothness_cost(model, names[t - 1], names[t], weight=w.smoothness))
+        if w.velocity > 0:
+            costs.append(ck.velocity_limit_cost(model, names[t - 1], names[t], dt, weight=w.velocity))
+    for t in range(2, timesteps - 2):
+        window = names[t - 2:t + 3]
+        if w.acceleration > 0:
+            costs.append(ck.acceleration_cost(model, window, dt, weight=w.acceleration, name=f"accel{t}"))
+        if w.jerk > 0:
+            costs.append(ck.jerk_cost(model, window, dt, weight=w.jerk, name=f"jerk{t}"))
+    for t in range(timesteps):
+        if w.limit > 0:
+            costs.append(ck.limit_cost(model, names[t], weight=w.limit, name=f"limit{t}"))
+        if w.rest > 0:
+            costs.append(ck.rest_cost(names[t], model.rest_pose, weight=w.rest, name=f"rest{t}"))
+        if w.self_collision > 0 and model.self_collision_pairs:
+            costs.append(ck.self_collision_cost(model, names[t], eta=eta_self, weight=w.self_collision,
+                                                name=f"self{t}"))
+        if w.world_collision > 0 and world.obstacles:
+            costs.append(ck.world_collision_cost(model, names[t], world, eta=eta_world, weight=w.world_collision,
+                                                 name=f"world{t}"))
+    if w.world_collision > 0 and world.obstacles:
+        for t in range(1, timesteps):
+            costs.append(ck.swept_collision_cost(model, names[t - 1], names[t], world, eta=eta_world,
+                                                 weight=w.world_collision, name=f"swept{t}"))
+    return Problem(variables, costs)
+
+
 class TrajectoryPlanner:
     """Batched plan_trajectory for one (robot, target link, T, dt, weights, options)."""
 

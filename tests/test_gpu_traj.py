@@ -235,3 +235,26 @@ def test_plan_trajectory_errors(arm7):
     near = k.link_transform(arm7, arm7.rest_pose, "flange")
     with pytest.raises(k.PlanningError, match="start"):
         k.plan_trajectory(k.TrajRequest(model=arm7, start_pose=far, goal_pose=near, ik_retries=1))
+
+
+def test_generic_solve_runs_trajectory_problems(arm7, golden_traj):
+    """solver.solve / solve_batch on the Problem plan_trajectory builds (the
+    trajectory path of the generic solve) == the planner's launch."""
+    g, T, obs, n_obs = _case(golden_traj, "scene1")
+    world = k.WorldModel([k.Sphere(r[1:4], r[7]) for r in obs])
+    pr = k.trajectory_problem(arm7, g("q_start"), g("q_goal"), T, 0.1, world)
+    rep = k.solve(pr, k.SolveOptions(max_iterations=150))
+    ref, _, _ = _solve(arm7, golden_traj, ["scene1"])
+    qs = np.stack([rep.final_values.value(f"q{t}") for t in range(T)])
+    np.testing.assert_array_equal(qs, ref["qs"][0])
+    assert rep.iterations_run == int(ref["iterations"][0])
+    hist = np.array(rep.cost_history)
+    h_ref = g("hist")[~np.isnan(g("hist"))]
+    m = min(len(hist), len(h_ref))
+    np.testing.assert_allclose(hist[:m], h_ref[:m], rtol=1e-8)
+    g0, T0, obs0, _ = _case(golden_traj, "scene0")
+    pr0 = k.trajectory_problem(arm7, g0("q_start"), g0("q_goal"), T0, 0.1,
+                               k.WorldModel([k.Sphere(r[1:4], r[7]) for r in obs0]))
+    reps = k.solve_batch([pr0, pr], k.SolveOptions(max_iterations=150))
+    np.testing.assert_array_equal(np.stack([reps[1].final_values.value(f"q{t}") for t in range(T)]), qs)
+    np.testing.assert_allclose(reps[0].final_cost, float(g0("cost")), rtol=1e-8)
