@@ -1107,7 +1107,38 @@ TreeLmParams<T> tree_params(const KopModel& m, const KopPoseCosts* pc) {
   }
   P.w_lim = T(pc->w_limit);
   P.w_rest = T(pc->w_rest);
+  // depth levels (joint order is topological: parents come first, robot.py:325-340)
+  std::vector<int> depth(t.nj, 0);
+  int maxd = 0;
+  for (int j = 0; j < t.nj; ++j) {
+    const int pj = P.parent_joint[j];
+    depth[j] = pj >= 0 ? depth[pj] + 1 : 0;
+    if (depth[j] > maxd) maxd = depth[j];
+  }
+  P.nlev = t.nj ? maxd + 1 : 0;
+  int at = 0;
+  for (int d = 0; d < P.nlev; ++d) {
+    P.lev_start[d] = at;
+    for (int j = 0; j < t.nj; ++j)
+      if (depth[j] == d) P.lev_joint[at++] = (int8_t)j;
+  }
+  P.lev_start[P.nlev] = at;
+  for (int j = 0; j < t.nj; ++j) {
+    if (t.kind[j] == 0 || t.qcol[j] < 0) continue;
+    const int c = t.qcol[j];
+    P.col_joint[c][P.col_nj[c]++] = (int8_t)j;  // bounded by tree_params_ok
+  }
   return P;
+}
+
+// shape limits of the tree kernel beyond the joint / dof counts
+bool tree_params_ok(const KopModel& m) {
+  int per[kTreeMaxDofs] = {0};
+  for (int j = 0; j < m.tree.nj; ++j) {
+    if (m.tree.kind[j] == 0 || m.tree.qcol[j] < 0) continue;
+    if (++per[m.tree.qcol[j]] > kTreeMaxPerCol) return false;
+  }
+  return true;
 }
 
 }  // namespace
@@ -1119,7 +1150,7 @@ int kop_multi_pose_solve(const KopModel* m, const KopPoseCosts* pc, const KopLmO
                          double* history_out, int32_t* iterations_out, int32_t* termination_out, void* stream) {
   if (!m || !pc || !o) return fail(KOP_EINVAL, "null argument");
   if (o->precision != KOP_FP32 && o->precision != KOP_FP64) return fail(KOP_EINVAL, "bad precision");
-  if (m->tree.n > kTreeMaxDofs || m->tree.nj > kTreeMaxJoints)
+  if (m->tree.n > kTreeMaxDofs || m->tree.nj > kTreeMaxJoints || !tree_params_ok(*m))
     return fail(KOP_EUNSUPPORTED, "tree solve supports up to 32 actuated and 64 total joints");
   if (pc->num_poses < 1 || pc->num_poses > kTreeMaxPoses)
     return fail(KOP_EUNSUPPORTED, "tree solve supports 1..8 pose costs");

@@ -6,17 +6,18 @@
 //
 // Warp mapping (a problem is too large for one thread's registers -- a 24x29
 // Jacobian, a 29x29 normal matrix):
-//   * FK:  lane l computes the world frame of tree joints l and l+32 by
-//         walking UP the tree (T = O_a Mot_a T for each ancestor a -- no
-//         stack), leaving its Pluecker axis (a, m = a x o) in shared memory;
-//         lanes e < E compute the end-effector frames the same way, then the
-//         pose residual xi_e and the weighted Jr^-1(xi_e) blocks.
+//   * FK:  level-synchronous over the tree depth: the lanes take the joints of
+//         one level, compose after(parent) * O_j * Mot_j from shared memory and
+//         leave the Pluecker axis (a, m = a x o) of each moving joint; lanes
+//         e < E read the end-effector frames, then form the pose residual
+//         xi_e and the weighted Jr^-1(xi_e) blocks.
 //   * J:   lane c owns Jacobian column c (its joint(s) via qcol), 6E entries
 //         in registers, mirrored to shared memory.
 //   * A:   lane i forms row i of J^T J from its own column and broadcast reads.
-//   * LM:  right-looking Cholesky of A + lam D in shared memory (row stride 33,
-//         conflict-free), triangular solves as warp-wide axpys, the rejection
-//         loop and terminations of solver.solve, warp-uniform control flow.
+//   * LM:  right-looking Cholesky of A + lam D with lane i holding row i of L
+//         in registers (pivot columns travel by shuffles), triangular solves
+//         as warp-wide axpys, the rejection loop and terminations of
+//         solver.solve, warp-uniform control flow.
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -25,15 +26,22 @@
 
 namespace kop {
 
-template <typename T>
-struct TreeScratch {  // per-warp shared memory
-  T q[32], qn[32], d[32];
+// Per-warp shared memory for NE end-effector slots (ne <= NE; the unused
+// slots are zero).  The FK frames and the Jacobian mirror live only inside an
+// evaluation, L only inside a solve, so they share storage.
+template <typename T, int NE>
+struct TreeScratch {
+  T q[32], qn[32];
   T am[kTreeMaxJoints][6];   // Pluecker axis of each moving tree joint
-  T ee[kTreeMaxPoses][48];   // per EE: r[6], R^T[9], p[3], At[9], Bt[9], Ab[9]
-  T J[6 * kTreeMaxPoses][32];
+  T ee[NE][48];              // per EE: r[6], R^T[9], p[3], At[9], Bt[9], Ab[9]
   T A[32 * 33];
-  T L[32 * 33];
-  T red[32];
+  union {
+    struct {
+      T wf[kTreeMaxJoints][7];  // world frame after each joint's motion (wxyz, xyz)
+      T J[6 * NE][32];
+    };
+    T L[32 * 33];
+  };
 };
 
 __device__ __forceinline__ float shfl_t(float v, int src) { return __shfl_sync(0xffffffffu, v, src); }
@@ -52,69 +60,58 @@ __device__ __forceinline__ T warp_max(T v) {
   return v;
 }
 
-// world frame AFTER the motion of tree joint j (identity for j < 0), walking up
-template <typename T>
-__device__ __forceinline__ void frame_after(const TreeLmParams<T>& P, const T* q, int j, quat<T>& wq, vec3<T>& wp) {
-  wq = {T(1), T(0), T(0), T(0)};
-  wp = {T(0), T(0), T(0)};
-  for (int a = j; a >= 0; a = P.parent_joint[a]) {
-    // M = O_a * Mot_a ; (wq, wp) <- M * (wq, wp)
-    quat<T> mq{T(P.oq[a][0]), T(P.oq[a][1]), T(P.oq[a][2]), T(P.oq[a][3])};
-    vec3<T> mp{P.op[a][0], P.op[a][1], P.op[a][2]};
-    if (P.kind[a] != 0) {
-      const T th = q[P.qcol[a]] * P.mult[a] + P.offset[a];
-      const vec3<T> ax{P.axis[a][0], P.axis[a][1], P.axis[a][2]};
-      if (P.kind[a] == 1) {
-        T s, c;
-        sincos_t(T(0.5) * th, &s, &c);
-        // Mot * (wq, wp): rotate by (c, s ax)
-        const quat<T> r{c, s * ax.x, s * ax.y, s * ax.z};
-        wp = qrot(r, wp);
-        wq = qmul(r, wq);
-      } else {
-        wp = {wp.x + th * ax.x, wp.y + th * ax.y, wp.z + th * ax.z};
-      }
-    }
-    const vec3<T> t = qrot(mq, wp);
-    wp = {t.x + mp.x, t.y + mp.y, t.z + mp.z};
-    wq = qmul(mq, wq);
-  }
-}
-
-// world frame BEFORE the motion of joint j (its joint frame): parent-after * O_j
-template <typename T>
-__device__ __forceinline__ void frame_before(const TreeLmParams<T>& P, const T* q, int j, quat<T>& wq, vec3<T>& wp) {
-  frame_after(P, q, P.parent_joint[j], wq, wp);
-  const vec3<T> t = qrot(wq, vec3<T>{P.op[j][0], P.op[j][1], P.op[j][2]});
-  wp = {wp.x + t.x, wp.y + t.y, wp.z + t.z};
-  wq = qmul(wq, quat<T>{T(P.oq[j][0]), T(P.oq[j][1]), T(P.oq[j][2]), T(P.oq[j][3])});
-}
-
 // Evaluate the stack at S.q (or S.qn when cand): returns the cost (all lanes);
 // JAC also forms A (S.A, stride 33) and g (register, lane i = g_i).
-template <typename T, bool JAC>
+template <typename T, int NE, bool JAC>
 __device__ __forceinline__ T tree_eval(const TreeLmParams<T>& P, const double* __restrict__ targets,
-                                       TreeScratch<T>& S, const T* q, int lane, T& g_out) {
+                                       TreeScratch<T, NE>& S, const T* q, int lane, T& g_out) {
   const int n = P.n, ne = P.ne;
-  // ---- FK: Pluecker axes of the moving joints --------------------------------
-  if (JAC) {
-    for (int j = lane; j < P.nj; j += 32) {
-      if (P.kind[j] == 0) continue;
-      quat<T> wq;
-      vec3<T> wp;
-      frame_before(P, q, j, wq, wp);
-      const vec3<T> a = qrot(wq, vec3<T>{P.axis[j][0], P.axis[j][1], P.axis[j][2]});
-      const vec3<T> m = cross(a, wp);
-      S.am[j][0] = a.x; S.am[j][1] = a.y; S.am[j][2] = a.z;
-      S.am[j][3] = m.x; S.am[j][4] = m.y; S.am[j][5] = m.z;
+  // ---- FK, level by level: world frame after every joint, Pluecker axes -------
+  // after(j) = after(parent) * O_j * Mot_j (robot.py:404-448 composition)
+  for (int d = 0; d < P.nlev; ++d) {
+    for (int idx = P.lev_start[d] + lane; idx < P.lev_start[d + 1]; idx += 32) {
+      const int j = P.lev_joint[idx], pj = P.parent_joint[j];
+      quat<T> wq{T(1), T(0), T(0), T(0)};
+      vec3<T> wp{T(0), T(0), T(0)};
+      if (pj >= 0) {
+        wq = {S.wf[pj][0], S.wf[pj][1], S.wf[pj][2], S.wf[pj][3]};
+        wp = {S.wf[pj][4], S.wf[pj][5], S.wf[pj][6]};
+      }
+      const vec3<T> t = qrot(wq, vec3<T>{P.op[j][0], P.op[j][1], P.op[j][2]});
+      wp = {wp.x + t.x, wp.y + t.y, wp.z + t.z};
+      wq = qmul(wq, quat<T>{P.oq[j][0], P.oq[j][1], P.oq[j][2], P.oq[j][3]});
+      if (P.kind[j] != 0) {
+        const vec3<T> ax{P.axis[j][0], P.axis[j][1], P.axis[j][2]};
+        const vec3<T> a = qrot(wq, ax);
+        if (JAC) {
+          const vec3<T> m = cross(a, wp);
+          S.am[j][0] = a.x; S.am[j][1] = a.y; S.am[j][2] = a.z;
+          S.am[j][3] = m.x; S.am[j][4] = m.y; S.am[j][5] = m.z;
+        }
+        const T th = q[P.qcol[j]] * P.mult[j] + P.offset[j];
+        if (P.kind[j] == 1) {
+          T sn, cs;
+          sincos_t(T(0.5) * th, &sn, &cs);
+          wq = qmul(wq, quat<T>{cs, sn * ax.x, sn * ax.y, sn * ax.z});
+        } else {
+          wp = {wp.x + th * a.x, wp.y + th * a.y, wp.z + th * a.z};
+        }
+      }
+      S.wf[j][0] = wq.w; S.wf[j][1] = wq.x; S.wf[j][2] = wq.y; S.wf[j][3] = wq.z;
+      S.wf[j][4] = wp.x; S.wf[j][5] = wp.y; S.wf[j][6] = wp.z;
     }
+    __syncwarp();
   }
   // ---- EE frames, pose residuals, Jr^-1 blocks ----------------------------------
   T cost_part = T(0);
   if (lane < ne) {
-    quat<T> wq;
-    vec3<T> wp;
-    frame_after(P, q, P.ee_joint[lane], wq, wp);
+    quat<T> wq{T(1), T(0), T(0), T(0)};
+    vec3<T> wp{T(0), T(0), T(0)};
+    const int ej = P.ee_joint[lane];
+    if (ej >= 0) {
+      wq = {S.wf[ej][0], S.wf[ej][1], S.wf[ej][2], S.wf[ej][3]};
+      wp = {S.wf[ej][4], S.wf[ej][5], S.wf[ej][6]};
+    }
     const double* tp = targets + 7 * lane;
     const TargetInv<T> tg = target_inverse_t<T>(tp);
     const quat<T> e_q = qmul(tg.q, wq);
@@ -152,17 +149,17 @@ __device__ __forceinline__ T tree_eval(const TreeLmParams<T>& P, const double* _
   if (!JAC) return cost;
   __syncwarp();
   // ---- Jacobian column `lane` -----------------------------------------------------
-  T col[6 * kTreeMaxPoses];
+  T col[6 * NE];
 #pragma unroll
-  for (int m = 0; m < 6 * kTreeMaxPoses; ++m) col[m] = T(0);
+  for (int m = 0; m < 6 * NE; ++m) col[m] = T(0);
   if (lane < n) {
-    for (int j = 0; j < P.nj; ++j) {
-      if (P.kind[j] == 0 || P.qcol[j] != lane) continue;
+    for (int cj = 0; cj < P.col_nj[lane]; ++cj) {
+      const int j = P.col_joint[lane][cj];
       const vec3<T> a{S.am[j][0], S.am[j][1], S.am[j][2]};
       const vec3<T> mm{S.am[j][3], S.am[j][4], S.am[j][5]};
       const T mu = P.mult[j];
 #pragma unroll
-      for (int e = 0; e < kTreeMaxPoses; ++e) {
+      for (int e = 0; e < NE; ++e) {
         if (e >= ne || !((P.anc_ee[e] >> j) & 1ull)) continue;
         const T* E = S.ee[e];
         vec3<T> lw, aw;
@@ -190,7 +187,7 @@ __device__ __forceinline__ T tree_eval(const TreeLmParams<T>& P, const double* _
     }
   }
 #pragma unroll
-  for (int m = 0; m < 6 * kTreeMaxPoses; ++m) S.J[m][lane] = col[m];
+  for (int m = 0; m < 6 * NE; ++m) S.J[m][lane] = col[m];
   __syncwarp();
   // ---- normal equations: lane i forms row i ----------------------------------------
   T g = T(0);
@@ -198,14 +195,12 @@ __device__ __forceinline__ T tree_eval(const TreeLmParams<T>& P, const double* _
     for (int j = 0; j < n; ++j) {
       T a = T(0);
 #pragma unroll
-      for (int m = 0; m < 6 * kTreeMaxPoses; ++m)
-        if (m < 6 * ne) a += col[m] * S.J[m][j];
+      for (int m = 0; m < 6 * NE; ++m) a += col[m] * S.J[m][j];  // unused slots are zero
       S.A[j * 33 + lane] = a;
     }
     S.A[lane * 33 + lane] += gl * gl + P.w_rest * P.w_rest;
 #pragma unroll
-    for (int m = 0; m < 6 * kTreeMaxPoses; ++m)
-      if (m < 6 * ne) g += col[m] * S.ee[m / 6][m % 6];
+    for (int m = 0; m < 6 * NE; ++m) g += col[m] * S.ee[m / 6][m % 6];
     g += gl * rl + P.w_rest * rr;
   }
   g_out = g;
@@ -214,40 +209,54 @@ __device__ __forceinline__ T tree_eval(const TreeLmParams<T>& P, const double* _
 }
 
 // delta (lane i -> d_i) = -(A + lam diag(max(diag A, 1e-8)))^-1 g; false if a pivot fails
-template <typename T>
-__device__ __forceinline__ bool tree_damped_solve(const TreeLmParams<T>& P, TreeScratch<T>& S, T g, T lam,
+template <typename T, int NE>
+__device__ __forceinline__ bool tree_damped_solve(const TreeLmParams<T>& P, TreeScratch<T, NE>& S, T g, T lam,
                                                   int lane, T& delta) {
+  // right-looking Cholesky with lane i holding row i of L in registers; the
+  // pivot column travels by shuffles (no shared-memory round trips)
   const int n = P.n;
-  if (lane < n)
-    for (int j = 0; j < n; ++j) S.L[j * 33 + lane] = S.A[j * 33 + lane];
-  __syncwarp();
-  if (lane < n) {
-    const T dd = S.A[lane * 33 + lane];
-    S.L[lane * 33 + lane] = dd + lam * tmax(dd, T(BeamConsts::diag_clamp));
+  T row[kTreeMaxDofs];
+#pragma unroll
+  for (int j = 0; j < kTreeMaxDofs; ++j) {
+    row[j] = (lane < n && j < n) ? S.A[j * 33 + lane] : T(0);
+    if (j == lane) row[j] += lam * tmax(row[j], T(BeamConsts::diag_clamp));
   }
-  __syncwarp();
   bool ok = true;
   T dinv_mine = T(0);
-  for (int k = 0; k < n; ++k) {
-    const T dk = S.L[k * 33 + k];
-    ok = ok && (dk > T(0)) && finite_t(dk);
-    const T inv = rsqrt_t(dk);
-    if (lane == k) dinv_mine = inv;
-    __syncwarp();
-    if (lane > k && lane < n) S.L[k * 33 + lane] *= inv;  // L[lane][k]
-    __syncwarp();
-    if (lane > k && lane < n) {
-      const T lik = S.L[k * 33 + lane];
-      for (int j = k + 1; j <= lane; ++j) S.L[j * 33 + lane] -= lik * S.L[k * 33 + j];
+#pragma unroll
+  for (int k = 0; k < kTreeMaxDofs; ++k) {
+    if (k < n) {  // warp-uniform
+      const T dk = shfl_t(row[k], k);
+      ok = ok && (dk > T(0)) && finite_t(dk);
+      const T inv = rsqrt_t(dk);
+      if (lane == k) {
+        row[k] = dk * inv;
+        dinv_mine = inv;
+      } else if (lane > k) {
+        row[k] *= inv;
+      }
+#pragma unroll
+      for (int j = k + 1; j < kTreeMaxDofs; ++j) {  // rows / lanes >= n are zero: no j < n test
+        const T ljk = shfl_t(row[k], j);
+        if (lane >= j) row[j] -= row[k] * ljk;
+      }
     }
-    __syncwarp();
   }
-  // forward: y = L^-1 (-g)
+  if (lane < n) {  // L(lane, j) for the backward sweep
+#pragma unroll
+    for (int j = 0; j < kTreeMaxDofs; ++j)
+      if (j <= lane && j < n) S.L[j * 33 + lane] = row[j];
+  }
+  __syncwarp();
+  // forward: y = L^-1 (-g), L(lane, k) from the registers
   T y = -g;
-  for (int k = 0; k < n; ++k) {
-    T yk = shfl_t(y * dinv_mine, k);
-    if (lane == k) y = yk;
-    if (lane > k && lane < n) y -= S.L[k * 33 + lane] * yk;
+#pragma unroll
+  for (int k = 0; k < kTreeMaxDofs; ++k) {
+    if (k < n) {
+      const T yk = shfl_t(y * dinv_mine, k);
+      if (lane == k) y = yk;
+      if (lane > k && lane < n) y -= row[k] * yk;
+    }
   }
   // backward: x = L^-T y
   T x = y;
@@ -260,7 +269,7 @@ __device__ __forceinline__ bool tree_damped_solve(const TreeLmParams<T>& P, Tree
   return ok;
 }
 
-template <typename T>
+template <typename T, int NE>
 __global__ void __launch_bounds__(128)
 k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const double* __restrict__ q0, int64_t B,
              const LmOptions O, double* __restrict__ q_out, double* __restrict__ cost_out,
@@ -270,13 +279,14 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
   if (b >= B) return;  // whole warp exits together
-  TreeScratch<T>& S = reinterpret_cast<TreeScratch<T>*>(smem_raw)[wib];
+  TreeScratch<T, NE>& S = reinterpret_cast<TreeScratch<T, NE>*>(smem_raw)[wib];
   const int n = P.n;
+  for (int i = lane; i < NE * 48; i += 32) (&S.ee[0][0])[i] = T(0);  // unused slots stay zero
   const double* tg = targets + b * 7 * P.ne;
   S.q[lane] = lane < n ? T(q0[b * n + lane]) : T(0);
   __syncwarp();
   T g;
-  T cost = tree_eval<T, true>(P, tg, S, S.q, lane, g);
+  T cost = tree_eval<T, NE, true>(P, tg, S, S.q, lane, g);
   const int hstride = O.max_iterations + 1;
   if (lane == 0) {
     if (hist_out) hist_out[b * hstride] = double(cost);
@@ -300,7 +310,7 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
         S.qn[lane] = S.q[lane] + d;
         __syncwarp();
         T gd;
-        const T cn = tree_eval<T, false>(P, tg, S, S.qn, lane, gd);
+        const T cn = tree_eval<T, NE, false>(P, tg, S, S.qn, lane, gd);
         if (!finite_t(cn)) {
           term = 5;
           break;
@@ -329,7 +339,7 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
       term = 2;
       break;
     }
-    tree_eval<T, true>(P, tg, S, S.q, lane, g);
+    tree_eval<T, NE, true>(P, tg, S, S.q, lane, g);
   }
   if (hist_out)
     for (int i = iters + 1 + lane; i < hstride; i += 32) hist_out[b * hstride + i] = NAN;
@@ -341,16 +351,24 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
   }
 }
 
+template <typename T, int NE>
+cudaError_t launch_tree_ne(const TreeLmParams<T>& P, const TreeLaunch& L, cudaStream_t st) {
+  const int warps = 4;
+  const size_t smem = sizeof(TreeScratch<T, NE>) * warps;
+  if (smem > 48 * 1024)
+    cudaFuncSetAttribute(k_tree_solve<T, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  k_tree_solve<T, NE><<<(unsigned)((L.B + warps - 1) / warps), 32 * warps, smem, st>>>(
+      P, L.targets, L.q0, L.B, L.opts, L.q_out, L.cost_out, L.init_cost, L.hist_out, L.iters, L.term);
+  return cudaGetLastError();
+}
+
 template <typename T>
 cudaError_t launch_tree_solve(const TreeLmParams<T>& P, const TreeLaunch& L, cudaStream_t st) {
   if (L.B == 0) return cudaSuccess;
-  const int warps = 4;
-  const size_t smem = sizeof(TreeScratch<T>) * warps;
-  if (smem > 48 * 1024)
-    cudaFuncSetAttribute(k_tree_solve<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  k_tree_solve<T><<<(unsigned)((L.B + warps - 1) / warps), 32 * warps, smem, st>>>(
-      P, L.targets, L.q0, L.B, L.opts, L.q_out, L.cost_out, L.init_cost, L.hist_out, L.iters, L.term);
-  return cudaGetLastError();
+  if (P.ne <= 1) return launch_tree_ne<T, 1>(P, L, st);
+  if (P.ne <= 2) return launch_tree_ne<T, 2>(P, L, st);
+  if (P.ne <= 4) return launch_tree_ne<T, 4>(P, L, st);
+  return launch_tree_ne<T, kTreeMaxPoses>(P, L, st);
 }
 
 template cudaError_t launch_tree_solve<float>(const TreeLmParams<float>&, const TreeLaunch&, cudaStream_t);

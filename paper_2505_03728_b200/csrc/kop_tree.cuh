@@ -11,6 +11,7 @@ namespace kop {
 constexpr int kTreeMaxJoints = 64;
 constexpr int kTreeMaxPoses = 8;
 constexpr int kTreeMaxDofs = 32;  // one warp lane per actuated joint
+constexpr int kTreeMaxPerCol = 4;  // moving joints driven by one column (leader + mimics)
 
 template <typename T>
 struct TreeLmParams {
@@ -24,6 +25,13 @@ struct TreeLmParams {
   T w_pos[kTreeMaxPoses], w_ori[kTreeMaxPoses];
   T lower[kTreeMaxDofs], upper[kTreeMaxDofs], rest[kTreeMaxDofs];
   T w_lim, w_rest;
+  // joints grouped by depth (parents in earlier levels): level d = lev_joint[lev_start[d] .. lev_start[d+1])
+  int32_t nlev;
+  int32_t lev_start[kTreeMaxJoints + 1];
+  int8_t lev_joint[kTreeMaxJoints];
+  // moving joints of each actuated column
+  int8_t col_nj[kTreeMaxDofs];
+  int8_t col_joint[kTreeMaxDofs][kTreeMaxPerCol];
 };
 
 struct TreeLaunch {
