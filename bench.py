@@ -365,9 +365,9 @@ def run_ours(args, rank, world, local_rank):
                 "d2h_bytes_per_step": int(d2h * world),
                 "api": "IkBeamSolver.solve_pinned: pinned host targets -> all IkResult fields in pinned host memory; "
                        "131072-target chunks, H2D / kernels / D2H overlapped on 3 streams",
-                "launches_per_step": 2 * -(-B // 131072), "bitwise_equal_to_device_run": e2e_match,
+                "launches_per_step": 3 * -(-B // 131072), "bitwise_equal_to_device_run": e2e_match,
                 "pcie_h2d_gbs": h2d_gbs, "pcie_d2h_gbs": d2h_gbs},
-        "gpu_launches": 2 * args.steps,
+        "gpu_launches": 3 * args.steps,  # stage 1, stage 2, FP64 errors
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,
                      "kernel": "k_beam_stage1 (seeds x 6 LM steps + prune)",

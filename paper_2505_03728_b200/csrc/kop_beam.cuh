@@ -243,13 +243,47 @@ __device__ __forceinline__ void beam_stage2_body(const MF& mf, const ChainParams
     for (int i = 0; i <= steps1; ++i) h[i] = double(rin[Rec<G>::hist + i]);
     for (int i = 0; i < steps2; ++i) h[steps1 + 1 + i] = double(hist[(size_t)i * bd + tid]);
   }
+  if (G::BASE) {  // mobile lanes: errors here (the base may not be written out)
+    double tinv[7];
+    target_inverse(targets + tgt * 7, tinv);
+    double pe, re;
+    pose_errors_f64<G::K>(Cd, qd, bd3, tinv, pe, re);
+    pos_err[tgt] = pe;
+    rot_err[tgt] = re;
+    success[tgt] = (pe < pos_tol && re < rot_tol) ? 1 : 0;
+  }
+}
+
+// FP64 pose errors and success of the winners (tasks.py:109-116, 147), one
+// thread per target after stage 2 (fixed-base shapes).  Kept out of stage 2 so
+// its LM loop is not diluted by FP64 code run by one lane in four.
+template <int K, int NQ>
+__global__ void __launch_bounds__(128)
+k_beam_errors(const ChainParams<double, K> Cd, const double* __restrict__ targets, int64_t B,
+              const double* __restrict__ q_out, double pos_tol, double rot_tol, double* __restrict__ pos_err,
+              double* __restrict__ rot_err, uint8_t* __restrict__ success) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= B) return;
+  double qd[NQ];
+#pragma unroll
+  for (int i = 0; i < NQ; ++i) qd[i] = q_out[t * NQ + i];
   double tinv[7];
-  target_inverse(targets + tgt * 7, tinv);
+  target_inverse(targets + t * 7, tinv);
   double pe, re;
-  pose_errors_f64<G::K>(Cd, qd, G::BASE ? bd3 : nullptr, tinv, pe, re);
-  pos_err[tgt] = pe;
-  rot_err[tgt] = re;
-  success[tgt] = (pe < pos_tol && re < rot_tol) ? 1 : 0;
+  pose_errors_f64<K>(Cd, qd, nullptr, tinv, pe, re);
+  pos_err[t] = pe;
+  rot_err[t] = re;
+  success[t] = (pe < pos_tol && re < rot_tol) ? 1 : 0;
+}
+
+template <class G>
+cudaError_t launch_beam_errors(const ChainParams<double, G::K>& Cd, const double* targets, int64_t B,
+                               const double* q_out, double pos_tol, double rot_tol, double* pos_err,
+                               double* rot_err, uint8_t* success, cudaStream_t st) {
+  if (G::BASE || B == 0) return cudaSuccess;
+  k_beam_errors<G::K, G::NQ><<<(unsigned)((B + 127) / 128), 128, 0, st>>>(Cd, targets, B, q_out, pos_tol, rot_tol,
+                                                                         pos_err, rot_err, success);
+  return cudaGetLastError();
 }
 
 }  // namespace kop

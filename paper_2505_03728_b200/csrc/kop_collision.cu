@@ -263,7 +263,10 @@ cudaError_t launch_col(const ChainParams<typename G::T, G::K>& C, const CostPara
                                                                Bm.steps2, Bm.keep, Bm.G, Bm.pos_tol, Bm.rot_tol,
                                                                Bm.q_out, Bm.cost_out, Bm.hist_out, Bm.pos_err,
                                                                Bm.rot_err, Bm.success);
-  return cudaGetLastError();
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_beam_errors<G>(Cd, Bm.targets, Bm.B, Bm.q_out, Bm.pos_tol, Bm.rot_tol, Bm.pos_err, Bm.rot_err,
+                               Bm.success, st);
 }
 
 #define KOP_COL_INSTANTIATE(T, NQ, K, ID)                                                                     \

@@ -3,7 +3,9 @@
 //   k_beam_stage1  one thread per (target, seed) lane: start + prune_after LM
 //                  steps + in-CTA stable top-`keep` prune (tasks.py:131-136)
 //   k_beam_stage2  one thread per survivor: remaining LM steps, segmented
-//                  warp-shuffle argmin, FP64 pose errors (tasks.py:137-161)
+//                  warp-shuffle argmin (tasks.py:137-161)
+//   k_beam_errors  one thread per target: FP64 pose errors / success of the
+//                  winner (tasks.py:109-116, 147)
 //   k_lane_*       the IkLaneProblem API (beam.py:133-240), one thread/lane
 //
 // Mapping: the workload is compute/latency bound (FP32 FMA + MUFU), so lanes
@@ -198,7 +200,10 @@ cudaError_t launch_beam(const ChainParams<typename G::T, G::K>& C, const CostPar
   k_beam_stage2<G><<<(unsigned)blocks2, tpb2, smem2, st>>>(
       C, W, Cd, L.targets, L.B, surv, rec, L.steps1, L.steps2, L.keep, L.G, L.pos_tol, L.rot_tol, L.q_out,
       L.base_out, L.cost_out, L.hist_out, L.pos_err, L.rot_err, L.success);
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  return launch_beam_errors<G>(Cd, L.targets, L.B, L.q_out, L.pos_tol, L.rot_tol, L.pos_err, L.rot_err, L.success,
+                               st);
 }
 
 template <class G>
