@@ -161,14 +161,14 @@ __device__ __forceinline__ void pose_errors_f64(const ChainParams<double, K>& C,
   re = sqrt(w.x * w.x + w.y * w.y + w.z * w.z);
 }
 
-// shared memory of stage 2 (128 threads): hist [steps2 * 128] | Ag | scratch
-template <class G>
+// shared memory of stage 2 (BD threads): hist [steps2 * BD] | Ag | scratch
+template <class G, int BD = 128>
 __host__ __device__ inline size_t beam_stage2_smem(int steps2, int extra) {
-  return sizeof(typename G::T) * ((size_t)(steps2 > 0 ? steps2 : 1) * 128 +
-                                  (size_t)(Tri<G::ND>::size + G::ND + extra) * 128);
+  return sizeof(typename G::T) * ((size_t)(steps2 > 0 ? steps2 : 1) * BD +
+                                  (size_t)(Tri<G::ND>::size + G::ND + extra) * BD);
 }
 
-template <class G, class MF>
+template <class G, int BD = 128, class MF>
 __device__ __forceinline__ void beam_stage2_body(const MF& mf, const ChainParams<double, G::K>& Cd,
                                                  const double* __restrict__ targets, int64_t B,
                                                  const typename G::T* __restrict__ surv, int rec, int steps1,
@@ -179,7 +179,7 @@ __device__ __forceinline__ void beam_stage2_body(const MF& mf, const ChainParams
                                                  uint8_t* __restrict__ success) {
   using T = typename G::T;
   constexpr int NQ = G::NQ;
-  constexpr int bd = 128;  // stage 2 always runs 128-thread blocks
+  constexpr int bd = BD;
   extern __shared__ unsigned char smem_raw[];
   T* hist = reinterpret_cast<T*>(smem_raw);  // [steps2 * bd]
   T* Ag = hist + (size_t)(steps2 > 0 ? steps2 : 1) * bd;  // [(Tri + ND) * bd]
@@ -211,7 +211,7 @@ __device__ __forceinline__ void beam_stage2_body(const MF& mf, const ChainParams
   st.cost = rin[Rec<G>::cost];
   const auto model = mf(tg, scratch + tid);
   for (int it = -1; it < steps2; ++it) {  // it == -1: re-derive A, g at the survivor
-    lm_iter<G, 128>(model, st, it < 0 ? 2 : 0);
+    lm_iter<G, BD>(model, st, it < 0 ? 2 : 0);
     if (it >= 0) hist[(size_t)it * bd + tid] = st.cost;
   }
   // winner = argmin over the keep survivors, ties -> lower stage-1 rank (tasks.py:139)

@@ -40,15 +40,18 @@ k_beam_stage1(const ChainParams<typename G::T, G::K> C, const CostParams<typenam
   beam_stage1_body<G, TPB>(PoseModelFactory<G>{C, W}, targets, B, seeds, S, P, steps1, keep, surv, rec);
 }
 
+constexpr int kStage2Threads = 128;
+
 template <class G>
-__global__ void __launch_bounds__(128, 4)
+__global__ void __launch_bounds__(kStage2Threads, 4)
 k_beam_stage2(const ChainParams<typename G::T, G::K> C, const CostParams<typename G::T, G::NQ> W,
               const ChainParams<double, G::K> Cd, const double* __restrict__ targets, int64_t B,
               const typename G::T* __restrict__ surv, int rec, int steps1, int steps2, int keep, int G2,
               double pos_tol, double rot_tol, double* __restrict__ q_out, double* __restrict__ base_out,
               double* __restrict__ cost_out, double* __restrict__ hist_out, double* __restrict__ pos_err,
               double* __restrict__ rot_err, uint8_t* __restrict__ success) {
-  beam_stage2_body<G>(PoseModelFactory<G>{C, W}, Cd, targets, B, surv, rec, steps1, steps2, keep, G2, pos_tol,
+  beam_stage2_body<G, kStage2Threads>(PoseModelFactory<G>{C, W}, Cd, targets, B, surv, rec, steps1, steps2, keep,
+                                      G2, pos_tol,
                       rot_tol, q_out, base_out, cost_out, hist_out, pos_err, rot_err, success);
 }
 
@@ -191,10 +194,10 @@ cudaError_t launch_beam(const ChainParams<typename G::T, G::K>& C, const CostPar
     if (e != cudaSuccess) return e;
   }
   if (!(L.stages & 2)) return cudaSuccess;
-  const int tpb2 = 128;
+  const int tpb2 = kStage2Threads;
   const int64_t lanes2 = L.B * L.G;
   const int64_t blocks2 = (lanes2 + tpb2 - 1) / tpb2;
-  const size_t smem2 = beam_stage2_smem<G>(L.steps2, 0);
+  const size_t smem2 = beam_stage2_smem<G, kStage2Threads>(L.steps2, 0);
   if (smem2 > 48 * 1024)
     cudaFuncSetAttribute(k_beam_stage2<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
   k_beam_stage2<G><<<(unsigned)blocks2, tpb2, smem2, st>>>(
