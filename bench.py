@@ -310,7 +310,7 @@ def run_ours(args, rank, world, local_rank):
     res = out.cpu()
 
     # ---- end-to-end through the public API: pinned host in, host results out ----
-    # IkBeamSolver.solve_pinned: chunked, H2D / kernels / D2H of consecutive chunks overlapped on 3 streams
+    # IkBeamSolver.solve_pinned: chunked, H2D / kernels / D2H of consecutive chunks overlapped on 4 streams
     host_t = targets.cpu().pin_memory()
     host_out = solver.alloc_host_outputs(B)
     h2d = host_t.numel() * host_t.element_size()
@@ -364,8 +364,8 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": int(h2d * world),
                 "d2h_bytes_per_step": int(d2h * world),
                 "api": "IkBeamSolver.solve_pinned: pinned host targets -> all IkResult fields in pinned host memory; "
-                       "131072-target chunks, H2D / kernels / D2H overlapped on 3 streams",
-                "launches_per_step": 3 * -(-B // 131072), "bitwise_equal_to_device_run": e2e_match,
+                       "65536-target chunks, H2D / kernels / D2H overlapped on 4 streams",
+                "launches_per_step": 3 * -(-B // 65536), "bitwise_equal_to_device_run": e2e_match,
                 "pcie_h2d_gbs": h2d_gbs, "pcie_d2h_gbs": d2h_gbs},
         "gpu_launches": 3 * args.steps,  # stage 1, stage 2, FP64 errors
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

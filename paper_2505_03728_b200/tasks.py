@@ -242,8 +242,8 @@ class IkBeamSolver:
                          mk(dev.pos_error, (batch,)), mk(dev.rot_error, (batch,)), mk(dev.success, (batch,)),
                          mk(dev.base, (batch, 3)))
 
-    def solve_pinned(self, host_targets, host_out: BeamBatch | None = None, chunk: int = 131072,
-                     n_streams: int = 3, history: bool = True) -> BeamBatch:
+    def solve_pinned(self, host_targets, host_out: BeamBatch | None = None, chunk: int = 65536,
+                     n_streams: int = 4, history: bool = True) -> BeamBatch:
         """Pinned host (B, 7) targets in, pinned host outputs out.  The batch runs
         in chunks round-robin over ``n_streams`` CUDA streams, so the host->device
         copy of one chunk, the kernels of another and the device->host copy of a

@@ -1,0 +1,23 @@
+"""Sweep chunk size / stream count of IkBeamSolver.solve_pinned (end-to-end rate)."""
+import json, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2505_03728_b200 as k
+from paper_2505_03728_b200.benchmark import reachable_target_array
+from paper_2505_03728_b200.tasks import IkBeamSolver
+
+B = 1_000_000
+m = k.load_robot(k.robot_path("arm7.urdf"), k.robot_path("arm7.sidecar.json"))
+s = IkBeamSolver(m, "flange", rng_seed=77)
+host = reachable_target_array(m, "flange", B, 77).cpu().pin_memory()
+out = s.alloc_host_outputs(B)
+for chunk in (65536, 131072, 200000, 262144, 500000):
+    for ns in (2, 3, 4):
+        s.solve_pinned(host, out, chunk=chunk, n_streams=ns); torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            s.solve_pinned(host, out, chunk=chunk, n_streams=ns)
+        e1.record(); torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 3
+        print(json.dumps({"chunk": chunk, "streams": ns, "ms": ms, "solves_per_s": B / ms * 1e3}), flush=True)
