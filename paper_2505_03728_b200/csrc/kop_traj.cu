@@ -771,11 +771,6 @@ k_traj_report(const ChainParams<double, G::K> C, const CollisionParams<double> P
 }
 
 template <class G>
-size_t traj_smem_bytes(int steps, int n_spheres) {
-  return TrajView<G>::bytes(steps, n_spheres);
-}
-
-template <class G>
 cudaError_t launch_traj(const ChainParams<typename G::T, G::K>& C, const CollisionParams<typename G::T>& P,
                         const TrajCosts<typename G::T>& W, const TrajLaunch& L, cudaStream_t st) {
   if (L.B == 0) return cudaSuccess;
@@ -821,7 +816,6 @@ template cudaError_t launch_traj_report<Cfg<double, 8, 8, false, false>>(const C
                                                                          const TrajReportLaunch&, cudaStream_t);
 
 #define KOP_TRAJ_INSTANTIATE(T, NQ, K, ID)                                                                   \
-  template size_t traj_smem_bytes<Cfg<T, NQ, K, ID, false>>(int, int);                                      \
   template cudaError_t launch_traj_normal<Cfg<T, NQ, K, ID, false>>(                                        \
       const ChainParams<T, K>&, const CollisionParams<T>&, const TrajCosts<T>&, const TrajLaunch&, cudaStream_t); \
   template cudaError_t launch_traj<Cfg<T, NQ, K, ID, false>>(const ChainParams<T, K>&,                      \

@@ -56,9 +56,6 @@ cudaError_t launch_traj_normal(const ChainParams<typename G::T, G::K>& C, const 
                                const TrajCosts<typename G::T>& W, const TrajLaunch& L, cudaStream_t st);
 
 template <class G>
-size_t traj_smem_bytes(int steps, int n_spheres);
-
-template <class G>
 cudaError_t launch_traj(const ChainParams<typename G::T, G::K>& C, const CollisionParams<typename G::T>& P,
                         const TrajCosts<typename G::T>& W, const TrajLaunch& L, cudaStream_t st);
 
