@@ -292,6 +292,12 @@ int compile_collision(const KopModel& m, const std::vector<LinkFrame>& frames, c
   P.eta_self = cc->eta_self > 0 ? cc->eta_self : 1.0;
   P.beta = cc->sharpness > 0 ? cc->sharpness : 100.0;
   P.hard = cc->hard_min;
+  for (int li = 0; li < P.nl; ++li)
+    P.lreach[li] = (P.hard || P.lcount[li] <= 1) ? 0.0 : log((double)P.lcount[li]) / P.beta;
+  for (int p = 0; p < P.np; ++p) {
+    const int c = P.lcount[P.pa[p]] * P.lcount[P.pb[p]];
+    P.preach[p] = (P.hard || c <= 1) ? 0.0 : log((double)c) / P.beta;
+  }
   return KOP_OK;
 }
 
@@ -331,6 +337,8 @@ CollisionParams<T> cast_collision(const CollisionParams<double>& D) {
   P.eta_self = T(D.eta_self);
   P.beta = T(D.beta);
   P.hard = D.hard;
+  for (int l = 0; l < kMaxSphereLinks; ++l) P.lreach[l] = T(D.lreach[l]);
+  for (int p = 0; p < kMaxSelfPairs; ++p) P.preach[p] = T(D.preach[p]);
   return P;
 }
 

@@ -44,6 +44,10 @@ struct CollisionParams {
   int32_t pa[kMaxSelfPairs], pb[kMaxSelfPairs];
   T w_world, eta_world, w_self, eta_self, beta;
   int32_t hard;                 // hard minimum instead of the softmin
+  // soft-minimum reach log(count)/beta (0 for the hard minimum) per sphere link
+  // and per self pair: the aggregate never lies below dmin - reach, so a row
+  // whose dmin - reach clears eta has activation exactly 0 and is skipped
+  T lreach[kMaxSphereLinks], preach[kMaxSelfPairs];
 };
 
 // scratch layout per lane (stride = block size): a_k, m_k [6 * K] | centres [3 * ns]
@@ -109,6 +113,25 @@ __device__ __forceinline__ T sphere_obstacle_t(const OB& P, int o, const vec3<T>
   }
   n = {v.x * inv, v.y * inv, v.z * inv};
   return nn - r - P.orad[o];
+}
+
+// distance only (no gradient): the screening pass of a collision row
+template <typename T, class OB>
+__device__ __forceinline__ T sphere_obstacle_dist_t(const OB& P, int o, const vec3<T>& c, T r) {
+  const int kind = P.okind[o];
+  const vec3<T> a{P.oa[o][0], P.oa[o][1], P.oa[o][2]};
+  if (kind == kObHalfSpace) return dot(a, c) - P.orad[o] - r;
+  vec3<T> p = a;
+  if (kind == kObCapsule) {
+    const vec3<T> d{P.ob[o][0] - a.x, P.ob[o][1] - a.y, P.ob[o][2] - a.z};
+    const T dd = dot(d, d);
+    T u = T(0);
+    if (!(dd < T(1e-16))) u = tmin(tmax(div_t(dot(vec3<T>{c.x - a.x, c.y - a.y, c.z - a.z}, d), dd), T(0)), T(1));
+    p = {a.x + u * d.x, a.y + u * d.y, a.z + u * d.z};
+  }
+  const vec3<T> v{c.x - p.x, c.y - p.y, c.z - p.z};
+  const T nn = norm_t(dot(v, v));
+  return (nn < T(1e-12) ? T(0) : nn) - r - P.orad[o];
 }
 
 template <class G>
@@ -231,7 +254,10 @@ __device__ __forceinline__ void col_forward(const ChainParams<typename G::T, G::
 // World (sphere link x obstacle) and self (link pair) activation rows from the
 // lane scratch filled by col_forward: adds their squares to the returned cost
 // and, if JAC, their rank-1 terms to A, g.  row/row_out/jac_out: parity output.
-template <class G, bool JAC, class OB = CollisionParams<typename G::T>>
+// SCREEN: a first distance-only pass skips rows that are inactive on every
+// lane of the warp (pays off when most rows are far from every obstacle, as in
+// trajectories; in IK-Beam the seeds of a warp rarely agree, so it is off).
+template <class G, bool JAC, class OB = CollisionParams<typename G::T>, bool SCREEN = false>
 __device__ __forceinline__ typename G::T col_rows(const ChainParams<typename G::T, G::K>& C,
                                                   const CollisionParams<typename G::T>& P, const ColLane<G>& L,
                                                   typename G::T (&A)[Tri<G::ND>::size], typename G::T (&g)[G::ND],
@@ -246,6 +272,17 @@ __device__ __forceinline__ typename G::T col_rows(const ChainParams<typename G::
     for (int li = 0; li < P.nl; ++li) {
       const int f = P.lfirst[li], nsph = P.lcount[li];
       for (int o = 0; o < O.no; ++o, ++row) {
+        if (SCREEN) {  // an inactive row (activation exactly 0) needs no gradient work
+          T dscr = inf_t<T>();
+          for (int s = 0; s < nsph; ++s)
+            dscr = tmin(dscr, sphere_obstacle_dist_t<T>(O, o, vec3<T>{L.cen(f + s, 0), L.cen(f + s, 1),
+                                                                     L.cen(f + s, 2)}, P.sr[f + s]));
+          // warp-uniform: lanes that skip would otherwise idle beside active ones
+          if (__all_sync(__activemask(), dscr - P.lreach[li] > P.eta_world * T(1.00001))) {
+            if (row_out) row_out[row] = 0.0;
+            continue;
+          }
+        }
         // one pass, online soft minimum: rescale the running sums whenever
         // the minimum drops (same value as costs.py:409-420's two passes)
         const bool hard = P.hard || nsph == 1;
@@ -310,6 +347,19 @@ __device__ __forceinline__ typename G::T col_rows(const ChainParams<typename G::
     for (int pi = 0; pi < P.np; ++pi, ++row) {
       const int la = P.pa[pi], lb = P.pb[pi];
       const int fa = P.lfirst[la], na = P.lcount[la], fb = P.lfirst[lb], nb = P.lcount[lb];
+      if (SCREEN) {
+        T dscr = inf_t<T>();
+        for (int i = 0; i < na; ++i)
+          for (int j = 0; j < nb; ++j) {
+            const vec3<T> v{L.cen(fa + i, 0) - L.cen(fb + j, 0), L.cen(fa + i, 1) - L.cen(fb + j, 1),
+                            L.cen(fa + i, 2) - L.cen(fb + j, 2)};
+            dscr = tmin(dscr, norm_t(dot(v, v)) - P.sr[fa + i] - P.sr[fb + j]);
+          }
+        if (__all_sync(__activemask(), dscr - P.preach[pi] > P.eta_self * T(1.00001))) {
+          if (row_out) row_out[row] = 0.0;
+          continue;
+        }
+      }
       const bool hard = P.hard || na * nb == 1;
       T dmin = inf_t<T>(), sumz = T(0);
       vec3<T> Ma{T(0), T(0), T(0)}, Mb{T(0), T(0), T(0)}, Gv{T(0), T(0), T(0)};

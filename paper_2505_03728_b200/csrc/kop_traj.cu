@@ -275,7 +275,7 @@ __device__ typename G::T traj_eval(const ChainParams<typename G::T, G::K>& C, co
       }
     }
     // world + self rows (world uses the per-problem obstacle table)
-    cost += col_rows<G, JAC, ObstacleTable<T>>(C, P, L, Ad, gd, 0, nullptr, nullptr, S.obs);
+    cost += col_rows<G, JAC, ObstacleTable<T>, true>(C, P, L, Ad, gd, 0, nullptr, nullptr, S.obs);
     // smoothness + velocity of the pair (t-1, t) (costs.py:198-231, 274-290)
     if (t >= 1) {
 #pragma unroll
