@@ -343,27 +343,44 @@ __device__ typename G::T traj_eval(const ChainParams<typename G::T, G::K>& C, co
     for (int li = 0; li < P.nl; ++li) {
       const int f = P.lfirst[li], nsph = P.lcount[li];
       for (int o = 0; o < S.obs->no; ++o) {
-        T dmin = inf_t<T>();
-        int kmin = 0;
-        for (int s = 0; s < nsph; ++s) {
-          vec3<T> ga, gb;
-          const T d = capsule_obstacle_t<T>(*S.obs, o, vec3<T>{L0.cen(f + s, 0), L0.cen(f + s, 1), L0.cen(f + s, 2)},
-                                            vec3<T>{L1.cen(f + s, 0), L1.cen(f + s, 1), L1.cen(f + s, 2)},
-                                            P.sr[f + s], ga, gb);
-          if (d < dmin) {
-            dmin = d;
-            kmin = s;
+        {  // screening, as in col_rows: skip rows inactive on every lane of the warp
+          T dscr = inf_t<T>();
+          for (int s = 0; s < nsph; ++s) {
+            vec3<T> ga, gb;
+            dscr = tmin(dscr, capsule_obstacle_t<T>(
+                                  *S.obs, o, vec3<T>{L0.cen(f + s, 0), L0.cen(f + s, 1), L0.cen(f + s, 2)},
+                                  vec3<T>{L1.cen(f + s, 0), L1.cen(f + s, 1), L1.cen(f + s, 2)}, P.sr[f + s], ga, gb));
           }
+          if (__all_sync(__activemask(), dscr - P.lreach[li] > W.eta_world * T(1.00001))) continue;
         }
+        // one pass, online soft minimum (costs.py:409-420)
         const bool hard = P.hard || nsph == 1;
-        T sumz = T(0);
+        T dmin = inf_t<T>(), sumz = T(0);
         vec3<T> M0{T(0), T(0), T(0)}, G0{T(0), T(0), T(0)}, M1{T(0), T(0), T(0)}, G1{T(0), T(0), T(0)};
         for (int s = 0; s < nsph; ++s) {
           const vec3<T> c0{L0.cen(f + s, 0), L0.cen(f + s, 1), L0.cen(f + s, 2)};
           const vec3<T> c1{L1.cen(f + s, 0), L1.cen(f + s, 1), L1.cen(f + s, 2)};
           vec3<T> ga, gb;
           const T d = capsule_obstacle_t<T>(*S.obs, o, c0, c1, P.sr[f + s], ga, gb);
-          const T z = hard ? (s == kmin ? T(1) : T(0)) : exp_t(-P.beta * (d - dmin));
+          T z;
+          if (hard) {
+            if (!(d < dmin)) continue;
+            dmin = d;
+            z = T(1);
+            sumz = T(0);
+            M0 = G0 = M1 = G1 = vec3<T>{T(0), T(0), T(0)};
+          } else {
+            if (d < dmin) {
+              const T sc = exp_t(-P.beta * (dmin - d));
+              sumz *= sc;
+              M0 = {M0.x * sc, M0.y * sc, M0.z * sc};
+              G0 = {G0.x * sc, G0.y * sc, G0.z * sc};
+              M1 = {M1.x * sc, M1.y * sc, M1.z * sc};
+              G1 = {G1.x * sc, G1.y * sc, G1.z * sc};
+              dmin = d;
+            }
+            z = exp_t(-P.beta * (d - dmin));
+          }
           sumz += z;
           if (JAC) {
             const vec3<T> x0 = cross(c0, ga), x1 = cross(c1, gb);
@@ -379,7 +396,7 @@ __device__ typename G::T traj_eval(const ChainParams<typename G::T, G::K>& C, co
         const T res = W.w_world * act;
         cost += res * res;
         if (JAC && dact != T(0)) {
-          const T inv = T(1) / sumz;
+          const T inv = div_t(T(1), sumz);
           M0 = {M0.x * inv, M0.y * inv, M0.z * inv};
           G0 = {G0.x * inv, G0.y * inv, G0.z * inv};
           M1 = {M1.x * inv, M1.y * inv, M1.z * inv};
