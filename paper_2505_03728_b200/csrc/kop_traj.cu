@@ -501,34 +501,39 @@ __device__ bool traj_damped_solve(const TrajView<G>& S, int N, typename G::T lam
   const int nblk = N / NQ;
   for (int jb = 0; jb < nblk; ++jb) {
     const int c0 = jb * NQ;
-    if (tid < 32) {  // 1: diagonal block + its slice of the forward substitution
-      const int a = tid;
-      T row[NQ];
+    if (tid == 0) {  // 1: diagonal block + its slice of the forward substitution, one thread, registers
+      T Lb[Tri<NQ>::size], yv[NQ];
 #pragma unroll
-      for (int b = 0; b < NQ; ++b) row[b] = (a < NQ && b <= a) ? S.l(c0 + a, a - b) : T(0);
-      T yv = a < NQ ? S.y[c0 + a] : T(0);
+      for (int a = 0; a < NQ; ++a) {
+#pragma unroll
+        for (int b = 0; b <= a; ++b) Lb[Tri<NQ>::at(a, b)] = S.l(c0 + a, a - b);
+        yv[a] = S.y[c0 + a];
+      }
 #pragma unroll
       for (int k = 0; k < NQ; ++k) {
-        const T dk = __shfl_sync(0xffffffffu, row[k], k);
+        const T dk = Lb[Tri<NQ>::at(k, k)];
         ok = ok && dk > T(0) && finite_t(dk);
         const T inv = rsqrt_t(dk);
-        if (a == k) row[k] = dk * inv;
-        else if (a > k) row[k] *= inv;
-        const T yk = __shfl_sync(0xffffffffu, yv, k) * inv;
-        if (a == k) yv = yk;
-        else if (a > k) yv -= row[k] * yk;
+        Lb[Tri<NQ>::at(k, k)] = dk * inv;
+        S.dinv[c0 + k] = inv;
+        const T yk = yv[k] * inv;
+        yv[k] = yk;
 #pragma unroll
-        for (int j = k + 1; j < NQ; ++j) {
-          const T ljk = __shfl_sync(0xffffffffu, row[k], j);
-          if (a >= j && a < NQ) row[j] -= row[k] * ljk;
+        for (int i = k + 1; i < NQ; ++i) {
+          const T lik = Lb[Tri<NQ>::at(i, k)] * inv;
+          Lb[Tri<NQ>::at(i, k)] = lik;
+          yv[i] -= lik * yk;
         }
-        if (a == 0) S.dinv[c0 + k] = inv;
-      }
-      if (a < NQ) {
 #pragma unroll
-        for (int b = 0; b < NQ; ++b)
-          if (b <= a) S.l(c0 + a, a - b) = row[b];
-        S.y[c0 + a] = yv;
+        for (int i = k + 1; i < NQ; ++i)
+#pragma unroll
+          for (int j = k + 1; j <= i; ++j) Lb[Tri<NQ>::at(i, j)] -= Lb[Tri<NQ>::at(i, k)] * Lb[Tri<NQ>::at(j, k)];
+      }
+#pragma unroll
+      for (int a = 0; a < NQ; ++a) {
+#pragma unroll
+        for (int b = 0; b <= a; ++b) S.l(c0 + a, a - b) = Lb[Tri<NQ>::at(a, b)];
+        S.y[c0 + a] = yv[a];
       }
     }
     __syncthreads();
