@@ -569,14 +569,34 @@ __device__ bool traj_damped_solve(const TrajView<G>& S, int N, typename G::T lam
     __syncthreads();
   }
   ok = __syncthreads_and(ok);
-  // back substitution L^T x = y, column sweep: x_k final, then y[k-d] -= L(k, k-d) x_k
+  // back substitution L^T x = y by blocks, warp 0: one thread solves the
+  // block's upper-triangular NQ x NQ system in registers, then BW lanes remove
+  // the block's contribution from the rows above it
   if (tid < 32) {
-    const int d = tid + 1;
-    for (int k = N - 1; k >= 0; --k) {
-      const T xk = S.y[k] * S.dinv[k];
+    for (int jb = nblk - 1; jb >= 0; --jb) {
+      const int c0 = jb * NQ;
+      if (tid == 0) {
+        T x[NQ];
+#pragma unroll
+        for (int bb = 0; bb < NQ; ++bb) {
+          const int b = NQ - 1 - bb;
+          T v = S.y[c0 + b];
+#pragma unroll
+          for (int m = 0; m < NQ; ++m)
+            if (m > b) v -= S.l(c0 + m, m - b) * x[m];
+          x[b] = v * S.dinv[c0 + b];
+          S.y[c0 + b] = x[b];
+        }
+      }
       __syncwarp();
-      if (d <= BW && k - d >= 0) S.y[k - d] -= S.l(k, d) * xk;
-      if (tid == 0) S.y[k] = xk;
+      const int c = c0 - 1 - tid;
+      if (tid < BW && c >= 0) {
+        T acc = T(0);
+#pragma unroll
+        for (int b = 0; b < NQ; ++b)
+          if (c0 + b - c <= BW) acc += S.l(c0 + b, c0 + b - c) * S.y[c0 + b];
+        S.y[c] -= acc;
+      }
       __syncwarp();
     }
   }
