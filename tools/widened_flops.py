@@ -17,7 +17,7 @@ FLOP_METRICS = ",".join(f"smsp__sass_thread_inst_executed_op_{op}_pred_on.sum"
                         for op in ("ffma", "fadd", "fmul", "dfma", "dadd", "dmul"))
 # (workload, kernel-name substring, precision tag in the template args, units)
 WORK = [
-    ("config4 collision IK-Beam", "k_col_beam_stage", "float", 2000),
+    ("config4 collision IK-Beam", ("k_col_beam_stage", "k_beam_errors"), "float", 2000),
     ("generic LM solve (collision stack)", "k_col_solve", "float", 2000),
     ("generic LM solve (collision stack)", "k_col_solve", "double", 2000),
     ("mobile-base IK-Beam", "k_beam_stage", "float", 2000),
@@ -103,7 +103,10 @@ def parse(path):
         f32 = f64 = 0.0
         kernels = set()
         for (lid, kname), mets in launches.items():
-            if sub not in kname or (f"Cfg<{prec}" not in kname and f"<{prec}>" not in kname):
+            subs = sub if isinstance(sub, tuple) else (sub,)
+            if not any(x in kname for x in subs):
+                continue
+            if "k_beam_errors" not in kname and not any(t in kname for t in (f"Cfg<{prec}", f"<{prec}>", f"<{prec},")):
                 continue
             if sub == "k_beam_stage" and "1, 1>" not in kname.replace("true", "1"):
                 continue  # mobile: BASE shapes only
