@@ -269,8 +269,13 @@ __device__ __forceinline__ bool tree_damped_solve(const TreeLmParams<T>& P, Tree
   return ok;
 }
 
+// warps per CTA: FP32 runs one-warp CTAs (a finished problem frees its slot at
+// once); FP64 keeps four (measured faster: register-limited residency)
+template <typename T>
+constexpr int tree_warps() { return sizeof(T) == 4 ? 1 : 4; }
+
 template <typename T, int NE>
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(32 * tree_warps<T>())
 k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const double* __restrict__ q0, int64_t B,
              const LmOptions O, double* __restrict__ q_out, double* __restrict__ cost_out,
              double* __restrict__ init_cost_out, double* __restrict__ hist_out, int32_t* __restrict__ iters_out,
@@ -353,7 +358,7 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
 
 template <typename T, int NE>
 cudaError_t launch_tree_ne(const TreeLmParams<T>& P, const TreeLaunch& L, cudaStream_t st) {
-  const int warps = 4;
+  constexpr int warps = tree_warps<T>();
   const size_t smem = sizeof(TreeScratch<T, NE>) * warps;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_tree_solve<T, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
