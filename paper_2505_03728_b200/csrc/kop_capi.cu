@@ -353,7 +353,8 @@ extern "C" {
 const char* kop_last_error(void) { return g_err.c_str(); }
 
 const char* kop_build_info(void) {
-  return "kinoptik_b200 sm_100a; fp32/fp64 x shapes {id2, id6, id7, gen8} + SE(2) base {id7, gen8}";
+  return "kinoptik_b200 sm_100a; fp32/fp64; IK lanes {id2, id6, id7, gen8} + SE(2) base {id7, gen8}; "
+         "collision lanes / LM / trajectories {id7, gen8}; tree LM (n <= 32, 1..8 poses)";
 }
 
 int kop_model_create(const KopModelDesc* d, KopModel** out) {
