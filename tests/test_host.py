@@ -178,3 +178,64 @@ def test_no_cpu_fallback_without_gpu(models):
         k.fk_arrays(models["arm7"], np.zeros(7))
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         k.solve_ik_beam(k.IkRequest(model=models["arm7"], target_link="flange", target_pose=k.Transform3.identity()))
+
+
+def _traj_costs(T=20, w_anchor=1e3, vl=None):
+    return _lib.KopTrajCosts(T, 0.1, w_anchor, 10.0, 10.0, 1.0, 0.1, 100.0, 0.0, 5.0, 0.01, 30.0, 0.05, 100.0, 0,
+                             None, None)
+
+
+def test_widened_entry_points_validate_before_touching_the_gpu(models):
+    """Argument checks of the trajectory / tree / collision entry points run on the
+    host and map to the reference's exceptions (no device call is made)."""
+    lib = _lib.lib()
+    h = models["arm7"]._handle
+    opts = _lib.KopLmOptions(150, 1e-4, 10.0, 1.0 / 3.0, 1e-8, 1e-10, 20, 1)
+    call = lambda c, n_obs=0, o=opts: lib.kop_traj_solve(h, 8, C.byref(c), C.byref(o), None, None, None, n_obs, 0,
+                                                        None, None, None, None, None, None, None)
+    assert call(_traj_costs(T=4)) == _lib.KOP_EINVAL and b"5 timesteps" in lib.kop_last_error()
+    assert call(_traj_costs(T=65)) == _lib.KOP_EUNSUPPORTED
+    assert call(_traj_costs(w_anchor=-1.0)) == _lib.KOP_EINVAL
+    assert call(_traj_costs(), n_obs=17) == _lib.KOP_EUNSUPPORTED
+    bad = _lib.KopLmOptions(150, 1e-4, 0.5, 1.0 / 3.0, 1e-8, 1e-10, 20, 1)
+    assert call(_traj_costs(), o=bad) == _lib.KOP_EINVAL and b"damping_increase" in lib.kop_last_error()
+    assert call(_traj_costs()) == _lib.KOP_OK  # batch 0: nothing to do
+    assert lib.kop_traj_report(h, 8, 0, None, None, 0, None, 0, None, None, None, None, None, None, None) \
+        == _lib.KOP_EINVAL
+    # tree solve: more than 8 end effectors / unknown link
+    links = np.arange(9, dtype=np.int32)
+    w = np.ones(9)
+    pc = _lib.KopPoseCosts(9, links.ctypes.data, w.ctypes.data, w.ctypes.data, 100.0, 0.01, None)
+    rc = lib.kop_multi_pose_solve(h, C.byref(pc), C.byref(opts), None, None, 0, None, None, None, None, None, None,
+                                  None)
+    assert rc == _lib.KOP_EUNSUPPORTED
+    links1 = np.array([42], dtype=np.int32)
+    pc1 = _lib.KopPoseCosts(1, links1.ctypes.data, w.ctypes.data, w.ctypes.data, 100.0, 0.01, None)
+    rc = lib.kop_multi_pose_solve(h, C.byref(pc1), C.byref(opts), None, None, 0, None, None, None, None, None, None,
+                                  None)
+    assert rc == _lib.KOP_EINVAL
+    # collision stack: too many obstacles, non-positive buffer distance
+    obs = (_lib.KopObstacle * 17)()
+    cc = _lib.KopCollisionCosts(50, 10, 100, 0.01, 20, 0.05, 5, 0.01, 100, 0, 17, obs)
+    assert lib.kop_collision_rows(h, 8, C.byref(cc)) == _lib.KOP_EUNSUPPORTED
+    cc = _lib.KopCollisionCosts(50, 10, 100, 0.01, 20, 0.0, 5, 0.01, 100, 0, 1, obs)
+    assert lib.kop_collision_rows(h, 8, C.byref(cc)) == _lib.KOP_EINVAL
+    cc = _lib.KopCollisionCosts(50, 10, 100, 0.01, 20, 0.05, 5, 0.01, 100, 0, 3, obs)
+    assert lib.kop_collision_rows(h, 8, C.byref(cc)) == 6 + 7 + 7 + 8 * 3 + len(models["arm7"].self_collision_pairs)
+
+
+def test_widened_apis_have_no_cpu_fallback(models):
+    torch = pytest.importorskip("torch")
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is visible")
+    m = models["arm7"]
+    world = k.WorldModel([k.Sphere([0.4, 0.0, 0.5], 0.1)])
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        k.trajectory_signed_distances(m, np.zeros((6, 7)), world)
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        k.solve(k.trajectory_problem(m, m.rest_pose, m.rest_pose + 0.1, 8, 0.1, world))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        k.plan_trajectory(k.TrajRequest(model=m, start_pose=k.Transform3.identity(),
+                                        goal_pose=k.Transform3.identity()))
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        k.solve_ik_collision_batch(m, "flange", np.array([[1.0, 0, 0, 0, 0.4, 0.0, 0.5]]), world=world)
