@@ -310,21 +310,22 @@ def run_ours(args, rank, world, local_rank):
     res = out.cpu()
 
     # ---- end-to-end through the public API: pinned host in, host results out ----
-    # IkBeamSolver.solve_pinned: chunked, H2D / kernels / D2H of consecutive chunks overlapped on 4 streams
+    # through the C ABI with HOST buffers (kop_ik_beam_host, IkBeamSolver.solve_host): the library
+    # pipelines 64K-target chunks over 4 streams, H2D / kernels / D2H overlapped
     host_t = targets.cpu().pin_memory()
     host_out = solver.alloc_host_outputs(B)
     h2d = host_t.numel() * host_t.element_size()
     d2h = sum(getattr(host_out, kk).numel() * getattr(host_out, kk).element_size()
               for kk in ("q", "cost", "history", "pos_error", "rot_error", "success"))
     for _ in range(max(1, args.warmup)):
-        solver.solve_pinned(host_t, host_out)
+        solver.solve_host(host_t, host_out)
     barrier()
     e2e_ms = 0.0
     for s in range(args.steps):
         flush.zero_()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        solver.solve_pinned(host_t, host_out)
+        solver.solve_host(host_t, host_out)
         e1.record()
         e1.synchronize()
         e2e_ms += e0.elapsed_time(e1)
@@ -363,8 +364,9 @@ def run_ours(args, rank, world, local_rank):
         "config": workload_config(B, args.precision),
         "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": int(h2d * world),
                 "d2h_bytes_per_step": int(d2h * world),
-                "api": "IkBeamSolver.solve_pinned: pinned host targets -> all IkResult fields in pinned host memory; "
-                       "65536-target chunks, H2D / kernels / D2H overlapped on 4 streams",
+                "api": "C ABI kop_ik_beam_host (IkBeamSolver.solve_host): pinned host targets -> all IkResult "
+                       "fields in pinned host memory; 65536-target chunks, H2D / kernels / D2H overlapped on 4 "
+                       "library streams",
                 "launches_per_step": 3 * -(-B // 65536), "bitwise_equal_to_device_run": e2e_match,
                 "pcie_h2d_gbs": h2d_gbs, "pcie_d2h_gbs": d2h_gbs},
         "gpu_launches": 3 * args.steps,  # stage 1, stage 2, FP64 errors

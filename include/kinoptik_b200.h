@@ -167,6 +167,20 @@ int kop_ik_beam_stage(const KopModel* model, int32_t link, const KopIkParams* pa
                       double* history_out, double* pos_err, double* rot_err, uint8_t* success,
                       void* stream);
 
+/* replaces: tasks.solve_ik_beam over B targets with HOST arrays end to end
+ * (the binding a NumPy caller uses, INTEGRATION.md seam 3b): targets host
+ * [B*7], seeds host [S*n]; outputs host, shapes as kop_ik_beam (base_out,
+ * history_out NULL ok).  The batch streams through `n_streams` (1..8, 0 = 4)
+ * internal CUDA streams in chunks of `chunk` targets (0 = 65536), overlapping
+ * host->device copies, kernels and device->host copies; pinned host memory
+ * gives full overlap.  Enqueued behind `stream` and joined back into it:
+ * host buffers must stay valid until `stream` completes.  Internal device
+ * buffers are cached per host thread and device (grow-only). */
+int kop_ik_beam_host(const KopModel* model, int32_t link, const KopIkParams* params, const double* targets,
+                     int64_t batch, const double* seeds, double* q_out, double* base_out, double* cost_out,
+                     double* history_out, double* pos_err, double* rot_err, uint8_t* success, int64_t chunk,
+                     int32_t n_streams, void* stream);
+
 /* --- collision IK (config 4) and the generic LM solve -------------------
  * Cost stack (the viewer's, server.py:60-97): pose (w_position,
  * w_orientation) | limit (w_limit) | rest (w_rest) | world collision, one

@@ -1413,3 +1413,162 @@ int kop_fma_peak_kernel(int32_t blocks, int32_t threads, int32_t iters, float* s
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// IK-Beam with host buffers end to end (the binding a NumPy caller uses)
+// ---------------------------------------------------------------------------
+namespace {
+
+// Per host thread and device: grow-only device buffers and streams of the
+// host pipeline.  Buffer set i is only ever used on stream i, so successive
+// calls are ordered by the streams themselves.
+struct HostPipe {
+  int device = -1;
+  int nstreams = 0;
+  int64_t chunk = 0, ws_bytes = 0, seeds_len = 0;
+  cudaStream_t st[8] = {};
+  cudaEvent_t done[8] = {};
+  void* buf[8] = {};
+  double* seeds = nullptr;
+  ~HostPipe() { release(); }
+  void release() {
+    for (int i = 0; i < 8; ++i) {
+      if (buf[i]) cudaFree(buf[i]);
+      if (st[i]) cudaStreamDestroy(st[i]);
+      if (done[i]) cudaEventDestroy(done[i]);
+      buf[i] = nullptr;
+      st[i] = nullptr;
+      done[i] = nullptr;
+    }
+    if (seeds) cudaFree(seeds);
+    seeds = nullptr;
+    nstreams = 0;
+    chunk = ws_bytes = seeds_len = 0;
+  }
+};
+thread_local HostPipe g_pipe;
+
+struct ChunkLayout {  // byte offsets of one buffer set
+  size_t tg, q, base, cost, hist, pe, re, ok, ws, total;
+};
+ChunkLayout chunk_layout(int64_t chunk, int n, int hist_len, int64_t ws_bytes) {
+  auto al = [](size_t v) { return (v + 255) / 256 * 256; };
+  ChunkLayout L{};
+  size_t at = 0;
+  L.tg = at; at = al(at + sizeof(double) * 7 * chunk);
+  L.q = at; at = al(at + sizeof(double) * n * chunk);
+  L.base = at; at = al(at + sizeof(double) * 3 * chunk);
+  L.cost = at; at = al(at + sizeof(double) * chunk);
+  L.hist = at; at = al(at + sizeof(double) * hist_len * chunk);
+  L.pe = at; at = al(at + sizeof(double) * chunk);
+  L.re = at; at = al(at + sizeof(double) * chunk);
+  L.ok = at; at = al(at + chunk);
+  L.ws = at; at = al(at + (size_t)ws_bytes);
+  L.total = at;
+  return L;
+}
+
+}  // namespace
+
+extern "C" {
+
+int kop_ik_beam_host(const KopModel* m, int32_t link, const KopIkParams* p, const double* targets, int64_t batch,
+                     const double* seeds, double* q_out, double* base_out, double* cost_out, double* history_out,
+                     double* pos_err, double* rot_err, uint8_t* success, int64_t chunk, int32_t n_streams,
+                     void* stream) {
+  if (!m || !p) return fail(KOP_EINVAL, "null argument");
+  if (batch < 0) return fail(KOP_EINVAL, "negative batch");
+  if (n_streams < 0 || n_streams > 8) return fail(KOP_EINVAL, "n_streams must be in 0..8");
+  if (chunk < 0) return fail(KOP_EINVAL, "negative chunk");
+  // validates the request (and the shape) without touching the device
+  const int64_t ws1 = kop_ik_beam_workspace_bytes(m, link, p, 1);
+  if (ws1 < 0) return (int)ws1;
+  if (batch == 0) return KOP_OK;
+  if (!targets || !seeds || !q_out || !cost_out || !pos_err || !rot_err || !success)
+    return fail(KOP_EINVAL, "null array argument");
+  const int n = m->tree.n, hist_len = p->total_steps + 1;
+  if (hist_len > 64 || n > 8) return fail(KOP_EUNSUPPORTED, "host pipeline compiled for <= 63 steps, <= 8 joints");
+  const int ns = n_streams ? n_streams : 4;
+  const int64_t ck = chunk ? (chunk < batch ? chunk : batch) : (batch < 65536 ? batch : 65536);
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return cuda_status(e);
+  HostPipe& P = g_pipe;
+  const int64_t ws = kop_ik_beam_workspace_bytes(m, link, p, ck);
+  if (P.device != dev || P.nstreams < ns || P.chunk < ck || P.ws_bytes < ws) {
+    const int64_t keep_chunk = P.device == dev && P.chunk > ck ? P.chunk : ck;
+    const int64_t keep_ws = P.device == dev && P.ws_bytes > ws ? P.ws_bytes : ws;
+    const int keep_ns = P.device == dev && P.nstreams > ns ? P.nstreams : ns;
+    if (P.device >= 0) cudaDeviceSynchronize();
+    P.release();
+    P.device = dev;
+    P.chunk = keep_chunk;
+    P.ws_bytes = keep_ws;
+    P.nstreams = keep_ns;
+    const ChunkLayout Lk = chunk_layout(P.chunk, 8, 64, P.ws_bytes);
+    for (int i = 0; i < P.nstreams; ++i) {
+      if ((e = cudaStreamCreateWithFlags(&P.st[i], cudaStreamNonBlocking)) != cudaSuccess ||
+          (e = cudaEventCreateWithFlags(&P.done[i], cudaEventDisableTiming)) != cudaSuccess ||
+          (e = cudaMalloc(&P.buf[i], Lk.total)) != cudaSuccess) {
+        P.release();
+        P.device = -1;
+        return cuda_status(e);
+      }
+    }
+  }
+  const ChunkLayout L = chunk_layout(P.chunk, 8, 64, P.ws_bytes);
+  const int64_t seeds_len = (int64_t)p->seeds * n;
+  if (P.seeds_len < seeds_len) {
+    if (P.seeds) cudaFree(P.seeds);
+    P.seeds = nullptr;
+    if ((e = cudaMalloc(&P.seeds, sizeof(double) * seeds_len)) != cudaSuccess) return cuda_status(e);
+    P.seeds_len = seeds_len;
+  }
+  cudaStream_t caller = (cudaStream_t)stream;
+  // seeds: copied on stream 0 after the caller's prior work; the other streams wait for them
+  cudaEvent_t start;
+  if ((e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming)) != cudaSuccess) return cuda_status(e);
+  cudaEventRecord(start, caller);
+  cudaStreamWaitEvent(P.st[0], start, 0);
+  cudaMemcpyAsync(P.seeds, seeds, sizeof(double) * seeds_len, cudaMemcpyHostToDevice, P.st[0]);
+  cudaEventRecord(start, P.st[0]);
+  for (int i = 1; i < ns; ++i) cudaStreamWaitEvent(P.st[i], start, 0);
+  int rc = KOP_OK;
+  for (int64_t lo = 0, c = 0; lo < batch && rc == KOP_OK; lo += ck, ++c) {
+    const int64_t cnt = (batch - lo) < ck ? (batch - lo) : ck;
+    const int i = (int)(c % ns);
+    cudaStream_t s = P.st[i];
+    char* b = static_cast<char*>(P.buf[i]);
+    double* dtg = reinterpret_cast<double*>(b + L.tg);
+    double* dq = reinterpret_cast<double*>(b + L.q);
+    double* dbase = reinterpret_cast<double*>(b + L.base);
+    double* dcost = reinterpret_cast<double*>(b + L.cost);
+    double* dhist = reinterpret_cast<double*>(b + L.hist);
+    double* dpe = reinterpret_cast<double*>(b + L.pe);
+    double* dre = reinterpret_cast<double*>(b + L.re);
+    uint8_t* dok = reinterpret_cast<uint8_t*>(b + L.ok);
+    cudaMemcpyAsync(dtg, targets + lo * 7, sizeof(double) * 7 * cnt, cudaMemcpyHostToDevice, s);
+    rc = kop_ik_beam_stage(m, link, p, 3, dtg, cnt, P.seeds, b + L.ws, P.ws_bytes, dq,
+                           p->optimize_base ? dbase : nullptr, dcost, history_out ? dhist : nullptr, dpe, dre, dok, s);
+    if (rc != KOP_OK) break;
+    cudaMemcpyAsync(q_out + lo * n, dq, sizeof(double) * n * cnt, cudaMemcpyDeviceToHost, s);
+    if (base_out && p->optimize_base)
+      cudaMemcpyAsync(base_out + lo * 3, dbase, sizeof(double) * 3 * cnt, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(cost_out + lo, dcost, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s);
+    if (history_out)
+      cudaMemcpyAsync(history_out + lo * hist_len, dhist, sizeof(double) * hist_len * cnt, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(pos_err + lo, dpe, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(rot_err + lo, dre, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(success + lo, dok, cnt, cudaMemcpyDeviceToHost, s);
+  }
+  // join: the caller's stream waits for every pipeline stream
+  for (int i = 0; i < ns; ++i) {
+    cudaEventRecord(P.done[i], P.st[i]);
+    cudaStreamWaitEvent(caller, P.done[i], 0);
+  }
+  cudaEventDestroy(start);
+  if (rc != KOP_OK) return rc;
+  return cuda_status(cudaGetLastError());
+}
+
+}  // extern "C"

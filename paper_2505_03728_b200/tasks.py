@@ -294,16 +294,44 @@ class IkBeamSolver:
             check(need, "kop_ik_beam_workspace_bytes")
         return need
 
-    def solve(self, targets) -> BeamBatch:
-        """Host in, host out (synchronous); large batches stream through ``solve_pinned``."""
-        arr = targets_to_array(targets)
-        if arr.shape[0] <= 131072:
-            return self.solve_device(dv.to_dev(arr)).cpu()
+    def solve_host(self, targets, out: BeamBatch | None = None, chunk: int = 0, n_streams: int = 0,
+                   history: bool = True) -> BeamBatch:
+        """Host arrays in, host arrays out through the C ABI (``kop_ik_beam_host``):
+        the library pipelines H2D copies, kernels and D2H copies over its own
+        streams.  ``targets``: (B, 7) float64 numpy array or CPU tensor (pinned
+        memory overlaps fully); ``out``: host BeamBatch to fill (numpy / CPU
+        tensors), default new numpy arrays.  Enqueued behind the current stream
+        and joined back into it; returns after synchronising unless ``out`` was
+        given (then the caller synchronises)."""
+        if self.collision is not None:
+            raise UnsupportedFeatureError("the host pipeline runs the plain IK lanes; use solve_device")
         t = dv.require_cuda()
-        host = t.from_numpy(np.ascontiguousarray(arr)).pin_memory()
-        res = self.solve_pinned(host)
-        t.cuda.current_stream().synchronize()
-        return res.cpu()
+        tg = targets if isinstance(targets, t.Tensor) else t.from_numpy(np.ascontiguousarray(targets_to_array(targets)))
+        if tg.dtype != t.float64 or tg.device.type != "cpu" or not tg.is_contiguous() or tg.shape[-1] != 7:
+            raise ValueError("targets must be a contiguous host (B, 7) float64 array")
+        b = tg.shape[0]
+        given = out is not None
+        if out is None:
+            n = self.model.actuated_count
+            out = BeamBatch(np.empty((b, n)), np.empty(b), np.empty((b, self.total_steps + 1)), np.empty(b),
+                            np.empty(b), np.empty(b, dtype=np.uint8), np.empty((b, 3)) if self.optimize_base else None)
+        if not hasattr(self, "_seeds_host"):
+            self._seeds_host = np.ascontiguousarray(self.seeds.cpu().numpy())
+        hp = lambda x: None if x is None else (x.data_ptr() if isinstance(x, t.Tensor) else x.ctypes.data)
+        check(lib().kop_ik_beam_host(self.model._handle, self.link_idx, C.byref(self.params), hp(tg), b,
+                                     self._seeds_host.ctypes.data, hp(out.q), hp(out.base), hp(out.cost),
+                                     hp(out.history) if history else None, hp(out.pos_error), hp(out.rot_error),
+                                     hp(out.success), chunk, n_streams, dv.stream_handle()), "kop_ik_beam_host")
+        if not given:
+            t.cuda.current_stream().synchronize()
+        return out
+
+    def solve(self, targets) -> BeamBatch:
+        """Host in, host out (synchronous), through the host pipeline of the C ABI."""
+        arr = targets_to_array(targets)
+        if self.collision is not None:
+            return self.solve_device(dv.to_dev(arr)).cpu()
+        return self.solve_host(arr)
 
 
 def solve_ik_beam_batch(model: RobotModel, link: str, targets, weights: ck.CostWeights | None = None,

@@ -357,3 +357,25 @@ def test_mobile_benchmark_acceptance(models):
     opt, static = out["results"]["optimized"], out["results"]["static"]
     assert opt["success_rate"] >= 0.99 and opt["pos_mean"] < 1e-4 and opt["rot_mean"] < 1e-3, opt
     assert static["success_rate"] <= 0.60, static
+
+
+@pytest.mark.parametrize("name,link,base", [("arm7", "flange", False), ("arm7", "flange", True),
+                                            ("planar_2r", None, False)])
+def test_host_pipeline_equals_device_run(models, name, link, base):
+    """kop_ik_beam_host (host buffers, chunked multi-stream pipeline) returns
+    exactly what the device-resident kop_ik_beam computes."""
+    m = models[name]
+    link = link or m.link_names[-1]
+    tg = reachable_target_array(m, link, 1000, 5).cpu().numpy()
+    if base:
+        tg[:, 4:] += np.array([0.6, -0.3, 0.0])
+    s = k.IkBeamSolver(m, link, rng_seed=3, optimize_base=base)
+    ref = s.solve_device(tg).cpu()
+    got = s.solve_host(tg, chunk=300, n_streams=3)
+    for f in ("q", "cost", "history", "pos_error", "rot_error", "success") + (("base",) if base else ()):
+        assert np.array_equal(getattr(got, f), getattr(ref, f)), f
+    pinned = torch.from_numpy(tg).pin_memory()
+    out = s.alloc_host_outputs(1000)
+    s.solve_host(pinned, out)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.q.numpy(), ref.q) and np.array_equal(out.success.numpy(), ref.success)
