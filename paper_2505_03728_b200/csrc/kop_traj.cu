@@ -452,98 +452,132 @@ __device__ typename G::T traj_eval(const ChainParams<typename G::T, G::K>& C, co
 
 // Banded damped Cholesky solve: y <- -(H + lam diag(max(diag H, 1e-8)))^-1 g.
 //
-// Blocked right-looking factorisation over timestep blocks of NQ columns
-// (three barriers per block instead of two per column), with the forward
-// substitution fused in:
-//   1  warp 0: Cholesky of the NQ x NQ diagonal block, lane a holding row a
-//      in registers (shuffles carry the pivot column), and y_blk <- D^-1 y_blk;
-//   2  threads 0..BW-1: the BW rows below solve x D^T = a (their NQ-wide slice
-//      of the block column) and y_r -= x . y_blk;
-//   3  all threads: trailing update L(r, c) -= x_r . x_c of the BW x BW
-//      lower triangle below the block.
-// Entries of the band beyond half-width BW are structural zeros of the
-// factor (the profile of row t*NQ+a starts at (t-4)*NQ+a), and the recurrences
-// keep them zero, so they are never stored.  The back substitution L^T x = y
-// is a column sweep by warp 0 (lane d updates y[k-d]).
+// Blocked right-looking factorisation over timestep blocks of NQ columns with
+// the forward substitution fused in and a one-block look-ahead:
+//   2  threads 0..BW-1: the BW rows below block jb solve x D^T = a (their
+//      NQ-wide slice of the block column) and y_r -= x . y_blk;
+//   3  warp 0 applies the trailing update to the NEXT diagonal block and one
+//      thread factors it in registers (carrying its slice of the forward
+//      substitution) while warps 1..3 apply the rest of the trailing update
+//      L(r, c) -= x_r . x_c of the BW x BW lower triangle below block jb.
+// Two barriers per block; the serial diagonal factorisation overlaps the
+// trailing update.  Entries of the band beyond half-width BW are structural
+// zeros of the factor (the profile of row t*NQ+a starts at (t-4)*NQ+a) and are
+// never stored.  The back substitution L^T x = y also runs by blocks.
 template <class G>
-__device__ __forceinline__ typename G::T lz(const TrajView<G>& S, int r, int c) {
-  const int d = r - c;
-  return d <= TrajView<G>::BW ? S.l(r, d) : typename G::T(0);
+__device__ __forceinline__ bool traj_factor_diag(const TrajView<G>& S, int c0) {
+  using T = typename G::T;
+  constexpr int NQ = G::NQ;
+  T Lb[Tri<NQ>::size], yv[NQ];
+  bool ok = true;
+#pragma unroll
+  for (int a = 0; a < NQ; ++a) {
+#pragma unroll
+    for (int b = 0; b <= a; ++b) Lb[Tri<NQ>::at(a, b)] = S.l(c0 + a, a - b);
+    yv[a] = S.y[c0 + a];
+  }
+#pragma unroll
+  for (int k = 0; k < NQ; ++k) {
+    const T dk = Lb[Tri<NQ>::at(k, k)];
+    ok = ok && dk > T(0) && finite_t(dk);
+    const T inv = rsqrt_t(dk);
+    Lb[Tri<NQ>::at(k, k)] = dk * inv;
+    S.dinv[c0 + k] = inv;
+    const T yk = yv[k] * inv;
+    yv[k] = yk;
+#pragma unroll
+    for (int i = k + 1; i < NQ; ++i) {
+      const T lik = Lb[Tri<NQ>::at(i, k)] * inv;
+      Lb[Tri<NQ>::at(i, k)] = lik;
+      yv[i] -= lik * yk;
+    }
+#pragma unroll
+    for (int i = k + 1; i < NQ; ++i)
+#pragma unroll
+      for (int j = k + 1; j <= i; ++j) Lb[Tri<NQ>::at(i, j)] -= Lb[Tri<NQ>::at(i, k)] * Lb[Tri<NQ>::at(j, k)];
+  }
+#pragma unroll
+  for (int a = 0; a < NQ; ++a) {
+#pragma unroll
+    for (int b = 0; b <= a; ++b) S.l(c0 + a, a - b) = Lb[Tri<NQ>::at(a, b)];
+    S.y[c0 + a] = yv[a];
+  }
+  return ok;
+}
+
+// L(r, c) -= sum_b L(r, c0 + b) L(c, c0 + b) for rows r = c0+NQ+ri, c = c0+NQ+ci
+template <class G>
+__device__ __forceinline__ void traj_trailing(const TrajView<G>& S, int c0, int ri, int ci) {
+  using T = typename G::T;
+  constexpr int NQ = G::NQ, BW = TrajView<G>::BW;
+  const int r = c0 + NQ + ri, c = c0 + NQ + ci;
+  const T* lr = S.L + r * (BW + 1) + NQ + ri;  // L(r, c0 + b) = lr[-b]
+  const T* lc = S.L + c * (BW + 1) + NQ + ci;
+  const int blo = NQ + ri - BW;  // both vanish for b < blo (band edge of row r)
+  T acc = T(0);
+#pragma unroll
+  for (int b = 0; b < NQ; ++b)
+    if (b >= blo) acc += lr[-b] * lc[-b];
+  S.l(r, ri - ci) -= acc;
 }
 
 template <class G>
 __device__ bool traj_damped_solve(const TrajView<G>& S, int N, typename G::T lam) {
   using T = typename G::T;
-  constexpr int NQ = G::NQ, BW = TrajView<G>::BW;
-  static_assert(BW <= 32, "band wider than a warp");
+  constexpr int NQ = G::NQ, BW = TrajView<G>::BW, NT = Tri<NQ>::size;
+  static_assert(BW <= 32 && NT <= 64, "band wider than a warp");
   const int tid = threadIdx.x;
   for (int i = tid; i < N; i += kTrajThreads) {
     for (int d = 0; d <= BW; ++d) S.l(i, d) = S.h(i, d);  // zero outside the compact blocks
     S.l(i, 0) += lam * tmax(S.h(i, 0), T(BeamConsts::diag_clamp));
     S.y[i] = -S.g[i];
   }
-  // trailing-update pairs (ri, ci), 0 <= ci <= ri < BW, dealt to the threads once
-  constexpr int NPAIR = BW * (BW + 1) / 2;
-  constexpr int PPT = (NPAIR + kTrajThreads - 1) / kTrajThreads;
+  // warps 1..3 take the trailing-update pairs (ri, ci), 0 <= ci <= ri < BW,
+  // that are not in the next diagonal block (ri < NQ); warp 0 lane l < NT takes
+  // diagonal-block pair l
+  constexpr int NPAIR = BW * (BW + 1) / 2 - NT;
+  constexpr int NW = kTrajThreads - 32;
+  constexpr int PPT = (NPAIR + NW - 1) / NW;
   int pri[PPT], pci[PPT];
+  {
+    int q = 0, tgt = tid - 32;
 #pragma unroll
-  for (int r = 0; r < PPT; ++r) {
-    int rem = tid + r * kTrajThreads, ri = 0;
-    while (ri < BW && rem > ri) {
+    for (int r = 0; r < PPT; ++r) pri[r] = BW;  // no pair
+    for (int ri = NQ; ri < BW && tid >= 32; ++ri)
+      for (int ci = 0; ci <= ri; ++ci, ++q)
+        if (q % NW == tgt && q / NW < PPT) {
+          pri[q / NW] = ri;
+          pci[q / NW] = ci;
+        }
+  }
+  int dri[2] = {BW, BW}, dci[2] = {0, 0};  // warp 0: diagonal-block pairs tid, tid + 32
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    int rem = tid + 32 * h, ri = 0;
+    if (tid >= 32 || rem >= NT) continue;
+    while (rem > ri) {
       rem -= ri + 1;
       ++ri;
     }
-    pri[r] = ri;  // >= BW: no pair
-    pci[r] = rem;
+    dri[h] = ri;
+    dci[h] = rem;
   }
   __syncthreads();
   bool ok = true;
   const int nblk = N / NQ;
+  if (tid == 0) ok = traj_factor_diag<G>(S, 0);
+  __syncthreads();
   for (int jb = 0; jb < nblk; ++jb) {
     const int c0 = jb * NQ;
-    if (tid == 0) {  // 1: diagonal block + its slice of the forward substitution, one thread, registers
-      T Lb[Tri<NQ>::size], yv[NQ];
-#pragma unroll
-      for (int a = 0; a < NQ; ++a) {
-#pragma unroll
-        for (int b = 0; b <= a; ++b) Lb[Tri<NQ>::at(a, b)] = S.l(c0 + a, a - b);
-        yv[a] = S.y[c0 + a];
-      }
-#pragma unroll
-      for (int k = 0; k < NQ; ++k) {
-        const T dk = Lb[Tri<NQ>::at(k, k)];
-        ok = ok && dk > T(0) && finite_t(dk);
-        const T inv = rsqrt_t(dk);
-        Lb[Tri<NQ>::at(k, k)] = dk * inv;
-        S.dinv[c0 + k] = inv;
-        const T yk = yv[k] * inv;
-        yv[k] = yk;
-#pragma unroll
-        for (int i = k + 1; i < NQ; ++i) {
-          const T lik = Lb[Tri<NQ>::at(i, k)] * inv;
-          Lb[Tri<NQ>::at(i, k)] = lik;
-          yv[i] -= lik * yk;
-        }
-#pragma unroll
-        for (int i = k + 1; i < NQ; ++i)
-#pragma unroll
-          for (int j = k + 1; j <= i; ++j) Lb[Tri<NQ>::at(i, j)] -= Lb[Tri<NQ>::at(i, k)] * Lb[Tri<NQ>::at(j, k)];
-      }
-#pragma unroll
-      for (int a = 0; a < NQ; ++a) {
-#pragma unroll
-        for (int b = 0; b <= a; ++b) S.l(c0 + a, a - b) = Lb[Tri<NQ>::at(a, b)];
-        S.y[c0 + a] = yv[a];
-      }
-    }
-    __syncthreads();
     if (tid < BW && c0 + NQ + tid < N) {  // 2: rows below the block
       const int r = c0 + NQ + tid;
+      const int blo = NQ + tid - BW;  // L(r, c0 + b) = 0 below the band for b < blo
+      const T* lr = S.L + r * (BW + 1) + NQ + tid;  // L(r, c0 + b) = lr[-b]
       T x[NQ];
       T yu = T(0);
 #pragma unroll
       for (int b = 0; b < NQ; ++b) {
-        T v = lz(S, r, c0 + b);
+        T v = b >= blo ? lr[-b] : T(0);
 #pragma unroll
         for (int m = 0; m < NQ; ++m)
           if (m < b) v -= x[m] * S.l(c0 + b, b - m);
@@ -556,14 +590,17 @@ __device__ bool traj_damped_solve(const TrajView<G>& S, int N, typename G::T lam
       S.y[r] -= yu;
     }
     __syncthreads();
+    if (jb + 1 < nblk) {  // 3 with look-ahead
+      if (tid < 32) {
 #pragma unroll
-    for (int p = 0; p < PPT; ++p) {  // 3: trailing update below the block
-      const int r = c0 + NQ + pri[p], c = c0 + NQ + pci[p];
-      if (pri[p] < BW && r < N) {
-        T acc = T(0);
+        for (int h = 0; h < 2; ++h)
+          if (dri[h] < BW) traj_trailing<G>(S, c0, dri[h], dci[h]);
+        __syncwarp();
+        if (tid == 0) ok = traj_factor_diag<G>(S, c0 + NQ) && ok;
+      } else {
 #pragma unroll
-        for (int b = 0; b < NQ; ++b) acc += lz(S, r, c0 + b) * lz(S, c, c0 + b);
-        S.l(r, r - c) -= acc;
+        for (int p = 0; p < PPT; ++p)
+          if (pri[p] < BW && c0 + NQ + pri[p] < N) traj_trailing<G>(S, c0, pri[p], pci[p]);
       }
     }
     __syncthreads();
