@@ -258,3 +258,28 @@ def test_generic_solve_runs_trajectory_problems(arm7, golden_traj):
     reps = k.solve_batch([pr0, pr], k.SolveOptions(max_iterations=150))
     np.testing.assert_array_equal(np.stack([reps[1].final_values.value(f"q{t}") for t in range(T)]), qs)
     np.testing.assert_allclose(reps[0].final_cost, float(g0("cost")), rtol=1e-8)
+
+
+def test_traj_generic_shape_planar_2r_vs_oracle(models, chains):
+    """Padded generic kernel shape (n = 2 < 8 -> NQ = 8, 36-entry diagonal
+    blocks) with spheres, a capsule obstacle and self pairs: FP64 device solve
+    vs the oracle's from the same anchors."""
+    m = models["planar_2r"]
+    ch = chains["planar_2r"]
+    sp = co.load_spheres_files(ch, robot_file("planar_2r.urdf"), robot_file("planar_2r.sidecar.json"))
+    qa, qb = np.array([0.2, 0.4]), np.array([1.4, -0.6])
+    T = 14
+    mid = k.link_transform(m, 0.5 * (qa + qb), m.link_names[-1]).translation
+    world = k.WorldModel([k.Capsule(mid - [0.05, 0.0, 0.2], mid + [0.05, 0.0, 0.2], 0.08)])
+    obs_o = [co.capsule(mid - [0.05, 0.0, 0.2], mid + [0.05, 0.0, 0.2], 0.08)]
+    tc = to.TrajCosts(timesteps=T)
+    with open(robot_file("planar_2r.urdf")) as f:
+        vl = to.velocity_limits(ch, f.read())
+    qs_o, cost_o, hist_o, _, _ = to.solve_traj(ch, sp, obs_o, to.straight_line(qa, qb, T), qa, qb, tc, vl)
+    planner = k.TrajectoryPlanner(m, m.link_names[-1], timesteps=T)
+    out = planner.solve_anchored_device(np.array([[qa, qb]]), k.collision.obstacle_rows(world.obstacles)[None], 1)
+    hist = out["history"][0].cpu().numpy()[:int(out["iterations"][0]) + 1]
+    mlen = min(len(hist), len(hist_o))
+    np.testing.assert_allclose(hist[:mlen], hist_o[:mlen], rtol=1e-8)
+    np.testing.assert_allclose(out["cost"][0].item(), cost_o, rtol=1e-8)
+    np.testing.assert_allclose(out["qs"][0].cpu().numpy(), qs_o, atol=1e-6)
