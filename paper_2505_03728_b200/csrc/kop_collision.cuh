@@ -75,6 +75,49 @@ __device__ __forceinline__ void activation_t(T d, T eta, T& a, T& da) {
   }
 }
 
+// Soft minimum over candidate distances (costs.py:409-420) accumulated in ONE
+// pass: the weights z = exp(-beta (d - dmin)) and the NV weighted gradient sums
+// are rescaled whenever the running minimum drops, which gives the reference's
+// two-pass value.  hard: argmin (first on ties) with weight 1.
+template <typename T, int NV>
+struct SoftMin {
+  T dmin, sumz;
+  vec3<T> acc[NV];
+  __device__ __forceinline__ SoftMin() : dmin(inf_t<T>()), sumz(T(0)) {
+#pragma unroll
+    for (int v = 0; v < NV; ++v) acc[v] = {T(0), T(0), T(0)};
+  }
+  // weight of a candidate at distance d (0: not part of the hard minimum)
+  __device__ __forceinline__ T weight(T d, T beta, bool hard) {
+    if (hard) {
+      if (!(d < dmin)) return T(0);
+      dmin = d;
+      sumz = T(0);
+#pragma unroll
+      for (int v = 0; v < NV; ++v) acc[v] = {T(0), T(0), T(0)};
+      return T(1);
+    }
+    if (d < dmin) {
+      const T sc = exp_t(-beta * (dmin - d));  // 0 for the first candidate
+      sumz *= sc;
+#pragma unroll
+      for (int v = 0; v < NV; ++v) acc[v] = {acc[v].x * sc, acc[v].y * sc, acc[v].z * sc};
+      dmin = d;
+    }
+    return exp_t(-beta * (d - dmin));
+  }
+  __device__ __forceinline__ void add(T z, int v, const vec3<T>& x) {
+    acc[v] = {acc[v].x + z * x.x, acc[v].y + z * x.y, acc[v].z + z * x.z};
+  }
+  __device__ __forceinline__ T aggregate(T beta, bool hard) const { return hard ? dmin : dmin - log_t(sumz) / beta; }
+  // the weight-normalised sums (the soft-min gradient weights z / sum z)
+  __device__ __forceinline__ void normalise() {
+    const T inv = div_t(T(1), sumz);
+#pragma unroll
+    for (int v = 0; v < NV; ++v) acc[v] = {acc[v].x * inv, acc[v].y * inv, acc[v].z * inv};
+  }
+};
+
 // Obstacle tables: CollisionParams (kernel parameter) or a per-problem copy in
 // shared memory (trajectories) -- any type with okind/oa/ob/orad members.
 template <typename T>
@@ -283,49 +326,28 @@ __device__ __forceinline__ typename G::T col_rows(const ChainParams<typename G::
             continue;
           }
         }
-        // one pass, online soft minimum: rescale the running sums whenever
-        // the minimum drops (same value as costs.py:409-420's two passes)
         const bool hard = P.hard || nsph == 1;
-        T dmin = inf_t<T>(), sumz = T(0);
-        vec3<T> M{T(0), T(0), T(0)}, Gv{T(0), T(0), T(0)};
+        SoftMin<T, 2> sm;  // acc[0] = sum z c x n, acc[1] = sum z n
         for (int s = 0; s < nsph; ++s) {
           const vec3<T> c{L.cen(f + s, 0), L.cen(f + s, 1), L.cen(f + s, 2)};
           vec3<T> n;
           const T d = sphere_obstacle_t<T>(O, o, c, P.sr[f + s], n);
-          T z;
-          if (hard) {  // argmin, first on ties
-            if (!(d < dmin)) continue;
-            dmin = d;
-            z = T(1);
-            sumz = T(0);
-            M = Gv = vec3<T>{T(0), T(0), T(0)};
-          } else {
-            if (d < dmin) {
-              const T sc = exp_t(-P.beta * (dmin - d));  // 0 on the first sphere
-              sumz *= sc;
-              M = {M.x * sc, M.y * sc, M.z * sc};
-              Gv = {Gv.x * sc, Gv.y * sc, Gv.z * sc};
-              dmin = d;
-            }
-            z = exp_t(-P.beta * (d - dmin));
-          }
-          sumz += z;
+          const T z = sm.weight(d, P.beta, hard);
+          if (z == T(0)) continue;  // zero weights add nothing (the reference skips them, costs.py:541)
+          sm.sumz += z;
           if (JAC) {
-            const vec3<T> cn = cross(c, n);
-            M = {M.x + z * cn.x, M.y + z * cn.y, M.z + z * cn.z};
-            Gv = {Gv.x + z * n.x, Gv.y + z * n.y, Gv.z + z * n.z};
+            sm.add(z, 0, cross(c, n));
+            sm.add(z, 1, n);
           }
         }
-        const T dagg = hard ? dmin : dmin - log_t(sumz) / P.beta;
         T act, dact;
-        activation_t(dagg, P.eta_world, act, dact);
+        activation_t(sm.aggregate(P.beta, hard), P.eta_world, act, dact);
         const T res = P.w_world * act;
         cost += res * res;
         if (row_out) row_out[row] = double(res);
         if (JAC && dact != T(0)) {
-          const T inv = div_t(T(1), sumz);
-          M = {M.x * inv, M.y * inv, M.z * inv};
-          Gv = {Gv.x * inv, Gv.y * inv, Gv.z * inv};
+          sm.normalise();
+          const vec3<T> M = sm.acc[0], Gv = sm.acc[1];
           col_row_accumulate<G>(C, L, P.lslot[li], M, -1, M, Gv, P.w_world * dact, res, A, g);
           if (jac_out) {  // parity output: recompute the row entries
             T Az[Tri<NQ>::size], gz[NQ];
@@ -361,8 +383,7 @@ __device__ __forceinline__ typename G::T col_rows(const ChainParams<typename G::
         }
       }
       const bool hard = P.hard || na * nb == 1;
-      T dmin = inf_t<T>(), sumz = T(0);
-      vec3<T> Ma{T(0), T(0), T(0)}, Mb{T(0), T(0), T(0)}, Gv{T(0), T(0), T(0)};
+      SoftMin<T, 3> sm;  // acc[0] = sum z ca x n, acc[1] = sum z cb x n, acc[2] = sum z n
       for (int i = 0; i < na; ++i)
         for (int j = 0; j < nb; ++j) {
           const vec3<T> ca{L.cen(fa + i, 0), L.cen(fa + i, 1), L.cen(fa + i, 2)};
@@ -370,45 +391,24 @@ __device__ __forceinline__ typename G::T col_rows(const ChainParams<typename G::
           const vec3<T> v{ca.x - cb.x, ca.y - cb.y, ca.z - cb.z};
           T dist, inv;
           norm_inv_t(dot(v, v), dist, inv);
-          const T d = dist - P.sr[fa + i] - P.sr[fb + j];
-          T z;
-          if (hard) {
-            if (!(d < dmin)) continue;
-            dmin = d;
-            z = T(1);
-            sumz = T(0);
-            Ma = Mb = Gv = vec3<T>{T(0), T(0), T(0)};
-          } else {
-            if (d < dmin) {
-              const T sc = exp_t(-P.beta * (dmin - d));
-              sumz *= sc;
-              Ma = {Ma.x * sc, Ma.y * sc, Ma.z * sc};
-              Mb = {Mb.x * sc, Mb.y * sc, Mb.z * sc};
-              Gv = {Gv.x * sc, Gv.y * sc, Gv.z * sc};
-              dmin = d;
-            }
-            z = exp_t(-P.beta * (d - dmin));
-          }
-          sumz += z;
+          const T z = sm.weight(dist - P.sr[fa + i] - P.sr[fb + j], P.beta, hard);
+          if (z == T(0)) continue;
+          sm.sumz += z;
           if (JAC && dist > T(1e-12)) {
             const vec3<T> n{v.x * inv, v.y * inv, v.z * inv};
-            const vec3<T> xa = cross(ca, n), xb = cross(cb, n);
-            Ma = {Ma.x + z * xa.x, Ma.y + z * xa.y, Ma.z + z * xa.z};
-            Mb = {Mb.x + z * xb.x, Mb.y + z * xb.y, Mb.z + z * xb.z};
-            Gv = {Gv.x + z * n.x, Gv.y + z * n.y, Gv.z + z * n.z};
+            sm.add(z, 0, cross(ca, n));
+            sm.add(z, 1, cross(cb, n));
+            sm.add(z, 2, n);
           }
         }
-      const T dagg = hard ? dmin : dmin - log_t(sumz) / P.beta;
       T act, dact;
-      activation_t(dagg, P.eta_self, act, dact);
+      activation_t(sm.aggregate(P.beta, hard), P.eta_self, act, dact);
       const T res = P.w_self * act;
       cost += res * res;
       if (row_out) row_out[row] = double(res);
       if (JAC && dact != T(0)) {
-        const T inv = div_t(T(1), sumz);
-        Ma = {Ma.x * inv, Ma.y * inv, Ma.z * inv};
-        Mb = {Mb.x * inv, Mb.y * inv, Mb.z * inv};
-        Gv = {Gv.x * inv, Gv.y * inv, Gv.z * inv};
+        sm.normalise();
+        const vec3<T> Ma = sm.acc[0], Mb = sm.acc[1], Gv = sm.acc[2];
         col_row_accumulate<G>(C, L, P.lslot[la], Ma, P.lslot[lb], Mb, Gv, P.w_self * dact, res, A, g);
         if (jac_out) {
           T Az[Tri<NQ>::size], gz[NQ];

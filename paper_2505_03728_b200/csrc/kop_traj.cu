@@ -353,54 +353,30 @@ __device__ typename G::T traj_eval(const ChainParams<typename G::T, G::K>& C, co
           }
           if (__all_sync(__activemask(), dscr - P.lreach[li] > W.eta_world * T(1.00001))) continue;
         }
-        // one pass, online soft minimum (costs.py:409-420)
         const bool hard = P.hard || nsph == 1;
-        T dmin = inf_t<T>(), sumz = T(0);
-        vec3<T> M0{T(0), T(0), T(0)}, G0{T(0), T(0), T(0)}, M1{T(0), T(0), T(0)}, G1{T(0), T(0), T(0)};
+        SoftMin<T, 4> sm;  // sum z c0 x ga, sum z ga, sum z c1 x gb, sum z gb
         for (int s = 0; s < nsph; ++s) {
           const vec3<T> c0{L0.cen(f + s, 0), L0.cen(f + s, 1), L0.cen(f + s, 2)};
           const vec3<T> c1{L1.cen(f + s, 0), L1.cen(f + s, 1), L1.cen(f + s, 2)};
           vec3<T> ga, gb;
           const T d = capsule_obstacle_t<T>(*S.obs, o, c0, c1, P.sr[f + s], ga, gb);
-          T z;
-          if (hard) {
-            if (!(d < dmin)) continue;
-            dmin = d;
-            z = T(1);
-            sumz = T(0);
-            M0 = G0 = M1 = G1 = vec3<T>{T(0), T(0), T(0)};
-          } else {
-            if (d < dmin) {
-              const T sc = exp_t(-P.beta * (dmin - d));
-              sumz *= sc;
-              M0 = {M0.x * sc, M0.y * sc, M0.z * sc};
-              G0 = {G0.x * sc, G0.y * sc, G0.z * sc};
-              M1 = {M1.x * sc, M1.y * sc, M1.z * sc};
-              G1 = {G1.x * sc, G1.y * sc, G1.z * sc};
-              dmin = d;
-            }
-            z = exp_t(-P.beta * (d - dmin));
-          }
-          sumz += z;
+          const T z = sm.weight(d, P.beta, hard);
+          if (z == T(0)) continue;  // zero weights add nothing (the reference skips them, costs.py:541)
+          sm.sumz += z;
           if (JAC) {
-            const vec3<T> x0 = cross(c0, ga), x1 = cross(c1, gb);
-            M0 = {M0.x + z * x0.x, M0.y + z * x0.y, M0.z + z * x0.z};
-            G0 = {G0.x + z * ga.x, G0.y + z * ga.y, G0.z + z * ga.z};
-            M1 = {M1.x + z * x1.x, M1.y + z * x1.y, M1.z + z * x1.z};
-            G1 = {G1.x + z * gb.x, G1.y + z * gb.y, G1.z + z * gb.z};
+            sm.add(z, 0, cross(c0, ga));
+            sm.add(z, 1, ga);
+            sm.add(z, 2, cross(c1, gb));
+            sm.add(z, 3, gb);
           }
         }
-        const T dagg = hard ? dmin : dmin - log_t(sumz) / P.beta;
         T act, dact;
-        activation_t(dagg, W.eta_world, act, dact);
+        activation_t(sm.aggregate(P.beta, hard), W.eta_world, act, dact);
         const T res = W.w_world * act;
         cost += res * res;
         if (JAC && dact != T(0)) {
-          const T inv = div_t(T(1), sumz);
-          M0 = {M0.x * inv, M0.y * inv, M0.z * inv};
-          G0 = {G0.x * inv, G0.y * inv, G0.z * inv};
-          M1 = {M1.x * inv, M1.y * inv, M1.z * inv};
-          G1 = {G1.x * inv, G1.y * inv, G1.z * inv};
+          sm.normalise();
+          const vec3<T> M0 = sm.acc[0], G0 = sm.acc[1], M1 = sm.acc[2], G1 = sm.acc[3];
           T j0[NQ], j1[NQ];
           col_row_entries<G>(C, L0, P.lslot[li], M0, G0, W.w_world * dact, j0);
           col_row_entries<G>(C, L1, P.lslot[li], M1, G1, W.w_world * dact, j1);
