@@ -116,6 +116,14 @@ int kop_fk(const KopModel* model, int32_t precision, const double* q, int64_t ba
            double* link_wxyz, double* link_xyz, double* joint_xyz, double* joint_axis,
            void* stream);
 
+/* replaces: robot.link_jacobian / point_jacobian (robot.py:461-506): the
+ * geometric Jacobian of `link` at q [B*n] (device).  points: device [B*3]
+ * world points rigidly attached to the link, or NULL for the link origin;
+ * rotational != 0 adds the angular rows.  jac: device [B*rows*n] double,
+ * rows = 6 (rotational) or 3, mimic joints folded into their source column. */
+int kop_jacobian(const KopModel* model, int32_t precision, const double* q, int64_t batch, int32_t link,
+                 const double* points, int32_t rotational, double* jac, void* stream);
+
 /* --- lane engine ----------------------------------------------------------
  * replaces: beam.IkLaneProblem(model, link, target, weights..., use_base,
  * base_reg_weight) with .residuals_and_jacobian (beam.py:133-180),

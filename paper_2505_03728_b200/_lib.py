@@ -104,6 +104,7 @@ SIGNATURES = {
                                             _p, _p, _p]),
     "kop_traj_report": (C.c_int, [_p, _i32, _i32, _p, _p, _i32, _p, _i64, _p, _p, _p, _p, _p, _p, _p]),
     "kop_sample_uniform": (C.c_int, [_u64, _u64, _i64, _i32, _p, _p, _p, _p, _p]),
+    "kop_jacobian": (C.c_int, [_p, _i32, _p, _i64, _i32, _p, _i32, _p, _p]),
     "kop_link_poses": (C.c_int, [_p, _i32, _p, _i64, _p, _p]),
     "kop_fma_peak_kernel": (C.c_int, [_i32, _i32, _i32, _p, C.POINTER(_f64), _p]),
     "kop_dfma_peak_kernel": (C.c_int, [_i32, _i32, _i32, _p, C.POINTER(_f64), _p]),

@@ -82,6 +82,90 @@ cudaError_t launch_fk_tree(const TreeParams& P, int precision, const double* q, 
   return cudaGetLastError();
 }
 
+// Geometric Jacobian (robot.py:461-506): rows 0-2 the world linear velocity of
+// a point rigidly attached to `link` (its origin when points == null), rows
+// 3-5 (rotational) the angular velocity; mimic joints fold into their source
+// column.  FK as k_fk_tree, then one pass over the link's ancestor joints.
+template <typename T>
+__global__ void __launch_bounds__(128)
+k_jacobian_tree(const TreeParams P, const double* __restrict__ q, int64_t B, int link,
+                unsigned long long anc, const double* __restrict__ points, int rotational,
+                double* __restrict__ jac) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  quat<T> lq[kMaxLinks];
+  vec3<T> lp[kMaxLinks], jp[kMaxTreeJoints], ja[kMaxTreeJoints];
+  lq[0] = {T(1), T(0), T(0), T(0)};
+  lp[0] = {T(0), T(0), T(0)};
+  const double* qb = q + b * P.n;
+  for (int j = 0; j < P.nj; ++j) {
+    const quat<T> pq = lq[P.parent[j]];
+    const vec3<T> pp = lp[P.parent[j]];
+    const quat<T> fq = qmul(pq, quat<T>{T(P.oq[j][0]), T(P.oq[j][1]), T(P.oq[j][2]), T(P.oq[j][3])});
+    const vec3<T> o = qrot(pq, vec3<T>{T(P.op[j][0]), T(P.op[j][1]), T(P.op[j][2])});
+    const vec3<T> fp{pp.x + o.x, pp.y + o.y, pp.z + o.z};
+    const vec3<T> axis{T(P.axis[j][0]), T(P.axis[j][1]), T(P.axis[j][2])};
+    const vec3<T> wa = qrot(fq, axis);
+    jp[j] = fp;
+    ja[j] = wa;
+    const int c = P.child[j];
+    if (P.kind[j] == 0) {
+      lq[c] = fq;
+      lp[c] = fp;
+      continue;
+    }
+    const T th = T(qb[P.qcol[j]]) * T(P.mult[j]) + T(P.offset[j]);
+    if (P.kind[j] == 1) {
+      T s, co;
+      sincos_t(T(0.5) * th, &s, &co);
+      lq[c] = qmul(fq, quat<T>{co, s * axis.x, s * axis.y, s * axis.z});
+      lp[c] = fp;
+    } else {
+      lq[c] = fq;
+      lp[c] = {fp.x + th * wa.x, fp.y + th * wa.y, fp.z + th * wa.z};
+    }
+  }
+  const vec3<T> pt = points ? vec3<T>{T(points[b * 3]), T(points[b * 3 + 1]), T(points[b * 3 + 2])} : lp[link];
+  const int rows = rotational ? 6 : 3;
+  double* J = jac + b * rows * P.n;
+  for (int i = 0; i < rows * P.n; ++i) J[i] = 0.0;
+  for (int j = 0; j < P.nj; ++j) {
+    if (!((anc >> j) & 1ull) || P.kind[j] == 0) continue;
+    const int col = P.qcol[j];
+    const T mu = T(P.mult[j]);
+    const vec3<T> a = ja[j];
+    if (P.kind[j] == 1) {
+      const vec3<T> lever{pt.x - jp[j].x, pt.y - jp[j].y, pt.z - jp[j].z};
+      const vec3<T> v = cross(a, lever);
+      J[0 * P.n + col] += double(mu * v.x);
+      J[1 * P.n + col] += double(mu * v.y);
+      J[2 * P.n + col] += double(mu * v.z);
+      if (rotational) {
+        J[3 * P.n + col] += double(mu * a.x);
+        J[4 * P.n + col] += double(mu * a.y);
+        J[5 * P.n + col] += double(mu * a.z);
+      }
+    } else {
+      J[0 * P.n + col] += double(mu * a.x);
+      J[1 * P.n + col] += double(mu * a.y);
+      J[2 * P.n + col] += double(mu * a.z);
+    }
+  }
+}
+
+cudaError_t launch_jacobian_tree(const TreeParams& P, int precision, const double* q, int64_t B, int link,
+                                 unsigned long long anc, const double* points, int rotational, double* jac,
+                                 cudaStream_t st) {
+  if (B == 0) return cudaSuccess;
+  const int tpb = 128;
+  const unsigned blocks = (unsigned)((B + tpb - 1) / tpb);
+  if (precision == 0)
+    k_jacobian_tree<float><<<blocks, tpb, 0, st>>>(P, q, B, link, anc, points, rotational, jac);
+  else
+    k_jacobian_tree<double><<<blocks, tpb, 0, st>>>(P, q, B, link, anc, points, rotational, jac);
+  return cudaGetLastError();
+}
+
 // ---------------------------------------------------------------------------
 // FK of one link along its root path (joints of `path` are consecutive:
 // each joint's parent is the previous joint's child), canonicalised like

@@ -472,6 +472,17 @@ int kop_fk(const KopModel* m, int32_t precision, const double* q, int64_t batch,
   return cuda_status(launch_fk_tree(m->tree, precision, q, batch, lq, lp, jp, ja, (cudaStream_t)stream));
 }
 
+int kop_jacobian(const KopModel* m, int32_t precision, const double* q, int64_t batch, int32_t link,
+                 const double* points, int32_t rotational, double* jac, void* stream) {
+  if (!m || batch < 0 || (batch > 0 && (!q || !jac))) return fail(KOP_EINVAL, "invalid Jacobian arguments");
+  if (precision != KOP_FP32 && precision != KOP_FP64) return fail(KOP_EINVAL, "bad precision");
+  if (link < 0 || link >= m->tree.nl) return fail(KOP_EINVAL, "unknown link index");
+  unsigned long long anc = 0;  // joints on the root -> link path
+  for (int j = m->parent_joint[link]; j >= 0; j = m->parent_joint[m->tree.parent[j]]) anc |= 1ull << j;
+  return cuda_status(launch_jacobian_tree(m->tree, precision, q, batch, link, anc, points, rotational ? 1 : 0, jac,
+                                          (cudaStream_t)stream));
+}
+
 int kop_link_poses(const KopModel* m, int32_t link, const double* q, int64_t count, double* poses,
                    void* stream) {
   if (!m || count < 0 || link < 0 || link >= m->tree.nl) return fail(KOP_EINVAL, "invalid arguments");

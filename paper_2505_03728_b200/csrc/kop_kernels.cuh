@@ -110,6 +110,9 @@ cudaError_t launch_link_pose(const TreeParams& path, const double* q, int64_t B,
                              cudaStream_t st);
 cudaError_t launch_philox(uint64_t key0, uint64_t key1_base, int64_t count, int n, const double* lo,
                           const double* range, const uint8_t* negate, double* out, cudaStream_t st);
+cudaError_t launch_jacobian_tree(const TreeParams& P, int precision, const double* q, int64_t B, int link,
+                                 unsigned long long anc, const double* points, int rotational, double* jac,
+                                 cudaStream_t st);
 cudaError_t launch_fma_peak(int blocks, int threads, int iters, float* sink, cudaStream_t st);
 cudaError_t launch_dfma_peak(int blocks, int threads, int iters, double* sink, cudaStream_t st);
 

@@ -379,3 +379,23 @@ def test_host_pipeline_equals_device_run(models, name, link, base):
     s.solve_host(pinned, out)
     torch.cuda.synchronize()
     assert np.array_equal(out.q.numpy(), ref.q) and np.array_equal(out.success.numpy(), ref.success)
+
+
+@pytest.mark.parametrize("name", ["arm7", "arm7_gripper", "planar_2r"])
+def test_link_and_point_jacobians_match_oracle(models, chains, name):
+    """robot.link_jacobian / point_jacobian on the device vs the oracle's
+    restatement of robot.py:461-506 (mimic and prismatic joints included)."""
+    m, ch = models[name], chains[name]
+    rng = np.random.default_rng(11)
+    lo = np.where(np.isfinite(ch.lower), ch.lower, -np.pi)
+    hi = np.where(np.isfinite(ch.upper), ch.upper, np.pi)
+    q = rng.uniform(lo, hi, (16, ch.n))
+    lq, lp, jp, ja = o.fk(ch, q)
+    for link in m.link_names[1:]:
+        li = m.link_index(link)
+        ref = o.point_jacobian(ch, lp[:, li], jp, ja, li, rotational=True)
+        np.testing.assert_allclose(k.link_jacobian(m, q, link), ref, rtol=0, atol=1e-12)
+        pts = lp[:, li] + rng.normal(size=(16, 3)) * 0.1
+        ref_p = o.point_jacobian(ch, pts, jp, ja, li, rotational=False)
+        np.testing.assert_allclose(k.point_jacobian(m, q, link, pts), ref_p, rtol=0, atol=1e-12)
+    assert k.link_jacobian(m, q[0], m.link_names[-1]).shape == (6, ch.n)
