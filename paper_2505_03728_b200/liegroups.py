@@ -83,6 +83,150 @@ def _hat(v):
     return np.array([[0.0, -v[2], v[1]], [v[2], 0.0, -v[0]], [-v[1], v[0], 0.0]])
 
 
+def skew(v) -> np.ndarray:
+    """[v]x over the last axis: (..., 3) -> (..., 3, 3)."""
+    v = np.asarray(v, dtype=float)
+    z = np.zeros(v.shape[:-1])
+    return np.stack([np.stack([z, -v[..., 2], v[..., 1]], -1), np.stack([v[..., 2], z, -v[..., 0]], -1),
+                     np.stack([-v[..., 1], v[..., 0], z], -1)], -2)
+
+
+def quat_from_matrix(m) -> np.ndarray:
+    """Rotation matrix (..., 3, 3) -> canonical quaternion (..., 4) (Shepperd's
+    method: the largest of w, x, y, z is recovered from the trace first)."""
+    m = np.asarray(m, dtype=float)
+    tr = m[..., 0, 0] + m[..., 1, 1] + m[..., 2, 2]
+    cand = np.stack([tr, m[..., 0, 0], m[..., 1, 1], m[..., 2, 2]], -1)
+    k = np.argmax(cand, axis=-1)
+    out = np.empty(m.shape[:-2] + (4,))
+    r = lambda i, j: m[..., i, j]
+    s0 = np.sqrt(np.maximum(1.0 + tr, 0.0)) * 2.0
+    s1 = np.sqrt(np.maximum(1.0 + r(0, 0) - r(1, 1) - r(2, 2), 0.0)) * 2.0
+    s2 = np.sqrt(np.maximum(1.0 - r(0, 0) + r(1, 1) - r(2, 2), 0.0)) * 2.0
+    s3 = np.sqrt(np.maximum(1.0 - r(0, 0) - r(1, 1) + r(2, 2), 0.0)) * 2.0
+    safe = lambda x: np.where(x == 0.0, 1.0, x)
+    q0 = np.stack([0.25 * s0, (r(2, 1) - r(1, 2)) / safe(s0), (r(0, 2) - r(2, 0)) / safe(s0),
+                   (r(1, 0) - r(0, 1)) / safe(s0)], -1)
+    q1 = np.stack([(r(2, 1) - r(1, 2)) / safe(s1), 0.25 * s1, (r(0, 1) + r(1, 0)) / safe(s1),
+                   (r(0, 2) + r(2, 0)) / safe(s1)], -1)
+    q2 = np.stack([(r(0, 2) - r(2, 0)) / safe(s2), (r(0, 1) + r(1, 0)) / safe(s2), 0.25 * s2,
+                   (r(1, 2) + r(2, 1)) / safe(s2)], -1)
+    q3 = np.stack([(r(1, 0) - r(0, 1)) / safe(s3), (r(0, 2) + r(2, 0)) / safe(s3), (r(1, 2) + r(2, 1)) / safe(s3),
+                   0.25 * s3], -1)
+    out = np.where((k == 0)[..., None], q0, np.where((k == 1)[..., None], q1, np.where((k == 2)[..., None], q2, q3)))
+    return quat_normalize_canonical(out)
+
+
+def _jl_coeffs(th):
+    """(1 - cos th) / th^2, (th - sin th) / th^3 with series below 1e-3 rad."""
+    small = th < 1e-3
+    t = np.where(small, 1.0, th)
+    t2 = th * th
+    a = np.where(small, 0.5 - t2 / 24.0 + t2 * t2 / 720.0, (1.0 - np.cos(t)) / (t * t))
+    b = np.where(small, 1.0 / 6.0 - t2 / 120.0 + t2 * t2 / 5040.0, (t - np.sin(t)) / t ** 3)
+    return a, b
+
+
+def so3_left_jacobian(omega) -> np.ndarray:
+    """Jl(omega) = I + a [w]x + b [w]x^2, (..., 3) -> (..., 3, 3)."""
+    omega = np.asarray(omega, dtype=float)
+    th = np.linalg.norm(omega, axis=-1)[..., None, None]
+    k = skew(omega)
+    a, b = _jl_coeffs(th)
+    return np.eye(3) + a * k + b * (k @ k)
+
+
+def so3_left_jacobian_inv(omega) -> np.ndarray:
+    """Jl(omega)^-1 = I - [w]x / 2 + c [w]x^2, c = (1 - (th/2) cot(th/2)) / th^2."""
+    omega = np.asarray(omega, dtype=float)
+    th = np.linalg.norm(omega, axis=-1)[..., None, None]
+    k = skew(omega)
+    small = th < 1e-3
+    t = np.where(small, 1.0, th)
+    h = 0.5 * t
+    c = np.where(small, 1.0 / 12.0 + th * th / 720.0, (1.0 - h * np.cos(h) / np.sin(h)) / (t * t))
+    return np.eye(3) - 0.5 * k + c * (k @ k)
+
+
+def se3_exp_arrays(xi):
+    """Translation-first twist (..., 6) -> (quaternion (..., 4), translation (..., 3))."""
+    xi = np.asarray(xi, dtype=float)
+    return quat_exp(xi[..., 3:]), np.einsum("...ij,...j->...i", so3_left_jacobian(xi[..., 3:]), xi[..., :3])
+
+
+def se3_log_arrays(q, t) -> np.ndarray:
+    """(quaternion, translation) -> translation-first twist (..., 6)."""
+    phi = quat_log(q)
+    rho = np.einsum("...ij,...j->...i", so3_left_jacobian_inv(phi), np.asarray(t, dtype=float))
+    return np.concatenate([rho, phi], axis=-1)
+
+
+def _se3_q(rho, phi):
+    """Barfoot's Q(rho, phi) block of the SE(3) left Jacobian, series below 1e-2 rad."""
+    th = np.linalg.norm(phi, axis=-1)[..., None, None]
+    P, R = skew(phi), skew(rho)
+    small = th < 1e-2
+    t = np.where(small, 1.0, th)
+    t2 = th * th
+    c1 = np.where(small, 1 / 6 - t2 / 120 + t2 * t2 / 5040, (t - np.sin(t)) / t ** 3)
+    c2 = np.where(small, 1 / 24 - t2 / 720 + t2 * t2 / 40320, (0.5 * t * t + np.cos(t) - 1.0) / t ** 4)
+    c3 = np.where(small, 1 / 120 - t2 / 2520 + t2 * t2 / 120960, (2 * t - 3 * np.sin(t) + t * np.cos(t)) / (2 * t ** 5))
+    PR, RP, PRP = P @ R, R @ P, P @ R @ P
+    return 0.5 * R + c1 * (PR + RP + PRP) + c2 * (P @ P @ R + R @ P @ P - 3.0 * PRP) + c3 * (PRP @ P + P @ PRP)
+
+
+def se3_left_jacobian_inv(xi) -> np.ndarray:
+    """SE(3) left Jacobian inverse [[A, -A Q A], [0, A]], A = Jl^-1(phi) (..., 6, 6)."""
+    xi = np.asarray(xi, dtype=float)
+    a = so3_left_jacobian_inv(xi[..., 3:])
+    out = np.zeros(xi.shape[:-1] + (6, 6))
+    out[..., :3, :3] = a
+    out[..., 3:, 3:] = a
+    out[..., :3, 3:] = -a @ _se3_q(xi[..., :3], xi[..., 3:]) @ a
+    return out
+
+
+def se3_right_jacobian_inv(xi) -> np.ndarray:
+    """Jr^-1(xi) = Jl^-1(-xi)."""
+    return se3_left_jacobian_inv(-np.asarray(xi, dtype=float))
+
+
+def se3_adjoint(q, t) -> np.ndarray:
+    """Adjoint of (q, t) on translation-first twists: [[R, [t]x R], [0, R]]."""
+    r = quat_to_matrix(q)
+    out = np.zeros(r.shape[:-2] + (6, 6))
+    out[..., :3, :3] = r
+    out[..., 3:, 3:] = r
+    out[..., :3, 3:] = skew(t) @ r
+    return out
+
+
+def se2_exp_arrays(delta):
+    """SE(2) tangent (vx, vy, w) (..., 3) -> (angle (...), translation (..., 2))."""
+    delta = np.asarray(delta, dtype=float)
+    w = delta[..., 2]
+    small = np.abs(w) < 1e-7
+    ws = np.where(small, 1.0, w)
+    s = np.where(small, 1.0 - w * w / 6.0, np.sin(ws) / ws)
+    c = np.where(small, 0.5 * w, (1.0 - np.cos(ws)) / ws)
+    vx, vy = delta[..., 0], delta[..., 1]
+    return w, np.stack([s * vx - c * vy, c * vx + s * vy], -1)
+
+
+def se2_log_arrays(angle, t) -> np.ndarray:
+    """Inverse of se2_exp_arrays: (angle, translation) -> (vx, vy, w)."""
+    w = np.asarray(angle, dtype=float)
+    t = np.asarray(t, dtype=float)
+    small = np.abs(w) < 1e-7
+    ws = np.where(small, 1.0, w)
+    s = np.where(small, 1.0 - w * w / 6.0, np.sin(ws) / ws)
+    c = np.where(small, 0.5 * w, (1.0 - np.cos(ws)) / ws)
+    det = s * s + c * c
+    vx = (s * t[..., 0] + c * t[..., 1]) / det
+    vy = (-c * t[..., 0] + s * t[..., 1]) / det
+    return np.stack([vx, vy, w], -1)
+
+
 def _jl(omega):
     th = float(np.linalg.norm(omega))
     k = _hat(omega)
@@ -130,6 +274,10 @@ class Rotation3:
     @staticmethod
     def exp(omega) -> "Rotation3":
         return Rotation3(quat_exp(np.asarray(omega, float).reshape(3)))
+
+    @staticmethod
+    def from_matrix(m) -> "Rotation3":
+        return Rotation3(quat_from_matrix(m))
 
     def log(self) -> np.ndarray:
         return quat_log(self.wxyz)
@@ -229,6 +377,14 @@ class Transform2:
     def apply(self, p) -> np.ndarray:
         return rot2(self.angle) @ np.asarray(p, float) + self.translation
 
+    @staticmethod
+    def exp(delta) -> "Transform2":
+        ang, t = se2_exp_arrays(np.asarray(delta, dtype=float).reshape(3))
+        return Transform2(float(ang), t)
+
+    def log(self) -> np.ndarray:
+        return se2_log_arrays(self.angle, self.translation)
+
     def to_transform3(self) -> Transform3:
         return Transform3(Rotation3.exp([0.0, 0.0, self.angle]),
                           np.array([self.translation[0], self.translation[1], 0.0]))
@@ -256,3 +412,27 @@ def so3_log(r: Rotation3) -> np.ndarray:
 
 def so3_exp(omega) -> Rotation3:
     return Rotation3.exp(omega)
+
+
+def apply(a, p) -> np.ndarray:
+    return a.apply(p)
+
+
+def interpolate(a: Transform3, b: Transform3, alpha: float) -> Transform3:
+    """a * exp(alpha * log(a^-1 b)): the constant-twist path from a to b."""
+    return a.compose(Transform3.exp(float(alpha) * a.inverse().compose(b).log()))
+
+
+def tangent_dim(x) -> int:
+    if isinstance(x, Transform3):
+        return 6
+    if isinstance(x, (Transform2, Rotation3)):
+        return 3
+    return int(np.asarray(x).size)
+
+
+def local_update(x, delta):
+    """Right-multiplicative retraction x * exp(delta) (vector spaces: x + delta)."""
+    if isinstance(x, (Transform3, Transform2, Rotation3)):
+        return x.compose(type(x).exp(delta))
+    return np.asarray(x, dtype=float) + np.asarray(delta, dtype=float)

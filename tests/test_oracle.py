@@ -227,3 +227,26 @@ def test_capsule_obstacle_kinds():
     np.testing.assert_allclose(d, [0.4])
     np.testing.assert_allclose(ga, [[1, 0, 0]])
     np.testing.assert_allclose(gb, [[0, 0, 0]])
+
+
+def test_host_collision_distance_helpers_match_oracle():
+    """collision.sphere_obstacle_distance / capsule_obstacle_distance (host API
+    helpers) vs the oracle's restatement of collision.py:192-237."""
+    import paper_2505_03728_b200 as k
+
+    rng = np.random.default_rng(8)
+    obs = [(k.Sphere([0.3, 0.1, 0.2], 0.1), co.sphere([0.3, 0.1, 0.2], 0.1)),
+           (k.Capsule([-0.2, 0.0, 0.1], [0.4, 0.3, 0.5], 0.05), co.capsule([-0.2, 0.0, 0.1], [0.4, 0.3, 0.5], 0.05)),
+           (k.HalfSpace([0.0, 0.2, 1.0], -0.1), co.halfspace([0.0, 0.2, 1.0], -0.1))]
+    for _ in range(20):
+        c0, c1, r = rng.normal(size=3) * 0.4, rng.normal(size=3) * 0.4, 0.07
+        for ob, ob_o in obs:
+            d, g = k.collision.sphere_obstacle_distance(c0, r, ob)
+            d_o, g_o = co.sphere_obstacle(c0[None], np.array([r]), ob_o)
+            np.testing.assert_allclose(d, d_o[0], atol=1e-14)
+            np.testing.assert_allclose(g, g_o[0], atol=1e-14)
+            d, ga, gb = k.collision.capsule_obstacle_distance(c0, c1, r, ob)
+            d_o, ga_o, gb_o = to.capsule_obstacle(c0[None], c1[None], r, ob_o)
+            np.testing.assert_allclose([d], d_o, atol=1e-14)
+            np.testing.assert_allclose(ga, ga_o[0], atol=1e-14)
+            np.testing.assert_allclose(gb, gb_o[0], atol=1e-14)
