@@ -92,6 +92,23 @@ class VariableSet:
     def values(self, var_ids) -> list:
         return [self._values[self.index(v)] for v in var_ids]
 
+    def tangent_slice(self, var_id: str) -> slice:
+        i = self.index(var_id)
+        return slice(self.tangent_offsets[i], self.tangent_offsets[i + 1])
+
+    def updated(self, delta) -> "VariableSet":
+        """A copy with the stacked tangent step applied through each variable's
+        retraction (solver.py:91-102)."""
+        from .liegroups import local_update
+
+        delta = np.asarray(delta, dtype=float)
+        if delta.shape != (self.tangent_dim,):
+            raise ValueError(f"tangent step has shape {delta.shape}, expected ({self.tangent_dim},)")
+        out = VariableSet()
+        for i, (vid, value) in enumerate(zip(self._ids, self._values)):
+            out.add(vid, local_update(value, delta[self.tangent_offsets[i]:self.tangent_offsets[i + 1]]))
+        return out
+
     def copy(self) -> "VariableSet":
         out = VariableSet()
         for vid, v in zip(self._ids, self._values):
@@ -139,6 +156,10 @@ class Problem:
     @property
     def residual_dim(self) -> int:
         return sum(c.residual_dim for c in self.costs)
+
+    def sparsity(self) -> list:
+        """Structurally nonzero (cost index, variable index) blocks (solver.py:166-172)."""
+        return [(ci, self.variables.index(ref)) for ci, cost in enumerate(self.costs) for ref in cost.variable_refs]
 
 
 @dataclass

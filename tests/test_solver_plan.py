@@ -61,3 +61,15 @@ def test_trajectory_builders_validate(arm7):
         k.velocity_limit_cost(arm7, "a", "b", 0.0)
     with pytest.raises(ValueError, match="no \\(link, obstacle\\)"):
         k.swept_collision_cost(arm7, "a", "b", k.WorldModel())
+
+
+def test_variable_bookkeeping(arm7):
+    vs = k.VariableSet.of(q=np.zeros(3), base=k.Transform2.identity(), pose=k.Transform3.identity())
+    assert vs.tangent_slice("base") == slice(3, 6) and vs.tangent_slice("pose") == slice(6, 12)
+    up = vs.updated(np.concatenate([[1.0, 2.0, 3.0], [0.1, 0.2, 0.3], np.zeros(6)]))
+    np.testing.assert_allclose(up.value("q"), [1, 2, 3])
+    np.testing.assert_allclose(up.value("base").log(), [0.1, 0.2, 0.3], atol=1e-12)
+    with pytest.raises(ValueError):
+        vs.updated(np.zeros(5))
+    pr = k.trajectory_problem(arm7, arm7.rest_pose, arm7.rest_pose, 6, 0.1)
+    assert pr.sparsity()[:3] == [(0, 0), (1, 5), (2, 0)]
