@@ -538,21 +538,24 @@ template <class G, int STRIDE, class M>
 __device__ __forceinline__ void lm_iter(const M& model, LaneState<G>& s, int mode) {
   using T = typename G::T;
   constexpr int NQ = G::NQ, ND = G::ND;
+  // A failed pivot (<= 0, or NaN input) poisons the step with inf / NaN, so the
+  // candidate's cost is non-finite and the step is rejected with damping x10
+  // -- the outcome of the reference's LinAlgError branch (beam.py:209-213) --
+  // without tracking a flag through the factorisation.
   T d[ND];
-  bool ok = true;
   if (mode == 0) {
     T A[Tri<ND>::size], g[ND];
     load_normal<STRIDE>(s, A, g);
-    ok = damped_solve<T, ND>(A, g, s.lam, d);
+    (void)damped_solve<T, ND>(A, g, s.lam, d);
   } else {
 #pragma unroll
     for (int i = 0; i < ND; ++i) d[i] = T(0);
   }
   T qn[NQ], bn[3];
 #pragma unroll
-  for (int i = 0; i < NQ; ++i) qn[i] = s.q[i] + (ok ? d[i] : T(0));
+  for (int i = 0; i < NQ; ++i) qn[i] = s.q[i] + d[i];
   if (G::BASE) {
-    if (mode == 0 && ok) {
+    if (mode == 0) {
       base_retract(s.base, d[NQ], d[NQ + 1], d[NQ + 2], bn);
     } else {
       bn[0] = s.base[0]; bn[1] = s.base[1]; bn[2] = s.base[2];
@@ -561,7 +564,7 @@ __device__ __forceinline__ void lm_iter(const M& model, LaneState<G>& s, int mod
   T An[Tri<ND>::size], gn[ND];
   const T raw = model.template eval<true>(qn, bn, An, gn);
   const T cn = finite_t(raw) ? raw : inf_t<T>();
-  const bool acc = mode != 0 || (ok && (cn < s.cost));
+  const bool acc = mode != 0 || cn < s.cost;
   if (acc) store_normal<STRIDE>(s, An, gn);  // one store site for start and accept
   if (mode != 0) {
     if (mode == 1) s.cost = raw;  // start_state keeps a non-finite cost as is
