@@ -44,6 +44,43 @@ struct TreeScratch {
   };
 };
 
+// Per-joint / per-column tables staged in shared memory once per CTA: lanes
+// index them by different joints, which the constant bank would serialise.
+template <typename T>
+struct TreeTable {
+  T oq[kTreeMaxJoints][4], op[kTreeMaxJoints][3], axis[kTreeMaxJoints][3];
+  T mult[kTreeMaxJoints], offset[kTreeMaxJoints];
+  T lower[kTreeMaxDofs], upper[kTreeMaxDofs], rest[kTreeMaxDofs];
+  int32_t parent[kTreeMaxJoints], kind[kTreeMaxJoints], qcol[kTreeMaxJoints];
+  int32_t col_nj[kTreeMaxDofs];
+  int8_t lev_joint[kTreeMaxJoints];
+  int8_t col_joint[kTreeMaxDofs][kTreeMaxPerCol];
+};
+
+template <typename T>
+__device__ __forceinline__ void stage_tree_table(const TreeLmParams<T>& P, TreeTable<T>& Q) {
+  for (int j = threadIdx.x; j < P.nj; j += blockDim.x) {
+    for (int i = 0; i < 4; ++i) Q.oq[j][i] = P.oq[j][i];
+    for (int i = 0; i < 3; ++i) {
+      Q.op[j][i] = P.op[j][i];
+      Q.axis[j][i] = P.axis[j][i];
+    }
+    Q.mult[j] = P.mult[j];
+    Q.offset[j] = P.offset[j];
+    Q.parent[j] = P.parent_joint[j];
+    Q.kind[j] = P.kind[j];
+    Q.qcol[j] = P.qcol[j];
+    Q.lev_joint[j] = P.lev_joint[j];
+  }
+  for (int c = threadIdx.x; c < P.n; c += blockDim.x) {
+    Q.lower[c] = P.lower[c];
+    Q.upper[c] = P.upper[c];
+    Q.rest[c] = P.rest[c];
+    Q.col_nj[c] = P.col_nj[c];
+    for (int i = 0; i < kTreeMaxPerCol; ++i) Q.col_joint[c][i] = P.col_joint[c][i];
+  }
+}
+
 __device__ __forceinline__ float shfl_t(float v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 __device__ __forceinline__ double shfl_t(double v, int src) { return __shfl_sync(0xffffffffu, v, src); }
 
@@ -63,33 +100,34 @@ __device__ __forceinline__ T warp_max(T v) {
 // Evaluate the stack at S.q (or S.qn when cand): returns the cost (all lanes);
 // JAC also forms A (S.A, stride 33) and g (register, lane i = g_i).
 template <typename T, int NE, bool JAC>
-__device__ __forceinline__ T tree_eval(const TreeLmParams<T>& P, const double* __restrict__ targets,
-                                       TreeScratch<T, NE>& S, const T* q, int lane, T& g_out) {
+__device__ __forceinline__ T tree_eval(const TreeLmParams<T>& P, const TreeTable<T>& Q,
+                                       const double* __restrict__ targets, TreeScratch<T, NE>& S, const T* q, int lane,
+                                       T& g_out) {
   const int n = P.n, ne = P.ne;
   // ---- FK, level by level: world frame after every joint, Pluecker axes -------
   // after(j) = after(parent) * O_j * Mot_j (robot.py:404-448 composition)
   for (int d = 0; d < P.nlev; ++d) {
     for (int idx = P.lev_start[d] + lane; idx < P.lev_start[d + 1]; idx += 32) {
-      const int j = P.lev_joint[idx], pj = P.parent_joint[j];
+      const int j = Q.lev_joint[idx], pj = Q.parent[j];
       quat<T> wq{T(1), T(0), T(0), T(0)};
       vec3<T> wp{T(0), T(0), T(0)};
       if (pj >= 0) {
         wq = {S.wf[pj][0], S.wf[pj][1], S.wf[pj][2], S.wf[pj][3]};
         wp = {S.wf[pj][4], S.wf[pj][5], S.wf[pj][6]};
       }
-      const vec3<T> t = qrot(wq, vec3<T>{P.op[j][0], P.op[j][1], P.op[j][2]});
+      const vec3<T> t = qrot(wq, vec3<T>{Q.op[j][0], Q.op[j][1], Q.op[j][2]});
       wp = {wp.x + t.x, wp.y + t.y, wp.z + t.z};
-      wq = qmul(wq, quat<T>{P.oq[j][0], P.oq[j][1], P.oq[j][2], P.oq[j][3]});
-      if (P.kind[j] != 0) {
-        const vec3<T> ax{P.axis[j][0], P.axis[j][1], P.axis[j][2]};
+      wq = qmul(wq, quat<T>{Q.oq[j][0], Q.oq[j][1], Q.oq[j][2], Q.oq[j][3]});
+      if (Q.kind[j] != 0) {
+        const vec3<T> ax{Q.axis[j][0], Q.axis[j][1], Q.axis[j][2]};
         const vec3<T> a = qrot(wq, ax);
         if (JAC) {
           const vec3<T> m = cross(a, wp);
           S.am[j][0] = a.x; S.am[j][1] = a.y; S.am[j][2] = a.z;
           S.am[j][3] = m.x; S.am[j][4] = m.y; S.am[j][5] = m.z;
         }
-        const T th = q[P.qcol[j]] * P.mult[j] + P.offset[j];
-        if (P.kind[j] == 1) {
+        const T th = q[Q.qcol[j]] * Q.mult[j] + Q.offset[j];
+        if (Q.kind[j] == 1) {
           T sn, cs;
           sincos_t(T(0.5) * th, &sn, &cs);
           wq = qmul(wq, quat<T>{cs, sn * ax.x, sn * ax.y, sn * ax.z});
@@ -140,9 +178,9 @@ __device__ __forceinline__ T tree_eval(const TreeLmParams<T>& P, const double* _
   T rl = T(0), gl = T(0), rr = T(0);
   if (lane < n) {
     const T qi = q[lane];
-    rl = P.w_lim * (tmax(T(0), qi - P.upper[lane]) + tmax(T(0), P.lower[lane] - qi));
-    gl = P.w_lim * ((qi > P.upper[lane] ? T(1) : T(0)) + (qi < P.lower[lane] ? T(-1) : T(0)));
-    rr = P.w_rest * (qi - P.rest[lane]);
+    rl = P.w_lim * (tmax(T(0), qi - Q.upper[lane]) + tmax(T(0), Q.lower[lane] - qi));
+    gl = P.w_lim * ((qi > Q.upper[lane] ? T(1) : T(0)) + (qi < Q.lower[lane] ? T(-1) : T(0)));
+    rr = P.w_rest * (qi - Q.rest[lane]);
     cost_part += rl * rl + rr * rr;
   }
   const T cost = warp_sum(cost_part);
@@ -153,17 +191,17 @@ __device__ __forceinline__ T tree_eval(const TreeLmParams<T>& P, const double* _
 #pragma unroll
   for (int m = 0; m < 6 * NE; ++m) col[m] = T(0);
   if (lane < n) {
-    for (int cj = 0; cj < P.col_nj[lane]; ++cj) {
-      const int j = P.col_joint[lane][cj];
+    for (int cj = 0; cj < Q.col_nj[lane]; ++cj) {
+      const int j = Q.col_joint[lane][cj];
       const vec3<T> a{S.am[j][0], S.am[j][1], S.am[j][2]};
       const vec3<T> mm{S.am[j][3], S.am[j][4], S.am[j][5]};
-      const T mu = P.mult[j];
+      const T mu = Q.mult[j];
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
         if (e >= ne || !((P.anc_ee[e] >> j) & 1ull)) continue;
         const T* E = S.ee[e];
         vec3<T> lw, aw;
-        if (P.kind[j] == 1) {
+        if (Q.kind[j] == 1) {
           const vec3<T> pe{E[15], E[16], E[17]};
           const vec3<T> x = cross(a, pe);
           lw = {x.x - mm.x, x.y - mm.y, x.z - mm.z};
@@ -283,15 +321,19 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
   extern __shared__ unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  TreeTable<T>& Q = *reinterpret_cast<TreeTable<T>*>(smem_raw);
+  TreeScratch<T, NE>& S =
+      reinterpret_cast<TreeScratch<T, NE>*>(smem_raw + (sizeof(TreeTable<T>) + 15) / 16 * 16)[wib];
+  stage_tree_table(P, Q);
+  __syncthreads();      // the only CTA-wide barrier: warps are independent from here on
   if (b >= B) return;  // whole warp exits together
-  TreeScratch<T, NE>& S = reinterpret_cast<TreeScratch<T, NE>*>(smem_raw)[wib];
   const int n = P.n;
   for (int i = lane; i < NE * 48; i += 32) (&S.ee[0][0])[i] = T(0);  // unused slots stay zero
   const double* tg = targets + b * 7 * P.ne;
   S.q[lane] = lane < n ? T(q0[b * n + lane]) : T(0);
   __syncwarp();
   T g;
-  T cost = tree_eval<T, NE, true>(P, tg, S, S.q, lane, g);
+  T cost = tree_eval<T, NE, true>(P, Q, tg, S, S.q, lane, g);
   const int hstride = O.max_iterations + 1;
   if (lane == 0) {
     if (hist_out) hist_out[b * hstride] = double(cost);
@@ -315,7 +357,7 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
         S.qn[lane] = S.q[lane] + d;
         __syncwarp();
         T gd;
-        const T cn = tree_eval<T, NE, false>(P, tg, S, S.qn, lane, gd);
+        const T cn = tree_eval<T, NE, false>(P, Q, tg, S, S.qn, lane, gd);
         if (!finite_t(cn)) {
           term = 5;
           break;
@@ -344,7 +386,7 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
       term = 2;
       break;
     }
-    tree_eval<T, NE, true>(P, tg, S, S.q, lane, g);
+    tree_eval<T, NE, true>(P, Q, tg, S, S.q, lane, g);
   }
   if (hist_out)
     for (int i = iters + 1 + lane; i < hstride; i += 32) hist_out[b * hstride + i] = NAN;
@@ -359,7 +401,7 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
 template <typename T, int NE>
 cudaError_t launch_tree_ne(const TreeLmParams<T>& P, const TreeLaunch& L, cudaStream_t st) {
   constexpr int warps = tree_warps<T>();
-  const size_t smem = sizeof(TreeScratch<T, NE>) * warps;
+  const size_t smem = (sizeof(TreeTable<T>) + 15) / 16 * 16 + sizeof(TreeScratch<T, NE>) * warps;
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_tree_solve<T, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_tree_solve<T, NE><<<(unsigned)((L.B + warps - 1) / warps), 32 * warps, smem, st>>>(
