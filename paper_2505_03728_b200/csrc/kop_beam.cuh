@@ -19,6 +19,31 @@ struct Rec {  // survivor record layout: q[NQ], base[3] (BASE), lam, cost, hist[
 };
 
 // ---------------------------------------------------------------------------
+// seed frames: the target-independent start evaluation, once per seed
+// ---------------------------------------------------------------------------
+template <class G>
+__global__ void __launch_bounds__(64)
+k_seed_frames(const ChainParams<typename G::T, G::K> C, const double* __restrict__ seeds, int S,
+              typename G::T* __restrict__ tab) {
+  using T = typename G::T;
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  T q[G::NQ];
+#pragma unroll
+  for (int i = 0; i < G::NQ; ++i) q[i] = T(seeds[(size_t)s * G::NQ + i]);
+  quat<T> sq;
+  vec3<T> sp;
+  T col[G::K + (G::BASE ? 3 : 0)][6];
+  pose_backward<G, true>(C, q, sq, sp, col);
+  tab[0 * S + s] = sq.w; tab[1 * S + s] = sq.x; tab[2 * S + s] = sq.y; tab[3 * S + s] = sq.z;
+  tab[4 * S + s] = sp.x; tab[5 * S + s] = sp.y; tab[6 * S + s] = sp.z;
+#pragma unroll
+  for (int k = 0; k < G::K; ++k)
+#pragma unroll
+    for (int m = 0; m < 6; ++m) tab[(7 + 6 * k + m) * S + s] = col[k][m];
+}
+
+// ---------------------------------------------------------------------------
 // IK-Beam stage 1
 // ---------------------------------------------------------------------------
 // shared memory of stage 1, in elements of T plus 8-byte keys:
@@ -29,10 +54,13 @@ __host__ __device__ inline size_t beam_stage1_smem(int tpb, int steps1, int extr
          8 * (size_t)tpb;
 }
 
-template <class G, int TPB, class MF>
+// SEED_TAB: the start state comes from the seeds' precomputed frames
+// (k_seed_frames) and the LM loop holds only the proposal step.
+template <class G, int TPB, bool SEED_TAB = false, class MF>
 __device__ __forceinline__ void beam_stage1_body(const MF& mf, const double* __restrict__ targets, int64_t B,
                                                  const double* __restrict__ seeds, int S, int P, int steps1,
-                                                 int keep, typename G::T* __restrict__ surv, int rec) {
+                                                 int keep, typename G::T* __restrict__ surv, int rec,
+                                                 const typename G::T* __restrict__ seed_tab = nullptr) {
   using T = typename G::T;
   constexpr int NQ = G::NQ;
   extern __shared__ unsigned char smem_raw[];
@@ -57,9 +85,21 @@ __device__ __forceinline__ void beam_stage1_body(const MF& mf, const double* __r
   st.base[0] = st.base[1] = st.base[2] = T(0);  // every seed starts with the base at identity
   st.lam = T(BeamConsts::damping_init);
   const auto model = mf(tg, scratch + tid);
-  for (int it = 0; it <= steps1; ++it) {  // it == 0: start_state
-    lm_iter<G, TPB>(model, st, it == 0 ? 1 : 0);
-    hist[(size_t)it * TPB + tid] = st.cost;
+  if constexpr (SEED_TAB) {  // start_state (beam.py:182-196) from the seed's frame
+    T A[Tri<G::ND>::size], g[G::ND];
+    const T raw = model.eval_seed(seed_tab, S, s < S ? s : 0, st.q, st.base, A, g);
+    store_normal<TPB>(st, A, g);
+    st.cost = raw;
+    hist[tid] = st.cost;
+    for (int it = 1; it <= steps1; ++it) {
+      lm_iter<G, TPB>(model, st, 0);
+      hist[(size_t)it * TPB + tid] = st.cost;
+    }
+  } else {
+    for (int it = 0; it <= steps1; ++it) {  // it == 0: start_state
+      lm_iter<G, TPB>(model, st, it == 0 ? 1 : 0);
+      hist[(size_t)it * TPB + tid] = st.cost;
+    }
   }
   // stable top-`keep` of the target's S lanes (tasks.py:135): rank = number of
   // lanes ordered before this one by (cost, seed index), NaN last

@@ -541,7 +541,9 @@ int64_t kop_ik_beam_workspace_bytes(const KopModel* m, int32_t link, const KopIk
   const int nq = kernel_nq(sh, m->tree.n);
   const size_t el = p->precision == KOP_FP64 ? 8 : 4;
   const int64_t rec = nq + (p->optimize_base ? 3 : 0) + 2 + p->prune_after + 1;
-  return batch * (int64_t)p->keep * rec * (int64_t)el + 256;
+  // survivor records, then (fixed base) the seed frame table: (7 + 6 K) x seeds, K <= 8
+  const int64_t surv = (batch * (int64_t)p->keep * rec * (int64_t)el + 255) / 256 * 256;
+  return surv + (int64_t)(7 + 6 * 8) * p->seeds * (int64_t)el + 256;
 }
 
 }  // extern "C"

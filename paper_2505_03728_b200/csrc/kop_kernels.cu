@@ -36,8 +36,11 @@ template <class G, int TPB>
 __global__ void __launch_bounds__(TPB, (TPB <= 256 ? 2 : 1))
 k_beam_stage1(const ChainParams<typename G::T, G::K> C, const CostParams<typename G::T, G::NQ> W,
               const double* __restrict__ targets, int64_t B, const double* __restrict__ seeds, int S, int P,
-              int steps1, int keep, typename G::T* __restrict__ surv, int rec) {
-  beam_stage1_body<G, TPB>(PoseModelFactory<G>{C, W}, targets, B, seeds, S, P, steps1, keep, surv, rec);
+              int steps1, int keep, typename G::T* __restrict__ surv, int rec,
+              const typename G::T* __restrict__ seed_tab) {
+  // fixed-base lanes start from the seed frames (k_seed_frames); mobile lanes evaluate in place
+  beam_stage1_body<G, TPB, !G::BASE>(PoseModelFactory<G>{C, W}, targets, B, seeds, S, P, steps1, keep, surv,
+                                     rec, seed_tab);
 }
 
 constexpr int kStage2Threads = 128;
@@ -173,7 +176,15 @@ cudaError_t launch_beam(const ChainParams<typename G::T, G::K>& C, const CostPar
   T* surv = reinterpret_cast<T*>(L.workspace);
   constexpr int kAg = Tri<G::ND>::size + G::ND;
   cudaError_t e = cudaSuccess;
+  // seed frame table after the survivor records (kop_ik_beam_workspace_bytes)
+  T* seed_tab = reinterpret_cast<T*>(static_cast<char*>(L.workspace) +
+                                     ((size_t)L.B * L.keep * rec * sizeof(T) + 255) / 256 * 256);
   if (L.stages & 1) {
+    if (!G::BASE) {
+      k_seed_frames<G><<<(L.S + 63) / 64, 64, 0, st>>>(C, L.seeds, L.S, seed_tab);
+      e = cudaGetLastError();
+      if (e != cudaSuccess) return e;
+    }
     // stage 1: P lanes per target (power of two >= S)
     const int tpb = L.P <= 256 ? 256 : 1024;  // P <= 1024 (seeds <= 1024)
     const int per_block = tpb / L.P;
@@ -183,12 +194,12 @@ cudaError_t launch_beam(const ChainParams<typename G::T, G::K>& C, const CostPar
       if (smem1 > 48 * 1024)
         cudaFuncSetAttribute(k_beam_stage1<G, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
       k_beam_stage1<G, 256><<<(unsigned)blocks1, 256, smem1, st>>>(C, W, L.targets, L.B, L.seeds, L.S, L.P,
-                                                                   L.steps1, L.keep, surv, rec);
+                                                                   L.steps1, L.keep, surv, rec, seed_tab);
     } else {
       if (smem1 > 48 * 1024)
         cudaFuncSetAttribute(k_beam_stage1<G, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
       k_beam_stage1<G, 1024><<<(unsigned)blocks1, 1024, smem1, st>>>(C, W, L.targets, L.B, L.seeds, L.S, L.P,
-                                                                     L.steps1, L.keep, surv, rec);
+                                                                     L.steps1, L.keep, surv, rec, seed_tab);
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;

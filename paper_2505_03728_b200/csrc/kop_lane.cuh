@@ -213,18 +213,20 @@ __device__ __forceinline__ void pose_finish(const ChainParams<typename G::T, G::
   }
 }
 
+// Target-independent part of a lane evaluation: the backward pass over the
+// compiled chain at q, giving the arm's EE pose S_0 = (sq, sp) and (JAC) the
+// body-frame Jacobian columns.  A function of q alone -- IK-Beam evaluates it
+// once per seed for the start state (k_seed_frames).
 template <class G, bool JAC>
-__device__ __forceinline__ void pose_rows(const ChainParams<typename G::T, G::K>& C,
-                                          const CostParams<typename G::T, G::NQ>& W,
-                                          const TargetInv<typename G::T>& tg, const typename G::T (&q)[G::NQ],
-                                          const typename G::T (&base)[3], typename G::T (&r)[6],
-                                          typename G::T (&J)[6][G::ND]) {
+__device__ __forceinline__ void pose_backward(const ChainParams<typename G::T, G::K>& C,
+                                              const typename G::T (&q)[G::NQ], quat<typename G::T>& sq_out,
+                                              vec3<typename G::T>& sp_out,
+                                              typename G::T (&col)[G::K + (G::BASE ? 3 : 0)][6]) {
   using T = typename G::T;
   constexpr int K = G::K, NQ = G::NQ, ND = G::ND;
   constexpr bool ID = G::ID;
   quat<T> sq{C.eq[0], C.eq[1], C.eq[2], C.eq[3]};
   vec3<T> sp{C.ep[0], C.ep[1], C.ep[2]};
-  T col[K + (G::BASE ? 3 : 0)][6];
 #pragma unroll
   for (int k = K - 1; k >= 0; --k) {
     if (ID || k < C.k) {
@@ -256,6 +258,22 @@ __device__ __forceinline__ void pose_rows(const ChainParams<typename G::T, G::K>
             C.tp[k][2] + (C.tr[k][2][0] * sp.x + C.tr[k][2][1] * sp.y + C.tr[k][2][2] * sp.z)};
     }
   }
+  sq_out = sq;
+  sp_out = sp;
+}
+
+template <class G, bool JAC>
+__device__ __forceinline__ void pose_rows(const ChainParams<typename G::T, G::K>& C,
+                                          const CostParams<typename G::T, G::NQ>& W,
+                                          const TargetInv<typename G::T>& tg, const typename G::T (&q)[G::NQ],
+                                          const typename G::T (&base)[3], typename G::T (&r)[6],
+                                          typename G::T (&J)[6][G::ND]) {
+  using T = typename G::T;
+  constexpr int K = G::K;
+  quat<T> sq;
+  vec3<T> sp;
+  T col[K + (G::BASE ? 3 : 0)][6];
+  pose_backward<G, JAC>(C, q, sq, sp, col);
   if (G::BASE) {
     if (JAC) {  // base tangent (vx, vy, w): prismatic x, prismatic y, revolute z at the arm root
       T rev[6], px[3], py[3], pz[3];
@@ -532,7 +550,27 @@ struct PoseModel {
                                     T (&g)[G::ND]) const {
     return lane_eval<G, JAC>(C, W, tg, q, base, A, g);
   }
+  // the start evaluation at seed s from its precomputed frame (k_seed_frames,
+  // field-major table tab[f * S + s]): only the target-dependent part remains
+  __device__ __forceinline__ T eval_seed(const T* __restrict__ tab, int S, int s, const T (&q)[G::NQ],
+                                         const T (&base)[3], T (&A)[Tri<G::ND>::size], T (&g)[G::ND]) const {
+    static_assert(!G::BASE, "seed frames exclude the mobile base");
+    const quat<T> sq{tab[0 * S + s], tab[1 * S + s], tab[2 * S + s], tab[3 * S + s]};
+    const vec3<T> sp{tab[4 * S + s], tab[5 * S + s], tab[6 * S + s]};
+    T col[G::K][6];
+#pragma unroll
+    for (int k = 0; k < G::K; ++k)
+#pragma unroll
+      for (int m = 0; m < 6; ++m) col[k][m] = tab[(7 + 6 * k + m) * S + s];
+    T r[6], J[6][G::ND];
+    pose_finish<G, true>(C, W, tg, sq, sp, col, r, J);
+    return assemble_rows<G, true>(W, q, base, r, J, A, g);
+  }
 };
+
+// seed frame table size in elements (per seed: EE quaternion, position, 6 K columns)
+template <class G>
+__host__ __device__ constexpr int seed_frame_fields() { return 7 + 6 * G::K; }
 
 template <class G, int STRIDE, class M>
 __device__ __forceinline__ void lm_iter(const M& model, LaneState<G>& s, int mode) {
