@@ -322,6 +322,21 @@ int kop_traj_report(const KopModel* model, int32_t link, int32_t timesteps, cons
                     double* static_out, double* swept_out, double* min_static, double* min_swept,
                     double* pos_err, double* rot_err, void* stream);
 
+/* Multi-end-effector IK-Beam on a tree (config 3 as SURVEY.md section 8 H6
+ * states it): IK-Beam (tasks.py:119-161) with the lane LM of beam.py:198-240
+ * over [pose_1..pose_E | limit | rest] (KopPoseCosts weights and rest; the
+ * params' w_* are ignored).  targets device [B*E*7]; seeds device [S*n].
+ * Outputs (device): q [B*n], cost [B], history [B*(total_steps+1)] (NULL ok),
+ * pos_err / rot_err [B*E] (FP64, tasks.py:109-116 per end effector),
+ * success [B] (every end effector within tolerance).  One warp per lane;
+ * keep <= 8, prune_after <= 31, total_steps - prune_after <= 32. */
+int64_t kop_multi_pose_beam_workspace_bytes(const KopModel* model, const KopPoseCosts* costs,
+                                            const KopIkParams* params, int64_t batch);
+int kop_multi_pose_beam(const KopModel* model, const KopPoseCosts* costs, const KopIkParams* params,
+                        const double* targets, int64_t batch, const double* seeds, void* workspace,
+                        int64_t workspace_bytes, double* q_out, double* cost_out, double* history_out,
+                        double* pos_err, double* rot_err, uint8_t* success, void* stream);
+
 /* --- counter-based sampling ---------------------------------------------
  * replaces: tasks.sample_seed_configurations (tasks.py:88-106) and the draws
  * of benchmark.generate_reachable_targets (benchmark.py:83-93): row i is

@@ -103,6 +103,9 @@ SIGNATURES = {
     "kop_traj_normal_equations": (C.c_int, [_p, _i32, C.POINTER(KopTrajCosts), _i32, _p, _p, _p, _i32, _i64, _p,
                                             _p, _p, _p]),
     "kop_traj_report": (C.c_int, [_p, _i32, _i32, _p, _p, _i32, _p, _i64, _p, _p, _p, _p, _p, _p, _p]),
+    "kop_multi_pose_beam_workspace_bytes": (C.c_int64, [_p, C.POINTER(KopPoseCosts), C.POINTER(KopIkParams), _i64]),
+    "kop_multi_pose_beam": (C.c_int, [_p, C.POINTER(KopPoseCosts), C.POINTER(KopIkParams), _p, _i64, _p, _p, _i64,
+                                      _p, _p, _p, _p, _p, _p, _p]),
     "kop_sample_uniform": (C.c_int, [_u64, _u64, _i64, _i32, _p, _p, _p, _p, _p]),
     "kop_jacobian": (C.c_int, [_p, _i32, _p, _i64, _i32, _p, _i32, _p, _p]),
     "kop_link_poses": (C.c_int, [_p, _i32, _p, _i64, _p, _p]),

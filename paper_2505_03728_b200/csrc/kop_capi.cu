@@ -1411,6 +1411,61 @@ int kop_traj_report(const KopModel* m, int32_t link, int32_t timesteps, const do
   return cuda_status(e);
 }
 
+int64_t kop_multi_pose_beam_workspace_bytes(const KopModel* m, const KopPoseCosts* pc, const KopIkParams* p,
+                                             int64_t batch) {
+  if (!m || !pc || !p || batch < 0) return fail(KOP_EINVAL, "invalid arguments");
+  const int rec = tree_beam_rec(m->tree.n, p->prune_after);
+  return ((int64_t)batch * p->seeds * rec * 4 + 255) / 256 * 256 + (int64_t)batch * p->keep * 4 + 256;
+}
+
+int kop_multi_pose_beam(const KopModel* m, const KopPoseCosts* pc, const KopIkParams* p, const double* targets,
+                        int64_t batch, const double* seeds, void* workspace, int64_t workspace_bytes, double* q_out,
+                        double* cost_out, double* history_out, double* pos_err, double* rot_err, uint8_t* success,
+                        void* stream) {
+  if (!m || !pc || !p) return fail(KOP_EINVAL, "null argument");
+  if (p->precision != KOP_FP32 && p->precision != KOP_FP64) return fail(KOP_EINVAL, "bad precision");
+  if (m->tree.n > kTreeMaxDofs || m->tree.nj > kTreeMaxJoints || !tree_params_ok(*m))
+    return fail(KOP_EUNSUPPORTED, "tree IK-Beam supports up to 32 actuated and 64 total joints");
+  if (pc->num_poses < 1 || pc->num_poses > kTreeMaxPoses)
+    return fail(KOP_EUNSUPPORTED, "tree IK-Beam supports 1..8 end effectors");
+  for (int e = 0; e < pc->num_poses; ++e)
+    if (pc->links[e] < 0 || pc->links[e] >= m->tree.nl) return fail(KOP_EINVAL, "unknown link index");
+  // IkRequest.__post_init__ (tasks.py:56-60)
+  if (!(0 < p->prune_after && p->prune_after < p->total_steps))
+    return fail(KOP_EINVAL, "need 0 < prune_after < total_steps");
+  if (!(1 <= p->keep && p->keep <= p->seeds)) return fail(KOP_EINVAL, "need 1 <= keep <= seeds");
+  if (p->keep > 8 || p->prune_after > 31 || p->total_steps - p->prune_after > 32)
+    return fail(KOP_EUNSUPPORTED, "tree IK-Beam compiled for keep <= 8 and <= 31 + 32 steps");
+  if (batch < 0) return fail(KOP_EINVAL, "negative batch");
+  if (batch == 0) return KOP_OK;
+  if (!targets || !seeds || !workspace || !q_out || !cost_out || !pos_err || !rot_err || !success)
+    return fail(KOP_EINVAL, "null array argument");
+  if (workspace_bytes < kop_multi_pose_beam_workspace_bytes(m, pc, p, batch))
+    return fail(KOP_EINVAL, "workspace too small");
+  TreeBeamLaunch L{};
+  L.targets = targets;
+  L.B = batch;
+  L.seeds = seeds;
+  L.S = p->seeds;
+  L.steps1 = p->prune_after;
+  L.steps2 = p->total_steps - p->prune_after;
+  L.keep = p->keep;
+  L.pos_tol = p->success_pos_tol;
+  L.rot_tol = p->success_rot_tol;
+  L.workspace = workspace;
+  L.q_out = q_out;
+  L.cost_out = cost_out;
+  L.hist_out = history_out;
+  L.pos_err = pos_err;
+  L.rot_err = rot_err;
+  L.success = success;
+  cudaStream_t st = (cudaStream_t)stream;
+  const TreeLmParams<double> Pd = tree_params<double>(*m, pc);
+  const cudaError_t e = p->precision == KOP_FP32 ? launch_tree_beam<float>(tree_params<float>(*m, pc), Pd, L, st)
+                                                 : launch_tree_beam<double>(Pd, Pd, L, st);
+  return cuda_status(e);
+}
+
 int kop_dfma_peak_kernel(int32_t blocks, int32_t threads, int32_t iters, double* sink, double* flops,
                          void* stream) {
   if (blocks <= 0 || threads <= 0 || iters <= 0 || !sink) return fail(KOP_EINVAL, "invalid arguments");

@@ -421,4 +421,239 @@ cudaError_t launch_tree_solve(const TreeLmParams<T>& P, const TreeLaunch& L, cud
 template cudaError_t launch_tree_solve<float>(const TreeLmParams<float>&, const TreeLaunch&, cudaStream_t);
 template cudaError_t launch_tree_solve<double>(const TreeLmParams<double>&, const TreeLaunch&, cudaStream_t);
 
+// ---------------------------------------------------------------------------
+// Multi-end-effector IK-Beam ("beam-style lanes
+// generalised to K pose blocks"): the lane LM of beam.py:198-240 (one proposal
+// per step, per-lane accept / damping x1/3 | x10) and the tasks.py:119-161
+// beam control flow, over the tree residual [pose_1..pose_K | limit | rest].
+// One warp per lane, as in the tree solve.
+// ---------------------------------------------------------------------------
+
+// one beam.py proposal at the state (S.q, cost, A in S.A, g): returns the new cost
+template <typename T, int NE>
+__device__ __forceinline__ T tree_beam_step(const TreeLmParams<T>& P, const TreeTable<T>& Q,
+                                            const double* __restrict__ tg, TreeScratch<T, NE>& S, int lane, T cost,
+                                            T& lam, T& g) {
+  T d;
+  bool ok = tree_damped_solve(P, S, g, lam, lane, d);
+  ok = __all_sync(0xffffffffu, ok && finite_t(d));
+  T cn = inf_t<T>();
+  if (ok) {  // a failed factorisation rejects the step (beam.py:209-213, per lane)
+    S.qn[lane] = S.q[lane] + d;
+    __syncwarp();
+    T gd;
+    const T raw = tree_eval<T, NE, false>(P, Q, tg, S, S.qn, lane, gd);
+    cn = finite_t(raw) ? raw : inf_t<T>();
+  }
+  if (cn < cost) {
+    S.q[lane] = S.qn[lane];
+    __syncwarp();
+    lam = tmax(lam * T(BeamConsts::damping_down), T(BeamConsts::damping_min));
+    tree_eval<T, NE, true>(P, Q, tg, S, S.q, lane, g);  // J at the accepted iterate (beam.py:202)
+    return cn;
+  }
+  lam = tmin(lam * T(BeamConsts::damping_up), T(BeamConsts::damping_max));
+  return cost;
+}
+
+template <typename T, int NE>
+__global__ void __launch_bounds__(32 * tree_warps<T>())
+k_tree_beam_stage1(const TreeLmParams<T> P, const double* __restrict__ targets, int64_t B,
+                   const double* __restrict__ seeds, int S, int steps1, float* __restrict__ recs) {
+  extern __shared__ unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t L = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;  // lane = target * S + seed
+  TreeTable<T>& Q = *reinterpret_cast<TreeTable<T>*>(smem_raw);
+  TreeScratch<T, NE>& Sc =
+      reinterpret_cast<TreeScratch<T, NE>*>(smem_raw + (sizeof(TreeTable<T>) + 15) / 16 * 16)[wib];
+  stage_tree_table(P, Q);
+  __syncthreads();
+  if (L >= B * S) return;
+  const int64_t b = L / S;
+  const int s = (int)(L % S), n = P.n;
+  for (int i = lane; i < NE * 48; i += 32) (&Sc.ee[0][0])[i] = T(0);
+  Sc.q[lane] = lane < n ? T(seeds[(size_t)s * n + lane]) : T(0);
+  __syncwarp();
+  const double* tg = targets + b * 7 * P.ne;
+  T g;
+  T cost = tree_eval<T, NE, true>(P, Q, tg, Sc, Sc.q, lane, g);  // start_state (beam.py:182-196)
+  T lam = T(BeamConsts::damping_init);
+  T hv = lane == 0 ? cost : T(0);  // lane h keeps hist[h]
+  for (int it = 1; it <= steps1; ++it) {
+    cost = tree_beam_step(P, Q, tg, Sc, lane, cost, lam, g);
+    if (lane == it) hv = cost;
+  }
+  const int rec = tree_beam_rec(n, steps1);
+  float* out = recs + L * rec;
+  if (lane < n) out[lane] = float(Sc.q[lane]);
+  if (lane == 0) {
+    out[n] = float(lam);
+    out[n + 1] = float(cost);
+  }
+  if (lane <= steps1) out[n + 2 + lane] = float(hv);
+}
+
+// stable top-`keep` seeds of each target by (final stage-1 cost, seed index),
+// NaN last (np.argsort(kind="stable"), tasks.py:135): one warp per target
+__global__ void __launch_bounds__(128)
+k_tree_beam_prune(const float* __restrict__ recs, int rec, int n, int64_t B, int S, int keep,
+                  int32_t* __restrict__ surv) {
+  const int lane = threadIdx.x & 31;
+  const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (b >= B) return;
+  const float* base = recs + b * S * rec + n + 1;
+  for (int s = lane; s < S; s += 32) {
+    const float c = base[(size_t)s * rec];
+    int rank = 0;
+    for (int j = 0; j < S; ++j) rank += rank_less(base[(size_t)j * rec], j, c, s) ? 1 : 0;
+    if (rank < keep) surv[b * keep + rank] = s;
+  }
+}
+
+// FP64 world frame after tree joint j (identity for j < 0), walking up the tree
+__device__ __forceinline__ void tree_frame_f64(const TreeLmParams<double>& P, const double* q, int j,
+                                               quat<double>& wq, vec3<double>& wp) {
+  wq = {1.0, 0.0, 0.0, 0.0};
+  wp = {0.0, 0.0, 0.0};
+  for (int a = j; a >= 0; a = P.parent_joint[a]) {  // (wq, wp) <- O_a Mot_a (wq, wp)
+    if (P.kind[a] != 0) {
+      const double th = q[P.qcol[a]] * P.mult[a] + P.offset[a];
+      const vec3<double> ax{P.axis[a][0], P.axis[a][1], P.axis[a][2]};
+      if (P.kind[a] == 1) {
+        double sn, cs;
+        sincos(0.5 * th, &sn, &cs);
+        const quat<double> r{cs, sn * ax.x, sn * ax.y, sn * ax.z};
+        wp = qrot(r, wp);
+        wq = qmul(r, wq);
+      } else {
+        wp = {wp.x + th * ax.x, wp.y + th * ax.y, wp.z + th * ax.z};
+      }
+    }
+    const quat<double> mq{P.oq[a][0], P.oq[a][1], P.oq[a][2], P.oq[a][3]};
+    const vec3<double> t = qrot(mq, wp);
+    wp = {t.x + P.op[a][0], t.y + P.op[a][1], t.z + P.op[a][2]};
+    wq = qmul(mq, wq);
+  }
+}
+
+// survivors of one target: one warp each, 10 more steps, winner = argmin
+// (ties -> better stage-1 rank, tasks.py:139), outputs and FP64 pose errors
+template <typename T, int NE>
+__global__ void __launch_bounds__(256)
+k_tree_beam_stage2(const TreeLmParams<T> P, const TreeLmParams<double> Pd, const double* __restrict__ targets,
+                   int64_t B, const float* __restrict__ recs, int S, const int32_t* __restrict__ surv, int steps1,
+                   int steps2, int keep, double pos_tol, double rot_tol, double* __restrict__ q_out,
+                   double* __restrict__ cost_out, double* __restrict__ hist_out, double* __restrict__ pos_err,
+                   double* __restrict__ rot_err, uint8_t* __restrict__ success) {
+  extern __shared__ unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31, r = threadIdx.x >> 5;  // warp r = survivor of stage-1 rank r
+  const int64_t b = blockIdx.x;
+  TreeTable<T>& Q = *reinterpret_cast<TreeTable<T>*>(smem_raw);
+  const size_t tab = (sizeof(TreeTable<T>) + 15) / 16 * 16;
+  TreeScratch<T, NE>& Sc = reinterpret_cast<TreeScratch<T, NE>*>(smem_raw + tab)[r];
+  T* wcost = reinterpret_cast<T*>(smem_raw + tab + sizeof(TreeScratch<T, NE>) * keep);
+  int* wsel = reinterpret_cast<int*>(wcost + keep);
+  stage_tree_table(P, Q);
+  __syncthreads();
+  const int n = P.n, rec = tree_beam_rec(n, steps1);
+  const float* in = recs + (b * S + surv[b * keep + r]) * rec;
+  for (int i = lane; i < NE * 48; i += 32) (&Sc.ee[0][0])[i] = T(0);
+  Sc.q[lane] = lane < n ? T(in[lane]) : T(0);
+  __syncwarp();
+  const double* tg = targets + b * 7 * P.ne;
+  T g;
+  tree_eval<T, NE, true>(P, Q, tg, Sc, Sc.q, lane, g);  // re-derive J; the carried cost is stage 1's
+  T lam = T(in[n]), cost = T(in[n + 1]);
+  T hv = T(0);  // lane h keeps stage-2 hist[h]
+  for (int it = 0; it < steps2; ++it) {
+    cost = tree_beam_step(P, Q, tg, Sc, lane, cost, lam, g);
+    if (lane == it) hv = cost;
+  }
+  if (lane == 0) wcost[r] = cost;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int best = 0;
+    for (int k = 1; k < keep; ++k)
+      if (wcost[k] < wcost[best] || (wcost[best] != wcost[best] && wcost[k] == wcost[k])) best = k;
+    *wsel = best;
+  }
+  __syncthreads();
+  if (r != *wsel) return;
+  if (lane < n) q_out[b * n + lane] = double(Sc.q[lane]);
+  if (lane == 0) cost_out[b] = double(cost);
+  if (hist_out) {
+    double* h = hist_out + b * (steps1 + 1 + steps2);
+    if (lane <= steps1) h[lane] = double(in[n + 2 + lane]);
+    if (lane < steps2) h[steps1 + 1 + lane] = double(hv);
+  }
+  // FP64 pose errors of every end effector (tasks.py:109-116); success = all in tolerance
+  double qd[kTreeMaxDofs];
+  for (int i = 0; i < n; ++i) qd[i] = double(Sc.q[i]);
+  bool ok = true;
+  if (lane < P.ne) {
+    quat<double> wq;
+    vec3<double> wp;
+    tree_frame_f64(Pd, qd, Pd.ee_joint[lane], wq, wp);
+    const double nq = sqrt(wq.w * wq.w + wq.x * wq.x + wq.y * wq.y + wq.z * wq.z);
+    wq = {wq.w / nq, wq.x / nq, wq.y / nq, wq.z / nq};
+    double ti[7];
+    target_inverse(tg + 7 * lane, ti);
+    const quat<double> iq{ti[0], ti[1], ti[2], ti[3]};
+    const quat<double> rq = qmul(iq, wq);
+    const vec3<double> rt0 = qrot(iq, wp);
+    const vec3<double> rt{ti[4] + rt0.x, ti[5] + rt0.y, ti[6] + rt0.z};
+    const double pe = sqrt(rt.x * rt.x + rt.y * rt.y + rt.z * rt.z);
+    const vec3<double> w = qlog(rq);
+    const double re = sqrt(w.x * w.x + w.y * w.y + w.z * w.z);
+    pos_err[b * P.ne + lane] = pe;
+    rot_err[b * P.ne + lane] = re;
+    ok = pe < pos_tol && re < rot_tol;
+  }
+  const bool all_ok = __all_sync(0xffffffffu, ok);
+  if (lane == 0) success[b] = all_ok ? 1 : 0;
+}
+
+template <typename T, int NE>
+cudaError_t launch_tree_beam_ne(const TreeLmParams<T>& P, const TreeLmParams<double>& Pd, const TreeBeamLaunch& L,
+                                cudaStream_t st) {
+  constexpr int warps = tree_warps<T>();
+  const size_t tab = (sizeof(TreeTable<T>) + 15) / 16 * 16;
+  const int rec = tree_beam_rec(P.n, L.steps1);
+  float* recs = static_cast<float*>(L.workspace);
+  int32_t* surv = reinterpret_cast<int32_t*>(static_cast<char*>(L.workspace) +
+                                             ((size_t)L.B * L.S * rec * sizeof(float) + 255) / 256 * 256);
+  const size_t smem1 = tab + sizeof(TreeScratch<T, NE>) * warps;
+  if (smem1 > 48 * 1024)
+    cudaFuncSetAttribute(k_tree_beam_stage1<T, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+  const int64_t lanes = L.B * L.S;
+  k_tree_beam_stage1<T, NE><<<(unsigned)((lanes + warps - 1) / warps), 32 * warps, smem1, st>>>(
+      P, L.targets, L.B, L.seeds, L.S, L.steps1, recs);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  k_tree_beam_prune<<<(unsigned)((L.B + 3) / 4), 128, 0, st>>>(recs, rec, P.n, L.B, L.S, L.keep, surv);
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  const size_t smem2 = tab + sizeof(TreeScratch<T, NE>) * L.keep + (sizeof(T) + sizeof(int)) * 32 + 16;
+  if (smem2 > 48 * 1024)
+    cudaFuncSetAttribute(k_tree_beam_stage2<T, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
+  k_tree_beam_stage2<T, NE><<<(unsigned)L.B, 32 * L.keep, smem2, st>>>(
+      P, Pd, L.targets, L.B, recs, L.S, surv, L.steps1, L.steps2, L.keep, L.pos_tol, L.rot_tol, L.q_out, L.cost_out,
+      L.hist_out, L.pos_err, L.rot_err, L.success);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_tree_beam(const TreeLmParams<T>& P, const TreeLmParams<double>& Pd, const TreeBeamLaunch& L,
+                             cudaStream_t st) {
+  if (L.B == 0) return cudaSuccess;
+  if (P.ne <= 1) return launch_tree_beam_ne<T, 1>(P, Pd, L, st);
+  if (P.ne <= 2) return launch_tree_beam_ne<T, 2>(P, Pd, L, st);
+  if (P.ne <= 4) return launch_tree_beam_ne<T, 4>(P, Pd, L, st);
+  return launch_tree_beam_ne<T, kTreeMaxPoses>(P, Pd, L, st);
+}
+
+template cudaError_t launch_tree_beam<float>(const TreeLmParams<float>&, const TreeLmParams<double>&,
+                                             const TreeBeamLaunch&, cudaStream_t);
+template cudaError_t launch_tree_beam<double>(const TreeLmParams<double>&, const TreeLmParams<double>&,
+                                              const TreeBeamLaunch&, cudaStream_t);
+
 }  // namespace kop

@@ -46,4 +46,22 @@ struct TreeLaunch {
 template <typename T>
 cudaError_t launch_tree_solve(const TreeLmParams<T>& P, const TreeLaunch& L, cudaStream_t st);
 
+// multi-end-effector IK-Beam (config 3 as SURVEY.md section 8 H6 states it)
+struct TreeBeamLaunch {
+  const double* targets;  // [B * ne * 7]
+  int64_t B;
+  const double* seeds;    // [S * n]
+  int S, steps1, steps2, keep;
+  double pos_tol, rot_tol;
+  void* workspace;        // lane records [B * S * rec] | survivor seeds [B * keep] int32
+  double *q_out, *cost_out, *hist_out, *pos_err, *rot_err;
+  uint8_t* success;
+};
+
+__host__ __device__ inline int tree_beam_rec(int n, int steps1) { return n + 2 + steps1 + 1; }  // q | lam | cost | hist
+
+template <typename T>
+cudaError_t launch_tree_beam(const TreeLmParams<T>& P, const TreeLmParams<double>& Pd, const TreeBeamLaunch& L,
+                             cudaStream_t st);
+
 }  // namespace kop

@@ -398,6 +398,68 @@ def solve_ik_collision_batch(model: RobotModel, link: str, targets, world=None, 
     return solver.solve(targets)
 
 
+@dataclass
+class MultiBeamBatch:
+    """Multi-end-effector IK-Beam outputs: q (B, n), cost (B,), history (B, total_steps+1),
+    pos_error / rot_error (B, E) per end effector, success (B,) (every end effector
+    within tolerance)."""
+
+    q: object
+    cost: object
+    history: object
+    pos_error: object
+    rot_error: object
+    success: object
+
+    def cpu(self) -> "MultiBeamBatch":
+        f = lambda x: x.cpu().numpy() if hasattr(x, "cpu") else x
+        return MultiBeamBatch(f(self.q), f(self.cost), f(self.history), f(self.pos_error), f(self.rot_error),
+                              f(self.success))
+
+
+def solve_ik_beam_multi(model: RobotModel, links, targets, weights: ck.CostWeights | None = None, seeds: int = 64,
+                        total_steps: int = 16, prune_after: int = 6, keep: int = 4, rng_seed: int = 0,
+                        precision="fp32", success_pos_tol: float = 0.005, success_rot_tol: float = 0.05,
+                        rest=None, device_out: bool = False) -> MultiBeamBatch:
+    """IK-Beam over several end effectors of a tree (config 3 as SURVEY.md section 8
+    H6 states it): every lane runs the beam.py lane LM over [pose_1..pose_E | limit |
+    rest]; the tasks.py:119-161 prune / continue / winner flow picks each target set's
+    solution.  ``targets``: (B, E, 7) poses (w, x, y, z, px, py, pz) of ``links``."""
+    from ._lib import KopPoseCosts
+
+    if not 0 < prune_after < total_steps:
+        raise ValueError("need 0 < prune_after < total_steps")
+    if not 1 <= keep <= seeds:
+        raise ValueError("need 1 <= keep <= seeds")
+    t = dv.require_cuda()
+    w = weights or ck.CostWeights()
+    links = list(links)
+    e = len(links)
+    tg = dv.to_dev(targets)
+    if tg.dim() != 3 or tg.shape[1] != e or tg.shape[2] != 7:
+        raise ValueError(f"targets must have shape (B, {e}, 7), got {tuple(tg.shape)}")
+    b, n = tg.shape[0], model.actuated_count
+    li = np.ascontiguousarray([model.link_index(l) for l in links], dtype=np.int32)
+    wp = np.full(e, float(w.pose_position))
+    wo = np.full(e, float(w.pose_orientation))
+    rp = np.ascontiguousarray(model.rest_pose if rest is None else rest, dtype=float)
+    pc = KopPoseCosts(e, li.ctypes.data, wp.ctypes.data, wo.ctypes.data, float(w.limit), float(w.rest), rp.ctypes.data)
+    params = KopIkParams(0.0, 0.0, 0.0, 0.0, seeds, total_steps, prune_after, keep, success_pos_tol, success_rot_tol,
+                         _precision(precision), 0, 0.0)
+    sd = sample_seed_configurations_device(model, seeds, rng_seed)
+    need = int(lib().kop_multi_pose_beam_workspace_bytes(model._handle, C.byref(pc), C.byref(params), b))
+    if need < 0:
+        check(need, "kop_multi_pose_beam_workspace_bytes")
+    ws = t.empty(max(need, 1), dtype=t.uint8, device="cuda")
+    out = MultiBeamBatch(dv.empty((b, n)), dv.empty(b), dv.empty((b, total_steps + 1)), dv.empty((b, e)),
+                         dv.empty((b, e)), t.empty(b, dtype=t.uint8, device="cuda"))
+    check(lib().kop_multi_pose_beam(model._handle, C.byref(pc), C.byref(params), dv.ptr(tg), b, dv.ptr(sd),
+                                    dv.ptr(ws), ws.numel(), dv.ptr(out.q), dv.ptr(out.cost), dv.ptr(out.history),
+                                    dv.ptr(out.pos_error), dv.ptr(out.rot_error), dv.ptr(out.success),
+                                    dv.stream_handle()), "kop_multi_pose_beam")
+    return out if device_out else out.cpu()
+
+
 # trajectory optimisation lives in trajectory.py; re-exported here where the reference keeps it (tasks.py:183-424)
 from .trajectory import (TrajectoryPlanner, TrajRequest, TrajResult, plan_trajectory,  # noqa: E402,F401
                          plan_trajectory_batch, trajectory_signed_distances)

@@ -82,3 +82,49 @@ def test_tree_solve_reachable_batch_converges(hum, chains):
     _, c_ref, _, _, _ = to.solve_multi_pose(ch, poses, ch.rest)
     rep64 = k.solve(probs[0])
     np.testing.assert_allclose(rep64.final_cost, c_ref, rtol=1e-5)
+
+
+def _hum_targets(hum, chh, count, seed):
+    rng = np.random.default_rng(seed)
+    qt = rng.uniform(chh.lower, chh.upper, (count, chh.n))
+    lq, lp, _, _ = o.fk(chh, qt)
+    links = [chh.link(e) for e in EES]
+    tq = np.stack([o.qcanon(lq[:, l]) for l in links], 1)
+    tt = np.stack([lp[:, l] for l in links], 1)
+    return links, tq, tt, np.concatenate([tq, tt], axis=2)
+
+
+def test_tree_ik_beam_fp64_matches_oracle(hum):
+    """Multi-EE IK-Beam (config 3, SURVEY H6 flavour) FP64 on the device vs the
+    oracle composed of the pinned lane / beam primitives."""
+    from oracle import tree_oracle as tro
+
+    chh = o.load_chain_files(k.robot_path("humanoid29.urdf"))
+    links, tq, tt, tg = _hum_targets(hum, chh, 12, 5)
+    seeds = o.sample_seeds(chh, 64, 3)
+    ref = tro.multi_ee_beam(chh, links, tq, tt, seeds, [50.0] * 4, [10.0] * 4)
+    got = k.solve_ik_beam_multi(hum, EES, tg, rng_seed=3, precision="fp64")
+    rel = np.abs(got.history - ref["hist"]) / ref["hist"]
+    assert np.mean(rel.max(axis=1) < 1e-6) >= 0.75, np.sort(rel.max(axis=1))
+    assert np.mean(got.success == ref["success"]) >= 0.9
+    same = rel.max(axis=1) < 1e-6
+    np.testing.assert_allclose(got.pos_error[same], ref["pos_err"][same], rtol=1e-4, atol=1e-9)
+
+
+def test_tree_ik_beam_fp32_and_single_ee(hum, models):
+    chh = o.load_chain_files(k.robot_path("humanoid29.urdf"))
+    links, tq, tt, tg = _hum_targets(hum, chh, 256, 6)
+    r32 = k.solve_ik_beam_multi(hum, EES, tg, rng_seed=3)
+    r64 = k.solve_ik_beam_multi(hum, EES, tg, rng_seed=3, precision="fp64")
+    assert abs(r32.success.mean() - r64.success.mean()) <= 0.05
+    assert np.all(np.diff(r32.history, axis=1) <= 0)
+    # one end effector on the Panda chain: the same lanes as the chain IK-Beam
+    m = models["arm7"]
+    from paper_2505_03728_b200.benchmark import reachable_target_array
+
+    tgt = reachable_target_array(m, "flange", 64, 77).cpu().numpy()
+    multi = k.solve_ik_beam_multi(m, ["flange"], tgt[:, None, :], rng_seed=77, precision="fp64")
+    chain = k.solve_ik_beam_batch(m, "flange", tgt, rng_seed=77, precision="fp64")
+    rel = np.abs(multi.history - chain.history) / chain.history
+    assert np.mean(rel.max(axis=1) < 1e-6) >= 0.9
+    assert np.mean(multi.success.astype(bool) == chain.success.astype(bool)) >= 0.98

@@ -250,3 +250,19 @@ def test_host_collision_distance_helpers_match_oracle():
             np.testing.assert_allclose([d], d_o, atol=1e-14)
             np.testing.assert_allclose(ga, ga_o[0], atol=1e-14)
             np.testing.assert_allclose(gb, gb_o[0], atol=1e-14)
+
+
+def test_multi_ee_beam_reduces_to_ik_beam(chains, golden):
+    """The config-3 multi-end-effector beam oracle with one end effector is the
+    single-link IK-Beam restatement (itself bit-equal to the reference goldens)."""
+    from oracle import tree_oracle as tro
+
+    ch = chains["arm7"]
+    tq, tt = golden["targets_arm7_77_wxyz"][:6], golden["targets_arm7_77_pos"][:6]
+    seeds = golden["seeds_arm7_77"]
+    one = o.ik_beam(ch, 8, tq, tt, seeds)
+    multi = tro.multi_ee_beam(ch, [8], tq[:, None], tt[:, None], seeds, [50.0], [10.0])
+    np.testing.assert_array_equal(multi["q"], one.q)
+    np.testing.assert_array_equal(multi["hist"], one.hist)
+    np.testing.assert_array_equal(multi["pos_err"][:, 0], one.pos_err)
+    np.testing.assert_array_equal(multi["success"], one.success)
