@@ -227,3 +227,26 @@ for prec in ("fp32", "fp64"):
                       "mean_iterations": outs[4].float().mean().item(),
                       "final_cost_p50": outs[1].median().item(),
                       "roofline": roofline("config3 humanoid multi-EE IK", prec, NH / ms * 1e3)}), flush=True)
+# config 3 in the SURVEY H6 flavour: multi-end-effector IK-Beam (64 seeds, 6 + 10 lane-LM steps, keep 4)
+for prec in ("fp32", "fp64"):
+    nb = NH if prec == "fp32" else min(NH, 20000)
+    k.solve_ik_beam_multi(hum, EES, tgh[:nb], precision=prec, device_out=True)
+    torch.cuda.synchronize()
+    t0e, t1e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0e.record()
+    res = k.solve_ik_beam_multi(hum, EES, tgh[:nb], precision=prec, device_out=True)
+    t1e.record(); torch.cuda.synchronize()
+    ms = t0e.elapsed_time(t1e)
+    cpu = None
+    if prec == "fp64" and CPU:
+        chh = o.load_chain_files(k.robot_path("humanoid29.urdf"))
+        tgc = tgh[:2].cpu().numpy()
+        links = [chh.link(e) for e in EES]
+        seeds = o.sample_seeds(chh, 64, 0)
+        cpu = cpu_time(lambda: tro.multi_ee_beam(chh, links, tgc[:, :, :4], tgc[:, :, 4:], seeds, [50.0] * 4,
+                                                 [10.0] * 4), 2, "solves/s",
+                       "2 target sets of this workload, oracle port (float64 NumPy), 1 core")
+    print(json.dumps({"cpu_baseline": cpu, "workload": "config3 humanoid multi-EE IK-Beam (n=29, 4 end effectors, "
+                      "64 seeds, 6+10 lane-LM steps, keep 4; SURVEY 8 H6)", "precision": prec, "targets": nb,
+                      "ms": ms, "solves_per_s": nb / ms * 1e3, "success": res.success.float().mean().item()}),
+          flush=True)

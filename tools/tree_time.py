@@ -37,3 +37,17 @@ ms = e0.elapsed_time(e1) / REPS
 print(json.dumps({"precision": PREC, "problems": NH, "ms": ms, "solves_per_s": NH / ms * 1e3,
                   "mean_iterations": outs[4].float().mean().item(), "cost_p50": outs[1].median().item(),
                   "terminations": torch.bincount(outs[5].long(), minlength=6).tolist()}))
+# multi-EE IK-Beam on the same targets (SURVEY H6 flavour of config 3)
+if os.environ.get("BEAM", "1") == "1":
+    NB = int(os.environ.get("NBEAM", str(NH)))
+    k.solve_ik_beam_multi(hum, EES, tgh[:NB], precision=PREC, device_out=True)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(REPS):
+        r = k.solve_ik_beam_multi(hum, EES, tgh[:NB], precision=PREC, device_out=True)
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / REPS
+    print(json.dumps({"workload": "multi-EE IK-Beam", "precision": PREC, "targets": NB, "ms": ms,
+                      "solves_per_s": NB / ms * 1e3, "success": r.success.float().mean().item(),
+                      "pos_err_p50": r.pos_error.median().item()}))
