@@ -25,6 +25,8 @@ WORK = [
     ("config5 trajectory optimisation T=64", "k_traj_solve", "double", 148),
     ("config3 humanoid multi-EE IK", "k_tree_solve", "float", 2000),
     ("config3 humanoid multi-EE IK", "k_tree_solve", "double", 2000),
+    ("config3 humanoid multi-EE IK-Beam", ("k_tree_beam_stage", "k_tree_beam_prune"), "float", 2000),
+    ("config3 humanoid multi-EE IK-Beam", ("k_tree_beam_stage", "k_tree_beam_prune"), "double", 2000),
 ]
 
 
@@ -85,6 +87,9 @@ def run():
         check(lib().kop_multi_pose_solve(hum._handle, C.byref(hp.costs), C.byref(opts), dv.ptr(tgh), dv.ptr(q0), n,
                                          *(dv.ptr(x) for x in outs), dv.stream_handle()), "tree")
     torch.cuda.synchronize()
+    for prec in ("fp32", "fp64"):  # multi-EE IK-Beam; the prune kernel is attributed to both (no FP work)
+        k.solve_ik_beam_multi(hum, ees, tgh, precision=prec, device_out=True)
+    torch.cuda.synchronize()
 
 
 def parse(path):
@@ -106,7 +111,8 @@ def parse(path):
             subs = sub if isinstance(sub, tuple) else (sub,)
             if not any(x in kname for x in subs):
                 continue
-            if "k_beam_errors" not in kname and not any(t in kname for t in (f"Cfg<{prec}", f"<{prec}>", f"<{prec},")):
+            if ("k_beam_errors" not in kname and "k_tree_beam_prune" not in kname
+                    and not any(t in kname for t in (f"Cfg<{prec}", f"<{prec}>", f"<{prec},"))):
                 continue
             if sub == "k_beam_stage" and "1, 1>" not in kname.replace("true", "1"):
                 continue  # mobile: BASE shapes only
