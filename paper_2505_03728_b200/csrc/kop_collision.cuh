@@ -300,7 +300,8 @@ __device__ __forceinline__ void col_forward(const ChainParams<typename G::T, G::
 // SCREEN: a first distance-only pass skips rows that are inactive on every
 // lane of the warp (pays off when most rows are far from every obstacle, as in
 // trajectories; in IK-Beam the seeds of a warp rarely agree, so it is off).
-template <class G, bool JAC, class OB = CollisionParams<typename G::T>, bool SCREEN = false>
+// PART: bit 0 world rows, bit 1 self rows (trajectories split them over two threads).
+template <class G, bool JAC, class OB = CollisionParams<typename G::T>, bool SCREEN = false, int PART = 3>
 __device__ __forceinline__ typename G::T col_rows(const ChainParams<typename G::T, G::K>& C,
                                                   const CollisionParams<typename G::T>& P, const ColLane<G>& L,
                                                   typename G::T (&A)[Tri<G::ND>::size], typename G::T (&g)[G::ND],
@@ -311,7 +312,7 @@ __device__ __forceinline__ typename G::T col_rows(const ChainParams<typename G::
   const OB& O = obs ? *obs : reinterpret_cast<const OB&>(P);
   T cost = T(0);
   // ---- world rows: (sphere link, obstacle), costs.py:499-551 ---------------
-  if (P.w_world > T(0)) {
+  if ((PART & 1) && P.w_world > T(0)) {
     for (int li = 0; li < P.nl; ++li) {
       const int f = P.lfirst[li], nsph = P.lcount[li];
       for (int o = 0; o < O.no; ++o, ++row) {
@@ -365,7 +366,7 @@ __device__ __forceinline__ typename G::T col_rows(const ChainParams<typename G::
   }
 
   // ---- self rows: link pairs, costs.py:435-496 ------------------------------
-  if (P.w_self > T(0)) {
+  if ((PART & 2) && P.w_self > T(0)) {
     for (int pi = 0; pi < P.np; ++pi, ++row) {
       const int la = P.pa[pi], lb = P.pb[pi];
       const int fa = P.lfirst[la], na = P.lcount[la], fb = P.lfirst[lb], nb = P.lcount[lb];

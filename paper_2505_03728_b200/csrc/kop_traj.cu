@@ -48,12 +48,12 @@ struct TrajView {
   using T = typename G::T;
   static constexpr int NQ = G::NQ, BW = 4 * NQ, NT = Tri<NQ>::size, HB = NT + NQ * NQ + 3 * NQ;
   ObstacleTable<T>* obs;
-  T *red, *anc, *q, *qn, *g, *y, *dinv, *H, *L, *scratch, *pbufA, *pbufg;
+  T *red, *anc, *q, *qn, *g, *y, *dinv, *H, *L, *scratch, *pbufA, *pbufg, *sbuf;
   int steps;
   __host__ __device__ static size_t bytes(int steps, int ns) {
     const size_t N = (size_t)steps * NQ;
     const size_t band = N * (BW + 1);
-    const size_t uni_b = (size_t)(6 * G::K + 3 * ns) * steps + (size_t)steps * (NT + NQ);
+    const size_t uni_b = (size_t)(6 * G::K + 3 * ns) * steps + (size_t)steps * (NT + NQ) * 2;
     const size_t head = (sizeof(ObstacleTable<T>) + 15) / 16 * 16;
     return head + sizeof(T) * (kTrajThreads + 2 * NQ + 5 * N + (size_t)steps * HB + (band > uni_b ? band : uni_b));
   }
@@ -72,7 +72,8 @@ struct TrajView {
     L = p;
     scratch = p; p += (6 * G::K + 3 * ns) * steps;
     pbufA = p; p += steps * NT;
-    pbufg = p;
+    pbufg = p; p += steps * NQ;
+    sbuf = p;  // self-row normal equations of each timestep (NT + NQ), from thread t + 64
   }
   __device__ __forceinline__ T* hd(int t) const { return H + t * HB; }            // D_t
   __device__ __forceinline__ T* hx(int t) const { return H + t * HB + NT; }       // X_t
@@ -249,14 +250,36 @@ __device__ typename G::T traj_eval(const ChainParams<typename G::T, G::K>& C, co
 #pragma unroll
   for (int i = 0; i < NQ; ++i) prevA_diag[i] = prev_g[i] = T(0);
   const int t = tid;
+  if (t < Tn) {  // FK of timestep t: Pluecker axes and sphere centres into the lane scratch
+    T q[NQ];
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) q[i] = x[t * NQ + i];
+    quat<T> eq;
+    vec3<T> ep;
+    col_forward<G>(C, P, S.lane(t), q, eq, ep);
+  }
+  __syncthreads();
+  const bool self_rows = P.np > 0 && P.w_self > T(0);
+  if (tid >= 64 && tid - 64 < Tn && self_rows) {  // self rows of timestep tid - 64, beside thread tid - 64
+    const int u = tid - 64;
+    T As[NT], gs[NQ];
+#pragma unroll
+    for (int i = 0; i < NT; ++i) As[i] = T(0);
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) gs[i] = T(0);
+    cost += col_rows<G, JAC, ObstacleTable<T>, true, 2>(C, P, S.lane(u), As, gs, 0, nullptr, nullptr, S.obs);
+    if (JAC) {
+#pragma unroll
+      for (int i = 0; i < NT; ++i) S.sbuf[u * (NT + NQ) + i] = As[i];
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) S.sbuf[u * (NT + NQ) + NT + i] = gs[i];
+    }
+  }
   if (t < Tn) {
     T q[NQ];
 #pragma unroll
     for (int i = 0; i < NQ; ++i) q[i] = x[t * NQ + i];
     const ColLane<G> L = S.lane(t);
-    quat<T> eq;
-    vec3<T> ep;
-    col_forward<G>(C, P, L, q, eq, ep);
     // limit (costs.py:174-195), rest (tasks.py:386-389), anchors (tasks.py:352-355)
 #pragma unroll
     for (int i = 0; i < NQ; ++i) {
@@ -274,8 +297,8 @@ __device__ typename G::T traj_eval(const ChainParams<typename G::T, G::K>& C, co
         gd[i] += W.anchor * ra;
       }
     }
-    // world + self rows (world uses the per-problem obstacle table)
-    cost += col_rows<G, JAC, ObstacleTable<T>, true>(C, P, L, Ad, gd, 0, nullptr, nullptr, S.obs);
+    // world rows (per-problem obstacle table); the self rows run on thread t + 64
+    cost += col_rows<G, JAC, ObstacleTable<T>, true, 1>(C, P, L, Ad, gd, 0, nullptr, nullptr, S.obs);
     // smoothness + velocity of the pair (t-1, t) (costs.py:198-231, 274-290)
     if (t >= 1) {
 #pragma unroll
@@ -411,6 +434,12 @@ __device__ typename G::T traj_eval(const ChainParams<typename G::T, G::K>& C, co
       for (int i = 0; i < NT; ++i) Ad[i] += S.pbufA[(t + 1) * NT + i];
 #pragma unroll
       for (int i = 0; i < NQ; ++i) gd[i] += S.pbufg[(t + 1) * NQ + i];
+    }
+    if (self_rows) {
+#pragma unroll
+      for (int i = 0; i < NT; ++i) Ad[i] += S.sbuf[t * (NT + NQ) + i];
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) gd[i] += S.sbuf[t * (NT + NQ) + NT + i];
     }
 #pragma unroll
     for (int a = 0; a < NQ; ++a) {
