@@ -48,12 +48,12 @@ struct TrajView {
   using T = typename G::T;
   static constexpr int NQ = G::NQ, BW = 4 * NQ, NT = Tri<NQ>::size, HB = NT + NQ * NQ + 3 * NQ;
   ObstacleTable<T>* obs;
-  T *red, *anc, *q, *qn, *g, *y, *dinv, *H, *L, *scratch, *pbufA, *pbufg, *sbuf;
+  T *red, *anc, *q, *qn, *g, *y, *dinv, *H, *L, *scratch, *pbufA, *pbufg, *sbuf, *dbuf;
   int steps;
   __host__ __device__ static size_t bytes(int steps, int ns) {
     const size_t N = (size_t)steps * NQ;
     const size_t band = N * (BW + 1);
-    const size_t uni_b = (size_t)(6 * G::K + 3 * ns) * steps + (size_t)steps * (NT + NQ) * 2;
+    const size_t uni_b = (size_t)(6 * G::K + 3 * ns) * steps + (size_t)steps * ((NT + NQ) * 2 + 2 * NQ);
     const size_t head = (sizeof(ObstacleTable<T>) + 15) / 16 * 16;
     return head + sizeof(T) * (kTrajThreads + 2 * NQ + 5 * N + (size_t)steps * HB + (band > uni_b ? band : uni_b));
   }
@@ -73,7 +73,8 @@ struct TrajView {
     scratch = p; p += (6 * G::K + 3 * ns) * steps;
     pbufA = p; p += steps * NT;
     pbufg = p; p += steps * NQ;
-    sbuf = p;  // self-row normal equations of each timestep (NT + NQ), from thread t + 64
+    sbuf = p; p += steps * (NT + NQ);  // block t parts of thread t + 64's rows (self, swept)
+    dbuf = p;  // diagonal block t-1 parts of the smoothness / velocity rows of pair (t-1, t)
   }
   __device__ __forceinline__ T* hd(int t) const { return H + t * HB; }            // D_t
   __device__ __forceinline__ T* hx(int t) const { return H + t * HB + NT; }       // X_t
@@ -228,6 +229,80 @@ __device__ __forceinline__ void col_row_entries(const ChainParams<typename G::T,
   }
 }
 
+// Swept-capsule rows of the pair (t-1, t) (costs.py:554-619): cost, the block
+// t-1 part (pA, pg), the block t part (Ad, gd) and the cross block H(t, t-1)
+// written into t's own compact rows.
+template <class G, bool JAC>
+__device__ __forceinline__ typename G::T traj_swept_rows(const ChainParams<typename G::T, G::K>& C,
+                                                         const CollisionParams<typename G::T>& P,
+                                                         const TrajCosts<typename G::T>& W, const TrajView<G>& S,
+                                                         int t, typename G::T (&pA)[Tri<G::NQ>::size],
+                                                         typename G::T (&pg)[G::NQ],
+                                                         typename G::T (&Ad)[Tri<G::NQ>::size],
+                                                         typename G::T (&gd)[G::NQ]) {
+  using T = typename G::T;
+  constexpr int NQ = G::NQ;
+  T cost = T(0);
+  const ColLane<G> L0 = S.lane(t - 1), L1 = S.lane(t);
+  for (int li = 0; li < P.nl; ++li) {
+    const int f = P.lfirst[li], nsph = P.lcount[li];
+    for (int o = 0; o < S.obs->no; ++o) {
+      {  // screening, as in col_rows: skip rows inactive on every lane of the warp
+        T dscr = inf_t<T>();
+        for (int s = 0; s < nsph; ++s) {
+          vec3<T> ga, gb;
+          dscr = tmin(dscr, capsule_obstacle_t<T>(
+                                *S.obs, o, vec3<T>{L0.cen(f + s, 0), L0.cen(f + s, 1), L0.cen(f + s, 2)},
+                                vec3<T>{L1.cen(f + s, 0), L1.cen(f + s, 1), L1.cen(f + s, 2)}, P.sr[f + s], ga, gb));
+        }
+        if (__all_sync(__activemask(), dscr - P.lreach[li] > W.eta_world * T(1.00001))) continue;
+      }
+      const bool hard = P.hard || nsph == 1;
+      SoftMin<T, 4> sm;  // sum z c0 x ga, sum z ga, sum z c1 x gb, sum z gb
+      for (int s = 0; s < nsph; ++s) {
+        const vec3<T> c0{L0.cen(f + s, 0), L0.cen(f + s, 1), L0.cen(f + s, 2)};
+        const vec3<T> c1{L1.cen(f + s, 0), L1.cen(f + s, 1), L1.cen(f + s, 2)};
+        vec3<T> ga, gb;
+        const T d = capsule_obstacle_t<T>(*S.obs, o, c0, c1, P.sr[f + s], ga, gb);
+        const T z = sm.weight(d, P.beta, hard);
+        if (z == T(0)) continue;  // zero weights add nothing (the reference skips them, costs.py:541)
+        sm.sumz += z;
+        if (JAC) {
+          sm.add(z, 0, cross(c0, ga));
+          sm.add(z, 1, ga);
+          sm.add(z, 2, cross(c1, gb));
+          sm.add(z, 3, gb);
+        }
+      }
+      T act, dact;
+      activation_t(sm.aggregate(P.beta, hard), W.eta_world, act, dact);
+      const T res = W.w_world * act;
+      cost += res * res;
+      if (JAC && dact != T(0)) {
+        sm.normalise();
+        const vec3<T> M0 = sm.acc[0], G0 = sm.acc[1], M1 = sm.acc[2], G1 = sm.acc[3];
+        T j0[NQ], j1[NQ];
+        col_row_entries<G>(C, L0, P.lslot[li], M0, G0, W.w_world * dact, j0);
+        col_row_entries<G>(C, L1, P.lslot[li], M1, G1, W.w_world * dact, j1);
+#pragma unroll
+        for (int a = 0; a < NQ; ++a) {
+#pragma unroll
+          for (int b = 0; b < NQ; ++b) {
+            if (b <= a) {
+              pA[Tri<NQ>::at(a, b)] += j0[a] * j0[b];
+              Ad[Tri<NQ>::at(a, b)] += j1[a] * j1[b];
+            }
+            S.hx(t)[a * NQ + b] += j1[a] * j0[b];  // H(t, t-1) block, own rows
+          }
+          pg[a] += j0[a] * res;
+          gd[a] += j1[a] * res;
+        }
+      }
+    }
+  }
+  return cost;
+}
+
 // Evaluate the trajectory stack at x (S.q or S.qn); JAC also forms the band
 // H and g.  Returns the cost on every thread.
 template <class G, bool JAC>
@@ -257,17 +332,37 @@ __device__ typename G::T traj_eval(const ChainParams<typename G::T, G::K>& C, co
     quat<T> eq;
     vec3<T> ep;
     col_forward<G>(C, P, S.lane(t), q, eq, ep);
+    if (JAC)  // the (t, t-1) block is accumulated by thread t + 64 (swept rows) and t (diagonal rows)
+      for (int i = 0; i < NQ * NQ; ++i) S.hx(t)[i] = T(0);
   }
   __syncthreads();
+  // thread t + 64: the self rows of timestep t and the swept rows of the pair
+  // (t-1, t), beside thread t's local / world / smoothness / stencil rows
   const bool self_rows = P.np > 0 && P.w_self > T(0);
-  if (tid >= 64 && tid - 64 < Tn && self_rows) {  // self rows of timestep tid - 64, beside thread tid - 64
+  const bool swept_rows = W.w_world > T(0) && S.obs->no > 0;
+  if (tid >= 64 && tid - 64 < Tn && (self_rows || swept_rows)) {
     const int u = tid - 64;
     T As[NT], gs[NQ];
 #pragma unroll
     for (int i = 0; i < NT; ++i) As[i] = T(0);
 #pragma unroll
     for (int i = 0; i < NQ; ++i) gs[i] = T(0);
-    cost += col_rows<G, JAC, ObstacleTable<T>, true, 2>(C, P, S.lane(u), As, gs, 0, nullptr, nullptr, S.obs);
+    if (self_rows)
+      cost += col_rows<G, JAC, ObstacleTable<T>, true, 2>(C, P, S.lane(u), As, gs, 0, nullptr, nullptr, S.obs);
+    if (swept_rows && u >= 1) {
+      T pA[NT], pg[NQ];  // block u-1 part
+#pragma unroll
+      for (int i = 0; i < NT; ++i) pA[i] = T(0);
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) pg[i] = T(0);
+      cost += traj_swept_rows<G, JAC>(C, P, W, S, u, pA, pg, As, gs);
+      if (JAC) {
+#pragma unroll
+        for (int i = 0; i < NT; ++i) S.pbufA[u * NT + i] = pA[i];
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) S.pbufg[u * NQ + i] = pg[i];
+      }
+    }
     if (JAC) {
 #pragma unroll
       for (int i = 0; i < NT; ++i) S.sbuf[u * (NT + NQ) + i] = As[i];
@@ -348,94 +443,30 @@ __device__ typename G::T traj_eval(const ChainParams<typename G::T, G::K>& C, co
       }
     }
   }
-  if (JAC && t < Tn) {  // own band rows: clear, then write the local parts
-    for (int i = 0; i < NQ; ++i)
-      for (int b = 0; b < NQ; ++b) S.hx(t)[i * NQ + b] = T(0);
-  }
-  __syncthreads();
-  // ---- B: swept-capsule rows of the pair (t-1, t) -----------------------------
-  T pA[NT], pg[NQ];  // contribution to block t-1
+  if (JAC && t >= 1 && t < Tn) {  // diagonal rows' block t-1 part of the pair (t-1, t)
 #pragma unroll
-  for (int i = 0; i < NT; ++i) pA[i] = T(0);
-#pragma unroll
-  for (int i = 0; i < NQ; ++i) pg[i] = prev_g[i];
-#pragma unroll
-  for (int i = 0; i < NQ; ++i) pA[Tri<NQ>::at(i, i)] = prevA_diag[i];
-  if (t >= 1 && t < Tn && W.w_world > T(0) && S.obs->no > 0) {
-    const ColLane<G> L0 = S.lane(t - 1), L1 = S.lane(t);
-    for (int li = 0; li < P.nl; ++li) {
-      const int f = P.lfirst[li], nsph = P.lcount[li];
-      for (int o = 0; o < S.obs->no; ++o) {
-        {  // screening, as in col_rows: skip rows inactive on every lane of the warp
-          T dscr = inf_t<T>();
-          for (int s = 0; s < nsph; ++s) {
-            vec3<T> ga, gb;
-            dscr = tmin(dscr, capsule_obstacle_t<T>(
-                                  *S.obs, o, vec3<T>{L0.cen(f + s, 0), L0.cen(f + s, 1), L0.cen(f + s, 2)},
-                                  vec3<T>{L1.cen(f + s, 0), L1.cen(f + s, 1), L1.cen(f + s, 2)}, P.sr[f + s], ga, gb));
-          }
-          if (__all_sync(__activemask(), dscr - P.lreach[li] > W.eta_world * T(1.00001))) continue;
-        }
-        const bool hard = P.hard || nsph == 1;
-        SoftMin<T, 4> sm;  // sum z c0 x ga, sum z ga, sum z c1 x gb, sum z gb
-        for (int s = 0; s < nsph; ++s) {
-          const vec3<T> c0{L0.cen(f + s, 0), L0.cen(f + s, 1), L0.cen(f + s, 2)};
-          const vec3<T> c1{L1.cen(f + s, 0), L1.cen(f + s, 1), L1.cen(f + s, 2)};
-          vec3<T> ga, gb;
-          const T d = capsule_obstacle_t<T>(*S.obs, o, c0, c1, P.sr[f + s], ga, gb);
-          const T z = sm.weight(d, P.beta, hard);
-          if (z == T(0)) continue;  // zero weights add nothing (the reference skips them, costs.py:541)
-          sm.sumz += z;
-          if (JAC) {
-            sm.add(z, 0, cross(c0, ga));
-            sm.add(z, 1, ga);
-            sm.add(z, 2, cross(c1, gb));
-            sm.add(z, 3, gb);
-          }
-        }
-        T act, dact;
-        activation_t(sm.aggregate(P.beta, hard), W.eta_world, act, dact);
-        const T res = W.w_world * act;
-        cost += res * res;
-        if (JAC && dact != T(0)) {
-          sm.normalise();
-          const vec3<T> M0 = sm.acc[0], G0 = sm.acc[1], M1 = sm.acc[2], G1 = sm.acc[3];
-          T j0[NQ], j1[NQ];
-          col_row_entries<G>(C, L0, P.lslot[li], M0, G0, W.w_world * dact, j0);
-          col_row_entries<G>(C, L1, P.lslot[li], M1, G1, W.w_world * dact, j1);
-#pragma unroll
-          for (int a = 0; a < NQ; ++a) {
-#pragma unroll
-            for (int b = 0; b < NQ; ++b) {
-              if (b <= a) {
-                pA[Tri<NQ>::at(a, b)] += j0[a] * j0[b];
-                Ad[Tri<NQ>::at(a, b)] += j1[a] * j1[b];
-              }
-              S.hx(t)[a * NQ + b] += j1[a] * j0[b];  // H(t, t-1) block, own rows
-            }
-            pg[a] += j0[a] * res;
-            gd[a] += j1[a] * res;
-          }
-        }
-      }
+    for (int i = 0; i < NQ; ++i) {
+      S.dbuf[t * 2 * NQ + i] = prevA_diag[i];
+      S.dbuf[t * 2 * NQ + NQ + i] = prev_g[i];
     }
-  }
-  if (JAC && t >= 1 && t < Tn) {
-#pragma unroll
-    for (int i = 0; i < NT; ++i) S.pbufA[(t) * NT + i] = pA[i];
-#pragma unroll
-    for (int i = 0; i < NQ; ++i) S.pbufg[(t) * NQ + i] = pg[i];
   }
   __syncthreads();
   // ---- C: assemble own block row -------------------------------------------------
   if (JAC && t < Tn) {
     if (t + 1 < Tn) {
 #pragma unroll
-      for (int i = 0; i < NT; ++i) Ad[i] += S.pbufA[(t + 1) * NT + i];
+      for (int i = 0; i < NQ; ++i) {
+        Ad[Tri<NQ>::at(i, i)] += S.dbuf[(t + 1) * 2 * NQ + i];
+        gd[i] += S.dbuf[(t + 1) * 2 * NQ + NQ + i];
+      }
+      if (swept_rows) {
 #pragma unroll
-      for (int i = 0; i < NQ; ++i) gd[i] += S.pbufg[(t + 1) * NQ + i];
+        for (int i = 0; i < NT; ++i) Ad[i] += S.pbufA[(t + 1) * NT + i];
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) gd[i] += S.pbufg[(t + 1) * NQ + i];
+      }
     }
-    if (self_rows) {
+    if (self_rows || swept_rows) {
 #pragma unroll
       for (int i = 0; i < NT; ++i) Ad[i] += S.sbuf[t * (NT + NQ) + i];
 #pragma unroll
