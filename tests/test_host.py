@@ -239,3 +239,36 @@ def test_widened_apis_have_no_cpu_fallback(models):
                                         goal_pose=k.Transform3.identity()))
     with pytest.raises(RuntimeError, match="no CPU fallback"):
         k.solve_ik_collision_batch(m, "flange", np.array([[1.0, 0, 0, 0, 0.4, 0.0, 0.5]]), world=world)
+
+
+@pytest.mark.parametrize("seed,n,fixed,pri,mim", [(1, 7, 2, True, True), (2, 6, 1, True, False),
+                                                  (3, 5, 0, False, True), (4, 3, 3, True, True),
+                                                  (5, 8, 2, False, False), (6, 7, 1, True, True)])
+def test_random_robot_tables_and_compiled_chain(seed, n, fixed, pri, mim):
+    """Random serial robots (tests/random_robots.py): parsed tables equal the
+    oracle's and the compiled +z-aligned chain composes to the oracle's FK."""
+    from random_robots import random_chain_urdf
+
+    doc = random_chain_urdf(seed, n, fixed, pri, mim)
+    m, ch = k.parse_urdf(doc), o.load_chain(doc)
+    np.testing.assert_array_equal(m.lower_limits, ch.lower)
+    np.testing.assert_array_equal(m.upper_limits, ch.upper)
+    np.testing.assert_allclose(m.rest_pose, ch.rest)
+    c = m.compiled_chain("tool")
+    li = ch.link("tool")
+    rng = np.random.default_rng(seed)
+    for _ in range(10):
+        q = o.sample_configuration(ch, rng)
+        pq, pp = np.array([1.0, 0, 0, 0]), np.zeros(3)
+        for j in range(len(c["qcol"])):
+            fq = o.qmul(pq, c["tq"][j])
+            fp = pp + o.qrot(pq, c["tp"][j])
+            th = q[c["qcol"][j]] * c["mult"][j] + c["offset"][j]
+            if c["prismatic"][j]:
+                pq, pp = fq, fp + th * o.qrot(fq, np.array([0, 0, 1.0]))
+            else:
+                pq, pp = o.qmul(fq, np.array([np.cos(th / 2), 0, 0, np.sin(th / 2)])), fp
+        eq, ep = o.qmul(pq, c["ee"][:4]), pp + o.qrot(pq, c["ee"][4:])
+        lq, lp, _, _ = o.fk(ch, q[None])
+        assert np.allclose(o.qcanon(eq), o.qcanon(lq[0, li]), atol=1e-12)
+        assert np.allclose(ep, lp[0, li], atol=1e-12)
