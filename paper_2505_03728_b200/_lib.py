@@ -11,7 +11,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libkinoptik_b200.so")
+# KOP_LIB selects another in-tree build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("KOP_LIB") or os.path.join(_HERE, "libkinoptik_b200.so")
 
 KOP_OK, KOP_EINVAL, KOP_EUNSUPPORTED, KOP_ECUDA = 0, -1, -2, -3
 KOP_FP32, KOP_FP64 = 0, 1

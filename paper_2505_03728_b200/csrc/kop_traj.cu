@@ -23,10 +23,12 @@
 //      thread t-1 through a per-pair buffer.
 //   C  thread t adds the handed-over part; block reduction of the cost.
 // LM: gradient test, banded Cholesky of H + lam diag(max(diag H, 1e-8)) with
-// two barriers per column, triangular solves by warp 0, rejection loop,
+// two barriers per timestep block, triangular solves by warp 0, rejection loop,
 // terminations -- the semantics of solver.solve.
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <type_traits>
 
 #include "kop_beam.cuh"
 #include "kop_collision.cuh"
@@ -35,33 +37,93 @@
 
 namespace kop {
 
-constexpr int kTrajThreads = 128;
+// Threads per trajectory CTA: 128 (4 warps) for FP32, whose CTAs (89 KB of
+// shared memory at T = 64) run two per SM; 256 (8 warps, the two-sided
+// factorisation) for FP64, whose 175 KB CTAs run one per SM.
+// Trailing-update pairs per thread: FP32 holds its table entries in registers
+// for the whole sweep and issues 4 dot products together; FP64, at the
+// register cap, reads one entry of the shared table per dot product (measured
+// at T = 64: both +30% / +0% over the other choice in FP64 / FP32).
+#ifndef KOP_TRAJ_CH32
+#define KOP_TRAJ_CH32 4
+#endif
+#ifndef KOP_TRAJ_CH64
+#define KOP_TRAJ_CH64 1
+#endif
+#ifndef KOP_TRAJ_FP32_THREADS
+#define KOP_TRAJ_FP32_THREADS 128
+#endif
+template <class G>
+constexpr int traj_threads() {
+  return std::is_same<typename G::T, double>::value ? 256 : KOP_TRAJ_FP32_THREADS;
+}
+
+#ifdef KOP_TRAJ_TIMELINE
+// debug timeline of the first damped solve of CTA 0: [role][block][event] clock64 stamps
+__device__ long long g_traj_tl[4][72][6];
+__device__ int g_traj_tl_on = 1;
+__device__ __forceinline__ long long tl_clock() {
+  long long t;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(t)::"memory");
+  return t;
+}
+#define KOP_TL(role, blk, ev) \
+  if (blockIdx.x == 0 && g_traj_tl_on && (threadIdx.x & 31) == 0 && (role) < 4 && (blk) < 72) g_traj_tl[role][blk][ev] = tl_clock()
+#else
+#define KOP_TL(role, blk, ev)
+#endif
+
+#ifdef KOP_TRAJ_PROFILE
+// debug instrumentation (tools/build_variant.py NAME -DKOP_TRAJ_PROFILE): clock64
+// cycles of thread 0 per phase, summed over CTAs:
+//   0 eval+J, 1 eval, 2 solve setup, 3 factor loop, 4 back substitution, 5 #solves, 6 #evals+J, 7 #evals,
+//   per block of a sweep (main lane 0): 8.. top sweep, 12.. bottom sweep, 16.. separator sweep:
+//   +0 rows, +1 barrier 1, +2 diagonal pairs + factor, +3 barrier 2
+__device__ unsigned long long g_traj_prof[20];
+#define KOP_PROF_T(v) long long v = clock64()
+#define KOP_PROF_SET(v) v = clock64()
+#define KOP_PROF_ADD(slot, cycles) \
+  if (threadIdx.x == 0) atomicAdd(&g_traj_prof[slot], (unsigned long long)(cycles))
+#else
+#define KOP_PROF_T(v)
+#define KOP_PROF_SET(v)
+#define KOP_PROF_ADD(slot, cycles)
+#endif
 
 // Shared-memory layout, sized by the trajectory length at launch:
-//   obstacle table | reduction buffer | q, qn, g, y, 1/diag(L)  [N each]
+//   obstacle table | trailing-update pair table | reduction buffer | q, qn, g, y, 1/diag(L)  [N each]
 //   H compact [T x HB]: per timestep D (lower NT) | X = H(t, t-1) (NQ^2, row-major) | E2, E3, E4 (NQ each)
-//   union { L band [N x (BW+1)], L(i, i-d) at [i][d]  |  FK scratch [(6K + 3 ns) x T] + pair buffers }
+//   union { L band [N x LW], L(i, i-d) at [i][d]  |  FK scratch [(6K + 3 ns) x T] + pair buffers }
 // The union is safe: L lives from the factorisation to the end of the
 // triangular solves, the scratch and pair buffers only inside an evaluation.
 template <class G>
 struct TrajView {
   using T = typename G::T;
   static constexpr int NQ = G::NQ, BW = 4 * NQ, NT = Tri<NQ>::size, HB = NT + NQ * NQ + 3 * NQ;
+  // trailing-update pairs (ri, ci), NQ <= ri < BW, 0 <= ci <= ri, taken by warps 1..3
+  static constexpr int NPAIR = BW * (BW + 1) / 2 - NT;
+  // band row stride: BW + 1 entries and one pad, so that rows r, r + 1 of one
+  // block column (stride LW + 1) fall in different banks
+  static constexpr int LW = BW + 2;
+  static constexpr int TH = traj_threads<G>();
+  static constexpr bool TWIST = TH == 256;  // two-sided factorisation
+  static constexpr size_t kHead = (sizeof(ObstacleTable<T>) + 15) / 16 * 16 + (NPAIR * 2 + 15) / 16 * 16;
   ObstacleTable<T>* obs;
+  uint16_t* pairs;  // ri | ci << 8
   T *red, *anc, *q, *qn, *g, *y, *dinv, *H, *L, *scratch, *pbufA, *pbufg, *sbuf, *dbuf;
   int steps;
   __host__ __device__ static size_t bytes(int steps, int ns) {
     const size_t N = (size_t)steps * NQ;
-    const size_t band = N * (BW + 1);
+    const size_t band = N * LW;
     const size_t uni_b = (size_t)(6 * G::K + 3 * ns) * steps + (size_t)steps * ((NT + NQ) * 2 + 2 * NQ);
-    const size_t head = (sizeof(ObstacleTable<T>) + 15) / 16 * 16;
-    return head + sizeof(T) * (kTrajThreads + 2 * NQ + 5 * N + (size_t)steps * HB + (band > uni_b ? band : uni_b));
+    return kHead + sizeof(T) * (TH + 2 * NQ + 5 * N + (size_t)steps * HB + (band > uni_b ? band : uni_b));
   }
   __device__ TrajView(unsigned char* base, int steps_, int ns) : steps(steps_) {
     const int N = steps * NQ;
     obs = reinterpret_cast<ObstacleTable<T>*>(base);
-    T* p = reinterpret_cast<T*>(base + (sizeof(ObstacleTable<T>) + 15) / 16 * 16);
-    red = p; p += kTrajThreads;
+    pairs = reinterpret_cast<uint16_t*>(base + (sizeof(ObstacleTable<T>) + 15) / 16 * 16);
+    T* p = reinterpret_cast<T*>(base + kHead);
+    red = p; p += TH;
     anc = p; p += 2 * NQ;
     q = p; p += N;
     qn = p; p += N;
@@ -76,6 +138,17 @@ struct TrajView {
     sbuf = p; p += steps * (NT + NQ);  // block t parts of thread t + 64's rows (self, swept)
     dbuf = p;  // diagonal block t-1 parts of the smoothness / velocity rows of pair (t-1, t)
   }
+  // pair q of the trailing update, in the order (ri = NQ, ci = 0..ri), (ri = NQ + 1, ...), ...
+  __device__ void build_pairs() const {
+    for (int q = threadIdx.x; q < NPAIR; q += blockDim.x) {
+      int ri = NQ, base = 0;
+      while (q >= base + ri + 1) {
+        base += ri + 1;
+        ++ri;
+      }
+      pairs[q] = uint16_t(ri | (q - base) << 8);
+    }
+  }
   __device__ __forceinline__ T* hd(int t) const { return H + t * HB; }            // D_t
   __device__ __forceinline__ T* hx(int t) const { return H + t * HB + NT; }       // X_t
   __device__ __forceinline__ T* he(int t) const { return H + t * HB + NT + NQ * NQ; }  // E2..E4
@@ -87,7 +160,7 @@ struct TrajView {
     const int m = d / NQ;
     return (d % NQ == 0 && t >= m) ? he(t)[(m - 2) * NQ + a] : T(0);
   }
-  __device__ __forceinline__ T& l(int i, int d) const { return L[i * (BW + 1) + d]; }
+  __device__ __forceinline__ T& l(int i, int d) const { return L[i * LW + d]; }
   __device__ __forceinline__ ColLane<G> lane(int t) const { return ColLane<G>{scratch + t, steps}; }
 };
 
@@ -95,7 +168,7 @@ template <typename T>
 __device__ __forceinline__ T block_sum(T v, T* red) {
   red[threadIdx.x] = v;
   __syncthreads();
-  for (int o = kTrajThreads / 2; o > 0; o >>= 1) {
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
     if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
     __syncthreads();
   }
@@ -108,7 +181,7 @@ template <typename T>
 __device__ __forceinline__ T block_max(T v, T* red) {
   red[threadIdx.x] = v;
   __syncthreads();
-  for (int o = kTrajThreads / 2; o > 0; o >>= 1) {
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
     if ((int)threadIdx.x < o) red[threadIdx.x] = tmax(red[threadIdx.x], red[threadIdx.x + o]);
     __syncthreads();
   }
@@ -488,20 +561,63 @@ __device__ typename G::T traj_eval(const ChainParams<typename G::T, G::K>& C, co
 
 // Banded damped Cholesky solve: y <- -(H + lam diag(max(diag H, 1e-8)))^-1 g.
 //
-// Blocked right-looking factorisation over timestep blocks of NQ columns with
-// the forward substitution fused in and a one-block look-ahead:
-//   2  threads 0..BW-1: the BW rows below block jb solve x D^T = a (their
-//      NQ-wide slice of the block column) and y_r -= x . y_blk;
-//   3  warp 0 applies the trailing update to the NEXT diagonal block and one
-//      thread factors it in registers (carrying its slice of the forward
-//      substitution) while warps 1..3 apply the rest of the trailing update
-//      L(r, c) -= x_r . x_c of the BW x BW lower triangle below block jb.
-// Two barriers per block; the serial diagonal factorisation overlaps the
-// trailing update.  Entries of the band beyond half-width BW are structural
-// zeros of the factor (the profile of row t*NQ+a starts at (t-4)*NQ+a) and are
-// never stored.  The back substitution L^T x = y also runs by blocks.
-template <class G>
-__device__ __forceinline__ bool traj_factor_diag(const TrajView<G>& S, int c0) {
+// Two-sided ("twisted") blocked factorisation over timestep blocks of NQ
+// columns.  The N unknowns are ordered [top | bottom (reversed) | separator]:
+// the separator is the 4 blocks (= the half-bandwidth BW) that decouple the
+// top blocks 0..nbA-1 from the bottom blocks nbA+4..nblk-1, so both halves
+// are eliminated at the same time, the top one downwards by warps 0 + 2 and
+// the bottom one upwards (the same code on the index-reversed band) by warps
+// 1 + 3, each pair synchronised by its own named barrier.  Their Schur
+// complements meet on the separator (the bottom one is added afterwards from
+// its stored factor columns, so no entry has two writers), which all four
+// warps then factor; the back substitution solves the separator, then both
+// halves outwards concurrently.  The serial chain -- one diagonal-block
+// factorisation per timestep -- is half as long as a one-sided sweep.
+//
+// Per eliminated block jb of a sweep:
+//   rows   main warp lanes 0..BW-1: the BW rows below block jb solve
+//          x D^T = a (their NQ-wide slice of the block column), y_r -= x . z;
+//   trail  the main warp updates the NEXT diagonal block and its lane 0
+//          factors it in registers (carrying the forward substitution) while
+//          the trailing warp(s) apply L(r, c) -= x_r . x_c to the rest of the
+//          BW x BW lower triangle below block jb (pairs from the smem table).
+// Two barriers per block.  Entries of the band beyond half-width BW are
+// structural zeros of the factor (the profile of row t*NQ+a starts at
+// (t-4)*NQ+a) and are never stored.
+//
+// Each routine below is inlined once per view direction (the sweeps and the
+// back substitutions are loops over phases with per-warp parameters): the
+// kernel is large, and more copies of the sweep thrash the instruction cache.
+
+// The band seen in forward or index-reversed (REV) order, as an affine map: view
+// entry (i, i - d) of the lower band of P A P, P the reversal, is
+// A(N-1-i+d, N-1-i) = storage (N-1-i+d, d); along a block column the view's
+// entries are sd apart in storage, down it 1 (reversed) or LW + 1 apart.
+template <class G, bool REV>
+struct BandView {
+  using T = typename G::T;
+  static constexpr int BW = 4 * G::NQ, LW = TrajView<G>::LW;
+  static constexpr int si = REV ? -LW : LW, sd = REV ? LW + 1 : 1, ys = REV ? -1 : 1;
+  T *L, *y, *dinv;
+  int o, yo;
+  __device__ BandView(const TrajView<G>& S, int N)
+      : L(S.L), y(S.y), dinv(S.dinv), o(REV ? (N - 1) * LW : 0), yo(REV ? N - 1 : 0) {}
+  __device__ __forceinline__ T& l(int i, int d) const { return L[(REV ? o : 0) + si * i + sd * d]; }
+  // p with p[-b * sd] = view L(r, c0 + b)
+  __device__ __forceinline__ T* rowp(int r, int c0) const { return L + (REV ? o : 0) + si * r + sd * (r - c0); }
+  __device__ __forceinline__ T& yv(int i) const { return y[(REV ? yo : 0) + ys * i]; }
+  __device__ __forceinline__ T& dv(int i) const { return dinv[(REV ? yo : 0) + ys * i]; }
+};
+
+// barrier `id` over `nthreads` (whole warps); the warp reconverges first so
+// that it arrives once (lane 0 may still be factoring when lanes 1..31 get here)
+__device__ __forceinline__ void named_bar(int id, int nthreads) {
+  __syncwarp();
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+template <class G, class V_>
+__device__ __forceinline__ bool traj_factor_diag(const V_& V, int c0) {
   using T = typename G::T;
   constexpr int NQ = G::NQ;
   T Lb[Tri<NQ>::size], yv[NQ];
@@ -509,8 +625,8 @@ __device__ __forceinline__ bool traj_factor_diag(const TrajView<G>& S, int c0) {
 #pragma unroll
   for (int a = 0; a < NQ; ++a) {
 #pragma unroll
-    for (int b = 0; b <= a; ++b) Lb[Tri<NQ>::at(a, b)] = S.l(c0 + a, a - b);
-    yv[a] = S.y[c0 + a];
+    for (int b = 0; b <= a; ++b) Lb[Tri<NQ>::at(a, b)] = V.l(c0 + a, a - b);
+    yv[a] = V.yv(c0 + a);
   }
 #pragma unroll
   for (int k = 0; k < NQ; ++k) {
@@ -518,7 +634,7 @@ __device__ __forceinline__ bool traj_factor_diag(const TrajView<G>& S, int c0) {
     ok = ok && dk > T(0) && finite_t(dk);
     const T inv = rsqrt_t(dk);
     Lb[Tri<NQ>::at(k, k)] = dk * inv;
-    S.dinv[c0 + k] = inv;
+    V.dv(c0 + k) = inv;
     const T yk = yv[k] * inv;
     yv[k] = yk;
 #pragma unroll
@@ -535,62 +651,45 @@ __device__ __forceinline__ bool traj_factor_diag(const TrajView<G>& S, int c0) {
 #pragma unroll
   for (int a = 0; a < NQ; ++a) {
 #pragma unroll
-    for (int b = 0; b <= a; ++b) S.l(c0 + a, a - b) = Lb[Tri<NQ>::at(a, b)];
-    S.y[c0 + a] = yv[a];
+    for (int b = 0; b <= a; ++b) V.l(c0 + a, a - b) = Lb[Tri<NQ>::at(a, b)];
+    V.yv(c0 + a) = yv[a];
   }
   return ok;
 }
 
-// L(r, c) -= sum_b L(r, c0 + b) L(c, c0 + b) for rows r = c0+NQ+ri, c = c0+NQ+ci
-template <class G>
-__device__ __forceinline__ void traj_trailing(const TrajView<G>& S, int c0, int ri, int ci) {
+// sum_b L(r, c0 + b) L(c, c0 + b) for view rows r = c0+NQ+ri >= c = c0+NQ+ci
+template <class G, class V_>
+__device__ __forceinline__ typename G::T traj_trailing_dot(const V_& V, int c0, int ri, int ci) {
   using T = typename G::T;
-  constexpr int NQ = G::NQ, BW = TrajView<G>::BW;
-  const int r = c0 + NQ + ri, c = c0 + NQ + ci;
-  const T* lr = S.L + r * (BW + 1) + NQ + ri;  // L(r, c0 + b) = lr[-b]
-  const T* lc = S.L + c * (BW + 1) + NQ + ci;
+  constexpr int NQ = G::NQ, BW = 4 * NQ;
+  const T* lr = V.rowp(c0 + NQ + ri, c0);
+  const T* lc = V.rowp(c0 + NQ + ci, c0);
   const int blo = NQ + ri - BW;  // both vanish for b < blo (band edge of row r)
   T acc = T(0);
 #pragma unroll
-  for (int b = 0; b < NQ; ++b)
-    if (b >= blo) acc += lr[-b] * lc[-b];
-  S.l(r, ri - ci) -= acc;
+  for (int b = 0; b < NQ; ++b) {  // branch-free; the index is clamped into the band (row N-1 ends the smem)
+    const int bb = (b >= blo ? b : blo) * V.sd;
+    acc += (b >= blo ? lr[-bb] : T(0)) * lc[-bb];
+  }
+  return acc;
 }
 
-template <class G>
-__device__ bool traj_damped_solve(const TrajView<G>& S, int N, typename G::T lam) {
+// One sweep: eliminate view blocks jb0 .. jb0+nb-1 with rows up to nlim.
+// Main warp (`main`; its lane 0 factors), nwt trailing threads (index tt >= 0),
+// barrier (bar, nbar).  defer: leave the separator x separator entries (view
+// columns >= sepv) and the separator right-hand side alone (the bottom sweep;
+// traj_bottom_schur adds them later).
+template <class G, class V_>
+__device__ __forceinline__ bool traj_sweep(const TrajView<G>& S, const V_& V, int jb0, int nb, int nlim,
+                                           int sepv, bool defer, bool main, int tt, int nwt, int bar, int nbar) {
   using T = typename G::T;
-  constexpr int NQ = G::NQ, BW = TrajView<G>::BW, NT = Tri<NQ>::size;
-  static_assert(BW <= 32 && NT <= 64, "band wider than a warp");
-  const int tid = threadIdx.x;
-  for (int i = tid; i < N; i += kTrajThreads) {
-    for (int d = 0; d <= BW; ++d) S.l(i, d) = S.h(i, d);  // zero outside the compact blocks
-    S.l(i, 0) += lam * tmax(S.h(i, 0), T(BeamConsts::diag_clamp));
-    S.y[i] = -S.g[i];
-  }
-  // warps 1..3 take the trailing-update pairs (ri, ci), 0 <= ci <= ri < BW,
-  // that are not in the next diagonal block (ri < NQ); warp 0 lane l < NT takes
-  // diagonal-block pair l
-  constexpr int NPAIR = BW * (BW + 1) / 2 - NT;
-  constexpr int NW = kTrajThreads - 32;
-  constexpr int PPT = (NPAIR + NW - 1) / NW;
-  int pri[PPT], pci[PPT];
-  {
-    int q = 0, tgt = tid - 32;
-#pragma unroll
-    for (int r = 0; r < PPT; ++r) pri[r] = BW;  // no pair
-    for (int ri = NQ; ri < BW && tid >= 32; ++ri)
-      for (int ci = 0; ci <= ri; ++ci, ++q)
-        if (q % NW == tgt && q / NW < PPT) {
-          pri[q / NW] = ri;
-          pci[q / NW] = ci;
-        }
-  }
-  int dri[2] = {BW, BW}, dci[2] = {0, 0};  // warp 0: diagonal-block pairs tid, tid + 32
+  constexpr int NQ = G::NQ, BW = 4 * NQ, NT = Tri<NQ>::size, NPAIR = TrajView<G>::NPAIR, CH = std::is_same<typename G::T, double>::value ? KOP_TRAJ_CH64 : KOP_TRAJ_CH32;
+  const int lane = threadIdx.x & 31;
+  int dri[2] = {BW, BW}, dci[2] = {0, 0};  // main warp: diagonal-block pairs lane, lane + 32
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    int rem = tid + 32 * h, ri = 0;
-    if (tid >= 32 || rem >= NT) continue;
+    int rem = lane + 32 * h, ri = 0;
+    if (!main || rem >= NT) continue;
     while (rem > ri) {
       rem -= ri + 1;
       ++ri;
@@ -598,87 +697,254 @@ __device__ bool traj_damped_solve(const TrajView<G>& S, int N, typename G::T lam
     dri[h] = ri;
     dci[h] = rem;
   }
-  __syncthreads();
   bool ok = true;
-  const int nblk = N / NQ;
-  if (tid == 0) ok = traj_factor_diag<G>(S, 0);
-  __syncthreads();
-  for (int jb = 0; jb < nblk; ++jb) {
+  if (nb <= 0) return ok;
+  // FP32: this thread's table entries q = tt + p * nwt, held for the whole sweep (nwt >= 96)
+  constexpr bool PREG = !std::is_same<T, double>::value;
+  constexpr int PPT = PREG ? (NPAIR + 95) / 96 : 1;
+  int pcode[PPT];
+#pragma unroll
+  for (int p = 0; p < PPT; ++p) {
+    const int q = tt + p * nwt;
+    pcode[p] = (PREG && tt >= 0 && q < NPAIR) ? S.pairs[q] : -1;
+  }
+  if (main && lane == 0) ok = traj_factor_diag<G, V_>(V, jb0 * NQ);
+  named_bar(bar, nbar);
+#ifdef KOP_TRAJ_PROFILE
+  long long ph[4] = {0, 0, 0, 0}, tq = clock64(), tn;
+#define KOP_PHASE(i) tn = clock64(), ph[i] += tn - tq, tq = tn
+#else
+#define KOP_PHASE(i)
+#endif
+  const int role = threadIdx.x >> 5;
+  for (int jb = jb0; jb < jb0 + nb; ++jb) {
     const int c0 = jb * NQ;
-    if (tid < BW && c0 + NQ + tid < N) {  // 2: rows below the block
-      const int r = c0 + NQ + tid;
-      const int blo = NQ + tid - BW;  // L(r, c0 + b) = 0 below the band for b < blo
-      const T* lr = S.L + r * (BW + 1) + NQ + tid;  // L(r, c0 + b) = lr[-b]
+    KOP_TL(role, jb, 0);
+    if (main && lane < BW && c0 + NQ + lane < nlim) {  // rows below the block
+      const int r = c0 + NQ + lane;
+      const int blo = NQ + lane - BW;  // L(r, c0 + b) = 0 below the band for b < blo
+      const T* lr = V.rowp(r, c0);     // L(r, c0 + b) = lr[-b * sd]
       T x[NQ];
       T yu = T(0);
 #pragma unroll
       for (int b = 0; b < NQ; ++b) {
-        T v = b >= blo ? lr[-b] : T(0);
+        T v = b >= blo ? lr[-(b >= blo ? b : blo) * V.sd] : T(0);  // clamped: never read past the band
 #pragma unroll
         for (int m = 0; m < NQ; ++m)
-          if (m < b) v -= x[m] * S.l(c0 + b, b - m);
-        x[b] = v * S.dinv[c0 + b];
-        yu += x[b] * S.y[c0 + b];
+          if (m < b) v -= x[m] * V.l(c0 + b, b - m);
+        x[b] = v * V.dv(c0 + b);
+        yu += x[b] * V.yv(c0 + b);
       }
 #pragma unroll
       for (int b = 0; b < NQ; ++b)
-        if (r - (c0 + b) <= BW) S.l(r, r - (c0 + b)) = x[b];
-      S.y[r] -= yu;
+        if (b >= blo) V.l(r, r - (c0 + b)) = x[b];
+      if (!defer || r < sepv) V.yv(r) -= yu;
     }
-    __syncthreads();
-    if (jb + 1 < nblk) {  // 3 with look-ahead
-      if (tid < 32) {
+    KOP_PHASE(0);
+    KOP_TL(role, jb, 1);
+    named_bar(bar, nbar);
+    KOP_TL(role, jb, 2);
+    KOP_PHASE(1);
+    if (c0 + NQ < nlim) {  // trailing update (and look-ahead factor) of the rows below
+      const bool next_own = jb + 1 < jb0 + nb;
+      if (main) {
+        if (!defer || next_own) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h)
-          if (dri[h] < BW) traj_trailing<G>(S, c0, dri[h], dci[h]);
+          for (int h = 0; h < 2; ++h)
+            if (dri[h] < BW) V.l(c0 + NQ + dri[h], dri[h] - dci[h]) -= traj_trailing_dot<G, V_>(V, c0, dri[h], dci[h]);
+        }
         __syncwarp();
-        if (tid == 0) ok = traj_factor_diag<G>(S, c0 + NQ) && ok;
-      } else {
+        if (lane == 0 && next_own) ok = traj_factor_diag<G, V_>(V, c0 + NQ) && ok;
+      } else if (tt >= 0) {
+        // pairs q = tt + p * nwt (ri >= NQ) of the table, CH dot products issued
+        // together (an unused slot reads row c0 + NQ and is dropped)
+        for (int p0 = 0; PREG ? p0 < PPT : tt + p0 * nwt < NPAIR; p0 += CH) {
+          T acc[CH];
+          int code[CH];
+          bool use[CH];
 #pragma unroll
-        for (int p = 0; p < PPT; ++p)
-          if (pri[p] < BW && c0 + NQ + pri[p] < N) traj_trailing<G>(S, c0, pri[p], pci[p]);
-      }
-    }
-    __syncthreads();
-  }
-  ok = __syncthreads_and(ok);
-  // back substitution L^T x = y by blocks, warp 0: one thread solves the
-  // block's upper-triangular NQ x NQ system in registers, then BW lanes remove
-  // the block's contribution from the rows above it
-  if (tid < 32) {
-    for (int jb = nblk - 1; jb >= 0; --jb) {
-      const int c0 = jb * NQ;
-      if (tid == 0) {
-        T x[NQ];
+          for (int p = 0; p < CH; ++p) {
+            bool has;
+            if constexpr (PREG) {
+              has = p0 + p < PPT && pcode[p0 + p] >= 0;
+              code[p] = has ? pcode[p0 + p] : 0;
+            } else {
+              const int q = tt + (p0 + p) * nwt;
+              has = q < NPAIR;
+              code[p] = has ? S.pairs[q] : 0;
+            }
+            const int ri = code[p] & 0xff, ci = code[p] >> 8;
+            use[p] = has && c0 + NQ + ri < nlim && (!defer || c0 + NQ + ci < sepv);
+            acc[p] = traj_trailing_dot<G, V_>(V, c0, use[p] ? ri : 0, use[p] ? ci : 0);
+          }
 #pragma unroll
-        for (int bb = 0; bb < NQ; ++bb) {
-          const int b = NQ - 1 - bb;
-          T v = S.y[c0 + b];
-#pragma unroll
-          for (int m = 0; m < NQ; ++m)
-            if (m > b) v -= S.l(c0 + m, m - b) * x[m];
-          x[b] = v * S.dinv[c0 + b];
-          S.y[c0 + b] = x[b];
+          for (int p = 0; p < CH; ++p)
+            if (use[p]) {
+              const int ri = code[p] & 0xff, ci = code[p] >> 8;
+              V.l(c0 + NQ + ri, ri - ci) -= acc[p];
+            }
         }
       }
-      __syncwarp();
-      const int c = c0 - 1 - tid;
-      if (tid < BW && c >= 0) {
-        T acc = T(0);
-#pragma unroll
-        for (int b = 0; b < NQ; ++b)
-          if (c0 + b - c <= BW) acc += S.l(c0 + b, c0 + b - c) * S.y[c0 + b];
-        S.y[c] -= acc;
+    }
+    KOP_PHASE(2);
+    KOP_TL(role, jb, 3);
+    named_bar(bar, nbar);
+    KOP_TL(role, jb, 4);
+    KOP_PHASE(3);
+  }
+#ifdef KOP_TRAJ_PROFILE
+  if (main && lane == 0)
+    for (int i = 0; i < 4; ++i)
+      atomicAdd(&g_traj_prof[(jb0 > 0 ? 16 : defer ? 12 : 8) + i], (unsigned long long)ph[i]);
+#endif
+#undef KOP_PHASE
+  return ok;
+}
+
+// The bottom sweep's deferred part of the separator Schur complement:
+// view (reversed) rows i >= j >= sepv: L(i, j) -= sum_{c < sepv} L(i, c) L(j, c),
+// y_i -= sum_{c < sepv} L(i, c) z_c.  All threads; deterministic order.
+template <class G>
+__device__ __forceinline__ void traj_bottom_schur(const BandView<G, true>& V, int sepv, int nsep) {
+  using T = typename G::T;
+  constexpr int NQ = G::NQ, BW = 4 * NQ;
+  const int ns = nsep * NQ, ntri = ns * (ns + 1) / 2;
+  for (int k = threadIdx.x; k < ntri + ns; k += blockDim.x) {
+    int i, j;
+    if (k < ntri) {
+      i = 0;
+      int rem = k;
+      while (rem > i) {
+        rem -= i + 1;
+        ++i;
       }
-      __syncwarp();
+      j = rem + sepv;
+    } else {
+      i = k - ntri;
+      j = -1;  // right-hand side
+    }
+    i += sepv;
+    const int lo = max(i - BW, 0);
+    T acc = T(0);
+    if (j < 0) {
+      for (int c = lo; c < sepv; ++c) acc += V.l(i, i - c) * V.yv(c);
+      V.yv(i) -= acc;
+    } else if (i - j <= BW) {
+      for (int c = lo; c < sepv; ++c) acc += V.l(i, i - c) * V.l(j, j - c);  // j - c <= i - c <= BW
+      V.l(i, i - j) -= acc;
     }
   }
+}
+
+// Back substitution L^T x = z over view blocks hi..lo by one warp: lane 0
+// solves the block's triangular system in registers (blocks >= known already
+// hold x), lanes < BW remove its contribution from the rows above.
+template <class G, class V_>
+__device__ __forceinline__ void traj_back(const V_& V, int hi, int lo, int known) {
+  using T = typename G::T;
+  constexpr int NQ = G::NQ, BW = 4 * NQ;
+  const int lane = threadIdx.x & 31;
+  for (int jb = hi; jb >= lo; --jb) {
+    const int c0 = jb * NQ;
+    if (lane == 0 && jb < known) {
+      T x[NQ];
+#pragma unroll
+      for (int bb = 0; bb < NQ; ++bb) {
+        const int b = NQ - 1 - bb;
+        T v = V.yv(c0 + b);
+#pragma unroll
+        for (int m = NQ - 1; m > b; --m) v -= V.l(c0 + m, m - b) * x[m];  // newest x last
+        x[b] = v * V.dv(c0 + b);
+        V.yv(c0 + b) = x[b];
+      }
+    }
+    __syncwarp();
+    const int c = c0 - 1 - lane;
+    if (lane < BW && c >= 0 && (jb < known || c < known * NQ)) {  // solved rows of a known block stay
+      T acc = T(0);
+#pragma unroll
+      for (int b = 0; b < NQ; ++b)
+        if (c0 + b - c <= BW) acc += V.l(c0 + b, c0 + b - c) * V.yv(c0 + b);
+      V.yv(c) -= acc;
+    }
+    __syncwarp();
+  }
+}
+
+template <class G>
+__device__ bool traj_damped_solve(const TrajView<G>& S, int N, typename G::T lam) {
+  using T = typename G::T;
+  constexpr int NQ = G::NQ, BW = TrajView<G>::BW, NT = Tri<NQ>::size, TH = TrajView<G>::TH;
+  static_assert(BW <= 32 && NT <= 64, "band wider than a warp");
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  KOP_PROF_T(pt0);
+  for (int i = tid; i < N; i += TH) {
+    for (int d = 0; d <= BW; ++d) S.l(i, d) = S.h(i, d);  // zero outside the compact blocks
+    S.l(i, 0) += lam * tmax(S.h(i, 0), T(BeamConsts::diag_clamp));
+    S.y[i] = -S.g[i];
+  }
+  const int nblk = N / NQ;
   __syncthreads();
+  KOP_PROF_T(pt1);
+  KOP_PROF_ADD(2, pt1 - pt0);
+  bool ok = true;
+  KOP_PROF_T(pt2);
+  if constexpr (TrajView<G>::TWIST) {
+    // phase 0: both halves at once -- top on the even warps (warp 0 main),
+    // bottom on the odd warps (warp 1 main) -- then the bottom half's share of
+    // the separator; phase 1: the separator on all warps (warp 0 main)
+    const int nsep = min(4, nblk), nbA = (nblk - nsep + 1) / 2, nbB = nblk - nsep - nbA;
+    const bool bottom = (warp & 1) != 0;
+    const BandView<G, false> A(S, N);
+    const BandView<G, true> Bv(S, N);
+    for (int ph = 0; ph < 2; ++ph) {
+      const bool sep = ph == 1;
+      const int tt = sep ? tid - 32 : warp >= 2 ? ((warp >> 1) - 1) * 32 + lane : -1;
+      if (!sep && bottom)
+        ok = traj_sweep<G>(S, Bv, 0, nbB, (nbB + nsep) * NQ, nbB * NQ, true, warp == 1, tt, TH / 2 - 32, 2, TH / 2);
+      else
+        ok = traj_sweep<G>(S, A, sep ? nbA : 0, sep ? nsep : nbA, (nbA + nsep) * NQ, N, false,
+                           sep ? warp == 0 : warp == 0, tt, sep ? TH - 32 : TH / 2 - 32, sep ? 0 : 1, sep ? TH : TH / 2) &&
+             ok;
+      __syncthreads();
+      if (ph == 0 && nbB > 0) {
+        traj_bottom_schur<G>(Bv, nbB * NQ, nsep);
+        __syncthreads();
+      }
+    }
+    ok = __syncthreads_and(ok);
+    KOP_PROF_SET(pt2);
+    KOP_PROF_ADD(3, pt2 - pt1);
+    // back substitution: phase 0 the separator (warp 0), phase 1 the top
+    // (warp 0) and the bottom (warp 1, starting with the separator's
+    // contributions to it) outwards
+    for (int ph = 0; ph < 2; ++ph) {
+      if (warp == 0) traj_back<G>(A, ph == 0 ? nbA + nsep - 1 : nbA - 1, ph == 0 ? nbA : 0, nblk);
+      if (ph == 0 && warp < 2) named_bar(3, 64);
+    }
+    if (warp == 1) traj_back<G>(Bv, nbB + nsep - 1, 0, nbB);
+  } else {
+    // one-sided: warp 0 main, warps 1..3 trailing, back substitution on warp 0
+    const BandView<G, false> V(S, N);
+    ok = traj_sweep<G>(S, V, 0, nblk, N, N, false, warp == 0, tid - 32, TH - 32, 0, TH);
+    ok = __syncthreads_and(ok);
+    KOP_PROF_SET(pt2);
+    KOP_PROF_ADD(3, pt2 - pt1);
+    if (warp == 0) traj_back<G>(V, nblk - 1, 0, nblk);
+  }
+#ifdef KOP_TRAJ_TIMELINE
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) g_traj_tl_on = 0;
+#endif
+  __syncthreads();
+  KOP_PROF_T(pt3);
+  KOP_PROF_ADD(4, pt3 - pt2);
+  KOP_PROF_ADD(5, 1);
   return ok;
 }
 
 template <class G>
-__global__ void __launch_bounds__(kTrajThreads)
+__global__ void __launch_bounds__(traj_threads<G>())
 k_traj_solve(const ChainParams<typename G::T, G::K> C, const CollisionParams<typename G::T> P,
              const TrajCosts<typename G::T> W, const double* __restrict__ q_init, const double* __restrict__ anchors,
              const double* __restrict__ obstacles, int n_obs, int64_t B, const LmOptions O,
@@ -690,12 +956,13 @@ k_traj_solve(const ChainParams<typename G::T, G::K> C, const CollisionParams<typ
   const TrajView<G> S(smem_raw, W.T_steps, P.ns);
   const int64_t b = blockIdx.x;
   const int tid = threadIdx.x, Tn = W.T_steps, N = Tn * NQ, n = W.n;
-  for (int i = tid; i < 2 * NQ; i += kTrajThreads) {
+  for (int i = tid; i < 2 * NQ; i += traj_threads<G>()) {
     const int c = i % NQ;
     S.anc[i] = c < n ? T(anchors[(b * 2 + i / NQ) * n + c]) : T(0);
   }
   load_obstacles(*S.obs, obstacles, b, n_obs);
-  for (int i = tid; i < N; i += kTrajThreads) {
+  S.build_pairs();
+  for (int i = tid; i < N; i += traj_threads<G>()) {
     const int tt = i / NQ, c = i % NQ;
     if (q_init) {
       S.q[i] = c < n ? T(q_init[(b * Tn + tt) * n + c]) : T(0);
@@ -716,7 +983,7 @@ k_traj_solve(const ChainParams<typename G::T, G::K> C, const CollisionParams<typ
   T damping = T(O.damping0);
   for (int it = 0; it < O.max_iterations && term == 0; ++it) {
     T gm = T(0);
-    for (int i = tid; i < N; i += kTrajThreads) gm = tmax(gm, fabs(S.g[i]));
+    for (int i = tid; i < N; i += traj_threads<G>()) gm = tmax(gm, fabs(S.g[i]));
     if (block_max(gm, S.red) < T(O.grad_tol)) {
       term = 1;
       break;
@@ -726,21 +993,25 @@ k_traj_solve(const ChainParams<typename G::T, G::K> C, const CollisionParams<typ
     for (int rj = 0; rj < O.max_rejections; ++rj) {
       const bool ok = traj_damped_solve<G>(S, N, damping);
       T fin = T(1);
-      for (int i = tid; i < N; i += kTrajThreads) {
+      for (int i = tid; i < N; i += traj_threads<G>()) {
         S.qn[i] = S.q[i] + S.y[i];
         if (!finite_t(S.y[i])) fin = T(0);
       }
       __syncthreads();
       const bool finite_ok = __syncthreads_and(fin > T(0));
       if (ok && finite_ok) {
+        KOP_PROF_T(pe0);
         const T cn = traj_eval<G, false>(C, P, W, S, S.qn);
+        KOP_PROF_T(pe1);
+        KOP_PROF_ADD(1, pe1 - pe0);
+        KOP_PROF_ADD(7, 1);
         if (!finite_t(cn)) {
           term = 5;
           break;
         }
         if (cn < cost) {
           T sm = T(0);
-          for (int i = tid; i < N; i += kTrajThreads) {
+          for (int i = tid; i < N; i += traj_threads<G>()) {
             sm = tmax(sm, fabs(S.y[i]));
             S.q[i] = S.qn[i];
           }
@@ -765,12 +1036,16 @@ k_traj_solve(const ChainParams<typename G::T, G::K> C, const CollisionParams<typ
       term = 2;
       break;
     }
+    KOP_PROF_T(pj0);
     traj_eval<G, true>(C, P, W, S, S.q);
+    KOP_PROF_T(pj1);
+    KOP_PROF_ADD(0, pj1 - pj0);
+    KOP_PROF_ADD(6, 1);
   }
   // outputs + hard-minimum static / swept signed distances (tasks.py:251-275)
   if (hist_out)
-    for (int i = iters + 1 + tid; i < hstride; i += kTrajThreads) hist_out[b * hstride + i] = NAN;
-  for (int i = tid; i < N; i += kTrajThreads) {
+    for (int i = iters + 1 + tid; i < hstride; i += traj_threads<G>()) hist_out[b * hstride + i] = NAN;
+  for (int i = tid; i < N; i += traj_threads<G>()) {
     const int tt = i / NQ, c = i % NQ;
     if (c < n) q_out[(b * Tn + tt) * n + c] = double(S.q[i]);
   }
@@ -784,7 +1059,7 @@ k_traj_solve(const ChainParams<typename G::T, G::K> C, const CollisionParams<typ
 // Normal equations of the trajectory problem at given trajectories (parity
 // hook): cost, gradient J^T r and the band of J^T J, unpadded to T*n dense.
 template <class G>
-__global__ void __launch_bounds__(kTrajThreads)
+__global__ void __launch_bounds__(traj_threads<G>())
 k_traj_normal(const ChainParams<typename G::T, G::K> C, const CollisionParams<typename G::T> P,
               const TrajCosts<typename G::T> W, const double* __restrict__ qs, const double* __restrict__ anchors,
               const double* __restrict__ obstacles, int n_obs, int64_t B, double* __restrict__ cost_out,
@@ -795,19 +1070,19 @@ k_traj_normal(const ChainParams<typename G::T, G::K> C, const CollisionParams<ty
   const TrajView<G> S(smem_raw, W.T_steps, P.ns);
   const int64_t b = blockIdx.x;
   const int tid = threadIdx.x, Tn = W.T_steps, N = Tn * NQ, n = W.n, Nr = Tn * n;
-  for (int i = tid; i < 2 * NQ; i += kTrajThreads) {
+  for (int i = tid; i < 2 * NQ; i += traj_threads<G>()) {
     const int c = i % NQ;
     S.anc[i] = c < n ? T(anchors[(b * 2 + i / NQ) * n + c]) : T(0);
   }
   load_obstacles(*S.obs, obstacles, b, n_obs);
-  for (int i = tid; i < N; i += kTrajThreads) {
+  for (int i = tid; i < N; i += traj_threads<G>()) {
     const int tt = i / NQ, c = i % NQ;
     S.q[i] = c < n ? T(qs[(b * Tn + tt) * n + c]) : T(0);
   }
   __syncthreads();
   const T cost = traj_eval<G, true>(C, P, W, S, S.q);
   if (tid == 0) cost_out[b] = double(cost);
-  for (int i = tid; i < N; i += kTrajThreads) {
+  for (int i = tid; i < N; i += traj_threads<G>()) {
     const int a = i % NQ;
     if (a >= n) continue;
     const int r1 = (i / NQ) * n + a;
@@ -827,7 +1102,7 @@ k_traj_normal(const ChainParams<typename G::T, G::K> C, const CollisionParams<ty
 // thread t runs the forward pass of q_t, then the static distances of
 // timestep t and the swept distances of the pair (t-1, t).
 template <class G>
-__global__ void __launch_bounds__(kTrajThreads)
+__global__ void __launch_bounds__(traj_threads<G>())
 k_traj_report(const ChainParams<double, G::K> C, const CollisionParams<double> P, int steps, int n,
               const double* __restrict__ qs, const double* __restrict__ obstacles, int n_obs,
               const double* __restrict__ targets, int64_t B, double* __restrict__ static_out,
@@ -892,7 +1167,7 @@ cudaError_t launch_traj(const ChainParams<typename G::T, G::K>& C, const Collisi
   const size_t smem = TrajView<G>::bytes(W.T_steps, P.ns);
   cudaError_t e = cudaFuncSetAttribute(k_traj_solve<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_traj_solve<G><<<(unsigned)L.B, kTrajThreads, smem, st>>>(C, P, W, L.q_init, L.anchors, L.obstacles, L.n_obs,
+  k_traj_solve<G><<<(unsigned)L.B, traj_threads<G>(), smem, st>>>(C, P, W, L.q_init, L.anchors, L.obstacles, L.n_obs,
                                                              L.B, L.opts, L.q_out, L.cost_out, L.init_cost,
                                                              L.hist_out, L.iters, L.term);
   return cudaGetLastError();
@@ -905,7 +1180,7 @@ cudaError_t launch_traj_normal(const ChainParams<typename G::T, G::K>& C, const 
   const size_t smem = TrajView<G>::bytes(W.T_steps, P.ns);
   cudaError_t e = cudaFuncSetAttribute(k_traj_normal<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_traj_normal<G><<<(unsigned)L.B, kTrajThreads, smem, st>>>(C, P, W, L.q_init, L.anchors, L.obstacles, L.n_obs,
+  k_traj_normal<G><<<(unsigned)L.B, traj_threads<G>(), smem, st>>>(C, P, W, L.q_init, L.anchors, L.obstacles, L.n_obs,
                                                               L.B, L.cost_out, L.grad_out, L.hess_out);
   return cudaGetLastError();
 }
@@ -917,7 +1192,7 @@ cudaError_t launch_traj_report(const ChainParams<double, G::K>& C, const Collisi
   const size_t smem = TrajView<G>::bytes(L.steps, P.ns);
   cudaError_t e = cudaFuncSetAttribute(k_traj_report<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_traj_report<G><<<(unsigned)L.B, kTrajThreads, smem, st>>>(C, P, L.steps, L.n, L.qs, L.obstacles, L.n_obs,
+  k_traj_report<G><<<(unsigned)L.B, traj_threads<G>(), smem, st>>>(C, P, L.steps, L.n, L.qs, L.obstacles, L.n_obs,
                                                               L.targets, L.B, L.static_out, L.swept_out,
                                                               L.min_static, L.min_swept, L.pos_err, L.rot_err);
   return cudaGetLastError();
@@ -940,3 +1215,19 @@ template cudaError_t launch_traj_report<Cfg<double, 8, 8, false, false>>(const C
 KOP_FOR_EACH_COLLISION_SHAPE(KOP_TRAJ_INSTANTIATE)
 
 }  // namespace kop
+
+#ifdef KOP_TRAJ_TIMELINE
+extern "C" int kop_debug_traj_timeline(long long* out) {
+  return (int)cudaMemcpyFromSymbol(out, kop::g_traj_tl, sizeof(kop::g_traj_tl));
+}
+#endif
+#ifdef KOP_TRAJ_PROFILE
+extern "C" int kop_debug_traj_profile(unsigned long long* out, int reset) {
+  cudaMemcpyFromSymbol(out, kop::g_traj_prof, sizeof(kop::g_traj_prof));
+  if (reset) {
+    unsigned long long z[20] = {};
+    cudaMemcpyToSymbol(kop::g_traj_prof, z, sizeof(z));
+  }
+  return 0;
+}
+#endif

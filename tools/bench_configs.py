@@ -246,5 +246,5 @@ for prec in ("fp32", "fp64"):
                        "2 target sets of this workload, oracle port (float64 NumPy), 1 core")
     print(json.dumps({"cpu_baseline": cpu, "workload": "config3 humanoid multi-EE IK-Beam (n=29, 4 end effectors, "
                       "64 seeds, 6+10 lane-LM steps, keep 4; SURVEY 8 H6)", "precision": prec, "targets": nb,
-                      "ms": ms, "solves_per_s": nb / ms * 1e3, "success": res.success.float().mean().item()}),
-          flush=True)
+                      "ms": ms, "solves_per_s": nb / ms * 1e3, "success": res.success.float().mean().item(),
+                      "roofline": roofline("config3 humanoid multi-EE IK-Beam", prec, nb / ms * 1e3)}), flush=True)

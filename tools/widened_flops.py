@@ -112,7 +112,7 @@ def parse(path):
             if not any(x in kname for x in subs):
                 continue
             if ("k_beam_errors" not in kname and "k_tree_beam_prune" not in kname
-                    and not any(t in kname for t in (f"Cfg<{prec}", f"<{prec}>", f"<{prec},"))):
+                    and not any(t in kname.split("(")[0] for t in (f"Cfg<{prec}", f"<{prec}>", f"<{prec},"))):
                 continue
             if sub == "k_beam_stage" and "1, 1>" not in kname.replace("true", "1"):
                 continue  # mobile: BASE shapes only
