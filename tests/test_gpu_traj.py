@@ -175,6 +175,31 @@ def test_traj_device_vs_oracle_capsule_world(arm7, chains, golden_traj):
     np.testing.assert_allclose(out["cost"][0].item(), cost_o, rtol=1e-8)
 
 
+@pytest.mark.parametrize("T", [5, 6, 7, 9, 64])
+def test_traj_device_vs_oracle_lengths(arm7, chains, golden_traj, T):
+    """Trajectory lengths at the edges of the FP64 two-sided factorisation:
+    T = 5 (separator only below one top block, no bottom half), 6 / 7 / 9
+    (bottom half of 1 / 1 / 2 blocks, odd and even splits) and the maximum
+    T = 64.  FP64 device solve vs the oracle's from the same anchors."""
+    ch = chains["arm7"]
+    sp = co.load_spheres_files(ch, robot_file("arm7.urdf"), robot_file("arm7.sidecar.json"))
+    g, _, _, _ = _case(golden_traj, "scene1")
+    qa, qb = g("q_start"), g("q_goal")
+    mid = k.link_transform(arm7, 0.5 * (qa + qb), "flange").translation
+    world = k.WorldModel([k.Sphere(mid + [0.02, 0.0, 0.0], 0.07)])
+    obs_o = [co.sphere(mid + [0.02, 0.0, 0.0], 0.07)]
+    tc = to.TrajCosts(timesteps=T)
+    qs_o, cost_o, hist_o, _, _ = to.solve_traj(ch, sp, obs_o, to.straight_line(qa, qb, T), qa, qb, tc,
+                                               golden_traj["velocity_limits"])
+    planner = k.TrajectoryPlanner(arm7, "flange", timesteps=T, precision="fp64")
+    out = planner.solve_anchored_device(np.array([[qa, qb]]), k.collision.obstacle_rows(world.obstacles)[None], 1)
+    hist = out["history"][0].cpu().numpy()[:int(out["iterations"][0]) + 1]
+    m = min(len(hist), len(hist_o))
+    np.testing.assert_allclose(hist[:m], hist_o[:m], rtol=1e-8)
+    np.testing.assert_allclose(out["cost"][0].item(), cost_o, rtol=1e-8)
+    np.testing.assert_allclose(out["qs"][0].cpu().numpy(), qs_o, atol=1e-6)
+
+
 def test_plan_trajectory_end_to_end(arm7, golden_traj):
     """plan_trajectory (endpoint IK + solve + report) on the reference's scenes."""
     reqs = []
