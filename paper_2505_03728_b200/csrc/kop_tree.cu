@@ -312,6 +312,14 @@ __device__ __forceinline__ bool tree_damped_solve(const TreeLmParams<T>& P, Tree
 template <typename T>
 constexpr int tree_warps() { return sizeof(T) == 4 ? 1 : 4; }
 
+// IK-Beam stage 1 runs a fixed step count (no early exit), so its warps finish
+// together and share one staged table per CTA
+#ifndef KOP_TREE_BEAM_WARPS32
+#define KOP_TREE_BEAM_WARPS32 4
+#endif
+template <typename T>
+constexpr int tree_beam_warps() { return sizeof(T) == 4 ? KOP_TREE_BEAM_WARPS32 : 4; }
+
 template <typename T, int NE>
 __global__ void __launch_bounds__(32 * tree_warps<T>())
 k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const double* __restrict__ q0, int64_t B,
@@ -457,7 +465,7 @@ __device__ __forceinline__ T tree_beam_step(const TreeLmParams<T>& P, const Tree
 }
 
 template <typename T, int NE>
-__global__ void __launch_bounds__(32 * tree_warps<T>())
+__global__ void __launch_bounds__(32 * tree_beam_warps<T>())
 k_tree_beam_stage1(const TreeLmParams<T> P, const double* __restrict__ targets, int64_t B,
                    const double* __restrict__ seeds, int S, int steps1, float* __restrict__ recs) {
   extern __shared__ unsigned char smem_raw[];
@@ -616,7 +624,7 @@ k_tree_beam_stage2(const TreeLmParams<T> P, const TreeLmParams<double> Pd, const
 template <typename T, int NE>
 cudaError_t launch_tree_beam_ne(const TreeLmParams<T>& P, const TreeLmParams<double>& Pd, const TreeBeamLaunch& L,
                                 cudaStream_t st) {
-  constexpr int warps = tree_warps<T>();
+  constexpr int warps = tree_beam_warps<T>();
   const size_t tab = (sizeof(TreeTable<T>) + 15) / 16 * 16;
   const int rec = tree_beam_rec(P.n, L.steps1);
   float* recs = static_cast<float*>(L.workspace);
