@@ -32,6 +32,7 @@ namespace kop {
 template <typename T, int NE>
 struct TreeScratch {
   T q[32], qn[32];
+  T cb[2][32];               // Cholesky pivot column, double-buffered (16-byte aligned rows)
   T am[kTreeMaxJoints][6];   // Pluecker axis of each moving tree joint
   T ee[NE][48];              // per EE: r[6], R^T[9], p[3], At[9], Bt[9], Ab[9]
   T A[32 * 33];
@@ -95,6 +96,17 @@ __device__ __forceinline__ T warp_max(T v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = tmax(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
+}
+
+// four consecutive shared-memory values (16-byte aligned for float, 32 for
+// double): one LDS.128 (two for double) instead of four scalar loads
+__device__ __forceinline__ void ld4(const float* p, float (&v)[4]) {
+  const float4 t = *reinterpret_cast<const float4*>(p);
+  v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+}
+__device__ __forceinline__ void ld4(const double* p, double (&v)[4]) {
+  const double2 a = reinterpret_cast<const double2*>(p)[0], b = reinterpret_cast<const double2*>(p)[1];
+  v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
 }
 
 // Evaluate the stack at S.q (or S.qn when cand): returns the cost (all lanes);
@@ -230,11 +242,17 @@ __device__ __forceinline__ T tree_eval(const TreeLmParams<T>& P, const TreeTable
   // ---- normal equations: lane i forms row i ----------------------------------------
   T g = T(0);
   if (lane < n) {
-    for (int j = 0; j < n; ++j) {
-      T a = T(0);
+    for (int j4 = 0; j4 < n; j4 += 4) {  // four columns of J per vector load; unused slots are zero
+      T a[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
-      for (int m = 0; m < 6 * NE; ++m) a += col[m] * S.J[m][j];  // unused slots are zero
-      S.A[j * 33 + lane] = a;
+      for (int m = 0; m < 6 * NE; ++m) {
+        T v[4];
+        ld4(&S.J[m][j4], v);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) a[t] += col[m] * v[t];
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) S.A[(j4 + t) * 33 + lane] = a[t];  // rows >= n: zero, unread
     }
     S.A[lane * 33 + lane] += gl * gl + P.w_rest * P.w_rest;
 #pragma unroll
@@ -251,7 +269,9 @@ template <typename T, int NE>
 __device__ __forceinline__ bool tree_damped_solve(const TreeLmParams<T>& P, TreeScratch<T, NE>& S, T g, T lam,
                                                   int lane, T& delta) {
   // right-looking Cholesky with lane i holding row i of L in registers; the
-  // pivot column travels by shuffles (no shared-memory round trips)
+  // scaled pivot column is published once per step in shared memory and read
+  // back as vector broadcasts.  Lanes update their whole row: the entries
+  // right of the diagonal are never read, so no per-entry lane test.
   const int n = P.n;
   T row[kTreeMaxDofs];
 #pragma unroll
@@ -267,16 +287,18 @@ __device__ __forceinline__ bool tree_damped_solve(const TreeLmParams<T>& P, Tree
       const T dk = shfl_t(row[k], k);
       ok = ok && (dk > T(0)) && finite_t(dk);
       const T inv = rsqrt_t(dk);
-      if (lane == k) {
-        row[k] = dk * inv;
-        dinv_mine = inv;
-      } else if (lane > k) {
-        row[k] *= inv;
-      }
+      row[k] *= inv;  // lane k: dk * inv = L(k, k); lanes > k: L(lane, k)
+      if (lane == k) dinv_mine = inv;
+      T* cb = S.cb[k & 1];  // the buffer of step k - 2 is free: every lane passed step k - 1's sync
+      cb[lane] = row[k];    // rows / lanes >= n are zero
+      __syncwarp();
 #pragma unroll
-      for (int j = k + 1; j < kTreeMaxDofs; ++j) {  // rows / lanes >= n are zero: no j < n test
-        const T ljk = shfl_t(row[k], j);
-        if (lane >= j) row[j] -= row[k] * ljk;
+      for (int j4 = (k + 1) & ~3; j4 < kTreeMaxDofs; j4 += 4) {
+        T l[4];
+        ld4(cb + j4, l);
+#pragma unroll
+        for (int t = 0; t < 4; ++t)
+          if (j4 + t > k) row[j4 + t] -= row[k] * l[t];
       }
     }
   }
@@ -326,7 +348,7 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
              const LmOptions O, double* __restrict__ q_out, double* __restrict__ cost_out,
              double* __restrict__ init_cost_out, double* __restrict__ hist_out, int32_t* __restrict__ iters_out,
              int32_t* __restrict__ term_out) {
-  extern __shared__ unsigned char smem_raw[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
   TreeTable<T>& Q = *reinterpret_cast<TreeTable<T>*>(smem_raw);
@@ -340,17 +362,24 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
   const double* tg = targets + b * 7 * P.ne;
   S.q[lane] = lane < n ? T(q0[b * n + lane]) : T(0);
   __syncwarp();
-  T g;
-  T cost = tree_eval<T, NE, true>(P, Q, tg, S, S.q, lane, g);
+  T g, cost = T(0);
   const int hstride = O.max_iterations + 1;
-  if (lane == 0) {
-    if (hist_out) hist_out[b * hstride] = double(cost);
-    init_cost_out[b] = double(cost);
-  }
-  int term = finite_t(cost) ? 0 : 5;
+  int term = 0;
   int iters = 0;
   T damping = T(O.damping0);
-  for (int it = 0; it < O.max_iterations && term == 0; ++it) {
+  // one J-evaluation site (start evaluation, then J at each accepted iterate):
+  // a single inlined copy keeps the kernel inside the instruction cache
+  for (int it = 0;; ++it) {
+    const T c = tree_eval<T, NE, true>(P, Q, tg, S, S.q, lane, g);
+    if (it == 0) {
+      cost = c;
+      if (lane == 0) {
+        if (hist_out) hist_out[b * hstride] = double(cost);
+        init_cost_out[b] = double(cost);
+      }
+      term = finite_t(cost) ? 0 : 5;
+    }
+    if (term != 0 || it >= O.max_iterations) break;
     if (warp_max(lane < n ? fabs(g) : T(0)) < T(O.grad_tol)) {
       term = 1;
       break;
@@ -394,7 +423,6 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
       term = 2;
       break;
     }
-    tree_eval<T, NE, true>(P, Q, tg, S, S.q, lane, g);
   }
   if (hist_out)
     for (int i = iters + 1 + lane; i < hstride; i += 32) hist_out[b * hstride + i] = NAN;
@@ -437,30 +465,50 @@ template cudaError_t launch_tree_solve<double>(const TreeLmParams<double>&, cons
 // One warp per lane, as in the tree solve.
 // ---------------------------------------------------------------------------
 
-// one beam.py proposal at the state (S.q, cost, A in S.A, g): returns the new cost
+// `steps` beam.py proposals from S.q (beam.py:198-240).  One J-evaluation
+// site: the start evaluation (cost = start_state's when `start`, else the
+// carried `cost`) and, after an accepted step that is not the last, J at the
+// accepted iterate (beam.py:202) -- one inlined copy of the evaluation keeps
+// the kernel inside the instruction cache.  Lane h0 + it keeps the cost after
+// step it in hv (and lane 0 the start cost when `start`).
 template <typename T, int NE>
-__device__ __forceinline__ T tree_beam_step(const TreeLmParams<T>& P, const TreeTable<T>& Q,
-                                            const double* __restrict__ tg, TreeScratch<T, NE>& S, int lane, T cost,
-                                            T& lam, T& g) {
-  T d;
-  bool ok = tree_damped_solve(P, S, g, lam, lane, d);
-  ok = __all_sync(0xffffffffu, ok && finite_t(d));
-  T cn = inf_t<T>();
-  if (ok) {  // a failed factorisation rejects the step (beam.py:209-213, per lane)
-    S.qn[lane] = S.q[lane] + d;
-    __syncwarp();
-    T gd;
-    const T raw = tree_eval<T, NE, false>(P, Q, tg, S, S.qn, lane, gd);
-    cn = finite_t(raw) ? raw : inf_t<T>();
+__device__ __forceinline__ T tree_beam_run(const TreeLmParams<T>& P, const TreeTable<T>& Q,
+                                           const double* __restrict__ tg, TreeScratch<T, NE>& S, int lane,
+                                           int steps, bool start, T cost, T& lam, int h0, T& hv) {
+  T g = T(0);
+  bool need = true;
+  for (int it = 0;; ++it) {
+    if (need) {
+      const T c = tree_eval<T, NE, true>(P, Q, tg, S, S.q, lane, g);
+      if (start && it == 0) {
+        cost = c;
+        if (lane == 0) hv = c;
+      }
+      need = false;
+    }
+    if (it == steps) break;
+    T d;
+    bool ok = tree_damped_solve(P, S, g, lam, lane, d);
+    ok = __all_sync(0xffffffffu, ok && finite_t(d));
+    T cn = inf_t<T>();
+    if (ok) {  // a failed factorisation rejects the step (beam.py:209-213, per lane)
+      S.qn[lane] = S.q[lane] + d;
+      __syncwarp();
+      T gd;
+      const T raw = tree_eval<T, NE, false>(P, Q, tg, S, S.qn, lane, gd);
+      cn = finite_t(raw) ? raw : inf_t<T>();
+    }
+    if (cn < cost) {
+      S.q[lane] = S.qn[lane];
+      __syncwarp();
+      lam = tmax(lam * T(BeamConsts::damping_down), T(BeamConsts::damping_min));
+      cost = cn;
+      need = it + 1 < steps;
+    } else {
+      lam = tmin(lam * T(BeamConsts::damping_up), T(BeamConsts::damping_max));
+    }
+    if (lane == h0 + it) hv = cost;
   }
-  if (cn < cost) {
-    S.q[lane] = S.qn[lane];
-    __syncwarp();
-    lam = tmax(lam * T(BeamConsts::damping_down), T(BeamConsts::damping_min));
-    tree_eval<T, NE, true>(P, Q, tg, S, S.q, lane, g);  // J at the accepted iterate (beam.py:202)
-    return cn;
-  }
-  lam = tmin(lam * T(BeamConsts::damping_up), T(BeamConsts::damping_max));
   return cost;
 }
 
@@ -468,7 +516,7 @@ template <typename T, int NE>
 __global__ void __launch_bounds__(32 * tree_beam_warps<T>())
 k_tree_beam_stage1(const TreeLmParams<T> P, const double* __restrict__ targets, int64_t B,
                    const double* __restrict__ seeds, int S, int steps1, float* __restrict__ recs) {
-  extern __shared__ unsigned char smem_raw[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t L = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;  // lane = target * S + seed
   TreeTable<T>& Q = *reinterpret_cast<TreeTable<T>*>(smem_raw);
@@ -483,14 +531,9 @@ k_tree_beam_stage1(const TreeLmParams<T> P, const double* __restrict__ targets, 
   Sc.q[lane] = lane < n ? T(seeds[(size_t)s * n + lane]) : T(0);
   __syncwarp();
   const double* tg = targets + b * 7 * P.ne;
-  T g;
-  T cost = tree_eval<T, NE, true>(P, Q, tg, Sc, Sc.q, lane, g);  // start_state (beam.py:182-196)
   T lam = T(BeamConsts::damping_init);
-  T hv = lane == 0 ? cost : T(0);  // lane h keeps hist[h]
-  for (int it = 1; it <= steps1; ++it) {
-    cost = tree_beam_step(P, Q, tg, Sc, lane, cost, lam, g);
-    if (lane == it) hv = cost;
-  }
+  T hv = T(0);  // lane h keeps hist[h]; start_state (beam.py:182-196) inside
+  const T cost = tree_beam_run(P, Q, tg, Sc, lane, steps1, true, T(0), lam, 1, hv);
   const int rec = tree_beam_rec(n, steps1);
   float* out = recs + L * rec;
   if (lane < n) out[lane] = float(Sc.q[lane]);
@@ -553,7 +596,7 @@ k_tree_beam_stage2(const TreeLmParams<T> P, const TreeLmParams<double> Pd, const
                    int steps2, int keep, double pos_tol, double rot_tol, double* __restrict__ q_out,
                    double* __restrict__ cost_out, double* __restrict__ hist_out, double* __restrict__ pos_err,
                    double* __restrict__ rot_err, uint8_t* __restrict__ success) {
-  extern __shared__ unsigned char smem_raw[];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, r = threadIdx.x >> 5;  // warp r = survivor of stage-1 rank r
   const int64_t b = blockIdx.x;
   TreeTable<T>& Q = *reinterpret_cast<TreeTable<T>*>(smem_raw);
@@ -569,14 +612,9 @@ k_tree_beam_stage2(const TreeLmParams<T> P, const TreeLmParams<double> Pd, const
   Sc.q[lane] = lane < n ? T(in[lane]) : T(0);
   __syncwarp();
   const double* tg = targets + b * 7 * P.ne;
-  T g;
-  tree_eval<T, NE, true>(P, Q, tg, Sc, Sc.q, lane, g);  // re-derive J; the carried cost is stage 1's
-  T lam = T(in[n]), cost = T(in[n + 1]);
-  T hv = T(0);  // lane h keeps stage-2 hist[h]
-  for (int it = 0; it < steps2; ++it) {
-    cost = tree_beam_step(P, Q, tg, Sc, lane, cost, lam, g);
-    if (lane == it) hv = cost;
-  }
+  T lam = T(in[n]);
+  T hv = T(0);  // lane h keeps stage-2 hist[h]; J re-derived, the carried cost is stage 1's
+  const T cost = tree_beam_run(P, Q, tg, Sc, lane, steps2, false, T(in[n + 1]), lam, 0, hv);
   if (lane == 0) wcost[r] = cost;
   __syncthreads();
   if (threadIdx.x == 0) {
