@@ -117,22 +117,29 @@ k_col_solve(const ChainParams<typename G::T, G::K> C, const CostParams<typename 
 #pragma unroll
   for (int i = 0; i < NQ; ++i) q[i] = T(q0[b * NQ + i]);
   const T zb[3] = {T(0), T(0), T(0)};
-  T cost;
-  {
-    T A[NT], g[NQ];
-    cost = model.template eval<true>(q, zb, A, g);
-#pragma unroll
-    for (int i = 0; i < NT; ++i) Ag[i * 128] = A[i];
-#pragma unroll
-    for (int i = 0; i < NQ; ++i) Ag[(NT + i) * 128] = g[i];
-  }
+  T cost = T(0);
   const int hstride = O.max_iterations + 1;
-  if (hist_out) hist_out[b * hstride] = double(cost);
-  init_cost_out[b] = double(cost);
-  int term = finite_t(cost) ? kMaxIterations : kNonFiniteCost;  // raw_residual raises on non-finite
+  int term = kMaxIterations;
   int iters = 0;
   T damping = T(O.damping0);
-  for (int it = 0; it < O.max_iterations && term == kMaxIterations; ++it) {
+  // one J-assembly site: the start evaluation, then J at each accepted iterate
+  // (solver.py:419) -- a single inlined copy of the collision stack
+  for (int it = 0;; ++it) {
+    {
+      T A[NT], g[NQ];
+      const T c = model.template eval<true>(q, zb, A, g);
+#pragma unroll
+      for (int i = 0; i < NT; ++i) Ag[i * 128] = A[i];
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) Ag[(NT + i) * 128] = g[i];
+      if (it == 0) {
+        cost = c;
+        if (hist_out) hist_out[b * hstride] = double(cost);
+        init_cost_out[b] = double(cost);
+        term = finite_t(cost) ? kMaxIterations : kNonFiniteCost;  // raw_residual raises on non-finite
+      }
+    }
+    if (term != kMaxIterations || it >= O.max_iterations) break;
     T gmax = T(0);
 #pragma unroll
     for (int i = 0; i < NQ; ++i) gmax = tmax(gmax, fabs(Ag[(NT + i) * 128]));
@@ -189,12 +196,6 @@ k_col_solve(const ChainParams<typename G::T, G::K> C, const CostParams<typename 
       term = kStepConverged;
       break;
     }
-    T A[NT], g[NQ];
-    model.template eval<true>(q, zb, A, g);  // re-assemble J at the accepted iterate (solver.py:419)
-#pragma unroll
-    for (int i = 0; i < NT; ++i) Ag[i * 128] = A[i];
-#pragma unroll
-    for (int i = 0; i < NQ; ++i) Ag[(NT + i) * 128] = g[i];
   }
   if (hist_out)
     for (int i = iters + 1; i < hstride; ++i) hist_out[b * hstride + i] = NAN;
