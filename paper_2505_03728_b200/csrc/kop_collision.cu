@@ -223,6 +223,7 @@ cudaError_t launch_col(const ChainParams<typename G::T, G::K>& C, const CostPara
   if (L.op == ColOp::kResJac) {
     if (L.lanes == 0) return cudaSuccess;
     const size_t smem = col_scratch_bytes<G>(P);
+    cudaFuncSetAttribute(k_col_resjac<G>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(k_col_resjac<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_col_resjac<G><<<(unsigned)((L.lanes + 127) / 128), 128, smem, st>>>(C, W, P, L.tinv, L.lane_target, L.q_in,
@@ -232,6 +233,7 @@ cudaError_t launch_col(const ChainParams<typename G::T, G::K>& C, const CostPara
   if (L.op == ColOp::kSolve) {
     if (L.B == 0) return cudaSuccess;
     const size_t smem = sizeof(T) * (Tri<G::NQ>::size + G::NQ) * 128 + col_scratch_bytes<G>(P);
+    cudaFuncSetAttribute(k_col_solve<G>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
     if (smem > 48 * 1024)
       cudaFuncSetAttribute(k_col_solve<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_col_solve<G><<<(unsigned)((L.B + 127) / 128), 128, smem, st>>>(C, W, P, L.targets, L.q_in, L.B, L.opts,
@@ -247,6 +249,7 @@ cudaError_t launch_col(const ChainParams<typename G::T, G::K>& C, const CostPara
   const int per_block = 128 / Bm.P;
   const int64_t blocks1 = (Bm.B + per_block - 1) / per_block;
   const size_t smem1 = beam_stage1_smem<G>(128, Bm.steps1, extra);
+  cudaFuncSetAttribute(k_col_beam_stage1<G>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (smem1 > 48 * 1024)
     cudaFuncSetAttribute(k_col_beam_stage1<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
   if (Bm.stages & 1) {
@@ -258,6 +261,7 @@ cudaError_t launch_col(const ChainParams<typename G::T, G::K>& C, const CostPara
   if (!(Bm.stages & 2)) return cudaSuccess;
   const int64_t blocks2 = (Bm.B * Bm.G + 127) / 128;
   const size_t smem2 = beam_stage2_smem<G>(Bm.steps2, extra);
+  cudaFuncSetAttribute(k_col_beam_stage2<G>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (smem2 > 48 * 1024)
     cudaFuncSetAttribute(k_col_beam_stage2<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
   k_col_beam_stage2<G><<<(unsigned)blocks2, 128, smem2, st>>>(C, W, P, Cd, Bm.targets, Bm.B, surv, rec, Bm.steps1,

@@ -1165,6 +1165,7 @@ cudaError_t launch_traj(const ChainParams<typename G::T, G::K>& C, const Collisi
                         const TrajCosts<typename G::T>& W, const TrajLaunch& L, cudaStream_t st) {
   if (L.B == 0) return cudaSuccess;
   const size_t smem = TrajView<G>::bytes(W.T_steps, P.ns);
+  cudaFuncSetAttribute(k_traj_solve<G>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   cudaError_t e = cudaFuncSetAttribute(k_traj_solve<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_traj_solve<G><<<(unsigned)L.B, traj_threads<G>(), smem, st>>>(C, P, W, L.q_init, L.anchors, L.obstacles, L.n_obs,
@@ -1178,6 +1179,7 @@ cudaError_t launch_traj_normal(const ChainParams<typename G::T, G::K>& C, const 
                                const TrajCosts<typename G::T>& W, const TrajLaunch& L, cudaStream_t st) {
   if (L.B == 0) return cudaSuccess;
   const size_t smem = TrajView<G>::bytes(W.T_steps, P.ns);
+  cudaFuncSetAttribute(k_traj_normal<G>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   cudaError_t e = cudaFuncSetAttribute(k_traj_normal<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_traj_normal<G><<<(unsigned)L.B, traj_threads<G>(), smem, st>>>(C, P, W, L.q_init, L.anchors, L.obstacles, L.n_obs,
@@ -1190,6 +1192,7 @@ cudaError_t launch_traj_report(const ChainParams<double, G::K>& C, const Collisi
                                const TrajReportLaunch& L, cudaStream_t st) {
   if (L.B == 0) return cudaSuccess;
   const size_t smem = TrajView<G>::bytes(L.steps, P.ns);
+  cudaFuncSetAttribute(k_traj_report<G>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   cudaError_t e = cudaFuncSetAttribute(k_traj_report<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   k_traj_report<G><<<(unsigned)L.B, traj_threads<G>(), smem, st>>>(C, P, L.steps, L.n, L.qs, L.obstacles, L.n_obs,

@@ -438,6 +438,7 @@ template <typename T, int NE>
 cudaError_t launch_tree_ne(const TreeLmParams<T>& P, const TreeLaunch& L, cudaStream_t st) {
   constexpr int warps = tree_warps<T>();
   const size_t smem = (sizeof(TreeTable<T>) + 15) / 16 * 16 + sizeof(TreeScratch<T, NE>) * warps;
+  cudaFuncSetAttribute(k_tree_solve<T, NE>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_tree_solve<T, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_tree_solve<T, NE><<<(unsigned)((L.B + warps - 1) / warps), 32 * warps, smem, st>>>(
@@ -669,6 +670,7 @@ cudaError_t launch_tree_beam_ne(const TreeLmParams<T>& P, const TreeLmParams<dou
   int32_t* surv = reinterpret_cast<int32_t*>(static_cast<char*>(L.workspace) +
                                              ((size_t)L.B * L.S * rec * sizeof(float) + 255) / 256 * 256);
   const size_t smem1 = tab + sizeof(TreeScratch<T, NE>) * warps;
+  cudaFuncSetAttribute(k_tree_beam_stage1<T, NE>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (smem1 > 48 * 1024)
     cudaFuncSetAttribute(k_tree_beam_stage1<T, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
   const int64_t lanes = L.B * L.S;
@@ -679,6 +681,7 @@ cudaError_t launch_tree_beam_ne(const TreeLmParams<T>& P, const TreeLmParams<dou
   k_tree_beam_prune<<<(unsigned)((L.B + 3) / 4), 128, 0, st>>>(recs, rec, P.n, L.B, L.S, L.keep, surv);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const size_t smem2 = tab + sizeof(TreeScratch<T, NE>) * L.keep + (sizeof(T) + sizeof(int)) * 32 + 16;
+  cudaFuncSetAttribute(k_tree_beam_stage2<T, NE>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (smem2 > 48 * 1024)
     cudaFuncSetAttribute(k_tree_beam_stage2<T, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
   k_tree_beam_stage2<T, NE><<<(unsigned)L.B, 32 * L.keep, smem2, st>>>(
