@@ -339,8 +339,11 @@ constexpr int tree_warps() { return sizeof(T) == 4 ? 1 : 4; }
 #ifndef KOP_TREE_BEAM_WARPS32
 #define KOP_TREE_BEAM_WARPS32 4
 #endif
+#ifndef KOP_TREE_BEAM_WARPS64
+#define KOP_TREE_BEAM_WARPS64 4
+#endif
 template <typename T>
-constexpr int tree_beam_warps() { return sizeof(T) == 4 ? KOP_TREE_BEAM_WARPS32 : 4; }
+constexpr int tree_beam_warps() { return sizeof(T) == 4 ? KOP_TREE_BEAM_WARPS32 : KOP_TREE_BEAM_WARPS64; }
 
 template <typename T, int NE>
 __global__ void __launch_bounds__(32 * tree_warps<T>())
