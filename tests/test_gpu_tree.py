@@ -128,3 +128,34 @@ def test_tree_ik_beam_fp32_and_single_ee(hum, models):
     rel = np.abs(multi.history - chain.history) / chain.history
     assert np.mean(rel.max(axis=1) < 1e-6) >= 0.9
     assert np.mean(multi.success.astype(bool) == chain.success.astype(bool)) >= 0.98
+
+
+@pytest.mark.parametrize("seed,n", [(21, 32), (22, 13), (23, 1)])
+def test_tree_ik_beam_random_chain_lane_edges(seed, n):
+    """Tree path at the lane-count edges vs the oracle (FP64): n = 32 fills the
+    warp, n = 13 leaves a partial column quad in the vectorised J^T J and in the
+    Cholesky's pivot-column broadcasts, n = 1 is a single column."""
+    from oracle import tree_oracle as tro
+    from random_robots import random_chain_urdf
+
+    doc = random_chain_urdf(seed, n, 2, True, False)
+    m = k.parse_urdf(doc)
+    ch = o.load_chain(doc)
+    assert m.actuated_count == ch.n == n
+    li = ch.link("tool")
+    rng = np.random.default_rng(seed)
+    lo = np.where(np.isfinite(ch.lower), ch.lower, -np.pi)
+    hi = np.where(np.isfinite(ch.upper), ch.upper, np.pi)
+    lq, lp, _, _ = o.fk(ch, rng.uniform(lo, hi, (4, n)))
+    tq = o.qcanon(lq[:, li])[:, None]
+    tt = lp[:, li][:, None]
+    seeds = o.sample_seeds(ch, 64, 3)
+    ref = tro.multi_ee_beam(ch, [li], tq, tt, seeds, [50.0], [10.0])
+    got = k.solve_ik_beam_multi(m, ["tool"], np.concatenate([tq, tt], axis=2), rng_seed=3, precision="fp64")
+    rel = np.abs(got.history - ref["hist"]) / np.maximum(ref["hist"], 1e-300)
+    if n > 1:  # one column: many seeds tie on the optimum, so the winner (and its start cost) is a coin flip
+        assert np.mean(rel.max(axis=1) < 1e-6) >= 0.75, np.sort(rel.max(axis=1))
+    np.testing.assert_allclose(got.history[:, -1], ref["hist"][:, -1], rtol=1e-6, atol=1e-12)
+    assert np.mean(got.success == ref["success"]) >= 0.75
+    r32 = k.solve_ik_beam_multi(m, ["tool"], np.concatenate([tq, tt], axis=2), rng_seed=3)
+    assert np.all(np.diff(r32.history, axis=1) <= 0)
