@@ -159,3 +159,26 @@ def test_tree_ik_beam_random_chain_lane_edges(seed, n):
     assert np.mean(got.success == ref["success"]) >= 0.75
     r32 = k.solve_ik_beam_multi(m, ["tool"], np.concatenate([tq, tt], axis=2), rng_seed=3)
     assert np.all(np.diff(r32.history, axis=1) <= 0)
+
+
+def test_tree_solve_32_columns_matches_oracle():
+    """solver.solve semantics on the tree path with every warp lane a column
+    (n = 32, one pose cost + limit + rest) vs the oracle's classic LM, FP64."""
+    from random_robots import random_chain_urdf
+
+    doc = random_chain_urdf(31, 32, 2, True, False)
+    m = k.parse_urdf(doc)
+    ch = o.load_chain(doc)
+    li = ch.link("tool")
+    rng = np.random.default_rng(31)
+    lo = np.where(np.isfinite(ch.lower), ch.lower, -np.pi)
+    hi = np.where(np.isfinite(ch.upper), ch.upper, np.pi)
+    lq, lp, _, _ = o.fk(ch, rng.uniform(lo, hi, (1, 32)))
+    w = k.CostWeights()
+    tgt = k.Transform3.from_parts(lq[0, li], lp[0, li])
+    costs = [k.pose_cost(m, "q", "tool", tgt, position_weight=w.pose_position, orientation_weight=w.pose_orientation),
+             k.limit_cost(m, "q", weight=w.limit), k.rest_cost("q", m.rest_pose, weight=w.rest)]
+    rep = k.solve(k.Problem(k.VariableSet.of(q=np.asarray(m.rest_pose, float).copy()), costs))
+    poses = [(li, o.qcanon(lq[0, li]), lp[0, li], w.pose_position, w.pose_orientation)]
+    _, c_ref, _, _, _ = to.solve_multi_pose(ch, poses, ch.rest)
+    np.testing.assert_allclose(rep.final_cost, c_ref, rtol=1e-5, atol=1e-12)
