@@ -110,7 +110,7 @@ def qexp(omega):
 
 def qlog(q):
     """so(3) log, angle in [0, pi] -- liegroups.py:130-141."""
-    q = q * np.where(q[..., :1] < 0.0, -1.0, 1.0)
+    q = q * np.where(q[..., :1] < 0.0, -1.0, 1.0).astype(q.dtype)  # dtype-preserving (float32 runs)
     w, v = q[..., :1], q[..., 1:]
     s = np.linalg.norm(v, axis=-1, keepdims=True)
     ang = 2.0 * np.arctan2(s, w)
@@ -555,6 +555,63 @@ class LaneEngine:
                               np.minimum(st.lam * LAMBDA_UP, LAMBDA_MAX)).astype(self.dt)
             st.hist.append(st.cost.copy())
         return st
+
+
+class CholeskyLaneEngine(LaneEngine):
+    """The lane engine with the damped normal equations solved by a per-lane
+    Cholesky factorisation in the ENGINE's dtype (float32 for the FP32 parity
+    bar), the way the device solves them.  The reference solves the same SPD
+    system with LU (``np.linalg.solve``, beam.py:207-208); for SPD systems the
+    two agree to rounding.  A lane whose pivot is not positive is rejected
+    (damping x10) -- in FP64 unreachable for finite inputs, since the damping
+    term keeps the system SPD."""
+
+    def _solve(self, h, g):
+        n = h.shape[-1]
+        dt = h.dtype
+        lo = np.zeros_like(h)
+        ok = np.ones(h.shape[0], dtype=bool)
+        for j in range(n):
+            s = h[:, j, j] - np.sum(lo[:, j, :j] * lo[:, j, :j], axis=-1)
+            ok &= s > 0
+            d = np.sqrt(np.where(s > 0, s, dt.type(1))).astype(dt)
+            lo[:, j, j] = d
+            for i in range(j + 1, n):
+                lo[:, i, j] = (h[:, i, j] - np.sum(lo[:, i, :j] * lo[:, j, :j], axis=-1)) / d
+        y = np.zeros_like(g)
+        for i in range(n):
+            y[:, i] = (g[:, i] - np.sum(lo[:, i, :i] * y[:, :i], axis=-1)) / lo[:, i, i]
+        x = np.zeros_like(g)
+        for i in reversed(range(n)):
+            x[:, i] = (y[:, i] - np.sum(lo[:, i + 1:, i] * x[:, i + 1:], axis=-1)) / lo[:, i, i]
+        return -x, ok
+
+
+def cholesky_engine(ch: Chain, link: int, weights=None, dtype=np.float32, **kw):
+    """``engine=`` factory for ik_beam: CholeskyLaneEngine lanes in ``dtype``."""
+    w = DEFAULT_WEIGHTS if weights is None else weights
+    return lambda q_, t_, group: CholeskyLaneEngine(ch, link, q_, t_, w, group=group, dtype=dtype, **kw)
+
+
+def history_agreement(h_dev, h_ref, rtol=1e-4, atol=1e-6):
+    """Per-step cost agreement of two (lanes, steps+1) cost histories up to each
+    lane's first accept/reject flip (the first step at which one run accepts its
+    proposal and the other rejects).  Returns (fraction of compared (lane, step)
+    pairs with |dc| <= rtol*c_ref + atol, flip rate = fraction of lanes that
+    flip, number of compared pairs, and the per-lane first flip step (steps+1
+    when the lane never flips))."""
+    h_dev = np.asarray(h_dev, dtype=float)
+    h_ref = np.asarray(h_ref, dtype=float)
+    acc_d = h_dev[:, 1:] < h_dev[:, :-1]
+    acc_r = h_ref[:, 1:] < h_ref[:, :-1]
+    diff = acc_d != acc_r
+    steps = h_dev.shape[1] - 1
+    first = np.where(diff.any(axis=1), diff.argmax(axis=1) + 1, steps + 1)
+    cols = np.arange(h_dev.shape[1])[None, :]
+    mask = cols < first[:, None]  # steps before the flip (the flip step itself is not compared)
+    ok = np.abs(h_dev - h_ref) <= rtol * np.abs(h_ref) + atol
+    n = int(mask.sum())
+    return float(ok[mask].mean()) if n else 1.0, float(np.mean(first <= steps)), n, first
 
 
 # ---------------------------------------------------------------------------

@@ -37,6 +37,9 @@ int fail(int code, const std::string& msg) {
 
 int cuda_status(cudaError_t e) {
   if (e == cudaSuccess) return KOP_OK;
+  if (e == cudaErrorNotSupported)  // launchers return it for request shapes over a per-block limit
+    return fail(KOP_EUNSUPPORTED, "request shape needs more shared memory per block than the device has "
+                                  "(e.g. FP64 IK-Beam with more than 256 seeds)");
   return fail(KOP_ECUDA, std::string("CUDA error: ") + cudaGetErrorString(e));
 }
 
@@ -1415,7 +1418,8 @@ int64_t kop_multi_pose_beam_workspace_bytes(const KopModel* m, const KopPoseCost
                                              int64_t batch) {
   if (!m || !pc || !p || batch < 0) return fail(KOP_EINVAL, "invalid arguments");
   const int rec = tree_beam_rec(m->tree.n, p->prune_after);
-  return ((int64_t)batch * p->seeds * rec * 4 + 255) / 256 * 256 + (int64_t)batch * p->keep * 4 + 256;
+  const int64_t elem = p->precision == KOP_FP64 ? 8 : 4;  // stage-1 records are stored in the solve precision
+  return ((int64_t)batch * p->seeds * rec * elem + 255) / 256 * 256 + (int64_t)batch * p->keep * 4 + 256;
 }
 
 int kop_multi_pose_beam(const KopModel* m, const KopPoseCosts* pc, const KopIkParams* p, const double* targets,
@@ -1598,6 +1602,9 @@ int kop_ik_beam_host(const KopModel* m, int32_t link, const KopIkParams* p, cons
   if ((e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming)) != cudaSuccess) return cuda_status(e);
   cudaEventRecord(start, caller);
   cudaStreamWaitEvent(P.st[0], start, 0);
+  // the seed buffer is shared by every buffer set: kernels of the previous call may still read it on
+  // any pipeline stream, so the overwrite waits for all of them (never-recorded events are no-ops)
+  for (int i = 1; i < P.nstreams; ++i) cudaStreamWaitEvent(P.st[0], P.done[i], 0);
   cudaMemcpyAsync(P.seeds, seeds, sizeof(double) * seeds_len, cudaMemcpyHostToDevice, P.st[0]);
   cudaEventRecord(start, P.st[0]);
   for (int i = 1; i < ns; ++i) cudaStreamWaitEvent(P.st[i], start, 0);

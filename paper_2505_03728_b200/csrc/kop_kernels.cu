@@ -190,14 +190,24 @@ cudaError_t launch_beam(const ChainParams<typename G::T, G::K>& C, const CostPar
     const int per_block = tpb / L.P;
     const int64_t blocks1 = (L.B + per_block - 1) / per_block;
     const size_t smem1 = beam_stage1_smem<G>(tpb, L.steps1, 0);
+    // FP64 with > 256 seeds needs ~350 KB per 1024-thread CTA: refuse instead of a generic launch failure
+    int dev = 0, optin = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess ||
+        (e = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev)) != cudaSuccess)
+      return e;
+    if (smem1 > (size_t)optin) return cudaErrorNotSupported;
     if (tpb == 256) {
-      if (smem1 > 48 * 1024)
-        cudaFuncSetAttribute(k_beam_stage1<G, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+      if (smem1 > 48 * 1024 &&
+          (e = cudaFuncSetAttribute(k_beam_stage1<G, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem1)) != cudaSuccess)
+        return e;
       k_beam_stage1<G, 256><<<(unsigned)blocks1, 256, smem1, st>>>(C, W, L.targets, L.B, L.seeds, L.S, L.P,
                                                                    L.steps1, L.keep, surv, rec, seed_tab);
     } else {
-      if (smem1 > 48 * 1024)
-        cudaFuncSetAttribute(k_beam_stage1<G, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem1);
+      if (smem1 > 48 * 1024 &&
+          (e = cudaFuncSetAttribute(k_beam_stage1<G, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    (int)smem1)) != cudaSuccess)
+        return e;
       k_beam_stage1<G, 1024><<<(unsigned)blocks1, 1024, smem1, st>>>(C, W, L.targets, L.B, L.seeds, L.S, L.P,
                                                                      L.steps1, L.keep, surv, rec, seed_tab);
     }

@@ -519,7 +519,7 @@ __device__ __forceinline__ T tree_beam_run(const TreeLmParams<T>& P, const TreeT
 template <typename T, int NE>
 __global__ void __launch_bounds__(32 * tree_beam_warps<T>())
 k_tree_beam_stage1(const TreeLmParams<T> P, const double* __restrict__ targets, int64_t B,
-                   const double* __restrict__ seeds, int S, int steps1, float* __restrict__ recs) {
+                   const double* __restrict__ seeds, int S, int steps1, T* __restrict__ recs) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t L = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;  // lane = target * S + seed
@@ -539,26 +539,27 @@ k_tree_beam_stage1(const TreeLmParams<T> P, const double* __restrict__ targets, 
   T hv = T(0);  // lane h keeps hist[h]; start_state (beam.py:182-196) inside
   const T cost = tree_beam_run(P, Q, tg, Sc, lane, steps1, true, T(0), lam, 1, hv);
   const int rec = tree_beam_rec(n, steps1);
-  float* out = recs + L * rec;
-  if (lane < n) out[lane] = float(Sc.q[lane]);
+  T* out = recs + L * rec;  // records in the solve precision: FP64 q / damping / cost are carried exactly
+  if (lane < n) out[lane] = Sc.q[lane];
   if (lane == 0) {
-    out[n] = float(lam);
-    out[n + 1] = float(cost);
+    out[n] = lam;
+    out[n + 1] = cost;
   }
-  if (lane <= steps1) out[n + 2 + lane] = float(hv);
+  if (lane <= steps1) out[n + 2 + lane] = hv;
 }
 
 // stable top-`keep` seeds of each target by (final stage-1 cost, seed index),
 // NaN last (np.argsort(kind="stable"), tasks.py:135): one warp per target
+template <typename T>
 __global__ void __launch_bounds__(128)
-k_tree_beam_prune(const float* __restrict__ recs, int rec, int n, int64_t B, int S, int keep,
+k_tree_beam_prune(const T* __restrict__ recs, int rec, int n, int64_t B, int S, int keep,
                   int32_t* __restrict__ surv) {
   const int lane = threadIdx.x & 31;
   const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (b >= B) return;
-  const float* base = recs + b * S * rec + n + 1;
+  const T* base = recs + b * S * rec + n + 1;
   for (int s = lane; s < S; s += 32) {
-    const float c = base[(size_t)s * rec];
+    const T c = base[(size_t)s * rec];
     int rank = 0;
     for (int j = 0; j < S; ++j) rank += rank_less(base[(size_t)j * rec], j, c, s) ? 1 : 0;
     if (rank < keep) surv[b * keep + rank] = s;
@@ -596,7 +597,7 @@ __device__ __forceinline__ void tree_frame_f64(const TreeLmParams<double>& P, co
 template <typename T, int NE>
 __global__ void __launch_bounds__(256)
 k_tree_beam_stage2(const TreeLmParams<T> P, const TreeLmParams<double> Pd, const double* __restrict__ targets,
-                   int64_t B, const float* __restrict__ recs, int S, const int32_t* __restrict__ surv, int steps1,
+                   int64_t B, const T* __restrict__ recs, int S, const int32_t* __restrict__ surv, int steps1,
                    int steps2, int keep, double pos_tol, double rot_tol, double* __restrict__ q_out,
                    double* __restrict__ cost_out, double* __restrict__ hist_out, double* __restrict__ pos_err,
                    double* __restrict__ rot_err, uint8_t* __restrict__ success) {
@@ -611,14 +612,14 @@ k_tree_beam_stage2(const TreeLmParams<T> P, const TreeLmParams<double> Pd, const
   stage_tree_table(P, Q);
   __syncthreads();
   const int n = P.n, rec = tree_beam_rec(n, steps1);
-  const float* in = recs + (b * S + surv[b * keep + r]) * rec;
+  const T* in = recs + (b * S + surv[b * keep + r]) * rec;
   for (int i = lane; i < NE * 48; i += 32) (&Sc.ee[0][0])[i] = T(0);
-  Sc.q[lane] = lane < n ? T(in[lane]) : T(0);
+  Sc.q[lane] = lane < n ? in[lane] : T(0);
   __syncwarp();
   const double* tg = targets + b * 7 * P.ne;
-  T lam = T(in[n]);
+  T lam = in[n];
   T hv = T(0);  // lane h keeps stage-2 hist[h]; J re-derived, the carried cost is stage 1's
-  const T cost = tree_beam_run(P, Q, tg, Sc, lane, steps2, false, T(in[n + 1]), lam, 0, hv);
+  const T cost = tree_beam_run(P, Q, tg, Sc, lane, steps2, false, in[n + 1], lam, 0, hv);
   if (lane == 0) wcost[r] = cost;
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -669,9 +670,9 @@ cudaError_t launch_tree_beam_ne(const TreeLmParams<T>& P, const TreeLmParams<dou
   constexpr int warps = tree_beam_warps<T>();
   const size_t tab = (sizeof(TreeTable<T>) + 15) / 16 * 16;
   const int rec = tree_beam_rec(P.n, L.steps1);
-  float* recs = static_cast<float*>(L.workspace);
+  T* recs = static_cast<T*>(L.workspace);
   int32_t* surv = reinterpret_cast<int32_t*>(static_cast<char*>(L.workspace) +
-                                             ((size_t)L.B * L.S * rec * sizeof(float) + 255) / 256 * 256);
+                                             ((size_t)L.B * L.S * rec * sizeof(T) + 255) / 256 * 256);
   const size_t smem1 = tab + sizeof(TreeScratch<T, NE>) * warps;
   cudaFuncSetAttribute(k_tree_beam_stage1<T, NE>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (smem1 > 48 * 1024)
@@ -681,7 +682,7 @@ cudaError_t launch_tree_beam_ne(const TreeLmParams<T>& P, const TreeLmParams<dou
       P, L.targets, L.B, L.seeds, L.S, L.steps1, recs);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  k_tree_beam_prune<<<(unsigned)((L.B + 3) / 4), 128, 0, st>>>(recs, rec, P.n, L.B, L.S, L.keep, surv);
+  k_tree_beam_prune<T><<<(unsigned)((L.B + 3) / 4), 128, 0, st>>>(recs, rec, P.n, L.B, L.S, L.keep, surv);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
   const size_t smem2 = tab + sizeof(TreeScratch<T, NE>) * L.keep + (sizeof(T) + sizeof(int)) * 32 + 16;
   cudaFuncSetAttribute(k_tree_beam_stage2<T, NE>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);

@@ -564,13 +564,18 @@ def _run_traj(plans, problems, options: SolveOptions) -> list:
     return out
 
 
+def _raise_non_finite(problem: Problem, rep: SolveReport):
+    """Device termination code 5 (a non-finite residual at the start or at a candidate) is where the
+    reference's raw_residual raises CostEvaluationError (solver.py:142-152) out of solve()."""
+    if rep.termination == "numerical_failure" and rep.message == TERMINATIONS[5][1]:
+        raise CostEvaluationError(problem.costs[0].name, "evaluator returned non-finite residual")
+
+
 def solve(problem: Problem, options: SolveOptions | None = None) -> SolveReport:
     """Minimise the sum of squared weighted residuals by LM on the device."""
     options = options or SolveOptions()
     rep = _run([plan(problem)], [problem], options)[0]
-    if rep.termination == "numerical_failure" and "non-finite" in rep.message and rep.iterations_run == 0 \
-            and not np.isfinite(rep.initial_cost):
-        raise CostEvaluationError(f"initial residual of '{problem.costs[0].name}' is non-finite")
+    _raise_non_finite(problem, rep)
     return rep
 
 
@@ -593,5 +598,11 @@ def solve_batch(problems: list, options: SolveOptions | None = None, workers: in
     for members in groups.values():
         idx = [i for i, _ in members]
         for i, rep in zip(idx, _run([p for _, p in members], [problems[i] for i in idx], options)):
-            reports[i] = rep
+            try:
+                _raise_non_finite(problems[i], rep)
+                reports[i] = rep
+            except CostEvaluationError as exc:  # the reference's isolated-failure report (solver.py:446-455)
+                reports[i] = SolveReport(final_values=problems[i].variables, initial_cost=float("nan"),
+                                         final_cost=float("nan"), iterations_run=0, termination="numerical_failure",
+                                         message=str(exc))
     return reports

@@ -306,8 +306,12 @@ class TrajectoryPlanner:
               "kop_traj_normal_equations")
         return cost, grad, hess
 
-    def plan(self, requests) -> list:
-        """plan_trajectory for every request (they must share this planner's settings)."""
+    def plan(self, requests, errors: str = "raise") -> list:
+        """plan_trajectory for every request (they must share this planner's settings).
+        errors="raise": the first request whose endpoint IK fails raises PlanningError (plan_trajectory);
+        errors="return": that request's slot holds the PlanningError and the others are still solved."""
+        if errors not in ("raise", "return"):
+            raise ValueError(f"errors must be 'raise' or 'return', got {errors!r}")
         start = time.perf_counter()
         b = len(requests)
         if b == 0:
@@ -324,11 +328,31 @@ class TrajectoryPlanner:
         poses = np.concatenate([np.stack(local_start), np.stack(local_goal)])
         q_end, found = self.endpoint_ik(poses, np.concatenate([seeds, seeds]),
                                         np.concatenate([obstacles, obstacles]), n_obs)
+        failed = {}
         for i in range(b):
             for j, label in ((i, "start"), (b + i, "goal")):
-                if not found[j]:
-                    raise PlanningError(f"could not find a collision-free IK solution for the {label} pose")
-        anchors = np.stack([q_end[:b], q_end[b:]], axis=1)
+                if not found[j] and i not in failed:
+                    failed[i] = PlanningError(f"could not find a collision-free IK solution for the {label} pose")
+                    if errors == "raise":
+                        raise failed[i]
+        if failed:  # solve the others only; failed requests keep their PlanningError
+            keep = [i for i in range(b) if i not in failed]
+            sub = self._solve_planned([requests[i] for i in keep], q_end[keep], q_end[[b + i for i in keep]],
+                                      obstacles[keep], n_obs, has_world[keep], start) if keep else []
+            out = [failed.get(i) for i in range(b)]
+            for i, r in zip(keep, sub):
+                out[i] = r
+            return out
+        return self._solve_planned(requests, q_end[:b], q_end[b:], obstacles, n_obs, has_world, start)
+
+    def _solve_planned(self, requests, q_start, q_goal, obstacles, n_obs, has_world, start) -> list:
+        b = len(requests)
+        local_start, local_goal = [], []
+        for r in requests:
+            base_inv = r.base_pose.inverse()
+            local_start.append(base_inv.compose(r.start_pose).as_array())
+            local_goal.append(base_inv.compose(r.goal_pose).as_array())
+        anchors = np.stack([q_start, q_goal], axis=1)
         out = self.solve_anchored_device(anchors, obstacles, n_obs)
         targets = np.stack([np.stack(local_start), np.stack(local_goal)], axis=1)
         rep = trajectory_signed_distances_batch(self.model, out["qs"], obstacles, n_obs, self.link, targets)
@@ -369,9 +393,11 @@ def plan_trajectory(req: TrajRequest) -> TrajResult:
     return _planner_for(req).plan([req])[0]
 
 
-def plan_trajectory_batch(requests) -> list:
+def plan_trajectory_batch(requests, errors: str = "return") -> list:
     """plan_trajectory over many requests; requests sharing robot, link, T, dt,
-    weights and options run as one batch."""
+    weights and options run as one batch.  A request whose endpoint IK fails
+    does not abort the others: its slot holds the PlanningError (errors="return",
+    default) or the first such error is raised (errors="raise")."""
     groups = {}
     for i, r in enumerate(requests):
         key = (id(r.model), r.target_link, r.timesteps, r.dt, tuple(r.weights.to_json().items()), r.eta_world,
@@ -379,7 +405,7 @@ def plan_trajectory_batch(requests) -> list:
         groups.setdefault(key, []).append(i)
     out = [None] * len(requests)
     for idx in groups.values():
-        res = _planner_for(requests[idx[0]]).plan([requests[i] for i in idx])
+        res = _planner_for(requests[idx[0]]).plan([requests[i] for i in idx], errors=errors)
         for i, r in zip(idx, res):
             out[i] = r
     return out

@@ -266,3 +266,34 @@ def test_multi_ee_beam_reduces_to_ik_beam(chains, golden):
     np.testing.assert_array_equal(multi["hist"], one.hist)
     np.testing.assert_array_equal(multi["pos_err"][:, 0], one.pos_err)
     np.testing.assert_array_equal(multi["success"], one.success)
+
+
+def test_cholesky_lane_engine_fp64_equals_lu_and_fp32_stays_fp32(chains, golden):
+    """The FP32 parity yardstick (CholeskyLaneEngine): in FP64 it follows the reference's LU
+    lanes to rounding; in float32 every quantity stays float32 (no silent float64 promotion)."""
+    ch = chains["arm7"]
+    tq, tt = golden["targets_arm7_77_wxyz"][:3], golden["targets_arm7_77_pos"][:3]
+    iq, it = o.target_inverse(tq, tt)
+    seeds = golden["seeds_arm7_77"]
+    lane_t = np.repeat(np.arange(3), len(seeds))
+    ref = o.LaneEngine(ch, 8, iq[lane_t], it[lane_t], o.DEFAULT_WEIGHTS, group=lane_t)
+    chol = o.CholeskyLaneEngine(ch, 8, iq[lane_t], it[lane_t], o.DEFAULT_WEIGHTS, group=lane_t)
+    q0 = np.tile(seeds, (3, 1))
+    h_ref = np.stack(ref.run(ref.start(q0), 16).hist, 1)
+    h_chol = np.stack(chol.run(chol.start(q0), 16).hist, 1)
+    frac, flip, n, _ = o.history_agreement(h_chol, h_ref, 1e-9, 0.0)
+    assert frac == 1.0 and flip < 0.02 and n > 0.95 * h_ref.size
+    e32 = o.CholeskyLaneEngine(ch, 8, iq[lane_t], it[lane_t], o.DEFAULT_WEIGHTS, group=lane_t, dtype=np.float32)
+    st = e32.run(e32.start(q0.astype(np.float32)), 2)
+    assert st.q.dtype == st.cost.dtype == st.lam.dtype == np.float32
+    assert all(h.dtype == np.float32 for h in st.hist)
+
+
+def test_history_agreement_semantics():
+    ref = np.array([[10.0, 5.0, 5.0, 4.0], [10.0, 9.0, 8.0, 7.0]])
+    dev = np.array([[10.0, 5.0001, 5.0001, 4.5], [10.0, 9.0, 9.0, 7.0]])
+    frac, flip, n, first = o.history_agreement(dev, ref, rtol=1e-4, atol=0.0)
+    # lane 0 never flips (accept pattern equal), its last step differs; lane 1 flips at step 2
+    assert list(first) == [4, 2]
+    assert n == 4 + 2 and flip == 0.5
+    assert frac == pytest.approx(5 / 6)
