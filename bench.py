@@ -528,6 +528,7 @@ def run_configs(torch, k, model, flush, peaks, nominals, cpu=True):
     from paper_2505_03728_b200.tasks import IkBeamSolver
 
     out = {}
+    finals = {}
     demo = k.WorldModel([k.Sphere([0.45, 0.1, 0.55], 0.12), k.Capsule([-0.5, -0.4, 0.2], [-0.5, 0.4, 0.6], 0.1),
                          k.HalfSpace([0.0, 0.0, 1.0], -0.3)])
     hum = k.load_robot(k.robot_path("humanoid29.urdf"))
@@ -591,12 +592,14 @@ def run_configs(torch, k, model, flush, peaks, nominals, cpu=True):
                                      *(dv.ptr(x) for x in outs), dv.stream_handle()), "kop_lm_solve")
         ms = float(np.median(device_time(torch, run_lm, 3, flush)))
         it = float(outs[4].float().mean())
+        finals[("c4", prec)] = outs[1].cpu().numpy()
         c4lm[prec] = {"ms": ms, "value": B4 / ms * 1e3, "unit": "solves/s", "mean_iterations": it,
-                      "terminations": torch.bincount(outs[5].long(), minlength=6).tolist(),
+                      "terminations": torch.bincount(outs[5].long(), minlength=7).tolist(),
                       "roofline": roof(lm_iter * it, B4 / ms * 1e3, peaks[prec], nominals[prec],
                                        "k_col_solve (single kernel): accepted iterations x lane-step constant")}
     if cpu:
         c4lm["cpu_baseline"] = cpu_leg("col_lm", list(tg4[:64].cpu().numpy()), "solves/s", "problems")
+    c4lm["fp32_vs_fp64_final_cost"] = final_cost_agreement(finals[("c4", "fp32")], finals[("c4", "fp64")])
     out["config4_generic_lm"] = c4lm
 
     # ---- config 3: humanoid multi-EE IK-Beam and solver.solve flavour ----
@@ -649,13 +652,15 @@ def run_configs(torch, k, model, flush, peaks, nominals, cpu=True):
                                              B3, *(dv.ptr(x) for x in outs), dv.stream_handle()), "tree")
         ms = float(np.median(device_time(torch, run_tl, 2, flush)))
         it = float(outs[4].float().mean())
+        finals[("c3", prec)] = outs[1].cpu().numpy()
         c3lm[prec] = {"ms": ms, "value": B3 / ms * 1e3, "unit": "solves/s", "mean_iterations": it,
-                      "terminations": torch.bincount(outs[5].long(), minlength=6).tolist(),
+                      "terminations": torch.bincount(outs[5].long(), minlength=7).tolist(),
                       "final_cost_p50": float(outs[1].median()),
                       "roofline": roof(c3_step * it, B3 / ms * 1e3, peaks[prec], nominals[prec],
                                        "k_tree_solve (single kernel): accepted iterations x lane-step constant")}
     if cpu:
         c3lm["cpu_baseline"] = cpu_leg("tree_lm", list(tgh[:64].cpu().numpy()), "solves/s", "problems")
+    c3lm["fp32_vs_fp64_final_cost"] = final_cost_agreement(finals[("c3", "fp32")], finals[("c3", "fp64")])
     out["config3_generic_lm"] = c3lm
 
     # ---- config 5: trajectories, T = 64, one r = 0.07 sphere at the FK of the joint-space midpoint ----
@@ -682,14 +687,16 @@ def run_configs(torch, k, model, flush, peaks, nominals, cpu=True):
         rep = k.trajectory.trajectory_signed_distances_batch(model, res["qs"], obsd, 1, "flange")
         free = float((torch.minimum(rep["min_static"], rep["min_swept"]) >= 0).float().mean())
         it = float(res["iterations"].float().mean())
+        finals[("c5", prec)] = res["cost"].cpu().numpy()
         c5[prec] = {"ms": ms, "value": NT / ms * 1e3, "unit": "trajectories/s", "mean_iterations": it,
                     "lm_iterations_per_s": it * NT / ms * 1e3, "collision_free_rate": free,
-                    "terminations": torch.bincount(res["termination"].long(), minlength=6).tolist(),
+                    "terminations": torch.bincount(res["termination"].long(), minlength=7).tolist(),
                     "roofline": roof(c5_iter * it, NT / ms * 1e3, peaks[prec], nominals[prec],
                                      "k_traj_solve (single kernel): accepted iterations x per-iteration constant")}
     c5["headline_precision"] = "fp64"
+    c5["fp32_vs_fp64_final_cost"] = final_cost_agreement(finals[("c5", "fp32")], finals[("c5", "fp64")])
     c5["termination_codes"] = ["max_iterations", "gradient_converged", "step_converged", "numerical_failure",
-                               "rejection_budget", "non_finite"]
+                               "rejection_budget", "non_finite", "fp32_resolution (FP32 only)"]
     if cpu:
         c5["cpu_baseline"] = cpu_leg("traj", [(qa[i], qb[i], mid[i]) for i in range(64)], "trajectories/s",
                                      "trajectories")
@@ -715,6 +722,14 @@ def run_configs(torch, k, model, flush, peaks, nominals, cpu=True):
         mob["cpu_baseline"] = cpu_leg("mobile", list(sh[:64]), "solves/s", "targets")
     out["mobile_base_ik_beam"] = mob
     return out
+
+
+def final_cost_agreement(c32, c64):
+    """Per-problem relative difference of the FP32 and FP64 final costs (same problems)."""
+    rel = (np.asarray(c32) - np.asarray(c64)) / np.abs(np.asarray(c64))
+    return {"rel_p10": float(np.percentile(rel, 10)), "rel_p50": float(np.percentile(rel, 50)),
+            "rel_p90": float(np.percentile(rel, 90)), "rel_p99": float(np.percentile(rel, 99)),
+            "within_1e-3": float(np.mean(np.abs(rel) <= 1e-3))}
 
 
 def traj_iteration_flops(model, T, anc, nsph, pairs):

@@ -12,6 +12,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
+
 #include "kop_beam.cuh"
 #include "kop_collision.cuh"
 #include "kop_kernels.cuh"
@@ -92,118 +94,150 @@ enum Termination : int32_t {
   kNumericalFailure = 3,      // damping above 1e10 ("no acceptable step below damping 1e10")
   kRejectionsExhausted = 4,   // step_converged, "rejection budget exhausted without descent"
   kNonFiniteCost = 5,         // numerical_failure: CostEvaluationError isolated by solve_batch
+  kFp32Resolution = 6,        // FP32 only: step_converged, no cost decrease resolvable in FP32
 };
 
-// solver.solve (solver.py:364-429) for one problem per thread.  The normal
-// equations at the current iterate live in shared memory because the
-// rejection loop re-factors them with growing damping.
+// FP32 stopping rule: a rejected trial whose quadratic-model
+// decrease -g.d + lam d^T D d is below kFp32Tau * cost cannot be resolved by a
+// float32 cost, so further damping increases only walk lambda up to 1e10 (the
+// FP64 run would stop by its gradient / step tolerance there instead).
+constexpr float kFp32Tau = 7.62939453125e-6f;  // 2^-17 = 64 float32 ulps of 1
+
+// solver.solve (solver.py:364-429), one problem per thread, written as a
+// UNIFORM TRIAL MACHINE: every pass of the loop is "solve the damped normal
+// equations held in shared memory, evaluate the candidate WITH its Jacobian";
+// the start evaluation is the trial with a zero step and an accepted
+// candidate's normal equations are the next iterate's (the assemble at the
+// new values, solver.py:419).  The rejection loop (:389-409) is a run of
+// rejected trials, so all 32 lanes of a warp execute the same instruction
+// stream whatever their accept / reject / iteration state, and a lane whose
+// problem terminates takes the next problem from a global queue (counter)
+// instead of idling until the warp's slowest problem finishes.
 template <class G>
 __global__ void __launch_bounds__(128)
 k_col_solve(const ChainParams<typename G::T, G::K> C, const CostParams<typename G::T, G::NQ> W,
             const CollisionParams<typename G::T> P, const double* __restrict__ targets,
             const double* __restrict__ q0, int64_t B, const LmOptions O, double* __restrict__ q_out,
             double* __restrict__ cost_out, double* __restrict__ init_cost_out, double* __restrict__ hist_out,
-            int32_t* __restrict__ iters_out, int32_t* __restrict__ term_out) {
+            int32_t* __restrict__ iters_out, int32_t* __restrict__ term_out, unsigned long long* __restrict__ queue) {
   using T = typename G::T;
   constexpr int NQ = G::NQ, NT = Tri<NQ>::size;
+  constexpr bool F32 = sizeof(T) == 4;
   extern __shared__ unsigned char smem_raw[];
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
   T* Ag = reinterpret_cast<T*>(smem_raw) + threadIdx.x;  // [(NT + NQ) * 128]
   T* scratch = reinterpret_cast<T*>(smem_raw) + (NT + NQ) * 128 + threadIdx.x;
-  const TargetInv<T> tg = target_inverse_t<T>(targets + b * 7);
-  const CollisionModel<G> model{C, W, P, tg, ColLane<G>{scratch, 128}};
-  T q[NQ];
-#pragma unroll
-  for (int i = 0; i < NQ; ++i) q[i] = T(q0[b * NQ + i]);
-  const T zb[3] = {T(0), T(0), T(0)};
-  T cost = T(0);
+  const int64_t first_wave = (int64_t)gridDim.x * blockDim.x;
+  int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int hstride = O.max_iterations + 1;
-  int term = kMaxIterations;
-  int iters = 0;
-  T damping = T(O.damping0);
-  // one J-assembly site: the start evaluation, then J at each accepted iterate
-  // (solver.py:419) -- a single inlined copy of the collision stack
-  for (int it = 0;; ++it) {
-    {
-      T A[NT], g[NQ];
-      const T c = model.template eval<true>(q, zb, A, g);
+  const T zb[3] = {T(0), T(0), T(0)};
+  T q[NQ], d[NQ];
+  T cost = T(0), damping = T(0), pred = T(0);
+  int iters = 0, rej = 0;
+  bool start = true;
+  TargetInv<T> tg{};
+  auto begin = [&](int64_t bb) {
+    tg = target_inverse_t<T>(targets + bb * 7);
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) {
+      q[i] = T(q0[bb * NQ + i]);
+      d[i] = T(0);
+    }
+    damping = T(O.damping0);
+    iters = rej = 0;
+    start = true;
+  };
+  if (b < B) begin(b);
+  while (b < B) {
+    // ---- the one evaluation site: candidate q + d (the start: d = 0) ----
+    T qc[NQ], A[NT], g[NQ];
+#pragma unroll
+    for (int i = 0; i < NQ; ++i) qc[i] = q[i] + d[i];
+    const CollisionModel<G> model{C, W, P, tg, ColLane<G>{scratch, 128}};
+    const T cn = model.template eval<true>(qc, zb, A, g);
+    int term = -1;
+    bool fresh = false;  // normal equations of a new iterate: iteration-start checks
+    if (start) {
+      start = false;
+      cost = cn;
+      init_cost_out[b] = double(cn);
+      if (hist_out) hist_out[b * hstride] = double(cn);
+      fresh = true;
+      if (!finite_t(cn)) term = kNonFiniteCost;  // raw_residual raises on non-finite
+    } else if (!finite_t(cn)) {
+      term = kNonFiniteCost;  // CostEvaluationError -> solve_batch's numerical_failure
+    } else if (cn < cost) {
+      T smax = T(0);
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) {
+        q[i] = qc[i];
+        smax = tmax(smax, fabs(d[i]));
+      }
+      cost = cn;
+      damping = tmax(damping * T(O.down), T(BeamConsts::damping_min));
+      rej = 0;
+      ++iters;
+      if (hist_out) hist_out[b * hstride + iters] = double(cost);
+      fresh = true;
+      if (smax < T(O.step_tol)) term = kStepConverged;
+    } else if (F32 && pred <= T(kFp32Tau) * cost) {
+      term = kFp32Resolution;
+    } else {
+      damping *= T(O.up);
+      ++rej;
+      if (damping > T(BeamConsts::damping_max)) term = kNumericalFailure;
+      else if (rej >= O.max_rejections) term = kRejectionsExhausted;
+    }
+    if (fresh) {
 #pragma unroll
       for (int i = 0; i < NT; ++i) Ag[i * 128] = A[i];
 #pragma unroll
       for (int i = 0; i < NQ; ++i) Ag[(NT + i) * 128] = g[i];
-      if (it == 0) {
-        cost = c;
-        if (hist_out) hist_out[b * hstride] = double(cost);
-        init_cost_out[b] = double(cost);
-        term = finite_t(cost) ? kMaxIterations : kNonFiniteCost;  // raw_residual raises on non-finite
+      if (term < 0) {
+        if (iters >= O.max_iterations) {
+          term = kMaxIterations;
+        } else {
+          T gmax = T(0);
+#pragma unroll
+          for (int i = 0; i < NQ; ++i) gmax = tmax(gmax, fabs(g[i]));
+          if (gmax < T(O.grad_tol)) term = kGradientConverged;
+        }
       }
     }
-    if (term != kMaxIterations || it >= O.max_iterations) break;
-    T gmax = T(0);
-#pragma unroll
-    for (int i = 0; i < NQ; ++i) gmax = tmax(gmax, fabs(Ag[(NT + i) * 128]));
-    if (gmax < T(O.grad_tol)) {
-      term = kGradientConverged;
-      break;
-    }
-    bool accepted = false;
-    T step[NQ];
-    for (int rj = 0; rj < O.max_rejections; ++rj) {
-      T A[NT], g[NQ], d[NQ];
+    // ---- the next trial's step (a failed factorisation is a rejected trial) ----
+    while (term < 0) {
 #pragma unroll
       for (int i = 0; i < NT; ++i) A[i] = Ag[i * 128];
 #pragma unroll
       for (int i = 0; i < NQ; ++i) g[i] = Ag[(NT + i) * 128];
       bool ok = damped_solve<T, NQ>(A, g, damping, d);
+      T gd = T(0), dd = T(0);
 #pragma unroll
-      for (int i = 0; i < NQ; ++i) ok = ok && finite_t(d[i]);
+      for (int i = 0; i < NQ; ++i) {
+        ok = ok && finite_t(d[i]);
+        gd += g[i] * d[i];
+        dd += tmax(A[Tri<NQ>::at(i, i)], T(BeamConsts::diag_clamp)) * d[i] * d[i];
+      }
       if (ok) {
-        T qn[NQ];
-#pragma unroll
-        for (int i = 0; i < NQ; ++i) qn[i] = q[i] + d[i];
-        const T cn = model.template eval<false>(qn, zb, A, g);
-        if (!finite_t(cn)) {  // CostEvaluationError -> solve_batch's numerical_failure
-          term = kNonFiniteCost;
-          break;
-        }
-        if (cn < cost) {
-#pragma unroll
-          for (int i = 0; i < NQ; ++i) {
-            q[i] = qn[i];
-            step[i] = d[i];
-          }
-          cost = cn;
-          damping = tmax(damping * T(O.down), T(BeamConsts::damping_min));
-          accepted = true;
-          break;
-        }
+        pred = damping * dd - gd;  // quadratic-model decrease of the trial
+        break;
       }
       damping *= T(O.up);
-      if (damping > T(BeamConsts::damping_max)) break;
+      ++rej;
+      if (damping > T(BeamConsts::damping_max)) term = kNumericalFailure;
+      else if (rej >= O.max_rejections) term = kRejectionsExhausted;
     }
-    if (term != kMaxIterations) break;
-    if (!accepted) {
-      term = damping > T(BeamConsts::damping_max) ? kNumericalFailure : kRejectionsExhausted;
-      break;
-    }
-    ++iters;
-    if (hist_out) hist_out[b * hstride + iters] = double(cost);
-    T smax = T(0);
+    if (term >= 0) {
+      if (hist_out)
+        for (int i = iters + 1; i < hstride; ++i) hist_out[b * hstride + i] = NAN;
 #pragma unroll
-    for (int i = 0; i < NQ; ++i) smax = tmax(smax, fabs(step[i]));
-    if (smax < T(O.step_tol)) {
-      term = kStepConverged;
-      break;
+      for (int i = 0; i < NQ; ++i) q_out[b * NQ + i] = double(q[i]);
+      cost_out[b] = double(cost);
+      iters_out[b] = iters;
+      term_out[b] = term;
+      b = first_wave + (int64_t)atomicAdd(queue, 1ull);
+      if (b < B) begin(b);
     }
   }
-  if (hist_out)
-    for (int i = iters + 1; i < hstride; ++i) hist_out[b * hstride + i] = NAN;
-#pragma unroll
-  for (int i = 0; i < NQ; ++i) q_out[b * NQ + i] = double(q[i]);
-  cost_out[b] = double(cost);
-  iters_out[b] = iters;
-  term_out[b] = term;
 }
 
 // ---------------------------------------------------------------------------
@@ -233,13 +267,29 @@ cudaError_t launch_col(const ChainParams<typename G::T, G::K>& C, const CostPara
   if (L.op == ColOp::kSolve) {
     if (L.B == 0) return cudaSuccess;
     const size_t smem = sizeof(T) * (Tri<G::NQ>::size + G::NQ) * 128 + col_scratch_bytes<G>(P);
+    cudaError_t e;
     cudaFuncSetAttribute(k_col_solve<G>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
-    if (smem > 48 * 1024)
-      cudaFuncSetAttribute(k_col_solve<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_col_solve<G><<<(unsigned)((L.B + 127) / 128), 128, smem, st>>>(C, W, P, L.targets, L.q_in, L.B, L.opts,
-                                                                      L.q_out, L.cost_out, L.init_cost, L.hist_out,
-                                                                      L.iters, L.term);
-    return cudaGetLastError();
+    if (smem > 48 * 1024 &&
+        (e = cudaFuncSetAttribute(k_col_solve<G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) !=
+            cudaSuccess)
+      return e;
+    // persistent grid: every resident CTA, lanes pull further problems from the queue
+    int dev = 0, sms = 0, per_sm = 0;
+    if ((e = cudaGetDevice(&dev)) != cudaSuccess ||
+        (e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess ||
+        (e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_col_solve<G>, 128, smem)) != cudaSuccess)
+      return e;
+    const int64_t need = (L.B + 127) / 128;
+    const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(need, (int64_t)sms * std::max(per_sm, 1)));
+    unsigned long long* queue = nullptr;
+    if ((e = cudaMallocAsync(reinterpret_cast<void**>(&queue), sizeof(unsigned long long), st)) != cudaSuccess)
+      return e;
+    cudaMemsetAsync(queue, 0, sizeof(unsigned long long), st);
+    k_col_solve<G><<<(unsigned)grid, 128, smem, st>>>(C, W, P, L.targets, L.q_in, L.B, L.opts, L.q_out, L.cost_out,
+                                                      L.init_cost, L.hist_out, L.iters, L.term, queue);
+    e = cudaGetLastError();
+    cudaFreeAsync(queue, st);
+    return e;
   }
   // IK-Beam over the collision stack
   const BeamLaunch& Bm = L.beam;

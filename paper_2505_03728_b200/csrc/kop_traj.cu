@@ -943,6 +943,10 @@ __device__ bool traj_damped_solve(const TrajView<G>& S, int N, typename G::T lam
   return ok;
 }
 
+// FP32 stopping rule, as in k_col_solve (kop_collision.cu): a rejected trial whose
+// quadratic-model decrease is below 2^-17 of the cost is not resolvable in FP32
+constexpr float kTrajFp32Tau = 7.62939453125e-6f;
+
 template <class G>
 __global__ void __launch_bounds__(traj_threads<G>())
 k_traj_solve(const ChainParams<typename G::T, G::K> C, const CollisionParams<typename G::T> P,
@@ -992,13 +996,16 @@ k_traj_solve(const ChainParams<typename G::T, G::K> C, const CollisionParams<typ
     T smax = T(0);
     for (int rj = 0; rj < O.max_rejections; ++rj) {
       const bool ok = traj_damped_solve<G>(S, N, damping);
-      T fin = T(1);
+      T fin = T(1), pp = T(0);
       for (int i = tid; i < N; i += traj_threads<G>()) {
         S.qn[i] = S.q[i] + S.y[i];
         if (!finite_t(S.y[i])) fin = T(0);
+        if (sizeof(T) == 4)  // quadratic-model decrease -g.d + lam d^T D d (the FP32 rule below)
+          pp += damping * tmax(S.h(i, 0), T(BeamConsts::diag_clamp)) * S.y[i] * S.y[i] - S.g[i] * S.y[i];
       }
       __syncthreads();
       const bool finite_ok = __syncthreads_and(fin > T(0));
+      const T pred = sizeof(T) == 4 ? block_sum(pp, S.red) : T(0);
       if (ok && finite_ok) {
         KOP_PROF_T(pe0);
         const T cn = traj_eval<G, false>(C, P, W, S, S.qn);
@@ -1019,6 +1026,10 @@ k_traj_solve(const ChainParams<typename G::T, G::K> C, const CollisionParams<typ
           cost = cn;
           damping = tmax(damping * T(O.down), T(BeamConsts::damping_min));
           accepted = true;
+          break;
+        }
+        if (sizeof(T) == 4 && pred <= T(kTrajFp32Tau) * cost) {  // FP32 rule (kop_collision.cu kFp32Tau)
+          term = 6;
           break;
         }
       }

@@ -389,6 +389,8 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
     }
     bool accepted = false;
     T step = T(0);
+    // diag of J^T J at the iterate (lane i), for the FP32 rule's model decrease
+    const T dg = lane < n ? tmax(S.A[lane * 33 + lane], T(BeamConsts::diag_clamp)) : T(0);
     for (int rj = 0; rj < O.max_rejections; ++rj) {
       T d;
       bool ok = tree_damped_solve(P, S, g, damping, lane, d);
@@ -409,6 +411,13 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
           damping = tmax(damping * T(O.down), T(BeamConsts::damping_min));
           accepted = true;
           __syncwarp();
+          break;
+        }
+        // FP32 rule (kop_collision.cu kFp32Tau): a rejected trial whose quadratic-model decrease
+        // -g.d + lam d^T D d is below 2^-17 of the cost is not resolvable in float32
+        if (sizeof(T) == 4 && warp_sum(lane < n ? damping * dg * d * d - g * d : T(0)) <=
+                                  T(7.62939453125e-6f) * cost) {
+          term = 6;
           break;
         }
       }

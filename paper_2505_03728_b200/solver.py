@@ -32,7 +32,8 @@ DIAG_CLAMP = 1e-8
 TERMINATIONS = {0: ("max_iterations", ""), 1: ("gradient_converged", ""), 2: ("step_converged", ""),
                 3: ("numerical_failure", "no acceptable step below damping 1e10"),
                 4: ("step_converged", "rejection budget exhausted without descent"),
-                5: ("numerical_failure", "cost evaluation returned a non-finite residual")}
+                5: ("numerical_failure", "cost evaluation returned a non-finite residual"),
+                6: ("step_converged", "no cost decrease resolvable in FP32 (model decrease below 2^-17 of the cost)")}
 
 
 def _tangent_dim(x) -> int:
