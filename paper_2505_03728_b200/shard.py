@@ -23,18 +23,25 @@ def shard_range(total: int, world: int, rank: int) -> tuple[int, int]:
 
 def gather_rows(local, total: int, group=None):
     """All-gather per-rank row blocks (torch tensors, same trailing shape) into the
-    full [total, ...] array in global index order."""
+    full [total, ...] array in global index order, on ``local``'s device.
+
+    NCCL gathers device tensors directly (NVLink / NVSwitch); a gloo group only
+    moves host tensors, so device blocks are staged through host memory there
+    (several ranks sharing one GPU, or a CPU-only test)."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
     sizes = [shard_range(total, world, r) for r in range(world)]
     width = max(e - s for s, e in sizes)
-    pad = torch.zeros((width,) + tuple(local.shape[1:]), dtype=local.dtype, device=local.device)
-    pad[: local.shape[0]] = local
+    via_host = dist.get_backend(group) == "gloo" and local.device.type != "cpu"
+    dev = torch.device("cpu") if via_host else local.device
+    pad = torch.zeros((width,) + tuple(local.shape[1:]), dtype=local.dtype, device=dev)
+    pad[: local.shape[0]] = local.to(dev)
     parts = [torch.empty_like(pad) for _ in range(world)]
     dist.all_gather(parts, pad, group=group)
-    return torch.cat([p[: e - s] for p, (s, e) in zip(parts, sizes)], dim=0)
+    full = torch.cat([p[: e - s] for p, (s, e) in zip(parts, sizes)], dim=0)
+    return full.to(local.device) if via_host else full
 
 
 def solve_sharded(solver, targets_for, total: int, group=None, gather: bool = True):
