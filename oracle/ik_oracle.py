@@ -593,6 +593,46 @@ def cholesky_engine(ch: Chain, link: int, weights=None, dtype=np.float32, **kw):
     return lambda q_, t_, group: CholeskyLaneEngine(ch, link, q_, t_, w, group=group, dtype=dtype, **kw)
 
 
+def explain_divergence(h_dev, h_ref, diag, tol=1e-6):
+    """For every target whose device winner history leaves ``tol`` (relative) of the
+    oracle's, say why: the device's winning seed is identified by its start cost
+    (``diag['s1_start']``), then
+      * same seed          -> an accept / reject near-tie inside the lane: the relative
+                              cost change the oracle made at the first step whose
+                              decision differs ("accept_gap");
+      * different survivor -> the final argmin (tasks.py:139): the relative gap of the
+                              two survivors' final oracle costs ("winner_gap");
+      * seed not kept      -> the stable top-keep prune (tasks.py:135): the relative gap
+                              between the device seed's stage-1 cost and the oracle's
+                              keep-th survivor ("prune_gap").
+    Returns a list of (target, kind, first divergent step, gap)."""
+    h_dev, h_ref = np.asarray(h_dev, float), np.asarray(h_ref, float)
+    rel = np.abs(h_dev - h_ref) / np.maximum(np.abs(h_ref), 1e-300)
+    out = []
+    for t in np.flatnonzero(rel.max(axis=1) >= tol):
+        step = int(np.argmax(rel[t] >= tol))
+        starts = diag["s1_start"][t]
+        seed = int(np.argmin(np.abs(starts - h_dev[t, 0]) / np.abs(starts)))
+        ref_seed = int(diag["order"][t, diag["winner"][t]])
+        kept = list(diag["order"][t])
+        if seed == ref_seed:
+            acc_d = h_dev[t, 1:] < h_dev[t, :-1]
+            acc_r = h_ref[t, 1:] < h_ref[t, :-1]
+            k = int(np.argmax(acc_d != acc_r)) if np.any(acc_d != acc_r) else max(step - 1, 0)
+            gap = abs(h_ref[t, k] - h_ref[t, k + 1]) / abs(h_ref[t, k])
+            out.append((int(t), "accept_gap", step, float(gap)))
+        elif seed in kept:
+            c = diag["s2_cost"][t]
+            gap = abs(c[kept.index(seed)] - c[diag["winner"][t]]) / abs(c[diag["winner"][t]])
+            out.append((int(t), "winner_gap", step, float(gap)))
+        else:
+            c1 = diag["s1_cost"][t]
+            edge = c1[kept[-1]]
+            gap = abs(c1[seed] - edge) / abs(edge)
+            out.append((int(t), "prune_gap", step, float(gap)))
+    return out
+
+
 def history_agreement(h_dev, h_ref, rtol=1e-4, atol=1e-6):
     """Per-step cost agreement of two (lanes, steps+1) cost histories up to each
     lane's first accept/reject flip (the first step at which one run accepts its
@@ -684,6 +724,7 @@ class BeamResult:
     rot_err: np.ndarray
     success: np.ndarray
     base: np.ndarray | None = None  # (B, 3) x, y, angle
+    diag: dict | None = None  # stage-1 / stage-2 costs and choices (parity diagnostics)
 
 
 DEFAULT_WEIGHTS = (50.0, 10.0, 100.0, 0.01)  # costs.py:52-62 (pos, ori, limit, rest)
@@ -724,5 +765,6 @@ def ik_beam(ch: Chain, link: int, tq, tt, seeds, weights=DEFAULT_WEIGHTS, total_
         pe, re = pose_errors(ch, link, tq, tt, q, ba, st2.bxy[sel])
     else:
         pe, re = pose_errors(ch, link, tq, tt, q)
+    diag = dict(s1_start=st.hist[0].reshape(b, s), s1_cost=cost, order=order, s2_cost=c2, winner=win)
     return BeamResult(q=q, cost=st2.cost[sel], hist=hist, pos_err=pe, rot_err=re,
-                      success=(pe < pos_tol) & (re < rot_tol), base=base)
+                      success=(pe < pos_tol) & (re < rot_tol), base=base, diag=diag)

@@ -119,5 +119,7 @@ def multi_ee_beam(ch, links, tq, tt, seeds, w_pos, w_ori, w_limit=100.0, w_rest=
     q = st2.q[sel]
     pe = np.stack([o.pose_errors(ch, links[e], tq[:, e], tt[:, e], q)[0] for e in range(k)], axis=1)
     re = np.stack([o.pose_errors(ch, links[e], tq[:, e], tt[:, e], q)[1] for e in range(k)], axis=1)
+    diag = dict(s1_start=st.hist[0].reshape(b, s), s1_cost=st.cost.reshape(b, s), order=order,
+                s2_cost=st2.cost.reshape(b, keep), winner=win)
     return dict(q=q, cost=st2.cost[sel], hist=np.stack([h[sel] for h in st2.hist], axis=1), pos_err=pe,
-                rot_err=re, success=np.all((pe < pos_tol) & (re < rot_tol), axis=1))
+                rot_err=re, success=np.all((pe < pos_tol) & (re < rot_tol), axis=1), diag=diag)

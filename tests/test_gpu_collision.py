@@ -5,8 +5,10 @@ Bars: collision residuals/Jacobians fp64 within 1e-9 of the oracle (which is
 pinned to the reference's world/self rows), fp32 within 2e-4 of the row
 scale; device ``solve`` fp64 cost histories within 1e-6 relative of the
 reference ``solver.solve`` with identical iteration counts; collision
-IK-Beam fp64 histories within 1e-6 on >= 80% of targets, fp32 success equal
-to the oracle's on >= 95% of targets.
+IK-Beam fp64 histories within 1e-6 on >= 95% of 128 targets with every other
+target an oracle near-tie (relative gap < 1e-12), fp32 success equal to the
+oracle's on >= 95% of targets; at 1000 targets the fp32 success rate within
+1 pp of the oracle's.
 """
 
 import numpy as np
@@ -24,6 +26,7 @@ import paper_2505_03728_b200 as k  # noqa: E402
 from conftest import robot_file  # noqa: E402
 from oracle import collision_oracle as co  # noqa: E402
 from oracle import ik_oracle as o  # noqa: E402
+from oracle_pool import assert_fp64_beam_parity, par_batched  # noqa: E402
 from paper_2505_03728_b200 import _device as dv  # noqa: E402
 from paper_2505_03728_b200._lib import check, lib  # noqa: E402
 from paper_2505_03728_b200.benchmark import reachable_target_array  # noqa: E402
@@ -140,15 +143,32 @@ def test_device_solve_fp32_and_unsupported(models, golden):
 def test_collision_beam_vs_oracle(models, chains):
     ch = chains["arm7"]
     sp = co.load_spheres_files(ch, robot_file("arm7.urdf"), robot_file("arm7.sidecar.json"))
-    tg = reachable_target_array(models["arm7"], "flange", 24, 31).cpu().numpy()
+    tg = reachable_target_array(models["arm7"], "flange", 128, 31).cpu().numpy()
     seeds = o.sample_seeds(ch, 64, 31)
-    ref = co.ik_beam_collision(ch, sp, DEMO_O, 8, tg[:, :4], tg[:, 4:], seeds, co.CollisionCosts())
+    ref = par_batched(co.ik_beam_collision, ch, sp, DEMO_O, 8, tq=tg[:, :4], tt=tg[:, 4:], seeds=seeds,
+                      cc=co.CollisionCosts(), split=("tq", "tt"))
     g64 = k.solve_ik_collision_batch(models["arm7"], "flange", tg, world=DEMO, rng_seed=31, precision="fp64")
-    rel = np.abs(g64.history - ref.hist) / ref.hist
-    assert np.mean(rel.max(axis=1) < 1e-6) >= 0.8, np.sort(rel.max(axis=1))
+    assert_fp64_beam_parity(g64.history, ref.hist, ref.diag)
     g32 = k.solve_ik_collision_batch(models["arm7"], "flange", tg, world=DEMO, rng_seed=31)
     assert np.mean(g32.success == ref.success) >= 0.95
     assert np.all(np.diff(g32.history, axis=1) <= 0)
     # the collision stack only adds non-negative rows: its cost is >= the plain IK cost on the same q
     plain = k.solve_ik_beam_batch(models["arm7"], "flange", tg, rng_seed=31, precision="fp64")
     assert np.median(g64.cost) >= 0.5 * np.median(plain.cost)
+
+
+def test_collision_beam_distribution_1000(models, chains):
+    """Config 4 at 1000 targets: the measured FP32 mode's success rate (91% -- the demo world
+    blocks some targets) within 1 pp of the oracle's, per-target agreement >= 98%."""
+    ch = chains["arm7"]
+    sp = co.load_spheres_files(ch, robot_file("arm7.urdf"), robot_file("arm7.sidecar.json"))
+    tg = reachable_target_array(models["arm7"], "flange", 1000, 77).cpu().numpy()
+    seeds = o.sample_seeds(ch, 64, 77)
+    ref = par_batched(co.ik_beam_collision, ch, sp, DEMO_O, 8, tq=tg[:, :4], tt=tg[:, 4:], seeds=seeds,
+                      cc=co.CollisionCosts(), split=("tq", "tt"))
+    g32 = k.solve_ik_collision_batch(models["arm7"], "flange", tg, world=DEMO, rng_seed=77)
+    agree = np.mean(g32.success.astype(bool) == ref.success)
+    print(f"\nconfig 4, 1000 targets: oracle success {ref.success.mean():.4f}, device FP32 {g32.success.mean():.4f}, "
+          f"per-target agreement {agree:.4f}")
+    assert abs(g32.success.mean() - ref.success.mean()) <= 0.01
+    assert agree >= 0.98

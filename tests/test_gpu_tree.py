@@ -14,6 +14,7 @@ if not torch.cuda.is_available():  # pragma: no cover
 import paper_2505_03728_b200 as k  # noqa: E402
 from oracle import ik_oracle as o  # noqa: E402
 from oracle import tree_oracle as to  # noqa: E402
+from oracle_pool import assert_fp64_beam_parity, par_batched  # noqa: E402
 
 EES = ["left_hand", "right_hand", "left_foot", "right_foot"]
 
@@ -100,14 +101,15 @@ def test_tree_ik_beam_fp64_matches_oracle(hum):
     from oracle import tree_oracle as tro
 
     chh = o.load_chain_files(k.robot_path("humanoid29.urdf"))
-    links, tq, tt, tg = _hum_targets(hum, chh, 12, 5)
+    links, tq, tt, tg = _hum_targets(hum, chh, 128, 5)
     seeds = o.sample_seeds(chh, 64, 3)
-    ref = tro.multi_ee_beam(chh, links, tq, tt, seeds, [50.0] * 4, [10.0] * 4)
+    ref = par_batched(tro.multi_ee_beam, chh, links, tq=tq, tt=tt, seeds=seeds, w_pos=[50.0] * 4,
+                      w_ori=[10.0] * 4, split=("tq", "tt"))
     got = k.solve_ik_beam_multi(hum, EES, tg, rng_seed=3, precision="fp64")
+    assert_fp64_beam_parity(got.history, ref["hist"], ref["diag"])
     rel = np.abs(got.history - ref["hist"]) / ref["hist"]
-    assert np.mean(rel.max(axis=1) < 1e-6) >= 0.75, np.sort(rel.max(axis=1))
-    assert np.mean(got.success == ref["success"]) >= 0.9
     same = rel.max(axis=1) < 1e-6
+    assert np.array_equal(got.success[same].astype(bool), ref["success"][same])
     np.testing.assert_allclose(got.pos_error[same], ref["pos_err"][same], rtol=1e-4, atol=1e-9)
 
 
@@ -146,17 +148,18 @@ def test_tree_ik_beam_random_chain_lane_edges(seed, n):
     rng = np.random.default_rng(seed)
     lo = np.where(np.isfinite(ch.lower), ch.lower, -np.pi)
     hi = np.where(np.isfinite(ch.upper), ch.upper, np.pi)
-    lq, lp, _, _ = o.fk(ch, rng.uniform(lo, hi, (4, n)))
+    lq, lp, _, _ = o.fk(ch, rng.uniform(lo, hi, (32, n)))
     tq = o.qcanon(lq[:, li])[:, None]
     tt = lp[:, li][:, None]
     seeds = o.sample_seeds(ch, 64, 3)
-    ref = tro.multi_ee_beam(ch, [li], tq, tt, seeds, [50.0], [10.0])
+    ref = par_batched(tro.multi_ee_beam, ch, [li], tq=tq, tt=tt, seeds=seeds, w_pos=[50.0], w_ori=[10.0],
+                      split=("tq", "tt"))
     got = k.solve_ik_beam_multi(m, ["tool"], np.concatenate([tq, tt], axis=2), rng_seed=3, precision="fp64")
-    rel = np.abs(got.history - ref["hist"]) / np.maximum(ref["hist"], 1e-300)
-    if n > 1:  # one column: many seeds tie on the optimum, so the winner (and its start cost) is a coin flip
-        assert np.mean(rel.max(axis=1) < 1e-6) >= 0.75, np.sort(rel.max(axis=1))
+    # one column: many seeds reach the same optimum, so prune / winner choices are exact ties and the
+    # winner's early history may be another tied seed's; every divergence must still be such a near-tie
+    assert_fp64_beam_parity(got.history, ref["hist"], ref["diag"], frac=0.95 if n > 1 else 0.0)
     np.testing.assert_allclose(got.history[:, -1], ref["hist"][:, -1], rtol=1e-6, atol=1e-12)
-    assert np.mean(got.success == ref["success"]) >= 0.75
+    assert np.mean(got.success == ref["success"]) >= 0.95
     r32 = k.solve_ik_beam_multi(m, ["tool"], np.concatenate([tq, tt], axis=2), rng_seed=3)
     assert np.all(np.diff(r32.history, axis=1) <= 0)
 
@@ -182,3 +185,25 @@ def test_tree_solve_32_columns_matches_oracle():
     poses = [(li, o.qcanon(lq[0, li]), lp[0, li], w.pose_position, w.pose_orientation)]
     _, c_ref, _, _, _ = to.solve_multi_pose(ch, poses, ch.rest)
     np.testing.assert_allclose(rep.final_cost, c_ref, rtol=1e-5, atol=1e-12)
+
+
+def test_humanoid_ik_beam_distribution_1000(hum):
+    """Config 3 at 1000 target sets: device FP32 (measured mode) and FP64 success rates vs the
+    oracle's (54% -- 4 end-effector targets from random in-limit configurations, 16 LM steps)."""
+    from oracle import tree_oracle as tro
+
+    chh = o.load_chain_files(k.robot_path("humanoid29.urdf"))
+    links, tq, tt, tg = _hum_targets(hum, chh, 1000, 29)
+    seeds = o.sample_seeds(chh, 64, 0)
+    ref = par_batched(tro.multi_ee_beam, chh, links, tq=tq, tt=tt, seeds=seeds, w_pos=[50.0] * 4,
+                      w_ori=[10.0] * 4, split=("tq", "tt"))
+    r64 = k.solve_ik_beam_multi(hum, EES, tg, rng_seed=0, precision="fp64")
+    r32 = k.solve_ik_beam_multi(hum, EES, tg, rng_seed=0)
+    s_ref = ref["success"].mean()
+    print(f"\nconfig 3, 1000 targets: oracle success {s_ref:.4f}, device FP64 {r64.success.mean():.4f} "
+          f"(per-target agreement {np.mean(r64.success.astype(bool) == ref['success']):.4f}), device FP32 "
+          f"{r32.success.mean():.4f}")
+    assert np.mean(r64.success.astype(bool) == ref["success"]) >= 0.99
+    assert abs(r32.success.mean() - s_ref) <= 0.02
+    for a, b in ((r32.pos_error.max(axis=1), ref["pos_err"].max(axis=1)),):
+        assert 0.5 * np.percentile(b, 50) <= np.percentile(a, 50) <= 2.0 * np.percentile(b, 50)
