@@ -361,6 +361,12 @@ int kop_fma_peak_kernel(int32_t blocks, int32_t threads, int32_t iters, float* s
 int kop_dfma_peak_kernel(int32_t blocks, int32_t threads, int32_t iters, double* sink, double* flops,
                          void* stream);
 
+/* --- checking builds ----------------------------------------------------
+ * Copies `words` 32-bit words of a probe kernel's never-written dynamic
+ * shared memory to device `out` (<= 12288 words).  In the shared-memory
+ * poison build (kop_build_info() names it) every word is 0xFFFFFFFF. */
+int kop_check_probe(uint32_t* out, int32_t words, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

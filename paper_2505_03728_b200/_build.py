@@ -24,7 +24,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
          "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 
 SOURCES = ["kop_kernels.cu", "kop_collision.cu", "kop_tree.cu", "kop_traj.cu", "kop_aux.cu", "kop_capi.cu"]
-HEADERS = ["kop_chain.h", "kop_lie.cuh", "kop_lane.cuh", "kop_beam.cuh", "kop_collision.cuh", "kop_kernels.cuh", "kop_tree.cuh", "kop_traj.cuh"]
+HEADERS = ["kop_check.cuh", "kop_chain.h", "kop_lie.cuh", "kop_lane.cuh", "kop_beam.cuh", "kop_collision.cuh", "kop_kernels.cuh", "kop_tree.cuh", "kop_traj.cuh"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:
@@ -34,15 +34,34 @@ def _stale(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, ptxas_info: bool = False, force: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+# checking builds (csrc/kop_check.cuh): same sources, extra defines, own objects,
+# libraries under variants/ (shipped to the GPU box with the repo snapshot)
+VARIANTS = {"poison": ["-DKOP_SMEM_POISON"], "jitter": ["-DKOP_JITTER"]}
+VARIANT_DIR = os.path.join(ROOT, "variants")
+
+
+def variant_lib(name: str) -> str:
+    return os.path.join(VARIANT_DIR, f"libkinoptik_b200_{name}.so")
+
+
+def build_variants(verbose: bool = False, force: bool = False) -> list:
+    """Build every checking variant (tests/test_gpu_checks.py)."""
+    return [build(verbose=verbose, force=force, variant=name) for name in VARIANTS]
+
+
+def build(verbose: bool = False, ptxas_info: bool = False, force: bool = False, variant: str | None = None) -> str:
+    extra = VARIANTS[variant] if variant else []
+    obj_dir = os.path.join(ROOT, "build", f"obj_{variant}") if variant else OBJ
+    lib_path = variant_lib(variant) if variant else LIB
+    os.makedirs(obj_dir, exist_ok=True)
+    os.makedirs(os.path.dirname(lib_path), exist_ok=True)
     hdrs = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "kinoptik_b200.h")]
     jobs = []
     for src in SOURCES:
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJ, src.replace(".cu", ".o"))
+        o = os.path.join(obj_dir, src.replace(".cu", ".o"))
         if force or _stale(o, [s] + hdrs):
-            cmd = [NVCC, *ARCH, *FLAGS, "-c", s, "-o", o]
+            cmd = [NVCC, *ARCH, *FLAGS, *extra, "-c", s, "-o", o]
             if ptxas_info:
                 cmd.insert(1, "-Xptxas=-v")
             jobs.append((src, cmd))
@@ -58,16 +77,17 @@ def build(verbose: bool = False, ptxas_info: bool = False, force: bool = False) 
                 sys.stderr.write(r.stdout + r.stderr)
             if r.returncode != 0:
                 raise RuntimeError(f"nvcc failed on {src}")
-    objs = [os.path.join(OBJ, s.replace(".cu", ".o")) for s in SOURCES]
-    if force or jobs or _stale(LIB, objs):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lcudart"]
+    objs = [os.path.join(obj_dir, s.replace(".cu", ".o")) for s in SOURCES]
+    if force or jobs or _stale(lib_path, objs):
+        cmd = [NVCC, *ARCH, "-shared", "-o", lib_path, *objs, "-lcudart"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             sys.stderr.write(r.stdout + r.stderr)
             raise RuntimeError("link failed")
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":
-    build(verbose=True, ptxas_info="-v" in sys.argv, force="-f" in sys.argv)
-    print(LIB)
+    print(build(verbose=True, ptxas_info="-v" in sys.argv, force="-f" in sys.argv))
+    if "--variants" in sys.argv:
+        print(build_variants(verbose=True, force="-f" in sys.argv))

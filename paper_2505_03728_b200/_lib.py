@@ -112,6 +112,7 @@ SIGNATURES = {
     "kop_link_poses": (C.c_int, [_p, _i32, _p, _i64, _p, _p]),
     "kop_fma_peak_kernel": (C.c_int, [_i32, _i32, _i32, _p, C.POINTER(_f64), _p]),
     "kop_dfma_peak_kernel": (C.c_int, [_i32, _i32, _i32, _p, C.POINTER(_f64), _p]),
+    "kop_check_probe": (C.c_int, [_p, _i32, _p]),
 }
 
 _lib = None

@@ -337,4 +337,19 @@ cudaError_t launch_dfma_peak(int blocks, int threads, int iters, double* sink, c
   return cudaGetLastError();
 }
 
+// Checking-build probe: copies its (never written) dynamic shared memory out.
+// In the poison build every word is 0xFFFFFFFF (the positive control of
+// tests/test_gpu_checks.py); in the normal build the values are undefined.
+__global__ void __launch_bounds__(128) k_check_probe(uint32_t* out, int words) {
+  extern __shared__ unsigned char smem_raw[];
+  KOP_SMEM_ENTRY(smem_raw);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(smem_raw);
+  for (int i = threadIdx.x; i < words; i += blockDim.x) out[i] = w[i];
+}
+
+cudaError_t launch_check_probe(uint32_t* out, int words, cudaStream_t st) {
+  k_check_probe<<<1, 128, (size_t)words * 4, st>>>(out, words);
+  return cudaGetLastError();
+}
+
 }  // namespace kop

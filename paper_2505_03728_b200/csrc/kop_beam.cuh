@@ -64,6 +64,7 @@ __device__ __forceinline__ void beam_stage1_body(const MF& mf, const double* __r
   using T = typename G::T;
   constexpr int NQ = G::NQ;
   extern __shared__ unsigned char smem_raw[];
+  KOP_SMEM_ENTRY(smem_raw);
   T* hist = reinterpret_cast<T*>(smem_raw);  // [(steps1+1) * TPB]
   unsigned long long* keys =                  // [TPB] 8-byte prune keys (or double costs)
       reinterpret_cast<unsigned long long*>(hist + (size_t)(steps1 + 1) * TPB);
@@ -221,6 +222,7 @@ __device__ __forceinline__ void beam_stage2_body(const MF& mf, const ChainParams
   constexpr int NQ = G::NQ;
   constexpr int bd = BD;
   extern __shared__ unsigned char smem_raw[];
+  KOP_SMEM_ENTRY(smem_raw);
   T* hist = reinterpret_cast<T*>(smem_raw);  // [steps2 * bd]
   T* Ag = hist + (size_t)(steps2 > 0 ? steps2 : 1) * bd;  // [(Tri + ND) * bd]
   T* scratch = Ag + (size_t)(Tri<G::ND>::size + G::ND) * bd;

@@ -355,9 +355,17 @@ extern "C" {
 
 const char* kop_last_error(void) { return g_err.c_str(); }
 
+#if defined(KOP_SMEM_POISON)
+#define KOP_CHECK_MODE "; checking build: shared-memory poison"
+#elif defined(KOP_JITTER)
+#define KOP_CHECK_MODE "; checking build: barrier jitter"
+#else
+#define KOP_CHECK_MODE ""
+#endif
+
 const char* kop_build_info(void) {
   return "kinoptik_b200 sm_100a; fp32/fp64; IK lanes {id2, id6, id7, gen8} + SE(2) base {id7, gen8}; "
-         "collision lanes / LM / trajectories {id7, gen8}; tree LM (n <= 32, 1..8 poses)";
+         "collision lanes / LM / trajectories {id7, gen8}; tree LM (n <= 32, 1..8 poses)" KOP_CHECK_MODE;
 }
 
 int kop_model_create(const KopModelDesc* d, KopModel** out) {
@@ -1475,6 +1483,11 @@ int kop_dfma_peak_kernel(int32_t blocks, int32_t threads, int32_t iters, double*
   if (blocks <= 0 || threads <= 0 || iters <= 0 || !sink) return fail(KOP_EINVAL, "invalid arguments");
   if (flops) *flops = 2.0 * 8.0 * (double)blocks * threads * (double)iters;
   return cuda_status(launch_dfma_peak(blocks, threads, iters, sink, (cudaStream_t)stream));
+}
+
+int kop_check_probe(uint32_t* out, int32_t words, void* stream) {
+  if (!out || words <= 0 || words > 12 * 1024) return fail(KOP_EINVAL, "invalid arguments");
+  return cuda_status(launch_check_probe(out, words, (cudaStream_t)stream));
 }
 
 int kop_fma_peak_kernel(int32_t blocks, int32_t threads, int32_t iters, float* sink, double* flops,

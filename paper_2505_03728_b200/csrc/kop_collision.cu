@@ -63,6 +63,7 @@ k_col_resjac(const ChainParams<typename G::T, G::K> C, const CostParams<typename
   using T = typename G::T;
   constexpr int NQ = G::NQ;
   extern __shared__ unsigned char smem_raw[];
+  KOP_SMEM_ENTRY(smem_raw);
   const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (l >= lanes) return;
   const TargetInv<T> tg = load_target_inv<T>(tinv + (int64_t)lane_target[l] * 7);
@@ -124,6 +125,7 @@ k_col_solve(const ChainParams<typename G::T, G::K> C, const CostParams<typename 
   constexpr int NQ = G::NQ, NT = Tri<NQ>::size;
   constexpr bool F32 = sizeof(T) == 4;
   extern __shared__ unsigned char smem_raw[];
+  KOP_SMEM_ENTRY(smem_raw);
   T* Ag = reinterpret_cast<T*>(smem_raw) + threadIdx.x;  // [(NT + NQ) * 128]
   T* scratch = reinterpret_cast<T*>(smem_raw) + (NT + NQ) * 128 + threadIdx.x;
   const int64_t first_wave = (int64_t)gridDim.x * blockDim.x;

@@ -143,8 +143,9 @@ k_lane_run(const ChainParams<typename G::T, G::K> C, const CostParams<typename G
            double* __restrict__ cost_io, double* __restrict__ hist) {
   using T = typename G::T;
   const int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (l >= lanes) return;
   extern __shared__ unsigned char smem_raw[];
+  KOP_SMEM_ENTRY(smem_raw);
+  if (l >= lanes) return;
   const TargetInv<T> tg = load_target_inv<T>(tinv + (int64_t)lane_target[l] * 7);
   LaneState<G> st;
   st.Ag = reinterpret_cast<T*>(smem_raw) + threadIdx.x;

@@ -115,5 +115,6 @@ cudaError_t launch_jacobian_tree(const TreeParams& P, int precision, const doubl
                                  cudaStream_t st);
 cudaError_t launch_fma_peak(int blocks, int threads, int iters, float* sink, cudaStream_t st);
 cudaError_t launch_dfma_peak(int blocks, int threads, int iters, double* sink, cudaStream_t st);
+cudaError_t launch_check_probe(uint32_t* out, int words, cudaStream_t st);
 
 }  // namespace kop

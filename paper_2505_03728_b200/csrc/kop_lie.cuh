@@ -17,6 +17,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include "kop_check.cuh"
+
 namespace kop {
 
 template <typename T>

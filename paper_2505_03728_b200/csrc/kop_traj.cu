@@ -614,6 +614,7 @@ struct BandView {
 __device__ __forceinline__ void named_bar(int id, int nthreads) {
   __syncwarp();
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+  KOP_JITTER_POINT();
 }
 
 template <class G, class V_>
@@ -957,6 +958,7 @@ k_traj_solve(const ChainParams<typename G::T, G::K> C, const CollisionParams<typ
   using T = typename G::T;
   constexpr int NQ = G::NQ;
   extern __shared__ unsigned char smem_raw[];
+  KOP_SMEM_ENTRY(smem_raw);
   const TrajView<G> S(smem_raw, W.T_steps, P.ns);
   const int64_t b = blockIdx.x;
   const int tid = threadIdx.x, Tn = W.T_steps, N = Tn * NQ, n = W.n;
@@ -1078,6 +1080,7 @@ k_traj_normal(const ChainParams<typename G::T, G::K> C, const CollisionParams<ty
   using T = typename G::T;
   constexpr int NQ = G::NQ, BW = TrajView<G>::BW;
   extern __shared__ unsigned char smem_raw[];
+  KOP_SMEM_ENTRY(smem_raw);
   const TrajView<G> S(smem_raw, W.T_steps, P.ns);
   const int64_t b = blockIdx.x;
   const int tid = threadIdx.x, Tn = W.T_steps, N = Tn * NQ, n = W.n, Nr = Tn * n;
@@ -1122,6 +1125,7 @@ k_traj_report(const ChainParams<double, G::K> C, const CollisionParams<double> P
   static_assert(sizeof(typename G::T) == 8, "reports run in FP64");
   constexpr int NQ = G::NQ;
   extern __shared__ unsigned char smem_raw[];
+  KOP_SMEM_ENTRY(smem_raw);
   const TrajView<G> S(smem_raw, steps, P.ns);
   const int64_t b = blockIdx.x;
   const int tid = threadIdx.x;

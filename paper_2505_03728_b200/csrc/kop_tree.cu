@@ -352,6 +352,7 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
              double* __restrict__ init_cost_out, double* __restrict__ hist_out, int32_t* __restrict__ iters_out,
              int32_t* __restrict__ term_out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  KOP_SMEM_ENTRY(smem_raw);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t b = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
   TreeTable<T>& Q = *reinterpret_cast<TreeTable<T>*>(smem_raw);
@@ -530,6 +531,7 @@ __global__ void __launch_bounds__(32 * tree_beam_warps<T>())
 k_tree_beam_stage1(const TreeLmParams<T> P, const double* __restrict__ targets, int64_t B,
                    const double* __restrict__ seeds, int S, int steps1, T* __restrict__ recs) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  KOP_SMEM_ENTRY(smem_raw);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t L = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;  // lane = target * S + seed
   TreeTable<T>& Q = *reinterpret_cast<TreeTable<T>*>(smem_raw);
@@ -611,6 +613,7 @@ k_tree_beam_stage2(const TreeLmParams<T> P, const TreeLmParams<double> Pd, const
                    double* __restrict__ cost_out, double* __restrict__ hist_out, double* __restrict__ pos_err,
                    double* __restrict__ rot_err, uint8_t* __restrict__ success) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  KOP_SMEM_ENTRY(smem_raw);
   const int lane = threadIdx.x & 31, r = threadIdx.x >> 5;  // warp r = survivor of stage-1 rank r
   const int64_t b = blockIdx.x;
   TreeTable<T>& Q = *reinterpret_cast<TreeTable<T>*>(smem_raw);

@@ -1,13 +1,14 @@
-"""Smoke-sized launches of every kernel family, for compute-sanitizer.
+"""Small launches of every kernel family, with their outputs saved.
 
-    compute-sanitizer --tool racecheck python tools/sanitize_smoke.py [fp32|fp64|both]
+    [KOP_LIB=variants/poison.so] python tools/kernel_smoke.py [fp32|fp64|both] [families] [--out FILE.npz]
 
-Each family runs a handful of problems so that a sanitizer pass (which
-serialises and instruments every access) finishes in minutes: IK-Beam
-(stage 1 / 2 / errors), lanes, FK, Philox, collision IK-Beam, generic LM
-(k_col_solve), tree solve + multi-EE beam, trajectories (+ report), mobile
-base, host pipeline.  Prints one line per family; exits non-zero on any
-Python-side failure (the sanitizer's own report is on stderr).
+Each family runs a handful of problems: IK-Beam (stage 1 / 2 / errors, ragged
+request shapes), lanes, FK, Philox, host pipeline, mobile base, collision
+IK-Beam, generic LM (k_col_solve), tree solve + multi-EE beam, trajectories
+(+ report).  tests/test_gpu_checks.py runs it against the normal library and
+the checking builds (kop_check.cuh: shared-memory poison, barrier jitter) and
+compares the saved outputs bit for bit -- the substitute for compute-sanitizer,
+which is closed on this GPU pool.
 """
 import os
 import sys
@@ -22,8 +23,34 @@ from paper_2505_03728_b200.benchmark import reachable_target_array
 from paper_2505_03728_b200.robot import fk_arrays_device, link_poses_device
 from paper_2505_03728_b200.tasks import IkBeamSolver
 
-PRECS = {"fp32": ["fp32"], "fp64": ["fp64"], "both": ["fp32", "fp64"]}[sys.argv[1] if len(sys.argv) > 1 else "both"]
-ONLY = set(sys.argv[2].split(",")) if len(sys.argv) > 2 else None
+ARGS = [a for a in sys.argv[1:] if not a.startswith("--")]
+OUT = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
+if OUT in ARGS:
+    ARGS.remove(OUT)
+PRECS = {"fp32": ["fp32"], "fp64": ["fp64"], "both": ["fp32", "fp64"]}[ARGS[0] if ARGS else "both"]
+ONLY = set(ARGS[1].split(",")) if len(ARGS) > 1 else None
+SAVED = {}
+
+
+def keep(name, prec, obj):
+    """Record every array field of obj (tensor / numpy / dict / BeamBatch-like) under name/prec."""
+    def arr(x):
+        return x.detach().cpu().numpy() if hasattr(x, "detach") else np.asarray(x)
+    if isinstance(obj, dict):
+        items = obj.items()
+    elif isinstance(obj, (list, tuple)):
+        items = enumerate(obj)
+    elif hasattr(obj, "__dataclass_fields__"):
+        items = ((f, getattr(obj, f)) for f in obj.__dataclass_fields__)
+    else:
+        items = [("value", obj)]
+    for key, v in items:
+        if v is None:
+            continue
+        if hasattr(v, "__dataclass_fields__") or isinstance(v, (dict, list, tuple)):
+            keep(f"{name}.{key}", prec, v)
+        else:
+            SAVED[f"{name}.{key}/{prec}"] = arr(v)
 
 DEMO = k.WorldModel([k.Sphere([0.45, 0.1, 0.55], 0.12), k.Capsule([-0.5, -0.4, 0.2], [-0.5, 0.4, 0.6], 0.1),
                      k.HalfSpace([0.0, 0.0, 1.0], -0.3)])
@@ -46,36 +73,44 @@ def done(name, prec):
     print(f"ok {name} {prec}", flush=True)
 
 
+from paper_2505_03728_b200._lib import lib  # noqa: E402
+
+print("build:", lib().kop_build_info().decode(), flush=True)
+probe = torch.zeros(4096, dtype=torch.int32, device="cuda")
+assert lib().kop_check_probe(probe.data_ptr(), 4096, torch.cuda.current_stream().cuda_stream) == 0
+torch.cuda.synchronize()
+print("smem probe all-poison:", bool((probe == -1).all()), flush=True)
 tg = reachable_target_array(m, "flange", 8, 77)
 for prec in PRECS:
     if fam("fk"):
         q = dv.to_dev(np.random.default_rng(0).uniform(m.lower_limits, m.upper_limits, (33, 7)))
-        fk_arrays_device(m, q, precision=prec)
+        keep("fk", prec, fk_arrays_device(m, q, precision=prec))
         done("fk", prec)
     if fam("beam"):
         s = IkBeamSolver(m, "flange", rng_seed=77, precision=prec)
-        s.solve_device(tg)
+        keep("beam", prec, s.solve_device(tg))
         done("beam", prec)
         # seeds not a multiple of a warp, keep 7
         s = IkBeamSolver(m, "flange", seeds=37, keep=7, rng_seed=3, precision=prec)
-        s.solve_device(tg[:5])
+        keep("beam-ragged", prec, s.solve_device(tg[:5]))
         done("beam-ragged", prec)
     if fam("host"):
         s = IkBeamSolver(m, "flange", rng_seed=77, precision=prec)
-        s.solve_host(tg.cpu().numpy(), chunk=3, n_streams=2)
+        keep("host", prec, s.solve_host(tg.cpu().numpy(), chunk=3, n_streams=2))
         done("host-pipeline", prec)
     if fam("mobile"):
         s = IkBeamSolver(m, "flange", rng_seed=77, precision=prec, optimize_base=True)
-        s.solve_device(tg[:4])
+        keep("mobile", prec, s.solve_device(tg[:4]))
         done("mobile", prec)
     if fam("lanes"):
         lp = kbeam.IkLaneProblem(m, "flange", pose(tg[0]), 50, 10, 100, 0.01, precision=prec)
         st = lp.start_state(k.sample_seed_configurations(m, 8, 1))
         lp.run(st, 3)
+        keep("lanes", prec, {"q": st.q, "cost": st.cost, "lam": st.damping, "hist": np.stack(st.history, 1)})
         done("lanes", prec)
     if fam("collision"):
         s = IkBeamSolver(m, "flange", rng_seed=77, precision=prec, world=DEMO, self_collision=True)
-        s.solve_device(tg[:3])
+        keep("collision-beam", prec, s.solve_device(tg[:3]))
         done("collision-beam", prec)
     if fam("lm"):
         probs = []
@@ -85,12 +120,15 @@ for prec in PRECS:
                 k.pose_cost(m, "q", "flange", T, position_weight=50, orientation_weight=10),
                 k.limit_cost(m, "q", weight=100), k.rest_cost("q", m.rest_pose, weight=0.01),
                 k.world_collision_cost(m, "q", DEMO, weight=20), k.self_collision_cost(m, "q", weight=5)]))
-        k.solve_batch(probs, k.SolveOptions(precision=prec, max_iterations=12))
+        reps = k.solve_batch(probs, k.SolveOptions(precision=prec, max_iterations=12))
+        keep("generic-lm", prec, {"q": np.stack([r.final_values.value("q") for r in reps]),
+                                  "hist": np.array([r.cost_history + [np.nan] * (13 - len(r.cost_history))
+                                                    for r in reps])})
         done("generic-lm", prec)
     if fam("tree"):
         qt = dv.to_dev(np.random.default_rng(29).uniform(hum.lower_limits, hum.upper_limits, (3, hum.actuated_count)))
         tgh = torch.stack([link_poses_device(hum, qt, e) for e in EES], dim=1).contiguous()
-        k.solve_ik_beam_multi(hum, EES, tgh, seeds=8, keep=2, precision=prec)
+        keep("tree-beam", prec, k.solve_ik_beam_multi(hum, EES, tgh, seeds=8, keep=2, precision=prec))
         done("tree-beam", prec)
         probs = []
         th = tgh.cpu().numpy()
@@ -99,7 +137,10 @@ for prec in PRECS:
                                    [k.pose_cost(hum, "q", e, pose(th[i, j]), position_weight=50,
                                                 orientation_weight=10) for j, e in enumerate(EES)]
                                    + [k.limit_cost(hum, "q", weight=100), k.rest_cost("q", hum.rest_pose, weight=0.01)]))
-        k.solve_batch(probs, k.SolveOptions(precision=prec, max_iterations=8))
+        reps = k.solve_batch(probs, k.SolveOptions(precision=prec, max_iterations=8))
+        keep("tree-solve", prec, {"q": np.stack([r.final_values.value("q") for r in reps]),
+                                  "hist": np.array([r.cost_history + [np.nan] * (9 - len(r.cost_history))
+                                                    for r in reps])})
         done("tree-solve", prec)
     if fam("traj"):
         rng = np.random.default_rng(5)
@@ -112,6 +153,10 @@ for prec in PRECS:
             obs[:, 0, 7] = 0.07
             pl = k.TrajectoryPlanner(m, "flange", timesteps=TT, precision=prec, max_iterations=4)
             res = pl.solve_anchored_device(dv.to_dev(np.stack([qa, qb], axis=1)), dv.to_dev(obs), 1)
-            ktraj.trajectory_signed_distances_batch(m, res["qs"], dv.to_dev(obs), 1, "flange")
+            keep(f"traj{TT}", prec, res)
+            keep(f"traj{TT}-report", prec,
+                 ktraj.trajectory_signed_distances_batch(m, res["qs"], dv.to_dev(obs), 1, "flange"))
             done(f"traj-T{TT}", prec)
-print("sanitize smoke complete", flush=True)
+if OUT:
+    np.savez_compressed(OUT, **SAVED)
+print(f"kernel smoke complete: {len(SAVED)} arrays", flush=True)
