@@ -361,6 +361,44 @@ int kop_fma_peak_kernel(int32_t blocks, int32_t threads, int32_t iters, float* s
 int kop_dfma_peak_kernel(int32_t blocks, int32_t threads, int32_t iters, double* sink, double* flops,
                          void* stream);
 
+/* --- per-term evaluation (FP64) ---------------------------------------------
+ * replaces: the evaluator / jacobian closures of the typed cost builders
+ * (costs.py:98-619) behind CostTerm.raw_residual (solver.py:142-152),
+ * CostTerm.jacobian and solver.assemble (solver.py:289-324): the RAW
+ * (unweighted) rows of one term at `count` evaluation points and the Jacobian
+ * block of each referenced variable, in the reference's row order.
+ * All arrays are device arrays; jacobian outputs may be null. */
+#define KOP_BASE_NONE 0
+#define KOP_BASE_SE2 1 /* base tangent (vx, vy, w)              */
+#define KOP_BASE_SE3 2 /* base tangent (vx, vy, vz, wx, wy, wz) */
+/* pose_cost (costs.py:98-166): r [count*6] = log(T_t^-1 (B) FK_link(q));
+ * jq [count*6*n], jb [count*6*db] (db = 3 | 6); base [count*7] (wxyz, xyz),
+ * SE(2) bases as their Transform3 (liegroups.py:450-454); target: host [7]. */
+int kop_term_pose(const KopModel* model, int32_t link, const double* target, int32_t base_kind, const double* q,
+                  const double* base, int64_t count, double* r, double* jq, double* jb, void* stream);
+#define KOP_TERM_LIMIT 0      /* q               (costs.py:174-195) */
+#define KOP_TERM_REST 1       /* q               (costs.py:259-271) */
+#define KOP_TERM_SMOOTHNESS 2 /* q_prev, q_curr  (costs.py:274-290) */
+#define KOP_TERM_VELOCITY 3   /* q_prev, q_curr  (costs.py:198-231) */
+#define KOP_TERM_STENCIL 4    /* q_0..q_4, coeffs = stencil / dt^k (costs.py:293-341) */
+/* joint-space rows: qs [count*nvars*n] (variable-major per point), r
+ * [count*n], jdiag [count*nvars*n] = the diagonal of each variable's block
+ * (every joint-space block is diagonal); rest, velocity_limits (+inf where
+ * unlimited): host [n]; coeffs: host [5]. */
+int kop_term_joint(const KopModel* model, int32_t kind, const double* rest, const double* velocity_limits, double dt,
+                   const double* coeffs, const double* qs, int64_t count, double* r, double* jdiag, void* stream);
+#define KOP_TERM_WORLD 5 /* q: one row per (sphere link, obstacle), link-major (costs.py:499-551) */
+#define KOP_TERM_SELF 6  /* q: one row per model self pair (costs.py:435-496)                     */
+#define KOP_TERM_SWEPT 7 /* q_prev, q_curr: capsules swept by every sphere (costs.py:554-619)     */
+/* activation rows of a collision family: r [count*rows], j0 / j1 [count*rows*n]
+ * (j1 for SWEPT only); obstacles: host, <= 16; returns the row count via
+ * kop_term_rows. */
+int kop_term_collision(const KopModel* model, int32_t kind, const KopObstacle* obstacles, int32_t num_obstacles,
+                       double eta, double sharpness, int32_t hard_min, const double* q0, const double* q1,
+                       int64_t count, double* r, double* j0, double* j1, void* stream);
+/* rows of a collision family for this model (negative status on error) */
+int kop_term_rows(const KopModel* model, int32_t kind, int32_t num_obstacles);
+
 /* --- checking builds ----------------------------------------------------
  * Copies `words` 32-bit words of a probe kernel's never-written dynamic
  * shared memory to device `out` (<= 12288 words).  In the shared-memory

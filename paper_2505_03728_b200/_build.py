@@ -23,8 +23,9 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 
-SOURCES = ["kop_kernels.cu", "kop_collision.cu", "kop_tree.cu", "kop_traj.cu", "kop_aux.cu", "kop_capi.cu"]
-HEADERS = ["kop_check.cuh", "kop_chain.h", "kop_lie.cuh", "kop_lane.cuh", "kop_beam.cuh", "kop_collision.cuh", "kop_kernels.cuh", "kop_tree.cuh", "kop_traj.cuh"]
+SOURCES = ["kop_kernels.cu", "kop_collision.cu", "kop_tree.cu", "kop_traj.cu", "kop_aux.cu", "kop_terms.cu",
+           "kop_capi.cu"]
+HEADERS = ["kop_check.cuh", "kop_chain.h", "kop_lie.cuh", "kop_lane.cuh", "kop_beam.cuh", "kop_collision.cuh", "kop_kernels.cuh", "kop_tree.cuh", "kop_traj.cuh", "kop_terms.cuh"]
 
 
 def _stale(target: str, deps: list[str]) -> bool:

@@ -16,6 +16,9 @@ LIB_PATH = os.environ.get("KOP_LIB") or os.path.join(_HERE, "libkinoptik_b200.so
 
 KOP_OK, KOP_EINVAL, KOP_EUNSUPPORTED, KOP_ECUDA = 0, -1, -2, -3
 KOP_FP32, KOP_FP64 = 0, 1
+KOP_BASE_NONE, KOP_BASE_SE2, KOP_BASE_SE3 = 0, 1, 2
+KOP_TERM_LIMIT, KOP_TERM_REST, KOP_TERM_SMOOTHNESS, KOP_TERM_VELOCITY, KOP_TERM_STENCIL = 0, 1, 2, 3, 4
+KOP_TERM_WORLD, KOP_TERM_SELF, KOP_TERM_SWEPT = 5, 6, 7
 
 _p = C.c_void_p
 _i32, _i64, _u64, _f64 = C.c_int32, C.c_int64, C.c_uint64, C.c_double
@@ -113,6 +116,11 @@ SIGNATURES = {
     "kop_fma_peak_kernel": (C.c_int, [_i32, _i32, _i32, _p, C.POINTER(_f64), _p]),
     "kop_dfma_peak_kernel": (C.c_int, [_i32, _i32, _i32, _p, C.POINTER(_f64), _p]),
     "kop_check_probe": (C.c_int, [_p, _i32, _p]),
+    "kop_term_pose": (C.c_int, [_p, _i32, _p, _i32, _p, _p, _i64, _p, _p, _p, _p]),
+    "kop_term_joint": (C.c_int, [_p, _i32, _p, _p, _f64, _p, _p, _i64, _p, _p, _p]),
+    "kop_term_collision": (C.c_int, [_p, _i32, C.POINTER(KopObstacle), _i32, _f64, _f64, _i32, _p, _p, _i64, _p, _p,
+                                     _p, _p]),
+    "kop_term_rows": (C.c_int, [_p, _i32, _i32]),
 }
 
 _lib = None

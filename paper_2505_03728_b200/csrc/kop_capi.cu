@@ -12,6 +12,7 @@
 #include "kop_collision.cuh"
 #include "kop_kernels.cuh"
 #include "kop_traj.cuh"
+#include "kop_terms.cuh"
 #include "kop_tree.cuh"
 
 using namespace kop;
@@ -1483,6 +1484,143 @@ int kop_dfma_peak_kernel(int32_t blocks, int32_t threads, int32_t iters, double*
   if (blocks <= 0 || threads <= 0 || iters <= 0 || !sink) return fail(KOP_EINVAL, "invalid arguments");
   if (flops) *flops = 2.0 * 8.0 * (double)blocks * threads * (double)iters;
   return cuda_status(launch_dfma_peak(blocks, threads, iters, sink, (cudaStream_t)stream));
+}
+
+namespace {
+LinkMap link_map(const KopModel& m) {
+  LinkMap L;
+  for (int l = 0; l < kMaxLinks; ++l) L.pj[l] = l < (int)m.parent_joint.size() ? m.parent_joint[l] : -1;
+  return L;
+}
+
+// sphere-bearing links in model order (spheres arrive grouped by link)
+std::vector<int> sphere_links(const KopModel& m) {
+  std::vector<int> links;
+  for (int l : m.sphere_link)
+    if (links.empty() || links.back() != l) links.push_back(l);
+  return links;
+}
+}  // namespace
+
+int kop_term_pose(const KopModel* m, int32_t link, const double* target, int32_t base_kind, const double* q,
+                  const double* base, int64_t count, double* r, double* jq, double* jb, void* stream) {
+  if (!m || !target || count < 0) return fail(KOP_EINVAL, "invalid arguments");
+  if (link < 0 || link >= m->tree.nl) return fail(KOP_EINVAL, "unknown link index");
+  if (base_kind < KOP_BASE_NONE || base_kind > KOP_BASE_SE3) return fail(KOP_EINVAL, "bad base kind");
+  if (count == 0) return KOP_OK;
+  if (!q || !r || (base_kind != KOP_BASE_NONE && !base)) return fail(KOP_EINVAL, "null array argument");
+  TermPose T{};
+  double tv[7];
+  HQ tq{target[0], -target[1], -target[2], -target[3]};  // Transform3.inverse, canonical (liegroups.py:388-390)
+  const double nq = sqrt(tq.w * tq.w + tq.x * tq.x + tq.y * tq.y + tq.z * tq.z);
+  tq = {tq.w / nq, tq.x / nq, tq.y / nq, tq.z / nq};
+  if (tq.w < 0.0) tq = {-tq.w, -tq.x, -tq.y, -tq.z};
+  double t[3];
+  hrot(tq, target + 4, t);
+  tv[0] = tq.w; tv[1] = tq.x; tv[2] = tq.y; tv[3] = tq.z;
+  tv[4] = -t[0]; tv[5] = -t[1]; tv[6] = -t[2];
+  memcpy(T.tinv, tv, sizeof(tv));
+  T.base_kind = base_kind;
+  return cuda_status(launch_term_pose(m->tree, link_map(*m), link, T, q, base, count, r, jq, jb,
+                                      (cudaStream_t)stream));
+}
+
+int kop_term_joint(const KopModel* m, int32_t kind, const double* rest, const double* velocity_limits, double dt,
+                   const double* coeffs, const double* qs, int64_t count, double* r, double* jdiag, void* stream) {
+  if (!m || count < 0) return fail(KOP_EINVAL, "invalid arguments");
+  TermJoint T{};
+  T.kind = kind;
+  const int n = m->tree.n;
+  switch (kind) {
+    case KOP_TERM_LIMIT: T.nvars = 1; break;
+    case KOP_TERM_REST:
+      if (!rest) return fail(KOP_EINVAL, "rest cost needs q_rest");
+      T.nvars = 1;
+      break;
+    case KOP_TERM_SMOOTHNESS: T.nvars = 2; break;
+    case KOP_TERM_VELOCITY:
+      if (!(dt > 0.0)) return fail(KOP_EINVAL, "dt must be positive");
+      if (!velocity_limits) return fail(KOP_EINVAL, "velocity cost needs the velocity limits");
+      T.nvars = 2;
+      break;
+    case KOP_TERM_STENCIL:
+      if (!coeffs) return fail(KOP_EINVAL, "stencil needs coefficients");
+      T.nvars = 5;
+      break;
+    default: return fail(KOP_EINVAL, "unknown joint-space term kind");
+  }
+  for (int i = 0; i < n; ++i) {
+    T.lower[i] = m->lower[i];
+    T.upper[i] = m->upper[i];
+    T.rest[i] = rest ? rest[i] : 0.0;
+    T.vlim[i] = velocity_limits ? velocity_limits[i] : INFINITY;
+  }
+  T.dt = dt;
+  for (int k = 0; k < 5; ++k) T.coeffs[k] = coeffs ? coeffs[k] : 0.0;
+  if (count == 0) return KOP_OK;
+  if (!qs || !r) return fail(KOP_EINVAL, "null array argument");
+  return cuda_status(launch_term_joint(T, n, qs, count, r, jdiag, (cudaStream_t)stream));
+}
+
+int kop_term_rows(const KopModel* m, int32_t kind, int32_t num_obstacles) {
+  if (!m) return fail(KOP_EINVAL, "null model");
+  if (kind == KOP_TERM_SELF) return (int)(m->pair_links.size() / 2);
+  if (kind == KOP_TERM_WORLD || kind == KOP_TERM_SWEPT) return (int)sphere_links(*m).size() * num_obstacles;
+  return fail(KOP_EINVAL, "not a collision term kind");
+}
+
+int kop_term_collision(const KopModel* m, int32_t kind, const KopObstacle* obstacles, int32_t num_obstacles,
+                       double eta, double sharpness, int32_t hard_min, const double* q0, const double* q1,
+                       int64_t count, double* r, double* j0, double* j1, void* stream) {
+  if (!m || count < 0) return fail(KOP_EINVAL, "invalid arguments");
+  if (kind != KOP_TERM_WORLD && kind != KOP_TERM_SELF && kind != KOP_TERM_SWEPT)
+    return fail(KOP_EINVAL, "not a collision term kind");
+  if (!(eta > 0.0)) return fail(KOP_EINVAL, "buffer distance must be positive");
+  if (kind != KOP_TERM_SELF && (num_obstacles < 1 || !obstacles))
+    return fail(KOP_EINVAL, "no (link, obstacle) pairs: empty world");
+  if (num_obstacles > kMaxObstacles) return fail(KOP_EUNSUPPORTED, "more than 16 obstacles (not compiled in)");
+  const std::vector<int> links = sphere_links(*m);
+  if ((int)m->sphere_link.size() > kMaxSpheres || (int)links.size() > kMaxSphereLinks ||
+      (int)m->pair_links.size() / 2 > kMaxSelfPairs)
+    return fail(KOP_EUNSUPPORTED, "more than 32 spheres / 16 sphere links / 64 self pairs (not compiled in)");
+  TermGeom G{};
+  G.ns = (int)m->sphere_link.size();
+  for (int s = 0; s < G.ns; ++s) {
+    G.s_link[s] = m->sphere_link[s];
+    for (int i = 0; i < 3; ++i) G.s_c[s][i] = m->sphere_center[3 * s + i];
+    G.s_r[s] = m->sphere_radius[s];
+  }
+  G.nl = (int)links.size();
+  for (int i = 0; i < G.nl; ++i) G.links[i] = links[i];
+  G.np = (int)m->pair_links.size() / 2;
+  for (int p = 0; p < G.np; ++p) {
+    G.pa[p] = m->pair_links[2 * p];
+    G.pb[p] = m->pair_links[2 * p + 1];
+  }
+  if (kind == KOP_TERM_SELF && G.np == 0) return fail(KOP_EINVAL, "model declares no self-collision pairs");
+  G.O.no = kind == KOP_TERM_SELF ? 0 : num_obstacles;
+  for (int o = 0; o < G.O.no; ++o) {
+    const KopObstacle& ob = obstacles[o];
+    if (ob.kind < 0 || ob.kind > 2) return fail(KOP_EINVAL, "unknown obstacle kind");
+    G.O.okind[o] = ob.kind;
+    double nrm = 1.0;
+    if (ob.kind == KOP_OBSTACLE_HALFSPACE) {
+      nrm = sqrt(ob.a[0] * ob.a[0] + ob.a[1] * ob.a[1] + ob.a[2] * ob.a[2]);
+      if (nrm < 1e-12) return fail(KOP_EINVAL, "half-space normal must be nonzero");
+    }
+    for (int i = 0; i < 3; ++i) {
+      G.O.oa[o][i] = ob.a[i] / nrm;
+      G.O.ob[o][i] = ob.b[i];
+    }
+    G.O.orad[o] = ob.radius;
+  }
+  G.eta = eta;
+  G.beta = sharpness > 0.0 ? sharpness : 100.0;
+  G.hard = hard_min;
+  if (count == 0) return KOP_OK;
+  if (!q0 || !r || (kind == KOP_TERM_SWEPT && !q1)) return fail(KOP_EINVAL, "null array argument");
+  return cuda_status(launch_term_collision(m->tree, link_map(*m), G, kind, q0, q1, count, r, j0,
+                                           kind == KOP_TERM_SWEPT ? j1 : nullptr, (cudaStream_t)stream));
 }
 
 int kop_check_probe(uint32_t* out, int32_t words, void* stream) {

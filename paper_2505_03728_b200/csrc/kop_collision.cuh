@@ -158,6 +158,76 @@ __device__ __forceinline__ T sphere_obstacle_t(const OB& P, int o, const vec3<T>
   return nn - r - P.orad[o];
 }
 
+// capsule (endpoints c0, c1, radius r) vs obstacle o: distance and the
+// gradients at both endpoints (collision.py:207-237 with :115-152)
+template <typename T, class OB>
+__device__ __forceinline__ T capsule_obstacle_t(const OB& O, int o, const vec3<T>& c0, const vec3<T>& c1, T r,
+                                                vec3<T>& ga, vec3<T>& gb) {
+  const int kind = O.okind[o];
+  const vec3<T> a{O.oa[o][0], O.oa[o][1], O.oa[o][2]};
+  if (kind == kObHalfSpace) {
+    const T da = dot(a, c0), db = dot(a, c1);
+    const vec3<T> z{T(0), T(0), T(0)};
+    if (da <= db) {
+      ga = a;
+      gb = z;
+    } else {
+      ga = z;
+      gb = a;
+    }
+    return tmin(da, db) - O.orad[o] - r;
+  }
+  const vec3<T> d1{c1.x - c0.x, c1.y - c0.y, c1.z - c0.z};
+  T s = T(0);
+  vec3<T> qpt = a;
+  if (kind == kObSphere) {
+    const T dd = dot(d1, d1);
+    if (!(dd < T(1e-16))) s = tmin(tmax(dot(vec3<T>{a.x - c0.x, a.y - c0.y, a.z - c0.z}, d1) / dd, T(0)), T(1));
+  } else {  // capsule-capsule: Ericson's clamped quadratic (collision.py:124-152)
+    const vec3<T> b{O.ob[o][0], O.ob[o][1], O.ob[o][2]};
+    const vec3<T> d2{b.x - a.x, b.y - a.y, b.z - a.z};
+    const vec3<T> rr{c0.x - a.x, c0.y - a.y, c0.z - a.z};
+    const T aa = dot(d1, d1), e = dot(d2, d2), f = dot(d2, rr);
+    T t = T(0);
+    if (aa < T(1e-16) && e < T(1e-16)) {
+      s = t = T(0);
+    } else if (aa < T(1e-16)) {
+      s = T(0);
+      t = tmin(tmax(f / e, T(0)), T(1));
+    } else {
+      const T c = dot(d1, rr);
+      if (e < T(1e-16)) {
+        s = tmin(tmax(-c / aa, T(0)), T(1));
+        t = T(0);
+      } else {
+        const T bb = dot(d1, d2);
+        const T den = aa * e - bb * bb;
+        s = den > T(1e-16) ? tmin(tmax((bb * f - c * e) / den, T(0)), T(1)) : T(0);
+        t = (bb * s + f) / e;
+        if (t < T(0)) {
+          t = T(0);
+          s = tmin(tmax(-c / aa, T(0)), T(1));
+        } else if (t > T(1)) {
+          t = T(1);
+          s = tmin(tmax((bb - c) / aa, T(0)), T(1));
+        }
+      }
+    }
+    qpt = {a.x + t * d2.x, a.y + t * d2.y, a.z + t * d2.z};
+  }
+  const vec3<T> p{c0.x + s * d1.x, c0.y + s * d1.y, c0.z + s * d1.z};
+  const vec3<T> v{p.x - qpt.x, p.y - qpt.y, p.z - qpt.z};
+  const T nn = sqrt_t(dot(v, v));
+  vec3<T> dir{T(0), T(0), T(0)};
+  if (!(nn < T(1e-12))) {
+    const T inv = T(1) / nn;
+    dir = {v.x * inv, v.y * inv, v.z * inv};
+  }
+  ga = {(T(1) - s) * dir.x, (T(1) - s) * dir.y, (T(1) - s) * dir.z};
+  gb = {s * dir.x, s * dir.y, s * dir.z};
+  return (nn < T(1e-12) ? T(0) : nn) - r - O.orad[o];
+}
+
 // distance only (no gradient): the screening pass of a collision row
 template <typename T, class OB>
 __device__ __forceinline__ T sphere_obstacle_dist_t(const OB& P, int o, const vec3<T>& c, T r) {

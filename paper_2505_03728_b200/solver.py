@@ -143,6 +143,19 @@ class CostTerm:
             raise ValueError(f"cost '{self.name}': weights must be nonnegative")
         self.weight = w
 
+    def raw_residual(self, values) -> np.ndarray:
+        """The unweighted residual at the referenced variables' values (solver.py:142-152);
+        typed terms evaluate on the device (terms.py)."""
+        if self.evaluator is None:
+            raise UnsupportedFeatureError(f"cost '{self.name}' has no evaluator")
+        r = np.asarray(self.evaluator(*values), dtype=float).reshape(-1)
+        if r.shape != (self.residual_dim,):
+            raise CostEvaluationError(self.name, f"evaluator returned shape {r.shape}, declared residual_dim "
+                                                 f"{self.residual_dim}")
+        if not np.all(np.isfinite(r)):
+            raise CostEvaluationError(self.name, "evaluator returned non-finite residual")
+        return r
+
 
 @dataclass
 class Problem:
@@ -158,6 +171,7 @@ class Problem:
     def residual_dim(self) -> int:
         return sum(c.residual_dim for c in self.costs)
 
+    @property
     def sparsity(self) -> list:
         """Structurally nonzero (cost index, variable index) blocks (solver.py:166-172)."""
         return [(ci, self.variables.index(ref)) for ci, cost in enumerate(self.costs) for ref in cost.variable_refs]
@@ -206,6 +220,95 @@ class SolveReport:
         if include_timing:
             out["solve_time_s"] = self.solve_time_s
         return out
+
+
+# ---------------------------------------------------------------------------
+# assembly of the weighted stack (solver.py:216-324): per-term evaluations
+# (device kernels for typed terms, terms.py) stacked into r and a block Jacobian
+# ---------------------------------------------------------------------------
+
+class BlockJacobian:
+    """Weighted Jacobian as per-(cost, variable) dense blocks (solver.py:216-257)."""
+
+    def __init__(self, problem: "Problem", row_offsets: list, blocks: dict):
+        self.problem = problem
+        self.row_offsets = row_offsets
+        self.blocks = blocks  # (cost index, variable index) -> (m, td)
+        self.shape = (row_offsets[-1], problem.variables.tangent_dim)
+
+    def to_dense(self) -> np.ndarray:
+        out = np.zeros(self.shape)
+        offsets = self.problem.variables.tangent_offsets
+        for (ci, vi), block in self.blocks.items():
+            r0 = self.row_offsets[ci]
+            out[r0:r0 + block.shape[0], offsets[vi]:offsets[vi] + block.shape[1]] = block
+        return out
+
+    def to_csr(self):
+        import scipy.sparse
+
+        offsets = self.problem.variables.tangent_offsets
+        rows, cols, vals = [], [], []
+        for (ci, vi), block in self.blocks.items():
+            m, td = block.shape
+            rr, cc = np.meshgrid(np.arange(m), np.arange(td), indexing="ij")
+            rows.append((rr + self.row_offsets[ci]).ravel())
+            cols.append((cc + offsets[vi]).ravel())
+            vals.append(block.ravel())
+        if not rows:
+            return scipy.sparse.csr_matrix(self.shape)
+        return scipy.sparse.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                                       shape=self.shape)
+
+
+def numeric_jacobian(cost: CostTerm, values, step: float = 1e-6) -> list:
+    """Central differences of the raw residual in tangent space (solver.py:260-279)."""
+    from .liegroups import local_update
+
+    blocks = []
+    for k, value in enumerate(values):
+        td = _tangent_dim(value)
+        block = np.empty((cost.residual_dim, td))
+        for j in range(td):
+            d = np.zeros(td)
+            d[j] = step
+            plus, minus = list(values), list(values)
+            plus[k] = local_update(value, d)
+            minus[k] = local_update(value, -d)
+            block[:, j] = (cost.raw_residual(plus) - cost.raw_residual(minus)) / (2 * step)
+        if not np.all(np.isfinite(block)):
+            raise CostEvaluationError(cost.name, "non-finite numeric Jacobian")
+        blocks.append(block)
+    return blocks
+
+
+def _residual_vector(problem: "Problem", at: VariableSet) -> np.ndarray:
+    parts = [c.weight * c.raw_residual(at.values(c.variable_refs)) for c in problem.costs]
+    return np.concatenate(parts) if parts else np.zeros(0)
+
+
+def assemble(problem: "Problem", at: VariableSet):
+    """Stacked weighted residual and block Jacobian at ``at`` (solver.py:289-324)."""
+    residuals, row_offsets, blocks = [], [0], {}
+    for ci, cost in enumerate(problem.costs):
+        values = at.values(cost.variable_refs)
+        r = cost.raw_residual(values)
+        residuals.append(cost.weight * r)
+        row_offsets.append(row_offsets[-1] + cost.residual_dim)
+        raw = cost.jacobian(*values) if cost.jacobian is not None else numeric_jacobian(cost, values)
+        if len(raw) != len(cost.variable_refs):
+            raise CostEvaluationError(cost.name, f"jacobian returned {len(raw)} blocks for "
+                                                 f"{len(cost.variable_refs)} variables")
+        for ref, block in zip(cost.variable_refs, raw):
+            vi = problem.variables.index(ref)
+            block = np.asarray(block, dtype=float)
+            expected = (cost.residual_dim, at.tangent_offsets[vi + 1] - at.tangent_offsets[vi])
+            if block.shape != expected:
+                raise CostEvaluationError(cost.name, f"jacobian block shape {block.shape}, expected {expected}")
+            weighted = cost.weight[:, None] * block
+            blocks[(ci, vi)] = blocks[(ci, vi)] + weighted if (ci, vi) in blocks else weighted
+    r = np.concatenate(residuals) if residuals else np.zeros(0)
+    return r, BlockJacobian(problem, row_offsets, blocks)
 
 
 # ---------------------------------------------------------------------------

@@ -72,4 +72,4 @@ def test_variable_bookkeeping(arm7):
     with pytest.raises(ValueError):
         vs.updated(np.zeros(5))
     pr = k.trajectory_problem(arm7, arm7.rest_pose, arm7.rest_pose, 6, 0.1)
-    assert pr.sparsity()[:3] == [(0, 0), (1, 5), (2, 0)]
+    assert pr.sparsity[:3] == [(0, 0), (1, 5), (2, 0)]
