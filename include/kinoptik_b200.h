@@ -271,6 +271,15 @@ int kop_multi_pose_solve(const KopModel* model, const KopPoseCosts* costs, const
                          const double* targets, const double* q0, int64_t batch, double* q_out,
                          double* cost_out, double* init_cost_out, double* history_out,
                          int32_t* iterations_out, int32_t* termination_out, void* stream);
+/* the same tree LM with a BASE VARIABLE shared by the pose costs (costs.py:98-166
+ * base_var; solver.py:36-108 typed variables): the tangent is [q | base],
+ * base_kind KOP_BASE_SE2 (state (angle, x, y), tangent (vx, vy, w)) or
+ * KOP_BASE_SE3 (state (wxyz, xyz), tangent (v, w)), retracted by local_update
+ * (liegroups.py:505-519).  base0 / base_out: device [batch * 3 | 7]. */
+int kop_multi_pose_solve_base(const KopModel* model, const KopPoseCosts* costs, const KopLmOptions* options,
+                              int32_t base_kind, const double* targets, const double* q0, const double* base0,
+                              int64_t batch, double* q_out, double* base_out, double* cost_out, double* init_cost_out,
+                              double* history_out, int32_t* iterations_out, int32_t* termination_out, void* stream);
 
 /* --- trajectory optimisation (config 5) -----------------------------------
  * replaces: the solve(...) call of plan_trajectory (tasks.py:347-403) over

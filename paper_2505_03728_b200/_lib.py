@@ -100,6 +100,8 @@ SIGNATURES = {
                                _p, _p, _p, _p, _p, _p, _p]),
     "kop_multi_pose_solve": (C.c_int, [_p, C.POINTER(KopPoseCosts), C.POINTER(KopLmOptions), _p, _p, _i64,
                                        _p, _p, _p, _p, _p, _p, _p]),
+    "kop_multi_pose_solve_base": (C.c_int, [_p, C.POINTER(KopPoseCosts), C.POINTER(KopLmOptions), _i32, _p, _p, _p,
+                                            _i64, _p, _p, _p, _p, _p, _p, _p, _p]),
     "kop_ik_beam_host": (C.c_int, [_p, _i32, C.POINTER(KopIkParams), _p, _i64, _p, _p, _p, _p, _p, _p, _p, _p,
                                    _i64, _i32, _p]),
     "kop_traj_solve": (C.c_int, [_p, _i32, C.POINTER(KopTrajCosts), C.POINTER(KopLmOptions), _p, _p, _p, _i32,

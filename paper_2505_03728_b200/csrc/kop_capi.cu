@@ -1182,7 +1182,20 @@ extern "C" {
 int kop_multi_pose_solve(const KopModel* m, const KopPoseCosts* pc, const KopLmOptions* o, const double* targets,
                          const double* q0, int64_t batch, double* q_out, double* cost_out, double* init_cost_out,
                          double* history_out, int32_t* iterations_out, int32_t* termination_out, void* stream) {
+  return kop_multi_pose_solve_base(m, pc, o, KOP_BASE_NONE, targets, q0, nullptr, batch, q_out, nullptr, cost_out,
+                                   init_cost_out, history_out, iterations_out, termination_out, stream);
+}
+
+int kop_multi_pose_solve_base(const KopModel* m, const KopPoseCosts* pc, const KopLmOptions* o, int32_t base_kind,
+                              const double* targets, const double* q0, const double* base0, int64_t batch,
+                              double* q_out, double* base_out, double* cost_out, double* init_cost_out,
+                              double* history_out, int32_t* iterations_out, int32_t* termination_out, void* stream) {
   if (!m || !pc || !o) return fail(KOP_EINVAL, "null argument");
+  if (base_kind < KOP_BASE_NONE || base_kind > KOP_BASE_SE3) return fail(KOP_EINVAL, "bad base kind");
+  if (m->tree.n + base_dim(base_kind) > kTreeMaxDofs)
+    return fail(KOP_EUNSUPPORTED, "actuated joints plus base tangent dimensions exceed 32");
+  if (base_kind != KOP_BASE_NONE && batch > 0 && (!base0 || !base_out))
+    return fail(KOP_EINVAL, "a base variable needs base0 and base_out");
   if (o->precision != KOP_FP32 && o->precision != KOP_FP64) return fail(KOP_EINVAL, "bad precision");
   if (m->tree.n > kTreeMaxDofs || m->tree.nj > kTreeMaxJoints || !tree_params_ok(*m))
     return fail(KOP_EUNSUPPORTED, "tree solve supports up to 32 actuated and 64 total joints");
@@ -1210,9 +1223,19 @@ int kop_multi_pose_solve(const KopModel* m, const KopPoseCosts* pc, const KopLmO
   L.hist_out = history_out;
   L.iters = iterations_out;
   L.term = termination_out;
+  L.base0 = base0;
+  L.base_out = base_out;
   cudaStream_t st = (cudaStream_t)stream;
-  const cudaError_t e = o->precision == KOP_FP32 ? launch_tree_solve<float>(tree_params<float>(*m, pc), L, st)
-                                                 : launch_tree_solve<double>(tree_params<double>(*m, pc), L, st);
+  cudaError_t e;
+  if (o->precision == KOP_FP32) {
+    TreeLmParams<float> P = tree_params<float>(*m, pc);
+    P.base_kind = base_kind;
+    e = launch_tree_solve<float>(P, L, st);
+  } else {
+    TreeLmParams<double> P = tree_params<double>(*m, pc);
+    P.base_kind = base_kind;
+    e = launch_tree_solve<double>(P, L, st);
+  }
   return cuda_status(e);
 }
 

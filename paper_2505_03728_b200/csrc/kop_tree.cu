@@ -32,6 +32,7 @@ namespace kop {
 template <typename T, int NE>
 struct TreeScratch {
   T q[32], qn[32];
+  T bs[8], bn[8];            // base variable: current / candidate (SE(2): angle, x, y; SE(3): wxyz, xyz)
   T cb[2][32];               // Cholesky pivot column, double-buffered (16-byte aligned rows)
   T am[kTreeMaxJoints][6];   // Pluecker axis of each moving tree joint
   T ee[NE][48];              // per EE: r[6], R^T[9], p[3], At[9], Bt[9], Ab[9]
@@ -111,18 +112,39 @@ __device__ __forceinline__ void ld4(const double* p, double (&v)[4]) {
 
 // Evaluate the stack at S.q (or S.qn when cand): returns the cost (all lanes);
 // JAC also forms A (S.A, stride 33) and g (register, lane i = g_i).
+// root frame of the tree: the base variable's pose (Transform2.to_transform3 for
+// SE(2), liegroups.py:450-454) or the identity
+template <typename T>
+__device__ __forceinline__ void base_frame(int kind, const T* base, quat<T>& bq, vec3<T>& bp) {
+  if (kind == 1) {
+    T s, c;
+    sincos_t(T(0.5) * base[0], &s, &c);
+    bq = {c, T(0), T(0), s};
+    bp = {base[1], base[2], T(0)};
+  } else if (kind == 2) {
+    bq = {base[0], base[1], base[2], base[3]};
+    bp = {base[4], base[5], base[6]};
+  } else {
+    bq = {T(1), T(0), T(0), T(0)};
+    bp = {T(0), T(0), T(0)};
+  }
+}
+
 template <typename T, int NE, bool JAC>
 __device__ __forceinline__ T tree_eval(const TreeLmParams<T>& P, const TreeTable<T>& Q,
-                                       const double* __restrict__ targets, TreeScratch<T, NE>& S, const T* q, int lane,
-                                       T& g_out) {
-  const int n = P.n, ne = P.ne;
+                                       const double* __restrict__ targets, TreeScratch<T, NE>& S, const T* q,
+                                       const T* base, int lane, T& g_out) {
+  const int n = P.n, ne = P.ne, nd = n + base_dim(P.base_kind);
+  quat<T> bq;
+  vec3<T> bp;
+  base_frame(P.base_kind, base, bq, bp);
   // ---- FK, level by level: world frame after every joint, Pluecker axes -------
   // after(j) = after(parent) * O_j * Mot_j (robot.py:404-448 composition)
   for (int d = 0; d < P.nlev; ++d) {
     for (int idx = P.lev_start[d] + lane; idx < P.lev_start[d + 1]; idx += 32) {
       const int j = Q.lev_joint[idx], pj = Q.parent[j];
-      quat<T> wq{T(1), T(0), T(0), T(0)};
-      vec3<T> wp{T(0), T(0), T(0)};
+      quat<T> wq = bq;
+      vec3<T> wp = bp;
       if (pj >= 0) {
         wq = {S.wf[pj][0], S.wf[pj][1], S.wf[pj][2], S.wf[pj][3]};
         wp = {S.wf[pj][4], S.wf[pj][5], S.wf[pj][6]};
@@ -155,8 +177,8 @@ __device__ __forceinline__ T tree_eval(const TreeLmParams<T>& P, const TreeTable
   // ---- EE frames, pose residuals, Jr^-1 blocks ----------------------------------
   T cost_part = T(0);
   if (lane < ne) {
-    quat<T> wq{T(1), T(0), T(0), T(0)};
-    vec3<T> wp{T(0), T(0), T(0)};
+    quat<T> wq = bq;
+    vec3<T> wp = bp;
     const int ej = P.ee_joint[lane];
     if (ej >= 0) {
       wq = {S.wf[ej][0], S.wf[ej][1], S.wf[ej][2], S.wf[ej][3]};
@@ -202,18 +224,37 @@ __device__ __forceinline__ T tree_eval(const TreeLmParams<T>& P, const TreeTable
   T col[6 * NE];
 #pragma unroll
   for (int m = 0; m < 6 * NE; ++m) col[m] = T(0);
-  if (lane < n) {
-    for (int cj = 0; cj < Q.col_nj[lane]; ++cj) {
-      const int j = Q.col_joint[lane][cj];
-      const vec3<T> a{S.am[j][0], S.am[j][1], S.am[j][2]};
-      const vec3<T> mm{S.am[j][3], S.am[j][4], S.am[j][5]};
-      const T mu = Q.mult[j];
+  // columns: lane c < n owns actuated column c (its moving joints via col_joint); lanes n .. nd-1
+  // the base tangent, which acts like virtual joints at the root frame B -- prismatic along B's
+  // axes (translation components), revolute about B's axes through B's origin (rotation
+  // components): the body column Ad(FK^-1) e_i of costs.py:140-146 (SE(2): x, y, and z-rotation)
+  const int nvirt = lane >= n && lane < nd ? 1 : 0;
+  const int ncj = lane < n ? Q.col_nj[lane] : nvirt;
+  for (int cj = 0; cj < ncj; ++cj) {
+    int j = -1, vk = 0;
+    vec3<T> a, mm;
+    T mu = T(1);
+    if (lane < n) {
+      j = Q.col_joint[lane][cj];
+      a = {S.am[j][0], S.am[j][1], S.am[j][2]};
+      mm = {S.am[j][3], S.am[j][4], S.am[j][5]};
+      mu = Q.mult[j];
+      vk = Q.kind[j];
+    } else {
+      const int c = lane - n;
+      const int comp = P.base_kind == 1 ? (c == 2 ? 5 : c) : c;  // se(3) component of the tangent column
+      const vec3<T> ei{comp % 3 == 0 ? T(1) : T(0), comp % 3 == 1 ? T(1) : T(0), comp % 3 == 2 ? T(1) : T(0)};
+      a = qrot(bq, ei);
+      mm = cross(a, bp);
+      vk = comp < 3 ? 2 : 1;
+    }
+    {
 #pragma unroll
       for (int e = 0; e < NE; ++e) {
-        if (e >= ne || !((P.anc_ee[e] >> j) & 1ull)) continue;
+        if (e >= ne || (j >= 0 && !((P.anc_ee[e] >> j) & 1ull))) continue;
         const T* E = S.ee[e];
         vec3<T> lw, aw;
-        if (Q.kind[j] == 1) {
+        if (vk == 1) {
           const vec3<T> pe{E[15], E[16], E[17]};
           const vec3<T> x = cross(a, pe);
           lw = {x.x - mm.x, x.y - mm.y, x.z - mm.z};
@@ -241,8 +282,8 @@ __device__ __forceinline__ T tree_eval(const TreeLmParams<T>& P, const TreeTable
   __syncwarp();
   // ---- normal equations: lane i forms row i ----------------------------------------
   T g = T(0);
-  if (lane < n) {
-    for (int j4 = 0; j4 < n; j4 += 4) {  // four columns of J per vector load; unused slots are zero
+  if (lane < nd) {
+    for (int j4 = 0; j4 < nd; j4 += 4) {  // four columns of J per vector load; unused slots are zero
       T a[4] = {T(0), T(0), T(0), T(0)};
 #pragma unroll
       for (int m = 0; m < 6 * NE; ++m) {
@@ -254,10 +295,10 @@ __device__ __forceinline__ T tree_eval(const TreeLmParams<T>& P, const TreeTable
 #pragma unroll
       for (int t = 0; t < 4; ++t) S.A[(j4 + t) * 33 + lane] = a[t];  // rows >= n: zero, unread
     }
-    S.A[lane * 33 + lane] += gl * gl + P.w_rest * P.w_rest;
+    if (lane < n) S.A[lane * 33 + lane] += gl * gl + P.w_rest * P.w_rest;
 #pragma unroll
     for (int m = 0; m < 6 * NE; ++m) g += col[m] * S.ee[m / 6][m % 6];
-    g += gl * rl + P.w_rest * rr;
+    g += gl * rl + P.w_rest * rr;  // zero on base lanes
   }
   g_out = g;
   __syncwarp();
@@ -272,7 +313,7 @@ __device__ __forceinline__ bool tree_damped_solve(const TreeLmParams<T>& P, Tree
   // scaled pivot column is published once per step in shared memory and read
   // back as vector broadcasts.  Lanes update their whole row: the entries
   // right of the diagonal are never read, so no per-entry lane test.
-  const int n = P.n;
+  const int n = P.n + base_dim(P.base_kind);  // the tangent: actuated columns, then the base's
   T row[kTreeMaxDofs];
 #pragma unroll
   for (int j = 0; j < kTreeMaxDofs; ++j) {
@@ -345,12 +386,59 @@ constexpr int tree_warps() { return sizeof(T) == 4 ? 1 : 4; }
 template <typename T>
 constexpr int tree_beam_warps() { return sizeof(T) == 4 ? KOP_TREE_BEAM_WARPS32 : KOP_TREE_BEAM_WARPS64; }
 
+// canonical unit quaternion (quat_normalize_canonical, liegroups.py:33-46)
+template <typename T>
+__device__ __forceinline__ quat<T> canon_t(quat<T> q) {
+  const T inv = T(1) / sqrt_t(q.w * q.w + q.x * q.x + q.y * q.y + q.z * q.z);
+  q = {q.w * inv, q.x * inv, q.y * inv, q.z * inv};
+  T sign = q.w < T(0) ? T(-1) : T(1);
+  if (q.w == T(0)) {
+    const T ax = fabs(q.x), ay = fabs(q.y), az = fabs(q.z);
+    const T lead = (ax >= ay && ax >= az) ? q.x : (ay >= az ? q.y : q.z);
+    sign = lead < T(0) ? T(-1) : T(1);
+  }
+  return {q.w * sign, q.x * sign, q.y * sign, q.z * sign};
+}
+
+// base <- base * exp(delta): Transform2.compose(Transform2.exp) (liegroups.py:431-445; the SE(2) state
+// is (angle, x, y)) or Transform3.compose(Transform3.exp) (liegroups.py:379-390, se3_exp_arrays :194-200;
+// state (wxyz, xyz)), i.e. local_update (liegroups.py:505-519) of the base variable
+template <typename T>
+__device__ __forceinline__ void tree_base_retract(int kind, const T* b, const T (&d)[6], T* out) {
+  if (kind == 1) {
+    const T cur[3] = {b[1], b[2], b[0]};
+    T nxt[3];
+    base_retract(cur, d[0], d[1], d[2], nxt);
+    out[0] = nxt[2];
+    out[1] = nxt[0];
+    out[2] = nxt[1];
+    return;
+  }
+  const vec3<T> rho{d[0], d[1], d[2]}, phi{d[3], d[4], d[5]};
+  const T t2 = dot(phi, phi), th = sqrt_t(t2);
+  const bool small = th < T(1e-7);
+  T sh, ch, s1, c1;
+  sincos_t(T(0.5) * th, &sh, &ch);
+  sincos_t(th, &s1, &c1);
+  const T k = small ? T(0.5) - t2 / T(48) : sh / th;
+  const quat<T> qe = canon_t(quat<T>{ch, k * phi.x, k * phi.y, k * phi.z});
+  const T a = small ? T(0.5) - t2 / T(24) : (T(1) - c1) / t2;
+  const T bb = small ? T(1) / T(6) - t2 / T(120) : (th - s1) / (t2 * th);
+  const vec3<T> pr = cross(phi, rho), ppr = cross(phi, pr);
+  const vec3<T> v{rho.x + a * pr.x + bb * ppr.x, rho.y + a * pr.y + bb * ppr.y, rho.z + a * pr.z + bb * ppr.z};
+  const quat<T> qb{b[0], b[1], b[2], b[3]};
+  const quat<T> qn = canon_t(qmul(qb, qe));
+  const vec3<T> tv = qrot(qb, v);
+  out[0] = qn.w; out[1] = qn.x; out[2] = qn.y; out[3] = qn.z;
+  out[4] = b[4] + tv.x; out[5] = b[5] + tv.y; out[6] = b[6] + tv.z;
+}
+
 template <typename T, int NE>
 __global__ void __launch_bounds__(32 * tree_warps<T>())
 k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const double* __restrict__ q0, int64_t B,
              const LmOptions O, double* __restrict__ q_out, double* __restrict__ cost_out,
              double* __restrict__ init_cost_out, double* __restrict__ hist_out, int32_t* __restrict__ iters_out,
-             int32_t* __restrict__ term_out) {
+             int32_t* __restrict__ term_out, const double* __restrict__ base0, double* __restrict__ base_out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   KOP_SMEM_ENTRY(smem_raw);
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -361,10 +449,11 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
   stage_tree_table(P, Q);
   __syncthreads();      // the only CTA-wide barrier: warps are independent from here on
   if (b >= B) return;  // whole warp exits together
-  const int n = P.n;
+  const int n = P.n, nd = n + base_dim(P.base_kind), bsz = base_state(P.base_kind);
   for (int i = lane; i < NE * 48; i += 32) (&S.ee[0][0])[i] = T(0);  // unused slots stay zero
   const double* tg = targets + b * 7 * P.ne;
   S.q[lane] = lane < n ? T(q0[b * n + lane]) : T(0);
+  if (lane < 8) S.bs[lane] = lane < bsz ? T(base0[b * bsz + lane]) : T(0);
   __syncwarp();
   T g, cost = T(0);
   const int hstride = O.max_iterations + 1;
@@ -374,7 +463,7 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
   // one J-evaluation site (start evaluation, then J at each accepted iterate):
   // a single inlined copy keeps the kernel inside the instruction cache
   for (int it = 0;; ++it) {
-    const T c = tree_eval<T, NE, true>(P, Q, tg, S, S.q, lane, g);
+    const T c = tree_eval<T, NE, true>(P, Q, tg, S, S.q, S.bs, lane, g);
     if (it == 0) {
       cost = c;
       if (lane == 0) {
@@ -384,29 +473,36 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
       term = finite_t(cost) ? 0 : 5;
     }
     if (term != 0 || it >= O.max_iterations) break;
-    if (warp_max(lane < n ? fabs(g) : T(0)) < T(O.grad_tol)) {
+    if (warp_max(lane < nd ? fabs(g) : T(0)) < T(O.grad_tol)) {
       term = 1;
       break;
     }
     bool accepted = false;
     T step = T(0);
     // diag of J^T J at the iterate (lane i), for the FP32 rule's model decrease
-    const T dg = lane < n ? tmax(S.A[lane * 33 + lane], T(BeamConsts::diag_clamp)) : T(0);
+    const T dg = lane < nd ? tmax(S.A[lane * 33 + lane], T(BeamConsts::diag_clamp)) : T(0);
     for (int rj = 0; rj < O.max_rejections; ++rj) {
       T d;
       bool ok = tree_damped_solve(P, S, g, damping, lane, d);
       ok = __all_sync(0xffffffffu, ok && finite_t(d));
       if (ok) {
         S.qn[lane] = S.q[lane] + d;
+        if (bsz) {  // the base moves by its own retraction (local_update)
+          T db[6];
+#pragma unroll
+          for (int c = 0; c < 6; ++c) db[c] = shfl_t(d, n + c < 32 ? n + c : 31);
+          if (lane == 0) tree_base_retract(P.base_kind, S.bs, db, S.bn);
+        }
         __syncwarp();
         T gd;
-        const T cn = tree_eval<T, NE, false>(P, Q, tg, S, S.qn, lane, gd);
+        const T cn = tree_eval<T, NE, false>(P, Q, tg, S, S.qn, S.bn, lane, gd);
         if (!finite_t(cn)) {
           term = 5;
           break;
         }
         if (cn < cost) {
           S.q[lane] = S.qn[lane];
+          if (lane < bsz) S.bs[lane] = S.bn[lane];
           step = d;
           cost = cn;
           damping = tmax(damping * T(O.down), T(BeamConsts::damping_min));
@@ -416,7 +512,7 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
         }
         // FP32 rule (kop_collision.cu kFp32Tau): a rejected trial whose quadratic-model decrease
         // -g.d + lam d^T D d is below 2^-17 of the cost is not resolvable in float32
-        if (sizeof(T) == 4 && warp_sum(lane < n ? damping * dg * d * d - g * d : T(0)) <=
+        if (sizeof(T) == 4 && warp_sum(lane < nd ? damping * dg * d * d - g * d : T(0)) <=
                                   T(7.62939453125e-6f) * cost) {
           term = 6;
           break;
@@ -440,6 +536,7 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
   if (hist_out)
     for (int i = iters + 1 + lane; i < hstride; i += 32) hist_out[b * hstride + i] = NAN;
   if (lane < n) q_out[b * n + lane] = double(S.q[lane]);
+  if (lane < bsz && base_out) base_out[b * bsz + lane] = double(S.bs[lane]);
   if (lane == 0) {
     cost_out[b] = double(cost);
     iters_out[b] = iters;
@@ -455,7 +552,8 @@ cudaError_t launch_tree_ne(const TreeLmParams<T>& P, const TreeLaunch& L, cudaSt
   if (smem > 48 * 1024)
     cudaFuncSetAttribute(k_tree_solve<T, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   k_tree_solve<T, NE><<<(unsigned)((L.B + warps - 1) / warps), 32 * warps, smem, st>>>(
-      P, L.targets, L.q0, L.B, L.opts, L.q_out, L.cost_out, L.init_cost, L.hist_out, L.iters, L.term);
+      P, L.targets, L.q0, L.B, L.opts, L.q_out, L.cost_out, L.init_cost, L.hist_out, L.iters, L.term, L.base0,
+      L.base_out);
   return cudaGetLastError();
 }
 
@@ -493,7 +591,7 @@ __device__ __forceinline__ T tree_beam_run(const TreeLmParams<T>& P, const TreeT
   bool need = true;
   for (int it = 0;; ++it) {
     if (need) {
-      const T c = tree_eval<T, NE, true>(P, Q, tg, S, S.q, lane, g);
+      const T c = tree_eval<T, NE, true>(P, Q, tg, S, S.q, nullptr, lane, g);
       if (start && it == 0) {
         cost = c;
         if (lane == 0) hv = c;
@@ -509,7 +607,7 @@ __device__ __forceinline__ T tree_beam_run(const TreeLmParams<T>& P, const TreeT
       S.qn[lane] = S.q[lane] + d;
       __syncwarp();
       T gd;
-      const T raw = tree_eval<T, NE, false>(P, Q, tg, S, S.qn, lane, gd);
+      const T raw = tree_eval<T, NE, false>(P, Q, tg, S, S.qn, nullptr, lane, gd);
       cn = finite_t(raw) ? raw : inf_t<T>();
     }
     if (cn < cost) {

@@ -32,11 +32,19 @@ struct TreeLmParams {
   // moving joints of each actuated column
   int8_t col_nj[kTreeMaxDofs];
   int8_t col_joint[kTreeMaxDofs][kTreeMaxPerCol];
+  // optional base variable of the pose costs (costs.py:98-166, base_var): 0 none, 1 SE(2), 2 SE(3);
+  // its tangent is columns n .. n + db - 1
+  int32_t base_kind;
 };
+
+__host__ __device__ inline int base_dim(int base_kind) { return base_kind == 1 ? 3 : (base_kind == 2 ? 6 : 0); }
+__host__ __device__ inline int base_state(int base_kind) { return base_kind == 1 ? 3 : (base_kind == 2 ? 7 : 0); }
 
 struct TreeLaunch {
   const double* targets;  // [B * ne * 7]
   const double* q0;       // [B * n]
+  const double* base0;    // [B * 3] (angle, x, y) for SE(2) | [B * 7] (wxyz, xyz) for SE(3) | null
+  double* base_out;       // same layout
   int64_t B;
   LmOptions opts;
   double *q_out, *cost_out, *init_cost, *hist_out;

@@ -330,6 +330,8 @@ class _Plan:
     path: str = "chain"
     targets: list = field(default_factory=list)  # tree path: one Transform3 per pose cost
     traj: dict = field(default_factory=dict)     # traj path: var ids, anchors, obstacle table
+    base: str | None = None                      # tree path: the pose costs' base variable (SE(2) / SE(3))
+    base_kind: int = 0
 
 
 def _obstacles(world):
@@ -369,9 +371,17 @@ def plan(problem: Problem) -> _Plan:
 
     if not problem.costs or problem.residual_dim < 1:
         raise ValueError("problem must declare at least one cost with residual rows")
-    if len(problem.variables.ids) > 1:
+    base_vars = {c.params.get("base_var") for c in problem.costs if c.kind == "pose"}
+    base_var = None
+    if base_vars - {None}:
+        if len(base_vars) != 1:
+            raise UnsupportedFeatureError("pose costs must all use the same base variable (or none)")
+        base_var = base_vars.pop()
+        if len(problem.variables.ids) != 2:
+            raise UnsupportedFeatureError("a base-variable device solve takes one configuration and one base variable")
+    elif len(problem.variables.ids) > 1:
         return _plan_trajectory(problem)
-    var = problem.variables.ids[0]
+    var = [v for v in problem.variables.ids if v != base_var][0]
     by, poses = {}, []
     for c in problem.costs:
         if c.kind not in _DEVICE_KINDS:
@@ -379,8 +389,6 @@ def plan(problem: Problem) -> _Plan:
                 f"cost '{c.name}' has no device kernel (custom Python costs cannot run on the GPU; "
                 "there is no CPU fallback)")
         if c.kind == "pose":
-            if c.params.get("base_var"):
-                raise UnsupportedFeatureError("pose costs with a base variable are not supported by the device solve")
             poses.append(c)
             continue
         if c.kind in by:
@@ -397,7 +405,21 @@ def plan(problem: Problem) -> _Plan:
             raise UnsupportedFeatureError("all costs of a device problem must use the same RobotModel")
     collision = "world_collision" in by or "self_collision" in by
     link = poses[0].params["link"]
-    chain_ok = model.actuated_count <= 8 and model.chain_length(link) >= 0
+    if base_var is not None:
+        from ._lib import KOP_BASE_SE2, KOP_BASE_SE3
+
+        bval = problem.variables.value(base_var)
+        if isinstance(bval, Transform2):
+            base_kind = KOP_BASE_SE2
+        elif isinstance(bval, Transform3):
+            base_kind = KOP_BASE_SE3
+        else:
+            raise UnsupportedFeatureError(f"base variable '{base_var}' must be a Transform2 or Transform3")
+        if collision:
+            raise UnsupportedFeatureError("collision costs with a base variable are not supported by the device solve")
+        if any(base_var in c.variable_refs for c in by.values()):
+            raise UnsupportedFeatureError("only pose costs may reference the base variable")
+    chain_ok = model.actuated_count <= 8 and model.chain_length(link) >= 0 and base_var is None
     w_lim = _uniform(by["limit"].weight, "limit") if "limit" in by else 0.0
     w_rest = _uniform(by["rest"].weight, "rest") if "rest" in by else 0.0
     if len(poses) == 1 and (chain_ok or collision):
@@ -437,9 +459,11 @@ def plan(problem: Problem) -> _Plan:
     rest = np.ascontiguousarray(by["rest"].params["q_rest"] if "rest" in by else model.rest_pose, dtype=float)
     pc = L.KopPoseCosts(len(poses), links.ctypes.data, wpos.ctypes.data, wori.ctypes.data, w_lim, w_rest,
                         rest.ctypes.data)
-    key = ("tree", id(model), tuple(links), tuple(wpos), tuple(wori), w_lim, w_rest, rest.tobytes())
+    key = ("tree", id(model), tuple(links), tuple(wpos), tuple(wori), w_lim, w_rest, rest.tobytes(),
+           base_kind if base_var else 0)
     return _Plan(model, poses[0].params["link"], var, poses[0].params["target"], pc, [links, wpos, wori, rest],
-                 key, "tree", [p.params["target"] for p in poses])
+                 key, "tree", [p.params["target"] for p in poses], base=base_var,
+                 base_kind=base_kind if base_var else 0)
 
 
 _TRAJ_KINDS = ("rest", "limit", "smoothness", "velocity", "acceleration", "jerk", "self_collision",
@@ -586,6 +610,21 @@ def _options(options: SolveOptions):
     return o
 
 
+def _base_state(value) -> np.ndarray:
+    """Base variable -> the kernel's state: SE(2) (angle, x, y), SE(3) (wxyz, xyz)."""
+    if isinstance(value, Transform2):
+        return np.array([value.angle, value.translation[0], value.translation[1]])
+    return value.as_array()
+
+
+def _base_value(kind: int, state):
+    from ._lib import KOP_BASE_SE2
+
+    if kind == KOP_BASE_SE2:
+        return Transform2(float(state[0]), np.array(state[1:3]))
+    return Transform3.from_parts(state[:4], state[4:7])
+
+
 def _run(plans, problems, options: SolveOptions) -> list:
     """One kop_lm_solve launch for problems sharing a plan key."""
     from . import _device as dv
@@ -608,7 +647,15 @@ def _run(plans, problems, options: SolveOptions) -> list:
     term = t.empty(b, dtype=t.int32, device="cuda")
     opts = _options(options)
     t0 = time.perf_counter()
-    if p0.path == "tree":
+    base_out = None
+    if p0.path == "tree" and p0.base is not None:
+        b0 = np.stack([_base_state(pr.variables.value(p.base)) for p, pr in zip(plans, problems)])
+        base0, base_out = dv.to_dev(b0), dv.empty(b0.shape)
+        check(lib().kop_multi_pose_solve_base(p0.model._handle, C.byref(p0.costs), C.byref(opts), p0.base_kind,
+                                              dv.ptr(tg), dv.ptr(q0), dv.ptr(base0), b, dv.ptr(q), dv.ptr(base_out),
+                                              dv.ptr(cost), dv.ptr(init), dv.ptr(hist), dv.ptr(iters), dv.ptr(term),
+                                              dv.stream_handle()), "kop_multi_pose_solve_base")
+    elif p0.path == "tree":
         check(lib().kop_multi_pose_solve(p0.model._handle, C.byref(p0.costs), C.byref(opts), dv.ptr(tg), dv.ptr(q0),
                                          b, dv.ptr(q), dv.ptr(cost), dv.ptr(init), dv.ptr(hist), dv.ptr(iters),
                                          dv.ptr(term), dv.stream_handle()), "kop_multi_pose_solve")
@@ -620,10 +667,18 @@ def _run(plans, problems, options: SolveOptions) -> list:
     ith, th = iters.cpu().numpy(), term.cpu().numpy()
     dt = (time.perf_counter() - t0) / b
     out = []
+    bh = base_out.cpu().numpy() if base_out is not None else None
     for i, (p, pr) in enumerate(zip(plans, problems)):
         termination, message = TERMINATIONS[int(th[i])]
         h = hh[i, : int(ith[i]) + 1]
-        out.append(SolveReport(final_values=VariableSet.of(**{p.var: qh[i]}), initial_cost=float(ih[i]),
+        if p.base is not None:  # both variables, in the problem's order
+            vals = {p.var: qh[i], p.base: _base_value(p.base_kind, bh[i])}
+            final = VariableSet()
+            for vid in pr.variables.ids:
+                final.add(vid, vals[vid])
+        else:
+            final = VariableSet.of(**{p.var: qh[i]})
+        out.append(SolveReport(final_values=final, initial_cost=float(ih[i]),
                                final_cost=float(ch[i]), iterations_run=int(ith[i]), termination=termination,
                                cost_history=[float(x) for x in h], solve_time_s=dt, message=message))
     return out

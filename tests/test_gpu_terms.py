@@ -230,3 +230,36 @@ def test_raw_residual_contract(arm7):
         c.raw_residual([np.zeros(3)])
     with pytest.raises(k.UnsupportedFeatureError):
         k.manipulability_cost(arm7, "q", "flange").raw_residual([arm7.rest_pose])
+
+
+@pytest.mark.parametrize("kind", ["se2", "se3"])
+def test_solve_with_base_variable_matches_reference(gt, arm7, kind):
+    """solver.solve with pose_cost(base_var=...) (costs.py:98-166) on the device tree LM
+    (kop_multi_pose_solve_base): the reference's own solve histories (60 iterations, targets
+    up to 1.5 m out of the fixed base's reach) within 1e-6, final q / base within 1e-6."""
+    probs = []
+    for i in range(4):
+        t = gt[f"solve_{kind}_targets"][i]
+        tgt = Transform3.from_parts(t[:4], t[4:])
+        base0 = Transform2.identity() if kind == "se2" else Transform3.identity()
+        vs = k.VariableSet.of(q=arm7.rest_pose.copy(), b=base0)
+        probs.append(k.Problem(vs, [k.pose_cost(arm7, "q", "flange", tgt, base_var="b", position_weight=50,
+                                                orientation_weight=10),
+                                    k.limit_cost(arm7, "q", weight=100), k.rest_cost("q", arm7.rest_pose, weight=0.01)]))
+    reps = k.solve_batch(probs, k.SolveOptions(max_iterations=60))
+    for i, rep in enumerate(reps):
+        gh = gt[f"solve_{kind}_hist"][i]
+        gh = gh[~np.isnan(gh)]
+        assert rep.iterations_run == gt[f"solve_{kind}_iters"][i]
+        h = np.array(rep.cost_history)
+        assert h.shape == gh.shape
+        assert np.max(np.abs(h - gh) / gh) < 1e-6, (i, np.max(np.abs(h - gh) / gh))
+        np.testing.assert_allclose(rep.final_values.value("q"), gt[f"solve_{kind}_q"][i], atol=1e-6)
+        b = rep.final_values.value("b")
+        got = np.array([b.angle, *b.translation]) if kind == "se2" else b.as_array()
+        np.testing.assert_allclose(got, gt[f"solve_{kind}_b"][i], atol=1e-6)
+    # FP32 reaches the same costs (its stopping rule may end it earlier, DESIGN.md section 4)
+    r32 = k.solve_batch(probs, k.SolveOptions(max_iterations=60, precision="fp32"))
+    for i, rep in enumerate(r32):
+        assert all(bb <= aa for aa, bb in zip(rep.cost_history, rep.cost_history[1:]))
+        assert rep.final_cost <= 1.05 * gt[f"solve_{kind}_hist"][i][60] + 1e-5
