@@ -50,8 +50,11 @@ def build_variants(verbose: bool = False, force: bool = False) -> list:
     return [build(verbose=verbose, force=force, variant=name) for name in VARIANTS]
 
 
-def build(verbose: bool = False, ptxas_info: bool = False, force: bool = False, variant: str | None = None) -> str:
-    extra = VARIANTS[variant] if variant else []
+def build(verbose: bool = False, ptxas_info: bool = False, force: bool = False, variant: str | None = None,
+          defines: list | None = None) -> str:
+    """The library (variant None) or a variant build: VARIANTS[variant] or the given -D defines
+    (instrumented / A-B builds, e.g. -DKOP_TRAJ_PROFILE) into variants/."""
+    extra = list(defines) if defines is not None else (VARIANTS[variant] if variant else [])
     obj_dir = os.path.join(ROOT, "build", f"obj_{variant}") if variant else OBJ
     lib_path = variant_lib(variant) if variant else LIB
     os.makedirs(obj_dir, exist_ok=True)

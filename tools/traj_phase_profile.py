@@ -1,8 +1,8 @@
 """Per-phase clock64 cycles of the trajectory kernel (thread 0 of each CTA),
 from a -DKOP_TRAJ_PROFILE build:
 
-  python tools/build_variant.py prof -DKOP_TRAJ_PROFILE
-  KOP_LIB=build/ab/prof.so python tools/traj_phase_profile.py
+  python -c "from paper_2505_03728_b200 import _build; _build.build(variant='trajprof', defines=['-DKOP_TRAJ_PROFILE'])"
+  KOP_LIB=variants/libkinoptik_b200_trajprof.so python tools/traj_phase_profile.py
 """
 import ctypes as C, json, os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
