@@ -500,6 +500,36 @@ def run_sweep(torch, k, model, solver_for, flush, peak, nominal):
     return out
 
 
+def hbm_peak():
+    """(GB/s, source): MEASURED_PEAKS.json's copy bandwidth, else the profiling guide's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (measured)"
+    except (OSError, ValueError, KeyError):
+        return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def run_fk(torch, model, flush, B=1_000_000):
+    """fk_arrays (robot.py:404-448) on the device: B configurations in, every link frame and
+    every joint anchor / axis out (FP64 outputs) -- HBM-write-bound, bytes roofline."""
+    from paper_2505_03728_b200 import _device as dv
+    from paper_2505_03728_b200.robot import fk_arrays_device
+
+    q = dv.to_dev(np.random.default_rng(3).uniform(model.lower_limits, model.upper_limits, (B, model.actuated_count)))
+    nl, nj, n = len(model.link_names), len(model.joints), model.actuated_count
+    byts = B * 8 * (n + 7 * nl + 6 * nj)
+    peak, src = hbm_peak()
+    out = {"workload": f"fk_arrays of {B} Panda configurations (all {nl} link frames + {nj} joint anchors / axes, "
+                       "float64 outputs)", "bytes_per_call": byts}
+    for prec in ("fp64", "fp32"):
+        ms = float(np.median(device_time(torch, lambda: fk_arrays_device(model, q, prec), 5, flush)))
+        gbs = byts / (ms * 1e-3) / 1e9
+        out[prec] = {"ms": ms, "configs_per_s": B / ms * 1e3,
+                     "roofline": {"bound": "hbm", "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                                  "peak_source": src, "kernel": "k_fk_tree"}}
+    return out
+
+
 def run_fp64_headline(torch, model, solver_for, flush, B, peak64, nominal64):
     from paper_2505_03728_b200.benchmark import reachable_target_array
 
@@ -946,6 +976,7 @@ def run_ours(args, rank, world, local_rank):
         t0 = time.perf_counter()
         line["batch_sweep"] = run_sweep(torch, k, model, solver_for, flush, peak, nominal)
         line["fp64"] = run_fp64_headline(torch, model, solver_for, flush, B, peak64, nominal64)
+        line["fk"] = run_fk(torch, model, flush)
         line["configs"] = run_configs(torch, k, model, flush, {"fp32": peak, "fp64": peak64},
                                       {"fp32": nominal, "fp64": nominal64}, cpu=not args.no_cpu_baseline)
         line["configs"]["peaks"] = {"fp32_live_ffma": peak, "fp64_live_dfma": peak64, "fp32_nominal": nominal,

@@ -13,73 +13,121 @@ namespace kop {
 // for each joint in topological order: fq = q_parent * q_origin,
 // fp = p_parent + R_parent p_origin; anchor = fp, world axis = R(fq) axis;
 // revolute: child = fq * (cos th/2, sin th/2 axis); prismatic: fp + th axis_w.
+//
+// HBM-write-bound (per configuration n doubles in, L * 7 + J * 6 doubles
+// out): every thread builds its frames in SHARED memory (thread-major,
+// [link][wxyz xyz] then [joint][anchor axis]), then the CTA writes its rows
+// of each output array as one contiguous, coalesced stream -- instead of each
+// thread storing its own L * 4 / L * 3 / J * 3 segments at a stride of a
+// whole row (round 1: per-thread local arrays, uncoalesced AoS stores).
 // ---------------------------------------------------------------------------
-template <typename T>
-__global__ void __launch_bounds__(128)
+template <typename T, bool KOP_FK_STAGE_JOINTS>
+__global__ void __launch_bounds__(256)
 k_fk_tree(const TreeParams P, const double* __restrict__ q, int64_t B, double* __restrict__ lq_out,
           double* __restrict__ lp_out, double* __restrict__ jp_out, double* __restrict__ ja_out) {
-  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (b >= B) return;
-  quat<T> lq[kMaxLinks];
-  vec3<T> lp[kMaxLinks];
-  lq[0] = {T(1), T(0), T(0), T(0)};
-  lp[0] = {T(0), T(0), T(0)};
-  const double* qb = q + b * P.n;
-  for (int j = 0; j < P.nj; ++j) {
-    const quat<T> pq = lq[P.parent[j]];
-    const vec3<T> pp = lp[P.parent[j]];
-    const quat<T> fq = qmul(pq, quat<T>{T(P.oq[j][0]), T(P.oq[j][1]), T(P.oq[j][2]), T(P.oq[j][3])});
-    const vec3<T> o = qrot(pq, vec3<T>{T(P.op[j][0]), T(P.op[j][1]), T(P.op[j][2])});
-    const vec3<T> fp{pp.x + o.x, pp.y + o.y, pp.z + o.z};
-    const vec3<T> axis{T(P.axis[j][0]), T(P.axis[j][1]), T(P.axis[j][2])};
-    const vec3<T> wa = qrot(fq, axis);
-    if (jp_out) {
-      double* d = jp_out + (b * P.nj + j) * 3;
-      d[0] = fp.x; d[1] = fp.y; d[2] = fp.z;
-    }
-    if (ja_out) {
-      double* d = ja_out + (b * P.nj + j) * 3;
-      d[0] = wa.x; d[1] = wa.y; d[2] = wa.z;
-    }
-    const int c = P.child[j];
-    if (P.kind[j] == 0) {
-      lq[c] = fq;
-      lp[c] = fp;
-      continue;
-    }
-    const T th = T(qb[P.qcol[j]]) * T(P.mult[j]) + T(P.offset[j]);
-    if (P.kind[j] == 1) {
-      T s, co;
-      sincos_t(T(0.5) * th, &s, &co);
-      lq[c] = qmul(fq, quat<T>{co, s * axis.x, s * axis.y, s * axis.z});
-      lp[c] = fp;
-    } else {
-      lq[c] = fq;
-      lp[c] = {fp.x + th * wa.x, fp.y + th * wa.y, fp.z + th * wa.z};
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int nl = P.nl, nj = P.nj, per = 7 * nl + (KOP_FK_STAGE_JOINTS ? 6 * nj : 0);  // T words per configuration
+  T* my = reinterpret_cast<T*>(smem_raw) + (size_t)threadIdx.x * per;
+  const int64_t b0 = (int64_t)blockIdx.x * blockDim.x;
+  const int64_t b = b0 + threadIdx.x;
+  const int rows = (int)(B - b0 < (int64_t)blockDim.x ? B - b0 : (int64_t)blockDim.x);
+  if (b < B) {
+    T* F = my;            // link frames [nl][7]
+    T* A = my + 7 * nl;   // joint anchor / axis [nj][6]
+    F[0] = T(1); F[1] = T(0); F[2] = T(0); F[3] = T(0); F[4] = T(0); F[5] = T(0); F[6] = T(0);
+    const double* qb = q + b * P.n;
+    for (int j = 0; j < nj; ++j) {
+      const T* pf = F + 7 * P.parent[j];
+      const quat<T> pq{pf[0], pf[1], pf[2], pf[3]};
+      const vec3<T> pp{pf[4], pf[5], pf[6]};
+      const quat<T> fq = qmul(pq, quat<T>{T(P.oq[j][0]), T(P.oq[j][1]), T(P.oq[j][2]), T(P.oq[j][3])});
+      const vec3<T> o = qrot(pq, vec3<T>{T(P.op[j][0]), T(P.op[j][1]), T(P.op[j][2])});
+      const vec3<T> fp{pp.x + o.x, pp.y + o.y, pp.z + o.z};
+      const vec3<T> axis{T(P.axis[j][0]), T(P.axis[j][1]), T(P.axis[j][2])};
+      const vec3<T> wa = qrot(fq, axis);
+      if (KOP_FK_STAGE_JOINTS) {
+        T* aj = A + 6 * j;
+        aj[0] = fp.x; aj[1] = fp.y; aj[2] = fp.z;
+        aj[3] = wa.x; aj[4] = wa.y; aj[5] = wa.z;
+      } else {  // anchors / axes straight to global (3 consecutive doubles each)
+        if (jp_out) {
+          double* d = jp_out + (b * nj + j) * 3;
+          d[0] = fp.x; d[1] = fp.y; d[2] = fp.z;
+        }
+        if (ja_out) {
+          double* d = ja_out + (b * nj + j) * 3;
+          d[0] = wa.x; d[1] = wa.y; d[2] = wa.z;
+        }
+      }
+      quat<T> cq = fq;
+      vec3<T> cp = fp;
+      if (P.kind[j] != 0) {
+        const T th = T(qb[P.qcol[j]]) * T(P.mult[j]) + T(P.offset[j]);
+        if (P.kind[j] == 1) {
+          T s, co;
+          sincos_t(T(0.5) * th, &s, &co);
+          cq = qmul(fq, quat<T>{co, s * axis.x, s * axis.y, s * axis.z});
+        } else {
+          cp = {fp.x + th * wa.x, fp.y + th * wa.y, fp.z + th * wa.z};
+        }
+      }
+      T* cf = F + 7 * P.child[j];
+      cf[0] = cq.w; cf[1] = cq.x; cf[2] = cq.y; cf[3] = cq.z;
+      cf[4] = cp.x; cf[5] = cp.y; cf[6] = cp.z;
     }
   }
-  for (int l = 0; l < P.nl; ++l) {
-    if (lq_out) {
-      double* d = lq_out + (b * P.nl + l) * 4;
-      d[0] = lq[l].w; d[1] = lq[l].x; d[2] = lq[l].y; d[3] = lq[l].z;
+  __syncthreads();
+  // coalesced write-out of this CTA's `rows` consecutive output rows of each array
+  const T* base = reinterpret_cast<const T*>(smem_raw);
+  auto stream = [&](double* out, int width, int stride_in_row, int off, int comps) {
+    if (!out) return;
+    const int64_t n_out = (int64_t)rows * width * comps;
+    double* dst = out + b0 * width * comps;
+    for (int64_t i = threadIdx.x; i < n_out; i += blockDim.x) {
+      const int r = (int)(i / (width * comps)), rem = (int)(i % (width * comps));
+      const int e = rem / comps, c = rem % comps;
+      dst[i] = double(base[(size_t)r * per + off + e * stride_in_row + c]);
     }
-    if (lp_out) {
-      double* d = lp_out + (b * P.nl + l) * 3;
-      d[0] = lp[l].x; d[1] = lp[l].y; d[2] = lp[l].z;
-    }
+  };
+  stream(lq_out, nl, 7, 0, 4);
+  stream(lp_out, nl, 7, 4, 3);
+  if (KOP_FK_STAGE_JOINTS) {
+    stream(jp_out, nj, 6, 7 * nl, 3);
+    stream(ja_out, nj, 6, 7 * nl + 3, 3);
   }
 }
 
 cudaError_t launch_fk_tree(const TreeParams& P, int precision, const double* q, int64_t B,
                            double* lq, double* lp, double* jp, double* ja, cudaStream_t st) {
   if (B == 0) return cudaSuccess;
-  const int tpb = 128;
+  const size_t word = precision == 0 ? sizeof(float) : sizeof(double);
+  // as many 32-thread groups as fit in ~96 KB of shared memory (2 CTAs per SM), <= 256 threads; the joint
+  // anchors / axes are staged too when that still leaves >= 128 threads per CTA, else stored directly
+  // (A/B, tools/fk_time.py: staging everything wins for the Panda in FP32, direct joint stores for the
+  // Panda in FP64 and for the humanoid, whose footprint would leave too few warps)
+  auto tpb_for = [&](size_t per) {
+    const int t = (int)((96 * 1024) / (per * 32)) * 32;
+    return t < 32 ? 32 : (t > 256 ? 256 : t);
+  };
+  const size_t per_all = word * (size_t)(7 * P.nl + 6 * P.nj), per_frames = word * (size_t)(7 * P.nl);
+  const bool stage = tpb_for(per_all) >= 128;
+  const size_t per = stage ? per_all : per_frames;
+  const int tpb = tpb_for(per);
+  const size_t smem = per * tpb;
   const unsigned blocks = (unsigned)((B + tpb - 1) / tpb);
+  cudaError_t e = cudaSuccess;
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024 &&
+        (e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)) != cudaSuccess)
+      return;
+    kern<<<blocks, tpb, smem, st>>>(P, q, B, lq, lp, jp, ja);
+    e = cudaGetLastError();
+  };
   if (precision == 0)
-    k_fk_tree<float><<<blocks, tpb, 0, st>>>(P, q, B, lq, lp, jp, ja);
+    stage ? go(k_fk_tree<float, true>) : go(k_fk_tree<float, false>);
   else
-    k_fk_tree<double><<<blocks, tpb, 0, st>>>(P, q, B, lq, lp, jp, ja);
-  return cudaGetLastError();
+    stage ? go(k_fk_tree<double, true>) : go(k_fk_tree<double, false>);
+  return e;
 }
 
 // Geometric Jacobian (robot.py:461-506): rows 0-2 the world linear velocity of

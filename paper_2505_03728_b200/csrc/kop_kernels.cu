@@ -32,8 +32,21 @@ struct PoseModelFactory {
   }
 };
 
+// resident 256-thread CTAs per SM the register allocation targets: FP32 2 (128 registers,
+// 16 warps); FP64 KOP_STAGE1_MINB64 (A/B-measured)
+#ifndef KOP_STAGE1_MINB64
+#define KOP_STAGE1_MINB64 2
+#endif
+#ifndef KOP_STAGE2_MINB64
+#define KOP_STAGE2_MINB64 4
+#endif
+template <class G>
+constexpr int stage1_min_blocks(int tpb) {
+  return tpb > 256 ? 1 : (sizeof(typename G::T) == 8 ? KOP_STAGE1_MINB64 : 2);
+}
+
 template <class G, int TPB>
-__global__ void __launch_bounds__(TPB, (TPB <= 256 ? 2 : 1))
+__global__ void __launch_bounds__(TPB, stage1_min_blocks<G>(TPB))
 k_beam_stage1(const ChainParams<typename G::T, G::K> C, const CostParams<typename G::T, G::NQ> W,
               const double* __restrict__ targets, int64_t B, const double* __restrict__ seeds, int S, int P,
               int steps1, int keep, typename G::T* __restrict__ surv, int rec,
@@ -46,7 +59,7 @@ k_beam_stage1(const ChainParams<typename G::T, G::K> C, const CostParams<typenam
 constexpr int kStage2Threads = 128;
 
 template <class G>
-__global__ void __launch_bounds__(kStage2Threads, 4)
+__global__ void __launch_bounds__(kStage2Threads, sizeof(typename G::T) == 8 ? KOP_STAGE2_MINB64 : 4)
 k_beam_stage2(const ChainParams<typename G::T, G::K> C, const CostParams<typename G::T, G::NQ> W,
               const ChainParams<double, G::K> Cd, const double* __restrict__ targets, int64_t B,
               const typename G::T* __restrict__ surv, int rec, int steps1, int steps2, int keep, int G2,
