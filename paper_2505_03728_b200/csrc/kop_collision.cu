@@ -32,8 +32,17 @@ struct CollisionModelFactory {
   }
 };
 
+// resident 128-thread CTAs per SM the register allocation targets: FP32 3 (168 registers);
+// FP64 2 (255 registers, 268 B spill instead of 168 registers with 1.6 KB / 3.6 KB spill stores /
+// loads: 204 -> 174 ms on 100K config-4 targets, A/B via KOP_COL_BEAM_MINB64)
+#ifndef KOP_COL_BEAM_MINB64
+#define KOP_COL_BEAM_MINB64 2
+#endif
 template <class G>
-__global__ void __launch_bounds__(128, 3)
+constexpr int col_beam_min_blocks() { return sizeof(typename G::T) == 8 ? KOP_COL_BEAM_MINB64 : 3; }
+
+template <class G>
+__global__ void __launch_bounds__(128, col_beam_min_blocks<G>())
 k_col_beam_stage1(const ChainParams<typename G::T, G::K> C, const CostParams<typename G::T, G::NQ> W,
                   const CollisionParams<typename G::T> P, const double* __restrict__ targets, int64_t B,
                   const double* __restrict__ seeds, int S, int Pw, int steps1, int keep,
@@ -43,7 +52,7 @@ k_col_beam_stage1(const ChainParams<typename G::T, G::K> C, const CostParams<typ
 }
 
 template <class G>
-__global__ void __launch_bounds__(128, 3)
+__global__ void __launch_bounds__(128, col_beam_min_blocks<G>())
 k_col_beam_stage2(const ChainParams<typename G::T, G::K> C, const CostParams<typename G::T, G::NQ> W,
                   const CollisionParams<typename G::T> P, const ChainParams<double, G::K> Cd,
                   const double* __restrict__ targets, int64_t B, const typename G::T* __restrict__ surv, int rec,
