@@ -405,6 +405,12 @@ int kop_term_joint(const KopModel* model, int32_t kind, const double* rest, cons
 int kop_term_collision(const KopModel* model, int32_t kind, const KopObstacle* obstacles, int32_t num_obstacles,
                        double eta, double sharpness, int32_t hard_min, const double* q0, const double* q1,
                        int64_t count, double* r, double* j0, double* j1, void* stream);
+/* manipulability_cost (costs.py:349-401): r [count] = 1 / (m + eps) with m the
+ * Yoshikawa measure of `link`'s translational Jacobian, jrow [count*n] its
+ * gradient row; jac [count*3*n] / djac [count*n*3*n] (nullable) = J and dJ/dq_a
+ * (robot.translational_jacobian_with_derivative, robot.py:509-566).  n <= 32. */
+int kop_term_manipulability(const KopModel* model, int32_t link, double eps, const double* q, int64_t count,
+                            double* r, double* jrow, double* jac, double* djac, void* stream);
 /* rows of a collision family for this model (negative status on error) */
 int kop_term_rows(const KopModel* model, int32_t kind, int32_t num_obstacles);
 

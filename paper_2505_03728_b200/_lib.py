@@ -123,6 +123,7 @@ SIGNATURES = {
     "kop_term_collision": (C.c_int, [_p, _i32, C.POINTER(KopObstacle), _i32, _f64, _f64, _i32, _p, _p, _i64, _p, _p,
                                      _p, _p]),
     "kop_term_rows": (C.c_int, [_p, _i32, _i32]),
+    "kop_term_manipulability": (C.c_int, [_p, _i32, _f64, _p, _i64, _p, _p, _p, _p, _p]),
 }
 
 _lib = None

@@ -208,9 +208,9 @@ def swept_collision_cost(model, prev_var: str, curr_var: str, world, eta: float 
 
 def manipulability_cost(model, q_var: str, link: str, weight: float = 1.0, eps: float = MANIP_EPS,
                         name: str | None = None, analytic: bool = True) -> CostTerm:
-    """1 / (Yoshikawa measure + eps) of the translational Jacobian (costs.py:349-401);
-    no device kernel (no configuration uses it)."""
+    """1 / (Yoshikawa measure + eps) of the translational Jacobian (costs.py:349-401): rows and
+    gradient evaluated on the device (kop_term_manipulability); no device solve includes it (no
+    configuration uses it)."""
     model.link_index(link)
-    return CostTerm(name=name or f"manipulability[{link}]", residual_dim=1, variable_refs=[q_var],
-                    weight=np.array([float(weight)]), kind="manipulability",
-                    params=dict(model=model, link=link, eps=float(eps), weight=float(weight)))
+    return _typed(name or f"manipulability[{link}]", 1, [q_var], np.array([float(weight)]), "manipulability",
+                  dict(model=model, link=link, eps=float(eps), weight=float(weight)), analytic)

@@ -1585,6 +1585,17 @@ int kop_term_joint(const KopModel* m, int32_t kind, const double* rest, const do
   return cuda_status(launch_term_joint(T, n, qs, count, r, jdiag, (cudaStream_t)stream));
 }
 
+int kop_term_manipulability(const KopModel* m, int32_t link, double eps, const double* q, int64_t count,
+                            double* r, double* jrow, double* jac, double* djac, void* stream) {
+  if (!m || count < 0) return fail(KOP_EINVAL, "invalid arguments");
+  if (link < 0 || link >= m->tree.nl) return fail(KOP_EINVAL, "unknown link index");
+  if (m->tree.n > kTreeMaxDofsTerms) return fail(KOP_EUNSUPPORTED, "manipulability supports <= 32 actuated joints");
+  if (count == 0) return KOP_OK;
+  if (!q) return fail(KOP_EINVAL, "null array argument");
+  return cuda_status(launch_term_manip(m->tree, link_map(*m), link, eps, q, count, r, jrow, jac, djac,
+                                       (cudaStream_t)stream));
+}
+
 int kop_term_rows(const KopModel* m, int32_t kind, int32_t num_obstacles) {
   if (!m) return fail(KOP_EINVAL, "null model");
   if (kind == KOP_TERM_SELF) return (int)(m->pair_links.size() / 2);

@@ -322,6 +322,150 @@ k_term_collision(const TreeParams P, const LinkMap link_pj, const TermGeom G, in
   }
 }
 
+// ---- manipulability_cost (costs.py:349-401) with translational_jacobian_with_derivative
+// (robot.py:509-566): J (3 x n) of `link`'s origin and dJ/dq_a, differentiating the geometric
+// column formulas joint by joint (mimic multipliers folded into both axes); measure
+// m = sqrt(det(J J^T)) (n >= 3) or sqrt(det(J^T J)) (n < 3); r = 1 / (m + eps), gradient
+// -0.5 m tr(G^-1 dG_a) / (m + eps)^2, zero at singularities (det <= 1e-18).
+__global__ void __launch_bounds__(32)
+k_term_manip(const TreeParams P, const LinkMap link_pj, int link, double eps, const double* __restrict__ q,
+             int64_t B, double* __restrict__ r_out, double* __restrict__ jrow_out, double* __restrict__ jac_out,
+             double* __restrict__ djac_out) {
+  const int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  const int n = P.n;
+  Frames F;
+  tree_fk(P, q + b * n, F);
+  const vec3<double> pe = F.lp[link];
+  int mv[kMaxTreeJoints], nm = 0;  // moving joints on the root -> link path
+  for (int j = link_pj.pj[link]; j >= 0; j = link_pj.pj[P.parent[j]])
+    if (P.kind[j] != 0) mv[nm++] = j;
+  vec3<double> raw[kMaxTreeJoints];
+  for (int k = 0; k < nm; ++k) {
+    const int j = mv[k];
+    raw[j] = P.kind[j] == 1 ? cross(F.ja[j], vec3<double>{pe.x - F.jp[j].x, pe.y - F.jp[j].y, pe.z - F.jp[j].z})
+                            : F.ja[j];
+  }
+  double* J = jac_out ? jac_out + b * 3 * n : nullptr;
+  double* dJ = djac_out ? djac_out + b * 3 * n * n : nullptr;
+  double Jl[3 * kTreeMaxDofsTerms];
+  for (int i = 0; i < 3 * n; ++i) Jl[i] = 0.0;
+  for (int k = 0; k < nm; ++k) {
+    const int j = mv[k], c = P.qcol[j];
+    Jl[0 * n + c] += P.mult[j] * raw[j].x;
+    Jl[1 * n + c] += P.mult[j] * raw[j].y;
+    Jl[2 * n + c] += P.mult[j] * raw[j].z;
+  }
+  if (J)
+    for (int i = 0; i < 3 * n; ++i) J[i] = Jl[i];
+  // s is an ancestor of joint i's frame: walking up from i's parent link meets s
+  auto upstream = [&](int s, int i) {
+    for (int j = link_pj.pj[P.parent[i]]; j >= 0; j = link_pj.pj[P.parent[j]])
+      if (j == s) return true;
+    return false;
+  };
+  // dJ[a][row][col], a = qcol of the differentiated joint s
+  double gram[9], ginv[9];
+  const bool wide = n >= 3;  // J J^T (3 x 3) or J^T J (n x n, n < 3)
+  const int gdim = wide ? 3 : n;
+  for (int u = 0; u < gdim; ++u)
+    for (int v = 0; v < gdim; ++v) {
+      double acc = 0.0;
+      if (wide)
+        for (int c = 0; c < n; ++c) acc += Jl[u * n + c] * Jl[v * n + c];
+      else
+        for (int rr = 0; rr < 3; ++rr) acc += Jl[rr * n + u] * Jl[rr * n + v];
+      gram[u * gdim + v] = acc;
+    }
+  double det;
+  if (gdim == 3) {
+    const double* g = gram;
+    det = g[0] * (g[4] * g[8] - g[5] * g[7]) - g[1] * (g[3] * g[8] - g[5] * g[6]) + g[2] * (g[3] * g[7] - g[4] * g[6]);
+    ginv[0] = (g[4] * g[8] - g[5] * g[7]) / det; ginv[1] = (g[2] * g[7] - g[1] * g[8]) / det;
+    ginv[2] = (g[1] * g[5] - g[2] * g[4]) / det; ginv[3] = (g[5] * g[6] - g[3] * g[8]) / det;
+    ginv[4] = (g[0] * g[8] - g[2] * g[6]) / det; ginv[5] = (g[2] * g[3] - g[0] * g[5]) / det;
+    ginv[6] = (g[3] * g[7] - g[4] * g[6]) / det; ginv[7] = (g[1] * g[6] - g[0] * g[7]) / det;
+    ginv[8] = (g[0] * g[4] - g[1] * g[3]) / det;
+  } else if (gdim == 2) {
+    det = gram[0] * gram[3] - gram[1] * gram[2];
+    ginv[0] = gram[3] / det; ginv[1] = -gram[1] / det; ginv[2] = -gram[2] / det; ginv[3] = gram[0] / det;
+  } else {
+    det = gram[0];
+    ginv[0] = 1.0 / det;
+  }
+  const bool singular = !(det > 1e-18);
+  const double m = singular ? 0.0 : sqrt(det);
+  if (r_out) r_out[b] = 1.0 / (m + eps);
+  double grad[kTreeMaxDofsTerms];
+  for (int a = 0; a < n; ++a) grad[a] = 0.0;
+  if (dJ)
+    for (int i = 0; i < 3 * n * n; ++i) dJ[i] = 0.0;
+  // d_col of column i w.r.t. theta_s (robot.py:544-565); dJa = dJ/dq_a accumulated per a
+  for (int a = 0; a < n; ++a) {
+    double dJa[3 * kTreeMaxDofsTerms];
+    for (int i = 0; i < 3 * n; ++i) dJa[i] = 0.0;
+    bool any = false;
+    for (int ks = 0; ks < nm; ++ks) {
+      const int s = mv[ks];
+      if (P.qcol[s] != a) continue;
+      any = true;
+      for (int ki = 0; ki < nm; ++ki) {
+        const int i = mv[ki];
+        const bool rev_i = P.kind[i] == 1;
+        vec3<double> dcol{0.0, 0.0, 0.0};
+        if (upstream(s, i)) {
+          vec3<double> dw{0.0, 0.0, 0.0}, dp;
+          if (P.kind[s] == 1) {
+            dw = cross(F.ja[s], F.ja[i]);
+            dp = cross(F.ja[s], vec3<double>{F.jp[i].x - F.jp[s].x, F.jp[i].y - F.jp[s].y, F.jp[i].z - F.jp[s].z});
+          } else {
+            dp = F.ja[s];
+          }
+          if (rev_i) {
+            const vec3<double> t1 = cross(dw, vec3<double>{pe.x - F.jp[i].x, pe.y - F.jp[i].y, pe.z - F.jp[i].z});
+            const vec3<double> t2 = cross(F.ja[i], vec3<double>{raw[s].x - dp.x, raw[s].y - dp.y, raw[s].z - dp.z});
+            dcol = {t1.x + t2.x, t1.y + t2.y, t1.z + t2.z};
+          } else {
+            dcol = dw;
+          }
+        } else if (rev_i) {
+          dcol = cross(F.ja[i], raw[s]);
+        }
+        const double mm = P.mult[i] * P.mult[s];
+        const int c = P.qcol[i];
+        dJa[0 * n + c] += mm * dcol.x;
+        dJa[1 * n + c] += mm * dcol.y;
+        dJa[2 * n + c] += mm * dcol.z;
+      }
+    }
+    if (!any) continue;
+    if (dJ)
+      for (int i = 0; i < 3 * n; ++i) dJ[a * 3 * n + i] = dJa[i];
+    if (singular) continue;
+    // tr(G^-1 dG), dG = dJa J^T + J dJa^T (wide) or dJa^T J + J^T dJa
+    double tr = 0.0;
+    for (int u = 0; u < gdim; ++u)
+      for (int v = 0; v < gdim; ++v) {
+        double dg = 0.0;
+        if (wide)
+          for (int c = 0; c < n; ++c) dg += dJa[u * n + c] * Jl[v * n + c] + Jl[u * n + c] * dJa[v * n + c];
+        else
+          for (int rr = 0; rr < 3; ++rr) dg += dJa[rr * n + u] * Jl[rr * n + v] + Jl[rr * n + u] * dJa[rr * n + v];
+        tr += ginv[v * gdim + u] * dg;
+      }
+    grad[a] = 0.5 * m * tr;
+  }
+  if (jrow_out)
+    for (int a = 0; a < n; ++a) jrow_out[b * n + a] = -grad[a] / ((m + eps) * (m + eps));
+}
+
+cudaError_t launch_term_manip(const TreeParams& P, const LinkMap& L, int link, double eps, const double* q,
+                              int64_t B, double* r, double* jrow, double* jac, double* djac, cudaStream_t st) {
+  if (B == 0) return cudaSuccess;
+  k_term_manip<<<(unsigned)((B + 31) / 32), 32, 0, st>>>(P, L, link, eps, q, B, r, jrow, jac, djac);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_term_pose(const TreeParams& P, const LinkMap& link_pj, int link, const TermPose& T,
                              const double* q, const double* base, int64_t B, double* r, double* jq, double* jb,
                              cudaStream_t st) {

@@ -7,6 +7,8 @@
 
 namespace kop {
 
+constexpr int kTreeMaxDofsTerms = 32;  // manipulability: actuated columns held per thread
+
 struct LinkMap {  // parent joint of every link (-1 for the root)
   int32_t pj[kMaxLinks];
 };
@@ -35,6 +37,8 @@ struct TermGeom {
 
 cudaError_t launch_term_pose(const TreeParams& P, const LinkMap& L, int link, const TermPose& T, const double* q,
                              const double* base, int64_t B, double* r, double* jq, double* jb, cudaStream_t st);
+cudaError_t launch_term_manip(const TreeParams& P, const LinkMap& L, int link, double eps, const double* q,
+                              int64_t B, double* r, double* jrow, double* jac, double* djac, cudaStream_t st);
 cudaError_t launch_term_joint(const TermJoint& T, int n, const double* qs, int64_t B, double* r, double* jd,
                               cudaStream_t st);
 cudaError_t launch_term_collision(const TreeParams& P, const LinkMap& L, const TermGeom& G, int kind,

@@ -419,7 +419,9 @@ def apply(a, p) -> np.ndarray:
 
 
 def interpolate(a: Transform3, b: Transform3, alpha: float) -> Transform3:
-    """a * exp(alpha * log(a^-1 b)): the constant-twist path from a to b."""
+    """a * exp(alpha * log(a^-1 b)): the constant-twist path from a to b (liegroups.py:490-494)."""
+    if not 0.0 <= alpha <= 1.0:
+        raise ValueError(f"interpolation parameter must be in [0, 1], got {alpha}")
     return a.compose(Transform3.exp(float(alpha) * a.inverse().compose(b).log()))
 
 

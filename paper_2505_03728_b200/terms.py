@@ -125,6 +125,27 @@ def collision_rows_batch(model, kind: str, q0, q1=None, world=None, eta: float =
     return tuple(out)
 
 
+def manipulability_batch(model, link: str, q, eps: float = 1e-6, jacobian: bool = True, derivative: bool = False):
+    """manipulability_cost rows (costs.py:349-401) at (B, n): r (B, 1), gradient rows (B, 1, n);
+    derivative=True also returns the translational Jacobian (B, 3, n) and dJ/dq (B, n, 3, n)."""
+    n = model.actuated_count
+    q = np.ascontiguousarray(np.asarray(q, dtype=float).reshape(-1, n))
+    b = q.shape[0]
+    qd = dv.to_dev(q)
+    r, jr = dv.empty((b, 1)), dv.empty((b, 1, n)) if jacobian else None
+    jac = dv.empty((b, 3, n)) if derivative else None
+    djac = dv.empty((b, n, 3, n)) if derivative else None
+    check(lib().kop_term_manipulability(model._handle, model.link_index(link), float(eps), dv.ptr(qd), b, dv.ptr(r),
+                                        dv.ptr(jr), dv.ptr(jac), dv.ptr(djac), dv.stream_handle()),
+          "kop_term_manipulability")
+    out = [r.cpu().numpy()]
+    if jacobian:
+        out.append(jr.cpu().numpy())
+    if derivative:
+        out += [jac.cpu().numpy(), djac.cpu().numpy()]
+    return tuple(out)
+
+
 def term_closures(kind: str, params: dict, nvars: int):
     """(evaluator(*values), jacobian(*values)) for one typed CostTerm, evaluated on the device
     at a single point -- the closures the reference's builders return."""
@@ -182,6 +203,14 @@ def term_closures(kind: str, params: dict, nvars: int):
         def jac(*values):
             out = collision_rows_batch(p["model"], kind, values[0], values[1] if len(values) > 1 else None, **kw)
             return [b[0] for b in out[1:]]
+        return ev, jac
+
+    if kind == "manipulability":
+        def ev(q):
+            return manipulability_batch(p["model"], p["link"], q, p["eps"], jacobian=False)[0][0]
+
+        def jac(q):
+            return [manipulability_batch(p["model"], p["link"], q, p["eps"])[1][0]]
         return ev, jac
 
     def unsupported(*values):

@@ -81,6 +81,13 @@ def main():
     record("self", ck.self_collision_cost(arm7, "q", eta=0.05), [(q,) for q in qs])
     record("swept", ck.swept_collision_cost(arm7, "a", "b", world, eta=0.08), list(zip(qs, q2)))
     record("world_hard", ck.world_collision_cost(arm7, "q", world, eta=0.3, hard_min=True), [(q,) for q in qs])
+    record("manip", ck.manipulability_cost(arm7, "q", "flange"), [(q,) for q in qs])
+    p2r = robot.load_robot(os.path.join(ROBOTS, "planar_2r.urdf"), os.path.join(ROBOTS, "planar_2r.sidecar.json"))
+    q2r = np.stack([p2r.sample_configuration(rng) for _ in range(N)])
+    g["q_p2r"] = q2r
+    record("manip_p2r", ck.manipulability_cost(p2r, "q", "ee"), [(q,) for q in q2r])
+    jd = [robot.translational_jacobian_with_derivative(arm7, q, "flange") for q in qs]
+    g["tjac"], g["tdjac"] = np.stack([a for a, _ in jd]), np.stack([b for _, b in jd])
     record("self_wide", ck.self_collision_cost(arm7, "q", eta=0.3), [(q,) for q in qs])
     record("self_hard", ck.self_collision_cost(arm7, "q", eta=0.3, hard_min=True), [(q,) for q in qs])
 
