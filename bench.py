@@ -928,9 +928,9 @@ def run_ours(args, rank, world, local_rank):
         "e2e": {"value": e2e_value, "unit": "solves/s", "h2d_bytes_per_step": int(h2d * world),
                 "d2h_bytes_per_step": int(d2h * world),
                 "api": "C ABI kop_ik_beam_host (IkBeamSolver.solve_host): pinned host targets -> all IkResult "
-                       "fields in pinned host memory; 65536-target chunks, H2D / kernels / D2H overlapped on 4 "
+                       "fields in pinned host memory; 16384-target chunks, H2D / kernels / D2H overlapped on 8 "
                        "library streams",
-                "launches_per_step": 3 * -(-B // 65536), "bitwise_equal_to_device_run": e2e_match,
+                "launches_per_step": 3 * -(-B // 16384), "bitwise_equal_to_device_run": e2e_match,
                 "pcie_h2d_gbs": h2d_gbs, "pcie_d2h_gbs": d2h_gbs,
                 "numpy_dropin": {"value": B / np_ms * 1e3, "unit": "solves/s", "wall_ms": np_ms,
                                  "api": "IkBeamSolver.solve(numpy (B,7)) -- the solve_ik_beam_batch path: pageable "

@@ -178,8 +178,8 @@ int kop_ik_beam_stage(const KopModel* model, int32_t link, const KopIkParams* pa
 /* replaces: tasks.solve_ik_beam over B targets with HOST arrays end to end
  * (the binding a NumPy caller uses, INTEGRATION.md seam 3b): targets host
  * [B*7], seeds host [S*n]; outputs host, shapes as kop_ik_beam (base_out,
- * history_out NULL ok).  The batch streams through `n_streams` (1..8, 0 = 4)
- * internal CUDA streams in chunks of `chunk` targets (0 = 65536), overlapping
+ * history_out NULL ok).  The batch streams through `n_streams` (1..8, 0 = 8)
+ * internal CUDA streams in chunks of `chunk` targets (0 = 16384), overlapping
  * host->device copies, kernels and device->host copies; pinned host memory
  * gives full overlap.  Enqueued behind `stream` and joined back into it:
  * host buffers must stay valid until `stream` completes.  Internal device

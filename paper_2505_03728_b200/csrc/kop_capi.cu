@@ -1745,8 +1745,10 @@ int kop_ik_beam_host(const KopModel* m, int32_t link, const KopIkParams* p, cons
     return fail(KOP_EINVAL, "null array argument");
   const int n = m->tree.n, hist_len = p->total_steps + 1;
   if (hist_len > 64 || n > 8) return fail(KOP_EUNSUPPORTED, "host pipeline compiled for <= 63 steps, <= 8 joints");
-  const int ns = n_streams ? n_streams : 4;
-  const int64_t ck = chunk ? (chunk < batch ? chunk : batch) : (batch < 65536 ? batch : 65536);
+  // defaults from a chunk x stream sweep at 1M targets (tools/e2e_host_sweep.py): 16K-target chunks over
+  // 8 streams overlap the small kernels' tails and the copies best (31.9M vs 30.5M solves/s at 64K x 4)
+  const int ns = n_streams ? n_streams : 8;
+  const int64_t ck = chunk ? (chunk < batch ? chunk : batch) : (batch < 16384 ? batch : 16384);
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return cuda_status(e);
