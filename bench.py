@@ -934,7 +934,8 @@ def run_ours(args, rank, world, local_rank):
                 "pcie_h2d_gbs": h2d_gbs, "pcie_d2h_gbs": d2h_gbs,
                 "numpy_dropin": {"value": B / np_ms * 1e3, "unit": "solves/s", "wall_ms": np_ms,
                                  "api": "IkBeamSolver.solve(numpy (B,7)) -- the solve_ik_beam_batch path: pageable "
-                                        "host arrays, output arrays allocated per call, host wall clock"}},
+                                        "host arrays (staged by the library through pinned buffers, copy-out "
+                                        "threads), output arrays allocated per call, host wall clock"}},
         "gpu_launches": 3 * args.steps,  # stage 1, stage 2, FP64 errors
         "roofline": {"bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                      "frac": achieved / peak, "traffic": traffic,

@@ -5,6 +5,8 @@
 #include <stdint.h>
 #include <string.h>
 
+#include <future>
+
 #include <string>
 #include <vector>
 
@@ -1686,17 +1688,26 @@ struct HostPipe {
   cudaStream_t st[8] = {};
   cudaEvent_t done[8] = {};
   void* buf[8] = {};
+  // pinned staging of one buffer set's host side (pageable callers), allocated on first use
+  void* stage[8] = {};
+  cudaEvent_t chunk_done[8] = {};
+  size_t stage_bytes = 0;
   double* seeds = nullptr;
   ~HostPipe() { release(); }
   void release() {
     for (int i = 0; i < 8; ++i) {
       if (buf[i]) cudaFree(buf[i]);
+      if (stage[i]) cudaFreeHost(stage[i]);
       if (st[i]) cudaStreamDestroy(st[i]);
       if (done[i]) cudaEventDestroy(done[i]);
+      if (chunk_done[i]) cudaEventDestroy(chunk_done[i]);
       buf[i] = nullptr;
+      stage[i] = nullptr;
       st[i] = nullptr;
       done[i] = nullptr;
+      chunk_done[i] = nullptr;
     }
+    stage_bytes = 0;
     if (seeds) cudaFree(seeds);
     seeds = nullptr;
     nstreams = 0;
@@ -1795,12 +1806,90 @@ int kop_ik_beam_host(const KopModel* m, int32_t link, const KopIkParams* p, cons
   cudaMemcpyAsync(P.seeds, seeds, sizeof(double) * seeds_len, cudaMemcpyHostToDevice, P.st[0]);
   cudaEventRecord(start, P.st[0]);
   for (int i = 1; i < ns; ++i) cudaStreamWaitEvent(P.st[i], start, 0);
+  // Pageable (not page-locked) host arrays -- the NumPy drop-in path: copies from pageable memory
+  // would serialise the pipeline, so each buffer set gets a pinned host staging area; this thread
+  // copies a chunk's targets into it before the H2D and the chunk's results out of it once its D2H
+  // completed (when the set comes round again), overlapping those CPU copies with the kernels and
+  // copies of the other sets.  The call then returns with the outputs written (synchronous).
+  auto pageable = [](const void* ptr) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+      cudaGetLastError();
+      return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+  };
+  const bool staged = pageable(targets) || pageable(q_out);
+  const ChunkLayout H = chunk_layout(P.chunk, 8, 64, 0);
+  if (staged && P.stage_bytes < H.total) {
+    for (int i = 0; i < P.nstreams; ++i) {
+      if (P.stage[i]) cudaFreeHost(P.stage[i]);
+      P.stage[i] = nullptr;
+    }
+    for (int i = 0; i < P.nstreams; ++i) {
+      if ((e = cudaHostAlloc(&P.stage[i], H.total, cudaHostAllocDefault)) != cudaSuccess ||
+          (!P.chunk_done[i] && (e = cudaEventCreateWithFlags(&P.chunk_done[i], cudaEventDisableTiming)) != cudaSuccess)) {
+        cudaEventDestroy(start);
+        return cuda_status(e);
+      }
+    }
+    P.stage_bytes = H.total;
+  }
+  // results of the chunk staged in set i -> the caller's arrays, on a helper thread per in-flight set
+  // (it waits for the chunk's D2H, then copies; first-touch page faults of fresh NumPy outputs make
+  // these copies the slow part, so several run at once, overlapped with the GPU work)
+  std::future<void> drains[8];
+  auto drain_async = [&](int i, int64_t lo, int64_t cnt) {
+    const char* h = static_cast<const char*>(P.stage[i]);
+    cudaEvent_t ev = P.chunk_done[i];
+    const bool with_base = base_out && p->optimize_base;
+    drains[i] = std::async(std::launch::async, [=]() {
+      cudaEventSynchronize(ev);
+      memcpy(q_out + lo * n, h + H.q, sizeof(double) * n * cnt);
+      if (with_base) memcpy(base_out + lo * 3, h + H.base, sizeof(double) * 3 * cnt);
+      memcpy(cost_out + lo, h + H.cost, sizeof(double) * cnt);
+      if (history_out) memcpy(history_out + lo * hist_len, h + H.hist, sizeof(double) * hist_len * cnt);
+      memcpy(pos_err + lo, h + H.pe, sizeof(double) * cnt);
+      memcpy(rot_err + lo, h + H.re, sizeof(double) * cnt);
+      memcpy(success + lo, h + H.ok, cnt);
+    });
+  };
+  auto drain = [&](int i) {  // set i's previous results copied out: its staging area is free again
+    if (drains[i].valid()) drains[i].get();
+  };
   int rc = KOP_OK;
   for (int64_t lo = 0, c = 0; lo < batch && rc == KOP_OK; lo += ck, ++c) {
     const int64_t cnt = (batch - lo) < ck ? (batch - lo) : ck;
     const int i = (int)(c % ns);
     cudaStream_t s = P.st[i];
     char* b = static_cast<char*>(P.buf[i]);
+    if (staged) {
+      drain(i);
+      char* h = static_cast<char*>(P.stage[i]);
+      memcpy(h + H.tg, targets + lo * 7, sizeof(double) * 7 * cnt);
+      double* dtg = reinterpret_cast<double*>(b + L.tg);
+      cudaMemcpyAsync(dtg, h + H.tg, sizeof(double) * 7 * cnt, cudaMemcpyHostToDevice, s);
+      rc = kop_ik_beam_stage(m, link, p, 3, dtg, cnt, P.seeds, b + L.ws, P.ws_bytes,
+                             reinterpret_cast<double*>(b + L.q),
+                             p->optimize_base ? reinterpret_cast<double*>(b + L.base) : nullptr,
+                             reinterpret_cast<double*>(b + L.cost),
+                             history_out ? reinterpret_cast<double*>(b + L.hist) : nullptr,
+                             reinterpret_cast<double*>(b + L.pe), reinterpret_cast<double*>(b + L.re),
+                             reinterpret_cast<uint8_t*>(b + L.ok), s);
+      if (rc != KOP_OK) break;
+      cudaMemcpyAsync(h + H.q, b + L.q, sizeof(double) * n * cnt, cudaMemcpyDeviceToHost, s);
+      if (base_out && p->optimize_base)
+        cudaMemcpyAsync(h + H.base, b + L.base, sizeof(double) * 3 * cnt, cudaMemcpyDeviceToHost, s);
+      cudaMemcpyAsync(h + H.cost, b + L.cost, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s);
+      if (history_out)
+        cudaMemcpyAsync(h + H.hist, b + L.hist, sizeof(double) * hist_len * cnt, cudaMemcpyDeviceToHost, s);
+      cudaMemcpyAsync(h + H.pe, b + L.pe, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s);
+      cudaMemcpyAsync(h + H.re, b + L.re, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s);
+      cudaMemcpyAsync(h + H.ok, b + L.ok, cnt, cudaMemcpyDeviceToHost, s);
+      cudaEventRecord(P.chunk_done[i], s);
+      drain_async(i, lo, cnt);
+      continue;
+    }
     double* dtg = reinterpret_cast<double*>(b + L.tg);
     double* dq = reinterpret_cast<double*>(b + L.q);
     double* dbase = reinterpret_cast<double*>(b + L.base);
@@ -1823,6 +1912,8 @@ int kop_ik_beam_host(const KopModel* m, int32_t link, const KopIkParams* p, cons
     cudaMemcpyAsync(rot_err + lo, dre, sizeof(double) * cnt, cudaMemcpyDeviceToHost, s);
     cudaMemcpyAsync(success + lo, dok, cnt, cudaMemcpyDeviceToHost, s);
   }
+  if (staged)
+    for (int i = 0; i < ns; ++i) drain(i);
   // join: the caller's stream waits for every pipeline stream
   for (int i = 0; i < ns; ++i) {
     cudaEventRecord(P.done[i], P.st[i]);
