@@ -46,8 +46,17 @@ def variant_lib(name: str) -> str:
 
 
 def build_variants(verbose: bool = False, force: bool = False) -> list:
-    """Build every checking variant (tests/test_gpu_checks.py)."""
-    return [build(verbose=verbose, force=force, variant=name) for name in VARIANTS]
+    """Build every checking variant (tests/test_gpu_checks.py), concurrently (separate object dirs)."""
+    with ThreadPoolExecutor(max_workers=len(VARIANTS)) as ex:
+        return list(ex.map(lambda name: build(verbose=verbose, force=force, variant=name), VARIANTS))
+
+
+def build_all(verbose: bool = False, force: bool = False) -> list:
+    """The library and every checking variant, all translation units compiling at once."""
+    with ThreadPoolExecutor(max_workers=1 + len(VARIANTS)) as ex:
+        jobs = [ex.submit(build, verbose, False, force)] + \
+               [ex.submit(build, verbose, False, force, name) for name in VARIANTS]
+        return [j.result() for j in jobs]
 
 
 def build(verbose: bool = False, ptxas_info: bool = False, force: bool = False, variant: str | None = None,
