@@ -29,6 +29,9 @@ from kinoptik import robot, solver  # noqa: E402
 from kinoptik.liegroups import Rotation3, Transform2, Transform3  # noqa: E402
 
 ROBOTS = os.path.join(REF, "kinoptik", "robots")
+# the humanoid fixture is this repository's own (config 3); the reference parses it
+HUMANOID = os.path.join(os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))),
+                        "paper_2505_03728_b200", "robots", "humanoid29.urdf")
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "reference_golden_terms.npz")
 
 
@@ -90,6 +93,45 @@ def main():
     g["tjac"], g["tdjac"] = np.stack([a for a, _ in jd]), np.stack([b for _, b in jd])
     record("self_wide", ck.self_collision_cost(arm7, "q", eta=0.3), [(q,) for q in qs])
     record("self_hard", ck.self_collision_cost(arm7, "q", eta=0.3, hard_min=True), [(q,) for q in qs])
+
+    # mimic + prismatic chain (arm7_gripper) and a tree (the humanoid fixture of this repo)
+    grip = robot.load_robot(os.path.join(ROBOTS, "arm7_gripper.urdf"))
+    qg = np.stack([grip.sample_configuration(rng) for _ in range(N)])
+    g["q_grip"] = qg
+    tg_grip = robot.link_transform(grip, grip.sample_configuration(rng), "finger_right")
+    g["target_grip"] = np.concatenate([tg_grip.rotation.wxyz, tg_grip.translation])
+    record("pose_grip", ck.pose_cost(grip, "q", "finger_right", tg_grip), [(q,) for q in qg])
+    record("manip_grip", ck.manipulability_cost(grip, "q", "finger_right"), [(q,) for q in qg])
+    hum = robot.load_robot(HUMANOID)
+    qh = np.stack([hum.sample_configuration(rng) for _ in range(N)])
+    g["q_hum"] = qh
+    tg_hum = robot.link_transform(hum, hum.sample_configuration(rng), "left_hand")
+    g["target_hum"] = np.concatenate([tg_hum.rotation.wxyz, tg_hum.translation])
+    bh = [Transform3(Rotation3.exp(rng.normal(size=3) * 0.3), rng.normal(size=3)) for _ in range(N)]
+    g["base_hum"] = np.array([np.concatenate([b.rotation.wxyz, b.translation]) for b in bh])
+    record("pose_hum_se3", ck.pose_cost(hum, "q", "left_hand", tg_hum, base_var="b"), list(zip(qh, bh)))
+    # humanoid IK with a planar floating base: 4 end-effector poses, SE(2) base, limit + rest (reference solve)
+    hh, hq, hb, hit, htg = [], [], [], [], []
+    ees = ["left_hand", "right_hand", "left_foot", "right_foot"]
+    for i in range(3):
+        qt = hum.sample_configuration(rng)
+        bt = Transform2(rng.uniform(-0.5, 0.5), rng.normal(size=2) * 0.3).to_transform3()
+        tgts = [bt.compose(robot.link_transform(hum, qt, e)) for e in ees]
+        vs = solver.VariableSet.of(q=hum.rest_pose.copy(), b=Transform2.identity())
+        prob = solver.Problem(vs, [ck.pose_cost(hum, "q", e, t, base_var="b", position_weight=50,
+                                                orientation_weight=10) for e, t in zip(ees, tgts)]
+                              + [ck.limit_cost(hum, "q", weight=100), ck.rest_cost("q", hum.rest_pose, weight=0.01)])
+        rep = solver.solve(prob, solver.SolveOptions(max_iterations=40))
+        h = np.full(41, np.nan)
+        h[:len(rep.cost_history)] = rep.cost_history
+        hh.append(h)
+        hq.append(rep.final_values.value("q"))
+        b = rep.final_values.value("b")
+        hb.append([b.angle, *b.translation])
+        hit.append(rep.iterations_run)
+        htg.append(np.stack([np.concatenate([t.rotation.wxyz, t.translation]) for t in tgts]))
+    g["hum_base_targets"], g["hum_base_hist"], g["hum_base_q"] = np.array(htg), np.array(hh), np.array(hq)
+    g["hum_base_b"], g["hum_base_iters"] = np.array(hb), np.array(hit)
 
     # solver.assemble on a mixed two-variable problem (pose with SE(2) base + limit + rest)
     vs = solver.VariableSet.of(q=qs[0].copy(), b=b2[0])
