@@ -767,35 +767,48 @@ __device__ __forceinline__ void traj_bottom_schur(const BandView<G, true>& V, in
   }
 }
 
-// Back substitution L^T x = z over view blocks hi..lo by one warp: lane 0
+// Back substitution L^T x = z over view blocks hi..lo by one warp.  Every lane
 // solves the block's triangular system in registers (blocks >= known already
-// hold x), lanes < BW remove its contribution from the rows above.
+// hold x; lane 0 stores the solution), so x needs no broadcast, and lanes < BW
+// remove its contribution from the rows above.  All of a block's loads (its
+// right-hand sides, factor entries and this lane's row-update entries) are
+// issued together at the top of the block, so the serial chain sees one
+// shared-memory latency per block.  Same operations in the same order as a
+// one-lane solve.
 template <class G, class V_>
 __device__ __forceinline__ void traj_back(const V_& V, int hi, int lo, int known) {
   using T = typename G::T;
   constexpr int NQ = G::NQ, BW = 4 * NQ;
   const int lane = threadIdx.x & 31;
   for (int jb = hi; jb >= lo; --jb) {
-    const int c0 = jb * NQ;
-    if (lane == 0 && jb < known) {
-      T x[NQ];
+    const int c0 = jb * NQ, c = c0 - 1 - lane;
+    const bool upd = lane < BW && c >= 0 && (jb < known || c < known * NQ);  // solved rows of a known block stay
+    T x[NQ], lu[NQ];
+#pragma unroll
+    for (int b = 0; b < NQ; ++b) {
+      x[b] = V.yv(c0 + b);
+      const bool in = upd && c0 + b - c <= BW;
+      const T v = V.l(c0 + b, in ? c0 + b - c : 0);  // clamped: a valid entry, dropped
+      lu[b] = in ? v : T(0);
+    }
+    if (jb < known) {
 #pragma unroll
       for (int bb = 0; bb < NQ; ++bb) {
         const int b = NQ - 1 - bb;
-        T v = V.yv(c0 + b);
+        T v = x[b];
 #pragma unroll
         for (int m = NQ - 1; m > b; --m) v -= V.l(c0 + m, m - b) * x[m];  // newest x last
         x[b] = v * V.dv(c0 + b);
-        V.yv(c0 + b) = x[b];
       }
+      if (lane == 0)
+#pragma unroll
+        for (int b = 0; b < NQ; ++b) V.yv(c0 + b) = x[b];
     }
-    __syncwarp();
-    const int c = c0 - 1 - lane;
-    if (lane < BW && c >= 0 && (jb < known || c < known * NQ)) {  // solved rows of a known block stay
+    if (upd) {
       T acc = T(0);
 #pragma unroll
       for (int b = 0; b < NQ; ++b)
-        if (c0 + b - c <= BW) acc += V.l(c0 + b, c0 + b - c) * V.yv(c0 + b);
+        if (c0 + b - c <= BW) acc += lu[b] * x[b];
       V.yv(c) -= acc;
     }
     __syncwarp();
