@@ -40,7 +40,10 @@ struct TreeScratch {
   union {
     struct {
       T wf[kTreeMaxJoints][7];  // world frame after each joint's motion (wxyz, xyz)
-      T J[6 * NE][32];
+      union {
+        T fb[kTreeMaxJoints][7];  // FK ping-pong buffer (tree_eval)
+        T J[6 * NE][32];
+      };
     };
     T L[32 * 33];
   };
@@ -56,6 +59,7 @@ struct TreeTable {
   int32_t parent[kTreeMaxJoints], kind[kTreeMaxJoints], qcol[kTreeMaxJoints];
   int32_t col_nj[kTreeMaxDofs];
   int8_t lev_joint[kTreeMaxJoints];
+  int8_t anc[6][kTreeMaxJoints];  // ancestor joint 2^r levels up (-1: past the root)
   int8_t col_joint[kTreeMaxDofs][kTreeMaxPerCol];
 };
 
@@ -73,6 +77,11 @@ __device__ __forceinline__ void stage_tree_table(const TreeLmParams<T>& P, TreeT
     Q.kind[j] = P.kind[j];
     Q.qcol[j] = P.qcol[j];
     Q.lev_joint[j] = P.lev_joint[j];
+    int a = j;
+    for (int r = 0; r < 6; ++r) {  // a: 2^(r-1) levels up -> 2^r levels up
+      for (int st = 0; st < (r ? 1 << (r - 1) : 1) && a >= 0; ++st) a = P.parent_joint[a];
+      Q.anc[r][j] = (int8_t)a;
+    }
   }
   for (int c = threadIdx.x; c < P.n; c += blockDim.x) {
     Q.lower[c] = P.lower[c];
@@ -138,6 +147,86 @@ __device__ __forceinline__ T tree_eval(const TreeLmParams<T>& P, const TreeTable
   quat<T> bq;
   vec3<T> bp;
   base_frame(P.base_kind, base, bq, bp);
+#ifndef KOP_TREE_FK_LEVELS
+  // ---- FK by pointer jumping over the tree: world frame after every joint ------
+  // after(j) = after(parent) * O_j * Mot_j (robot.py:404-448).  Every joint's
+  // local transform X_j = O_j Mot_j at once (lanes j, j + 32); round r then
+  // composes each partial product with the one 2^r levels up the tree, so
+  // after ceil(log2(depth)) rounds joint j holds root -> after(j): log2(depth)
+  // warp-wide rounds instead of depth-many levels of a few lanes each.  (The
+  // products associate differently from a root-to-leaf walk: rounding only.)
+  {
+    const int nj = P.nj;
+    const int R = P.nlev > 1 ? 32 - __clz(P.nlev - 1) : 0;
+    T* const fbuf[2] = {&S.wf[0][0], &S.fb[0][0]};
+    int cur = R & 1;  // the last round writes wf
+    for (int j = lane; j < nj; j += 32) {
+      const quat<T> oq{Q.oq[j][0], Q.oq[j][1], Q.oq[j][2], Q.oq[j][3]};
+      quat<T> xq = oq;
+      vec3<T> xp{Q.op[j][0], Q.op[j][1], Q.op[j][2]};
+      if (Q.kind[j] != 0) {
+        const vec3<T> ax{Q.axis[j][0], Q.axis[j][1], Q.axis[j][2]};
+        const T th = q[Q.qcol[j]] * Q.mult[j] + Q.offset[j];
+        if (Q.kind[j] == 1) {
+          T sn, cs;
+          sincos_t(T(0.5) * th, &sn, &cs);
+          xq = qmul(oq, quat<T>{cs, sn * ax.x, sn * ax.y, sn * ax.z});
+        } else {
+          const vec3<T> t = qrot(oq, ax);
+          xp = {xp.x + th * t.x, xp.y + th * t.y, xp.z + th * t.z};
+        }
+      }
+      T* d = fbuf[cur] + 7 * j;
+      d[0] = xq.w; d[1] = xq.x; d[2] = xq.y; d[3] = xq.z;
+      d[4] = xp.x; d[5] = xp.y; d[6] = xp.z;
+    }
+    __syncwarp();
+    for (int r = 0; r < R; ++r) {
+      const T* src = fbuf[cur];
+      T* dst = fbuf[cur ^ 1];
+      for (int j = lane; j < nj; j += 32) {
+        const T* o = src + 7 * j;
+        quat<T> wq{o[0], o[1], o[2], o[3]};
+        vec3<T> wp{o[4], o[5], o[6]};
+        const int a = Q.anc[r][j];
+        if (a >= 0) {  // (A_a) o (A_j)
+          const T* u = src + 7 * a;
+          const quat<T> uq{u[0], u[1], u[2], u[3]};
+          const vec3<T> t = qrot(uq, wp);
+          wp = {u[4] + t.x, u[5] + t.y, u[6] + t.z};
+          wq = qmul(uq, wq);
+        }
+        T* d = dst + 7 * j;
+        d[0] = wq.w; d[1] = wq.x; d[2] = wq.y; d[3] = wq.z;
+        d[4] = wp.x; d[5] = wp.y; d[6] = wp.z;
+      }
+      cur ^= 1;
+      __syncwarp();
+    }
+    // the base pose, then the Pluecker axis (a, m = a x o) of each moving joint:
+    // its axis is invariant under its own motion and a x (th a) = 0, so both come
+    // from the frame after the motion
+    for (int j = lane; j < nj; j += 32) {
+      T* w = &S.wf[j][0];
+      quat<T> wq{w[0], w[1], w[2], w[3]};
+      vec3<T> wp{w[4], w[5], w[6]};
+      if (P.base_kind != 0) {
+        const vec3<T> t = qrot(bq, wp);
+        wp = {bp.x + t.x, bp.y + t.y, bp.z + t.z};
+        wq = qmul(bq, wq);
+        w[0] = wq.w; w[1] = wq.x; w[2] = wq.y; w[3] = wq.z;
+        w[4] = wp.x; w[5] = wp.y; w[6] = wp.z;
+      }
+      if (JAC && Q.kind[j] != 0) {
+        const vec3<T> a = qrot(wq, vec3<T>{Q.axis[j][0], Q.axis[j][1], Q.axis[j][2]});
+        const vec3<T> m = cross(a, wp);
+        S.am[j][0] = a.x; S.am[j][1] = a.y; S.am[j][2] = a.z;
+        S.am[j][3] = m.x; S.am[j][4] = m.y; S.am[j][5] = m.z;
+      }
+    }
+    __syncwarp();
+  }
+#else
   // ---- FK, level by level: world frame after every joint, Pluecker axes -------
   // after(j) = after(parent) * O_j * Mot_j (robot.py:404-448 composition)
   for (int d = 0; d < P.nlev; ++d) {
@@ -174,6 +263,7 @@ __device__ __forceinline__ T tree_eval(const TreeLmParams<T>& P, const TreeTable
     }
     __syncwarp();
   }
+#endif
   // ---- EE frames, pose residuals, Jr^-1 blocks ----------------------------------
   T cost_part = T(0);
   if (lane < ne) {
