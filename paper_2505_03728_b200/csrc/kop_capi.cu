@@ -1107,31 +1107,86 @@ int kop_lm_solve(const KopModel* m, int32_t link, const KopCollisionCosts* cc, c
 
 namespace {
 
+// double-precision pose (wxyz, xyz) composition a o b
+struct HostPose {
+  double q[4] = {1, 0, 0, 0}, p[3] = {0, 0, 0};
+};
+HostPose host_compose(const HostPose& a, const HostPose& b) {
+  HostPose r;
+  const double *x = a.q, *y = b.q;
+  r.q[0] = x[0] * y[0] - x[1] * y[1] - x[2] * y[2] - x[3] * y[3];
+  r.q[1] = x[0] * y[1] + x[1] * y[0] + x[2] * y[3] - x[3] * y[2];
+  r.q[2] = x[0] * y[2] - x[1] * y[3] + x[2] * y[0] + x[3] * y[1];
+  r.q[3] = x[0] * y[3] + x[1] * y[2] - x[2] * y[1] + x[3] * y[0];
+  // p_a + R(q_a) p_b
+  const double w = x[0], vx = x[1], vy = x[2], vz = x[3], *v = b.p;
+  const double tx = 2 * (vy * v[2] - vz * v[1]), ty = 2 * (vz * v[0] - vx * v[2]), tz = 2 * (vx * v[1] - vy * v[0]);
+  r.p[0] = a.p[0] + v[0] + w * tx + (vy * tz - vz * ty);
+  r.p[1] = a.p[1] + v[1] + w * ty + (vz * tx - vx * tz);
+  r.p[2] = a.p[2] + v[2] + w * tz + (vx * ty - vy * tx);
+  return r;
+}
+
+// Kernel view of the tree.  fold: fixed joints are folded into their children's
+// origin transforms (and into the end-effector offsets) in double, so the
+// kernel's FK runs over the moving joints only -- the humanoid's 34 joints
+// become 29, one warp pass; the composed transforms are exact up to the final
+// rounding.  Unfolded (fold = false) for the FP64 pose errors, which follow
+// the reference's joint-by-joint walk.
 template <typename T>
-TreeLmParams<T> tree_params(const KopModel& m, const KopPoseCosts* pc) {
+TreeLmParams<T> tree_params(const KopModel& m, const KopPoseCosts* pc, bool fold = true) {
   TreeLmParams<T> P;
   memset(&P, 0, sizeof(P));
   const TreeParams& t = m.tree;
-  P.nj = t.nj;
+  const int nj0 = t.nj;
+  std::vector<int> pj(nj0), nid(nj0, -1), eff(nj0, -1);
+  std::vector<HostPose> acc(nj0);  // fixed joint j: after(j) = after(eff[j]) o acc[j]
+  int nj = 0;
+  for (int j = 0; j < nj0; ++j) {
+    pj[j] = m.parent_joint[t.parent[j]];
+    HostPose o;
+    for (int i = 0; i < 4; ++i) o.q[i] = t.oq[j][i];
+    for (int i = 0; i < 3; ++i) o.p[i] = t.op[j][i];
+    const bool pfix = fold && pj[j] >= 0 && nid[pj[j]] < 0;  // parent folded away
+    const HostPose pre = pfix ? acc[pj[j]] : HostPose();
+    const int par = pj[j] < 0 ? -1 : (pfix ? eff[pj[j]] : pj[j]);
+    if (fold && t.kind[j] == 0) {
+      eff[j] = par;
+      acc[j] = pfix ? host_compose(pre, o) : o;
+      continue;
+    }
+    const int k = nj++;
+    nid[j] = k;
+    const HostPose oj = pfix ? host_compose(pre, o) : o;
+    P.parent_joint[k] = par < 0 ? -1 : nid[par];
+    P.kind[k] = t.kind[j];
+    P.qcol[k] = t.qcol[j];
+    for (int i = 0; i < 4; ++i) P.oq[k][i] = T(oj.q[i]);
+    for (int i = 0; i < 3; ++i) {
+      P.op[k][i] = T(oj.p[i]);
+      P.axis[k][i] = T(t.axis[j][i]);
+    }
+    P.mult[k] = T(t.mult[j]);
+    P.offset[k] = T(t.offset[j]);
+  }
+  P.nj = nj;
   P.n = t.n;
   P.ne = pc->num_poses;
-  for (int j = 0; j < t.nj; ++j) {
-    P.parent_joint[j] = m.parent_joint[t.parent[j]];
-    P.kind[j] = t.kind[j];
-    P.qcol[j] = t.qcol[j];
-    for (int i = 0; i < 4; ++i) P.oq[j][i] = T(t.oq[j][i]);
-    for (int i = 0; i < 3; ++i) {
-      P.op[j][i] = T(t.op[j][i]);
-      P.axis[j][i] = T(t.axis[j][i]);
-    }
-    P.mult[j] = T(t.mult[j]);
-    P.offset[j] = T(t.offset[j]);
-  }
   for (int e = 0; e < pc->num_poses; ++e) {
-    const int link = pc->links[e];
-    P.ee_joint[e] = m.parent_joint[link];
+    const int ej = m.parent_joint[pc->links[e]];
+    HostPose off;
+    int k = -1;
+    if (ej >= 0 && nid[ej] >= 0) {
+      k = nid[ej];
+    } else if (ej >= 0) {
+      k = eff[ej] < 0 ? -1 : nid[eff[ej]];
+      off = acc[ej];
+    }
+    P.ee_joint[e] = k;
+    for (int i = 0; i < 4; ++i) P.ee_oq[e][i] = T(off.q[i]);
+    for (int i = 0; i < 3; ++i) P.ee_op[e][i] = T(off.p[i]);
     unsigned long long mask = 0;
-    for (int j = m.parent_joint[link]; j >= 0; j = m.parent_joint[t.parent[j]]) mask |= 1ull << j;
+    for (int a = k; a >= 0; a = P.parent_joint[a]) mask |= 1ull << a;
     P.anc_ee[e] = mask;
     P.w_pos[e] = T(pc->w_position[e]);
     P.w_ori[e] = T(pc->w_orientation[e]);
@@ -1144,24 +1199,24 @@ TreeLmParams<T> tree_params(const KopModel& m, const KopPoseCosts* pc) {
   P.w_lim = T(pc->w_limit);
   P.w_rest = T(pc->w_rest);
   // depth levels (joint order is topological: parents come first, robot.py:325-340)
-  std::vector<int> depth(t.nj, 0);
+  std::vector<int> depth(nj, 0);
   int maxd = 0;
-  for (int j = 0; j < t.nj; ++j) {
-    const int pj = P.parent_joint[j];
-    depth[j] = pj >= 0 ? depth[pj] + 1 : 0;
+  for (int j = 0; j < nj; ++j) {
+    const int p = P.parent_joint[j];
+    depth[j] = p >= 0 ? depth[p] + 1 : 0;
     if (depth[j] > maxd) maxd = depth[j];
   }
-  P.nlev = t.nj ? maxd + 1 : 0;
+  P.nlev = nj ? maxd + 1 : 0;
   int at = 0;
   for (int d = 0; d < P.nlev; ++d) {
     P.lev_start[d] = at;
-    for (int j = 0; j < t.nj; ++j)
+    for (int j = 0; j < nj; ++j)
       if (depth[j] == d) P.lev_joint[at++] = (int8_t)j;
   }
   P.lev_start[P.nlev] = at;
-  for (int j = 0; j < t.nj; ++j) {
-    if (t.kind[j] == 0 || t.qcol[j] < 0) continue;
-    const int c = t.qcol[j];
+  for (int j = 0; j < nj; ++j) {
+    if (P.kind[j] == 0 || P.qcol[j] < 0) continue;
+    const int c = P.qcol[j];
     P.col_joint[c][P.col_nj[c]++] = (int8_t)j;  // bounded by tree_params_ok
   }
   return P;
@@ -1498,9 +1553,9 @@ int kop_multi_pose_beam(const KopModel* m, const KopPoseCosts* pc, const KopIkPa
   L.rot_err = rot_err;
   L.success = success;
   cudaStream_t st = (cudaStream_t)stream;
-  const TreeLmParams<double> Pd = tree_params<double>(*m, pc);
+  const TreeLmParams<double> Pd = tree_params<double>(*m, pc, false);  // FP64 pose errors: the joint-by-joint walk
   const cudaError_t e = p->precision == KOP_FP32 ? launch_tree_beam<float>(tree_params<float>(*m, pc), Pd, L, st)
-                                                 : launch_tree_beam<double>(Pd, Pd, L, st);
+                                                 : launch_tree_beam<double>(tree_params<double>(*m, pc), Pd, L, st);
   return cuda_status(e);
 }
 

@@ -274,6 +274,11 @@ __device__ __forceinline__ T tree_eval(const TreeLmParams<T>& P, const TreeTable
       wq = {S.wf[ej][0], S.wf[ej][1], S.wf[ej][2], S.wf[ej][3]};
       wp = {S.wf[ej][4], S.wf[ej][5], S.wf[ej][6]};
     }
+    {  // folded fixed joints between that frame and the link (identity: exact no-op)
+      const vec3<T> t = qrot(wq, vec3<T>{P.ee_op[lane][0], P.ee_op[lane][1], P.ee_op[lane][2]});
+      wp = {wp.x + t.x, wp.y + t.y, wp.z + t.z};
+      wq = qmul(wq, quat<T>{P.ee_oq[lane][0], P.ee_oq[lane][1], P.ee_oq[lane][2], P.ee_oq[lane][3]});
+    }
     const double* tp = targets + 7 * lane;
     const TargetInv<T> tg = target_inverse_t<T>(tp);
     const quat<T> e_q = qmul(tg.q, wq);

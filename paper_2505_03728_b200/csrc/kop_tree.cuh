@@ -21,6 +21,7 @@ struct TreeLmParams {
   T oq[kTreeMaxJoints][4], op[kTreeMaxJoints][3], axis[kTreeMaxJoints][3];
   T mult[kTreeMaxJoints], offset[kTreeMaxJoints];
   int32_t ee_joint[kTreeMaxPoses];          // joint owning each end-effector link (-1: root)
+  T ee_oq[kTreeMaxPoses][4], ee_op[kTreeMaxPoses][3];  // fixed offset of the link from that joint's frame
   unsigned long long anc_ee[kTreeMaxPoses]; // ancestor-joint mask of each end effector
   T w_pos[kTreeMaxPoses], w_ori[kTreeMaxPoses];
   T lower[kTreeMaxDofs], upper[kTreeMaxDofs], rest[kTreeMaxDofs];
