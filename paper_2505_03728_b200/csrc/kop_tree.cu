@@ -6,14 +6,14 @@
 //
 // Warp mapping (a problem is too large for one thread's registers -- a 24x29
 // Jacobian, a 29x29 normal matrix):
-//   * FK:  level-synchronous over the tree depth: the lanes take the joints of
-//         one level, compose after(parent) * O_j * Mot_j from shared memory and
-//         leave the Pluecker axis (a, m = a x o) of each moving joint; lanes
-//         e < E read the end-effector frames, then form the pose residual
-//         xi_e and the weighted Jr^-1(xi_e) blocks.
+//   * FK:  every joint's local transform at once, then log2(depth) pointer-
+//         jumping composition rounds over the tree (fixed joints folded into
+//         their children on the host), the Pluecker axis (a, m = a x o) of
+//         each moving joint; lanes e < E read the end-effector frames, then
+//         form the pose residual xi_e and the weighted Jr^-1(xi_e) blocks.
 //   * J:   lane c owns Jacobian column c (its joint(s) via qcol), 6E entries
 //         in registers, mirrored to shared memory.
-//   * A:   lane i forms row i of J^T J from its own column and broadcast reads.
+//   * A:   lane i forms row i of J^T J (its lower part) from its own column and broadcast reads.
 //   * LM:  right-looking Cholesky of A + lam D with lane i holding row i of L
 //         in registers (pivot columns travel by shuffles), triangular solves
 //         as warp-wide axpys, the rejection loop and terminations of
@@ -27,22 +27,30 @@
 namespace kop {
 
 // Per-warp shared memory for NE end-effector slots (ne <= NE; the unused
-// slots are zero).  The FK frames and the Jacobian mirror live only inside an
-// evaluation, L only inside a solve, so they share storage.
+// slots are zero).  The FK frames, Pluecker axes and the Jacobian mirror live
+// only inside an evaluation (in that order, each pair overlapping once the
+// first is dead), L only inside a solve, so they share storage.
+// A(i, j), i >= j: column j holds rows j .. 31 (lane i reads column j at
+// consecutive addresses: conflict-free)
+constexpr int kTreePacked = 32 * 33 / 2;
+__host__ __device__ constexpr int tree_pa(int i, int j) { return j * 32 - j * (j - 1) / 2 + (i - j); }
 template <typename T, int NE>
 struct TreeScratch {
   T q[32], qn[32];
   T bs[8], bn[8];            // base variable: current / candidate (SE(2): angle, x, y; SE(3): wxyz, xyz)
   T cb[2][32];               // Cholesky pivot column, double-buffered (16-byte aligned rows)
-  T am[kTreeMaxJoints][6];   // Pluecker axis of each moving tree joint
+  T dg[32];                  // undamped diagonal of A (A's diagonal holds the damped one during a solve)
   T ee[NE][48];              // per EE: r[6], R^T[9], p[3], At[9], Bt[9], Ab[9]
-  T A[32 * 33];
+  T A[kTreePacked];          // lower triangle of J^T J, packed by columns (tree_pa)
   union {
     struct {
-      T wf[kTreeMaxJoints][7];  // world frame after each joint's motion (wxyz, xyz)
       union {
-        T fb[kTreeMaxJoints][7];  // FK ping-pong buffer (tree_eval)
-        T J[6 * NE][32];
+        T fb[kTreeMaxJoints][7];  // FK ping-pong buffer, then
+        T am[kTreeMaxJoints][6];  // the Pluecker axis of each moving tree joint
+      };
+      union {
+        T wf[kTreeMaxJoints][7];  // world frame after each joint's motion (wxyz, xyz), then
+        T J[6 * NE][32];          // the Jacobian (formed after the end-effector frames are read)
       };
     };
     T L[32 * 33];
@@ -120,7 +128,7 @@ __device__ __forceinline__ void ld4(const double* p, double (&v)[4]) {
 }
 
 // Evaluate the stack at S.q (or S.qn when cand): returns the cost (all lanes);
-// JAC also forms A (S.A, stride 33) and g (register, lane i = g_i).
+// JAC also forms A (S.A, packed lower triangle) and g (register, lane i = g_i).
 // root frame of the tree: the base variable's pose (Transform2.to_transform3 for
 // SE(2), liegroups.py:450-454) or the identity
 template <typename T>
@@ -388,9 +396,11 @@ __device__ __forceinline__ T tree_eval(const TreeLmParams<T>& P, const TreeTable
         for (int t = 0; t < 4; ++t) a[t] += col[m] * v[t];
       }
 #pragma unroll
-      for (int t = 0; t < 4; ++t) S.A[(j4 + t) * 33 + lane] = a[t];  // rows >= n: zero, unread
+      for (int t = 0; t < 4; ++t)
+        if (j4 + t <= lane) S.A[tree_pa(lane, j4 + t)] = a[t];  // rows >= n: zero, unread
     }
-    if (lane < n) S.A[lane * 33 + lane] += gl * gl + P.w_rest * P.w_rest;
+    if (lane < n) S.A[tree_pa(lane, lane)] += gl * gl + P.w_rest * P.w_rest;
+    S.dg[lane] = S.A[tree_pa(lane, lane)];
 #pragma unroll
     for (int m = 0; m < 6 * NE; ++m) g += col[m] * S.ee[m / 6][m % 6];
     g += gl * rl + P.w_rest * rr;  // zero on base lanes
@@ -409,12 +419,11 @@ __device__ __forceinline__ bool tree_damped_solve(const TreeLmParams<T>& P, Tree
   // back as vector broadcasts.  Lanes update their whole row: the entries
   // right of the diagonal are never read, so no per-entry lane test.
   const int n = P.n + base_dim(P.base_kind);  // the tangent: actuated columns, then the base's
-  T row[kTreeMaxDofs];
+  if (lane < n) S.A[tree_pa(lane, lane)] = S.dg[lane] + lam * tmax(S.dg[lane], T(BeamConsts::diag_clamp));
+  __syncwarp();
+  T row[kTreeMaxDofs];  // entries right of the diagonal start at zero (never read)
 #pragma unroll
-  for (int j = 0; j < kTreeMaxDofs; ++j) {
-    row[j] = (lane < n && j < n) ? S.A[j * 33 + lane] : T(0);
-    if (j == lane) row[j] += lam * tmax(row[j], T(BeamConsts::diag_clamp));
-  }
+  for (int j = 0; j < kTreeMaxDofs; ++j) row[j] = (lane < n && j < n && j <= lane) ? S.A[tree_pa(lane, j)] : T(0);
   bool ok = true;
   T dinv_mine = T(0);
 #pragma unroll
@@ -575,7 +584,7 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
     bool accepted = false;
     T step = T(0);
     // diag of J^T J at the iterate (lane i), for the FP32 rule's model decrease
-    const T dg = lane < nd ? tmax(S.A[lane * 33 + lane], T(BeamConsts::diag_clamp)) : T(0);
+    const T dg = lane < nd ? tmax(S.dg[lane], T(BeamConsts::diag_clamp)) : T(0);
     for (int rj = 0; rj < O.max_rejections; ++rj) {
       T d;
       bool ok = tree_damped_solve(P, S, g, damping, lane, d);
