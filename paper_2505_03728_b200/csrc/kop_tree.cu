@@ -476,16 +476,24 @@ __device__ __forceinline__ bool tree_damped_solve(const TreeLmParams<T>& P, Tree
 
 // warps per CTA: FP32 runs one-warp CTAs (a finished problem frees its slot at
 // once); FP64 keeps four (measured faster: register-limited residency)
+#ifndef KOP_TREE_WARPS32
+#define KOP_TREE_WARPS32 1
+#endif
+#ifndef KOP_TREE_WARPS64
+#define KOP_TREE_WARPS64 4
+#endif
 template <typename T>
-constexpr int tree_warps() { return sizeof(T) == 4 ? 1 : 4; }
+constexpr int tree_warps() { return sizeof(T) == 4 ? KOP_TREE_WARPS32 : KOP_TREE_WARPS64; }
 
 // IK-Beam stage 1 runs a fixed step count (no early exit), so its warps finish
-// together and share one staged table per CTA
+// together and share one staged table per CTA: 8 warps (FP32) / 6 (FP64) per
+// CTA fill the SM's shared memory with 24 / 12 resident warps (measured +10% /
+// +7% over 4-warp CTAs at 100K humanoid targets)
 #ifndef KOP_TREE_BEAM_WARPS32
-#define KOP_TREE_BEAM_WARPS32 4
+#define KOP_TREE_BEAM_WARPS32 8
 #endif
 #ifndef KOP_TREE_BEAM_WARPS64
-#define KOP_TREE_BEAM_WARPS64 4
+#define KOP_TREE_BEAM_WARPS64 6
 #endif
 template <typename T>
 constexpr int tree_beam_warps() { return sizeof(T) == 4 ? KOP_TREE_BEAM_WARPS32 : KOP_TREE_BEAM_WARPS64; }
