@@ -559,6 +559,7 @@ def run_configs(torch, k, model, flush, peaks, nominals, cpu=True):
 
     out = {}
     finals = {}
+    legs = []  # CPU legs run after every device timing: forked pools perturb the host enqueue of the timed calls
     demo = k.WorldModel([k.Sphere([0.45, 0.1, 0.55], 0.12), k.Capsule([-0.5, -0.4, 0.2], [-0.5, 0.4, 0.6], 0.1),
                          k.HalfSpace([0.0, 0.0, 1.0], -0.3)])
     hum = k.load_robot(k.robot_path("humanoid29.urdf"))
@@ -600,7 +601,7 @@ def run_configs(torch, k, model, flush, peaks, nominals, cpu=True):
                                      dominant_frac=(c4_s1 * B4 / (share * ms * 1e-3) / 1e12 / peaks[prec])
                                      if share else None)}
     if cpu:
-        c4["cpu_baseline"] = cpu_leg("col_beam", list(tg4[:64].cpu().numpy()), "solves/s", "targets")
+        legs.append((c4, ("col_beam", list(tg4[:64].cpu().numpy()), "solves/s", "targets")))
     out["config4_collision_ik_beam"] = c4
 
     # ---- config 4, solver.solve flavour: the generic LM (k_col_solve) on the same stack ----
@@ -620,15 +621,17 @@ def run_configs(torch, k, model, flush, peaks, nominals, cpu=True):
         def run_lm():
             check(lib().kop_lm_solve(model._handle, 8, C.byref(p.costs), C.byref(opts), dv.ptr(tg4), dv.ptr(q0), B4,
                                      *(dv.ptr(x) for x in outs), dv.stream_handle()), "kop_lm_solve")
-        ms = float(np.median(device_time(torch, run_lm, 3, flush)))
+        reps = device_time(torch, run_lm, 5, flush)
+        ms = float(np.median(reps))
         it = float(outs[4].float().mean())
         finals[("c4", prec)] = outs[1].cpu().numpy()
-        c4lm[prec] = {"ms": ms, "value": B4 / ms * 1e3, "unit": "solves/s", "mean_iterations": it,
+        c4lm[prec] = {"ms": ms, "rep_ms": [round(x, 3) for x in reps], "value": B4 / ms * 1e3, "unit": "solves/s",
+                      "mean_iterations": it,
                       "terminations": torch.bincount(outs[5].long(), minlength=7).tolist(),
                       "roofline": roof(lm_iter * it, B4 / ms * 1e3, peaks[prec], nominals[prec],
                                        "k_col_solve (single kernel): accepted iterations x lane-step constant")}
     if cpu:
-        c4lm["cpu_baseline"] = cpu_leg("col_lm", list(tg4[:64].cpu().numpy()), "solves/s", "problems")
+        legs.append((c4lm, ("col_lm", list(tg4[:64].cpu().numpy()), "solves/s", "problems")))
     c4lm["fp32_vs_fp64_final_cost"] = final_cost_agreement(finals[("c4", "fp32")], finals[("c4", "fp64")])
     out["config4_generic_lm"] = c4lm
 
@@ -660,7 +663,7 @@ def run_configs(torch, k, model, flush, peaks, nominals, cpu=True):
                                      dominant_frac=(c3_s1 * B3 / (share * ms * 1e-3) / 1e12 / peaks[prec])
                                      if share else None)}
     if cpu:
-        c3["cpu_baseline"] = cpu_leg("tree_beam", list(tgh[:64].cpu().numpy()), "solves/s", "target sets")
+        legs.append((c3, ("tree_beam", list(tgh[:64].cpu().numpy()), "solves/s", "target sets")))
     out["config3_humanoid_ik_beam"] = c3
 
     w0 = k.CostWeights()
@@ -689,7 +692,7 @@ def run_configs(torch, k, model, flush, peaks, nominals, cpu=True):
                       "roofline": roof(c3_step * it, B3 / ms * 1e3, peaks[prec], nominals[prec],
                                        "k_tree_solve (single kernel): accepted iterations x lane-step constant")}
     if cpu:
-        c3lm["cpu_baseline"] = cpu_leg("tree_lm", list(tgh[:64].cpu().numpy()), "solves/s", "problems")
+        legs.append((c3lm, ("tree_lm", list(tgh[:64].cpu().numpy()), "solves/s", "problems")))
     c3lm["fp32_vs_fp64_final_cost"] = final_cost_agreement(finals[("c3", "fp32")], finals[("c3", "fp64")])
     out["config3_generic_lm"] = c3lm
 
@@ -728,8 +731,7 @@ def run_configs(torch, k, model, flush, peaks, nominals, cpu=True):
     c5["termination_codes"] = ["max_iterations", "gradient_converged", "step_converged", "numerical_failure",
                                "rejection_budget", "non_finite", "fp32_resolution (FP32 only)"]
     if cpu:
-        c5["cpu_baseline"] = cpu_leg("traj", [(qa[i], qb[i], mid[i]) for i in range(64)], "trajectories/s",
-                                     "trajectories")
+        legs.append((c5, ("traj", [(qa[i], qb[i], mid[i]) for i in range(64)], "trajectories/s", "trajectories")))
     out["config5_trajectories"] = c5
 
     # ---- mobile base (SE(2) lanes, f2) ----
@@ -749,8 +751,10 @@ def run_configs(torch, k, model, flush, peaks, nominals, cpu=True):
                     "roofline": roof(msolve, Bm / ms * 1e3, peaks["fp32"], nominals["fp32"],
                                      "whole solve, SURVEY 8(d) rules")}}
     if cpu:
-        mob["cpu_baseline"] = cpu_leg("mobile", list(sh[:64]), "solves/s", "targets")
+        legs.append((mob, ("mobile", list(sh[:64]), "solves/s", "targets")))
     out["mobile_base_ik_beam"] = mob
+    for box, a in legs:
+        box["cpu_baseline"] = cpu_leg(*a)
     return out
 
 
@@ -955,6 +959,19 @@ def run_ours(args, rank, world, local_rank):
     }
     if dist:
         line["backend"] = args.backend
+    if world == 1 and not args.quick:
+        peak64, _ = fma_peak(torch, lib(), fp64=True)
+        nominal64 = sms * NOMINAL_FP64_FLOP_PER_CLK_SM * 1965.0e6 / 1e12
+        t0 = time.perf_counter()
+        line["batch_sweep"] = run_sweep(torch, k, model, solver_for, flush, peak, nominal)
+        line["fp64"] = run_fp64_headline(torch, model, solver_for, flush, B, peak64, nominal64)
+        line["fk"] = run_fk(torch, model, flush)
+        line["configs"] = run_configs(torch, k, model, flush, {"fp32": peak, "fp64": peak64},
+                                      {"fp32": nominal, "fp64": nominal64}, cpu=not args.no_cpu_baseline)
+        line["configs"]["peaks"] = {"fp32_live_ffma": peak, "fp64_live_dfma": peak64, "fp32_nominal": nominal,
+                                    "fp64_nominal": nominal64}
+        line["extended_wall_s"] = time.perf_counter() - t0
+    # host-CPU baseline last: its forked pool must not overlap any device-timed call
     if world == 1 and not args.no_cpu_baseline:
         targets_cpu = targets[:4096].cpu().numpy()
         arm = CpuArm(targets_cpu)
@@ -971,18 +988,6 @@ def run_ours(args, rank, world, local_rank):
             "gpu_success_agreement_same_targets": float(np.mean(res.success[:n].astype(bool) == cpu_succ)),
             "gpu_success_rate_same_targets": float(np.mean(res.success[:n])),
         }
-    if world == 1 and not args.quick:
-        peak64, _ = fma_peak(torch, lib(), fp64=True)
-        nominal64 = sms * NOMINAL_FP64_FLOP_PER_CLK_SM * 1965.0e6 / 1e12
-        t0 = time.perf_counter()
-        line["batch_sweep"] = run_sweep(torch, k, model, solver_for, flush, peak, nominal)
-        line["fp64"] = run_fp64_headline(torch, model, solver_for, flush, B, peak64, nominal64)
-        line["fk"] = run_fk(torch, model, flush)
-        line["configs"] = run_configs(torch, k, model, flush, {"fp32": peak, "fp64": peak64},
-                                      {"fp32": nominal, "fp64": nominal64}, cpu=not args.no_cpu_baseline)
-        line["configs"]["peaks"] = {"fp32_live_ffma": peak, "fp64_live_dfma": peak64, "fp32_nominal": nominal,
-                                    "fp64_nominal": nominal64}
-        line["extended_wall_s"] = time.perf_counter() - t0
     print(json.dumps(line), flush=True)
 
 

@@ -49,7 +49,7 @@ for prec in ("fp32", "fp64"):
         ts.append(e0.elapsed_time(e1))
     ms = float(np.median(ts))
     res[prec] = {"cost": outs[1].cpu().numpy(), "q": outs[0].cpu().numpy()}
-    print(json.dumps({"precision": prec, "problems": B, "ms": ms, "solves_per_s": B / ms * 1e3,
+    print(json.dumps({"precision": prec, "problems": B, "ms": ms, "rep_ms": [round(t, 2) for t in ts], "solves_per_s": B / ms * 1e3,
                       "mean_iterations": float(outs[4].float().mean()),
                       "terminations": torch.bincount(outs[5].long(), minlength=7).tolist()}), flush=True)
 c32, c64 = res["fp32"]["cost"], res["fp64"]["cost"]
