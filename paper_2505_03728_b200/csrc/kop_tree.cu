@@ -147,10 +147,12 @@ __device__ __forceinline__ void base_frame(int kind, const T* base, quat<T>& bq,
   }
 }
 
-template <typename T, int NE, bool JAC>
+// JAC (warp-uniform) selects the Jacobian / normal-equation part at run time, so
+// a caller with one evaluation site carries one inlined copy of the code
+template <typename T, int NE>
 __device__ __forceinline__ T tree_eval(const TreeLmParams<T>& P, const TreeTable<T>& Q,
                                        const double* __restrict__ targets, TreeScratch<T, NE>& S, const T* q,
-                                       const T* base, int lane, T& g_out) {
+                                       const T* base, int lane, T& g_out, const bool JAC) {
   const int n = P.n, ne = P.ne, nd = n + base_dim(P.base_kind);
   quat<T> bq;
   vec3<T> bp;
@@ -575,7 +577,7 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
   // one J-evaluation site (start evaluation, then J at each accepted iterate):
   // a single inlined copy keeps the kernel inside the instruction cache
   for (int it = 0;; ++it) {
-    const T c = tree_eval<T, NE, true>(P, Q, tg, S, S.q, S.bs, lane, g);
+    const T c = tree_eval<T, NE>(P, Q, tg, S, S.q, S.bs, lane, g, true);
     if (it == 0) {
       cost = c;
       if (lane == 0) {
@@ -607,7 +609,7 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
         }
         __syncwarp();
         T gd;
-        const T cn = tree_eval<T, NE, false>(P, Q, tg, S, S.qn, S.bn, lane, gd);
+        const T cn = tree_eval<T, NE>(P, Q, tg, S, S.qn, S.bn, lane, gd, false);
         if (!finite_t(cn)) {
           term = 5;
           break;
@@ -699,28 +701,35 @@ template <typename T, int NE>
 __device__ __forceinline__ T tree_beam_run(const TreeLmParams<T>& P, const TreeTable<T>& Q,
                                            const double* __restrict__ tg, TreeScratch<T, NE>& S, int lane,
                                            int steps, bool start, T cost, T& lam, int h0, T& hv) {
+  // one evaluation site for both kinds (J at the iterate, cost at the candidate):
+  // a single inlined copy of the evaluation keeps the kernel's hot code smaller
   T g = T(0);
-  bool need = true;
-  for (int it = 0;; ++it) {
-    if (need) {
-      const T c = tree_eval<T, NE, true>(P, Q, tg, S, S.q, nullptr, lane, g);
-      if (start && it == 0) {
-        cost = c;
-        if (lane == 0) hv = c;
-      }
-      need = false;
-    }
-    if (it == steps) break;
-    T d;
-    bool ok = tree_damped_solve(P, S, g, lam, lane, d);
-    ok = __all_sync(0xffffffffu, ok && finite_t(d));
+  bool need = true;  // J-evaluation at S.q pending
+  for (int it = 0;;) {
+    if (!need && it == steps) break;
     T cn = inf_t<T>();
-    if (ok) {  // a failed factorisation rejects the step (beam.py:209-213, per lane)
-      S.qn[lane] = S.q[lane] + d;
-      __syncwarp();
-      T gd;
-      const T raw = tree_eval<T, NE, false>(P, Q, tg, S, S.qn, nullptr, lane, gd);
-      cn = finite_t(raw) ? raw : inf_t<T>();
+    bool eval = true;
+    if (!need) {
+      T d;
+      bool ok = tree_damped_solve(P, S, g, lam, lane, d);
+      ok = __all_sync(0xffffffffu, ok && finite_t(d));
+      if (ok) {  // a failed factorisation rejects the step (beam.py:209-213, per lane)
+        S.qn[lane] = S.q[lane] + d;
+        __syncwarp();
+      }
+      eval = ok;
+    }
+    if (eval) {
+      const T c = tree_eval<T, NE>(P, Q, tg, S, need ? S.q : S.qn, nullptr, lane, g, need);
+      if (need) {
+        if (start && it == 0) {
+          cost = c;
+          if (lane == 0) hv = c;
+        }
+        need = false;
+        continue;
+      }
+      cn = finite_t(c) ? c : inf_t<T>();
     }
     if (cn < cost) {
       S.q[lane] = S.qn[lane];
@@ -732,6 +741,7 @@ __device__ __forceinline__ T tree_beam_run(const TreeLmParams<T>& P, const TreeT
       lam = tmin(lam * T(BeamConsts::damping_up), T(BeamConsts::damping_max));
     }
     if (lane == h0 + it) hv = cost;
+    ++it;
   }
   return cost;
 }
