@@ -428,14 +428,21 @@ __device__ __forceinline__ bool tree_damped_solve(const TreeLmParams<T>& P, Tree
   for (int j = 0; j < kTreeMaxDofs; ++j) row[j] = (lane < n && j < n && j <= lane) ? S.A[tree_pa(lane, j)] : T(0);
   bool ok = true;
   T dinv_mine = T(0);
+  // forward substitution y = L^-1 (-g) carried along: lane k's y is final
+  // when column k is factored
+  T y = -g;
 #pragma unroll
   for (int k = 0; k < kTreeMaxDofs; ++k) {
     if (k < n) {  // warp-uniform
       const T dk = shfl_t(row[k], k);
+      const T yr = shfl_t(y, k);
       ok = ok && (dk > T(0)) && finite_t(dk);
       const T inv = rsqrt_t(dk);
       row[k] *= inv;  // lane k: dk * inv = L(k, k); lanes > k: L(lane, k)
       if (lane == k) dinv_mine = inv;
+      const T yk = yr * inv;
+      if (lane == k) y = yk;
+      if (lane > k && lane < n) y -= row[k] * yk;
       T* cb = S.cb[k & 1];  // the buffer of step k - 2 is free: every lane passed step k - 1's sync
       cb[lane] = row[k];    // rows / lanes >= n are zero
       __syncwarp();
@@ -452,25 +459,27 @@ __device__ __forceinline__ bool tree_damped_solve(const TreeLmParams<T>& P, Tree
   if (lane < n) {  // L(lane, j) for the backward sweep
 #pragma unroll
     for (int j = 0; j < kTreeMaxDofs; ++j)
-      if (j <= lane && j < n) S.L[j * 33 + lane] = row[j];
+      if (j < lane && j < n) S.L[j * 33 + lane] = row[j];
+    S.L[lane * 33 + lane] = dinv_mine;  // the diagonal slot carries 1 / L(lane, lane)
   }
   __syncwarp();
-  // forward: y = L^-1 (-g), L(lane, k) from the registers
-  T y = -g;
-#pragma unroll
-  for (int k = 0; k < kTreeMaxDofs; ++k) {
-    if (k < n) {
-      const T yk = shfl_t(y * dinv_mine, k);
-      if (lane == k) y = yk;
-      if (lane > k && lane < n) y -= row[k] * yk;
-    }
-  }
-  // backward: x = L^-T y
+  // backward: x = L^-T y, two rows per step: every lane forms x_k and x_{k-1}
+  // from lanes k, k-1 (the same operations as row-by-row), so the serial
+  // chain is one shuffle round per two rows
   T x = y;
-  for (int k = n - 1; k >= 0; --k) {
-    const T xk = shfl_t(x * dinv_mine, k);
+  int k = n - 1;
+  for (; k >= 1; k -= 2) {
+    const T lkk = S.L[(k - 1) * 33 + k], dk1 = S.L[(k - 1) * 33 + k - 1];  // L(k, k-1), 1 / L(k-1, k-1)
+    const T lk = lane < k ? S.L[lane * 33 + k] : T(0), lk1 = lane < k - 1 ? S.L[lane * 33 + k - 1] : T(0);
+    const T xk = shfl_t(x * dinv_mine, k), xr = shfl_t(x, k - 1);
+    const T xk1 = (xr - lkk * xk) * dk1;
     if (lane == k) x = xk;
-    if (lane < k) x -= S.L[lane * 33 + k] * xk;  // L[k][lane]
+    if (lane == k - 1) x = xk1;
+    if (lane < k - 1) x = x - lk * xk - lk1 * xk1;  // L[k][lane], L[k-1][lane]
+  }
+  if (k == 0) {
+    const T x0 = shfl_t(x * dinv_mine, 0);
+    if (lane == 0) x = x0;
   }
   delta = lane < n ? x : T(0);
   return ok;
