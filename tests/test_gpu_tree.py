@@ -207,3 +207,50 @@ def test_humanoid_ik_beam_distribution_1000(hum):
     assert abs(r32.success.mean() - s_ref) <= 0.02
     for a, b in ((r32.pos_error.max(axis=1), ref["pos_err"].max(axis=1)),):
         assert 0.5 * np.percentile(b, 50) <= np.percentile(a, 50) <= 2.0 * np.percentile(b, 50)
+
+
+# A branched tree with consecutive fixed joints (fx1 -> fx2 before j1, fxA1 -> fxA2
+# after the prismatic j2 ending at end effector tipA) and a branch that leaves
+# through a fixed joint (fb): the host folds fixed joints into their children's
+# origins and the end-effector offsets (kop_capi.cu tree_params).
+_LIM = '<limit lower="-2.5" upper="2.5" effort="1" velocity="1"/>'
+_FOLD_TREE = (
+    '<robot name="fold">'
+    + "".join(f'<link name="{n}"/>' for n in ["base", "a", "b", "c", "d", "e", "f", "g", "h", "tipA", "tipB"])
+    + f'<joint name="j0" type="revolute"><parent link="base"/><child link="a"/><origin xyz="0 0 0.1" rpy="0.1 0 0.2"/><axis xyz="0 0 1"/>{_LIM}</joint>'
+    + '<joint name="fx1" type="fixed"><parent link="a"/><child link="b"/><origin xyz="0.05 0 0.12" rpy="0.3 0.1 0"/></joint>'
+    + '<joint name="fx2" type="fixed"><parent link="b"/><child link="c"/><origin xyz="0 0.04 0.08" rpy="0 -0.2 0.4"/></joint>'
+    + f'<joint name="j1" type="revolute"><parent link="c"/><child link="d"/><origin xyz="0 0 0.15" rpy="0 0.3 0"/><axis xyz="0 1 0"/>{_LIM}</joint>'
+    + '<joint name="j2" type="prismatic"><parent link="d"/><child link="e"/><origin xyz="0.02 0 0.1" rpy="0 0 0.5"/><axis xyz="0.6 0 0.8"/><limit lower="-0.1" upper="0.2" effort="1" velocity="1"/></joint>'
+    + '<joint name="fxA1" type="fixed"><parent link="e"/><child link="f"/><origin xyz="0.03 0.01 0.06" rpy="0.2 0 -0.1"/></joint>'
+    + '<joint name="fxA2" type="fixed"><parent link="f"/><child link="tipA"/><origin xyz="0 0 0.05" rpy="0 0.4 0"/></joint>'
+    + '<joint name="fb" type="fixed"><parent link="b"/><child link="g"/><origin xyz="-0.04 0.02 0.07" rpy="-0.3 0 0.2"/></joint>'
+    + f'<joint name="j3" type="revolute"><parent link="g"/><child link="h"/><origin xyz="0 0 0.12" rpy="0 0 0.3"/><axis xyz="1 0 0"/>{_LIM}</joint>'
+    + f'<joint name="j4" type="revolute"><parent link="h"/><child link="tipB"/><origin xyz="0 0.02 0.1" rpy="0.2 0 0"/><axis xyz="0 0.6 0.8"/>{_LIM}</joint>'
+    + '</robot>')
+
+
+@pytest.mark.parametrize("prec", ["fp64", "fp32"])
+def test_tree_ik_beam_folded_fixed_joints(prec):
+    from oracle import tree_oracle as tro
+
+    m = k.parse_urdf(_FOLD_TREE)
+    ch = o.load_chain(_FOLD_TREE)
+    ees = ["tipA", "tipB"]
+    links = [ch.link(e) for e in ees]
+    rng = np.random.default_rng(41)
+    lq, lp, _, _ = o.fk(ch, rng.uniform(ch.lower, ch.upper, (48, ch.n)))
+    tq = np.stack([o.qcanon(lq[:, li]) for li in links], 1)
+    tt = np.stack([lp[:, li] for li in links], 1)
+    seeds = o.sample_seeds(ch, 64, 3)
+    ref = par_batched(tro.multi_ee_beam, ch, links, tq=tq, tt=tt, seeds=seeds, w_pos=[50.0] * 2,
+                      w_ori=[10.0] * 2, split=("tq", "tt"))
+    got = k.solve_ik_beam_multi(m, ees, np.concatenate([tq, tt], axis=2), rng_seed=3, precision=prec)
+    # reachable targets and 5 columns: most seeds reach the same minimum, so prune / winner
+    # choices are exact ties (as for the one-column chain above) -- every divergence must be one
+    if prec == "fp64":
+        assert_fp64_beam_parity(got.history, ref["hist"], ref["diag"], frac=0.0)
+        np.testing.assert_allclose(got.history[:, -1], ref["hist"][:, -1], rtol=1e-6, atol=1e-12)
+    else:
+        assert np.all(got.cost <= ref["hist"][:, -1] * 1.01 + 1e-6)
+    assert np.mean(got.success == ref["success"]) >= 0.95
