@@ -254,3 +254,23 @@ def test_tree_ik_beam_folded_fixed_joints(prec):
     else:
         assert np.all(got.cost <= ref["hist"][:, -1] * 1.01 + 1e-6)
     assert np.mean(got.success == ref["success"]) >= 0.95
+
+
+def test_tree_solve_folded_fixed_joints_matches_oracle():
+    """solver.solve semantics on the folded tree (two pose costs + limit + rest) vs the
+    oracle's classic LM, FP64."""
+    m = k.parse_urdf(_FOLD_TREE)
+    ch = o.load_chain(_FOLD_TREE)
+    rng = np.random.default_rng(43)
+    lq, lp, _, _ = o.fk(ch, rng.uniform(ch.lower, ch.upper, (1, ch.n)))
+    w = k.CostWeights()
+    costs, poses = [], []
+    for e in ("tipA", "tipB"):
+        li = ch.link(e)
+        costs.append(k.pose_cost(m, "q", e, k.Transform3.from_parts(lq[0, li], lp[0, li]),
+                                 position_weight=w.pose_position, orientation_weight=w.pose_orientation))
+        poses.append((li, o.qcanon(lq[0, li]), lp[0, li], w.pose_position, w.pose_orientation))
+    costs += [k.limit_cost(m, "q", weight=w.limit), k.rest_cost("q", m.rest_pose, weight=w.rest)]
+    rep = k.solve(k.Problem(k.VariableSet.of(q=np.asarray(m.rest_pose, float).copy()), costs))
+    _, c_ref, _, _, _ = to.solve_multi_pose(ch, poses, ch.rest)
+    np.testing.assert_allclose(rep.final_cost, c_ref, rtol=1e-5, atol=1e-12)
