@@ -653,7 +653,7 @@ def run_configs(torch, k, model, flush, peaks, nominals, cpu=True):
 
         def run_tb():
             box["r"] = k.solve_ik_beam_multi(hum, ees, tgh, precision=prec, device_out=True)
-        ms = float(np.median(device_time(torch, run_tb, 2, flush)))
+        ms = float(np.median(device_time(torch, run_tb, 3, flush)))
         share = load_share(f"config3_{prec}")
         c3[prec] = {"ms": ms, "value": B3 / ms * 1e3, "unit": "solves/s",
                     "success_rate": float(box["r"].success.float().mean()),
@@ -683,7 +683,7 @@ def run_configs(torch, k, model, flush, peaks, nominals, cpu=True):
         def run_tl():
             check(lib().kop_multi_pose_solve(hum._handle, C.byref(hp.costs), C.byref(opts), dv.ptr(tgh), dv.ptr(q0),
                                              B3, *(dv.ptr(x) for x in outs), dv.stream_handle()), "tree")
-        ms = float(np.median(device_time(torch, run_tl, 2, flush)))
+        ms = float(np.median(device_time(torch, run_tl, 3, flush)))
         it = float(outs[4].float().mean())
         finals[("c3", prec)] = outs[1].cpu().numpy()
         c3lm[prec] = {"ms": ms, "value": B3 / ms * 1e3, "unit": "solves/s", "mean_iterations": it,
@@ -716,7 +716,7 @@ def run_configs(torch, k, model, flush, peaks, nominals, cpu=True):
 
         def run_tr():
             res.update(pl.solve_anchored_device(anchors, obsd, 1, history=False))
-        ms = float(np.median(device_time(torch, run_tr, 2, flush)))
+        ms = float(np.median(device_time(torch, run_tr, 3, flush)))
         rep = k.trajectory.trajectory_signed_distances_batch(model, res["qs"], obsd, 1, "flange")
         free = float((torch.minimum(rep["min_static"], rep["min_swept"]) >= 0).float().mean())
         it = float(res["iterations"].float().mean())
