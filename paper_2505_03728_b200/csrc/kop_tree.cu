@@ -583,29 +583,18 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
   int term = 0;
   int iters = 0;
   T damping = T(O.damping0);
-  // one J-evaluation site (start evaluation, then J at each accepted iterate):
-  // a single inlined copy keeps the kernel inside the instruction cache
-  for (int it = 0;; ++it) {
-    const T c = tree_eval<T, NE>(P, Q, tg, S, S.q, S.bs, lane, g, true);
-    if (it == 0) {
-      cost = c;
-      if (lane == 0) {
-        if (hist_out) hist_out[b * hstride] = double(cost);
-        init_cost_out[b] = double(cost);
-      }
-      term = finite_t(cost) ? 0 : 5;
-    }
-    if (term != 0 || it >= O.max_iterations) break;
-    if (warp_max(lane < nd ? fabs(g) : T(0)) < T(O.grad_tol)) {
-      term = 1;
-      break;
-    }
-    bool accepted = false;
-    T step = T(0);
-    // diag of J^T J at the iterate (lane i), for the FP32 rule's model decrease
-    const T dg = lane < nd ? tmax(S.dg[lane], T(BeamConsts::diag_clamp)) : T(0);
-    for (int rj = 0; rj < O.max_rejections; ++rj) {
-      T d;
+  // ONE evaluation site for both kinds -- J at the iterate (the start evaluation
+  // and each accepted iterate) or the candidate's cost in the rejection loop --
+  // selected at run time: a single inlined copy keeps the kernel's hot code
+  // inside the instruction cache.  The control flow is solver.solve's
+  // (solver.py:381-419): per iteration a gradient test, then damped trials
+  // until one decreases the cost (x down) or the damping / rejection budget
+  // runs out (x up per rejected or failed trial).
+  bool jac = true;  // next evaluation: J at the iterate
+  int it = 0, rj = 0;
+  T dg = T(0), d = T(0);
+  for (;;) {
+    if (!jac) {  // a damped trial from the iterate
       bool ok = tree_damped_solve(P, S, g, damping, lane, d);
       ok = __all_sync(0xffffffffu, ok && finite_t(d));
       if (ok) {
@@ -617,42 +606,71 @@ k_tree_solve(const TreeLmParams<T> P, const double* __restrict__ targets, const 
           if (lane == 0) tree_base_retract(P.base_kind, S.bs, db, S.bn);
         }
         __syncwarp();
-        T gd;
-        const T cn = tree_eval<T, NE>(P, Q, tg, S, S.qn, S.bn, lane, gd, false);
-        if (!finite_t(cn)) {
-          term = 5;
+      } else {  // a failed factorisation is a rejected trial without an evaluation
+        damping *= T(O.up);
+        if (damping > T(BeamConsts::damping_max) || ++rj >= O.max_rejections) {
+          term = damping > T(BeamConsts::damping_max) ? 3 : 4;
           break;
         }
-        if (cn < cost) {
-          S.q[lane] = S.qn[lane];
-          if (lane < bsz) S.bs[lane] = S.bn[lane];
-          step = d;
-          cost = cn;
-          damping = tmax(damping * T(O.down), T(BeamConsts::damping_min));
-          accepted = true;
-          __syncwarp();
-          break;
-        }
-        // FP32 rule (kop_collision.cu kFp32Tau): a rejected trial whose quadratic-model decrease
-        // -g.d + lam d^T D d is below 2^-17 of the cost is not resolvable in float32
-        if (sizeof(T) == 4 && warp_sum(lane < nd ? damping * dg * d * d - g * d : T(0)) <=
-                                  T(7.62939453125e-6f) * cost) {
-          term = 6;
-          break;
-        }
+        continue;
       }
-      damping *= T(O.up);
-      if (damping > T(BeamConsts::damping_max)) break;
     }
-    if (term != 0) break;
-    if (!accepted) {
-      term = damping > T(BeamConsts::damping_max) ? 3 : 4;
+    T gd;
+    const T c = tree_eval<T, NE>(P, Q, tg, S, jac ? S.q : S.qn, jac ? S.bs : S.bn, lane, jac ? g : gd, jac);
+    if (jac) {
+      if (it == 0) {
+        cost = c;
+        if (lane == 0) {
+          if (hist_out) hist_out[b * hstride] = double(cost);
+          init_cost_out[b] = double(cost);
+        }
+        term = finite_t(cost) ? 0 : 5;
+      }
+      if (term != 0 || it >= O.max_iterations) break;
+      if (warp_max(lane < nd ? fabs(g) : T(0)) < T(O.grad_tol)) {
+        term = 1;
+        break;
+      }
+      // diag of J^T J at the iterate (lane i), for the FP32 rule's model decrease
+      dg = lane < nd ? tmax(S.dg[lane], T(BeamConsts::diag_clamp)) : T(0);
+      if (O.max_rejections <= 0) {  // no trial allowed
+        term = damping > T(BeamConsts::damping_max) ? 3 : 4;
+        break;
+      }
+      rj = 0;
+      jac = false;
+      continue;
+    }
+    if (!finite_t(c)) {
+      term = 5;
       break;
     }
-    ++iters;
-    if (lane == 0 && hist_out) hist_out[b * hstride + iters] = double(cost);
-    if (warp_max(fabs(step)) < T(O.step_tol)) {
-      term = 2;
+    if (c < cost) {  // accepted
+      S.q[lane] = S.qn[lane];
+      if (lane < bsz) S.bs[lane] = S.bn[lane];
+      cost = c;
+      damping = tmax(damping * T(O.down), T(BeamConsts::damping_min));
+      __syncwarp();
+      ++iters;
+      if (lane == 0 && hist_out) hist_out[b * hstride + iters] = double(cost);
+      if (warp_max(fabs(d)) < T(O.step_tol)) {
+        term = 2;
+        break;
+      }
+      ++it;
+      jac = true;
+      continue;
+    }
+    // FP32 rule (kop_collision.cu kFp32Tau): a rejected trial whose quadratic-model decrease
+    // -g.d + lam d^T D d is below 2^-17 of the cost is not resolvable in float32
+    if (sizeof(T) == 4 && warp_sum(lane < nd ? damping * dg * d * d - g * d : T(0)) <=
+                              T(7.62939453125e-6f) * cost) {
+      term = 6;
+      break;
+    }
+    damping *= T(O.up);
+    if (damping > T(BeamConsts::damping_max) || ++rj >= O.max_rejections) {
+      term = damping > T(BeamConsts::damping_max) ? 3 : 4;
       break;
     }
   }
