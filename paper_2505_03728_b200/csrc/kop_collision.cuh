@@ -376,7 +376,8 @@ __device__ __forceinline__ typename G::T col_rows(const ChainParams<typename G::
                                                   const CollisionParams<typename G::T>& P, const ColLane<G>& L,
                                                   typename G::T (&A)[Tri<G::ND>::size], typename G::T (&g)[G::ND],
                                                   int row = 0, double* row_out = nullptr,
-                                                  double* jac_out = nullptr, const OB* obs = nullptr) {
+                                                  double* jac_out = nullptr, const OB* obs = nullptr,
+                                                  int pair0 = 0, int pair1 = 1 << 30) {
   using T = typename G::T;
   constexpr int NQ = G::NQ;
   const OB& O = obs ? *obs : reinterpret_cast<const OB&>(P);
@@ -437,7 +438,8 @@ __device__ __forceinline__ typename G::T col_rows(const ChainParams<typename G::
 
   // ---- self rows: link pairs, costs.py:435-496 ------------------------------
   if ((PART & 2) && P.w_self > T(0)) {
-    for (int pi = 0; pi < P.np; ++pi, ++row) {
+    const int pend = P.np < pair1 ? P.np : pair1;  // self pairs [pair0, pend) (split across threads: trajectories)
+    for (int pi = pair0; pi < pend; ++pi, ++row) {
       const int la = P.pa[pi], lb = P.pb[pi];
       const int fa = P.lfirst[la], na = P.lcount[la], fb = P.lfirst[lb], nb = P.lcount[lb];
       if (SCREEN) {

@@ -110,12 +110,15 @@ struct TrajView {
   static constexpr size_t kHead = (sizeof(ObstacleTable<T>) + 15) / 16 * 16 + (NPAIR * 2 + 15) / 16 * 16;
   ObstacleTable<T>* obs;
   uint16_t* pairs;  // ri | ci << 8
-  T *red, *anc, *q, *qn, *g, *y, *dinv, *H, *L, *scratch, *pbufA, *pbufg, *sbuf, *dbuf;
+  T *red, *anc, *q, *qn, *g, *y, *dinv, *H, *L, *scratch, *pbufA, *pbufg, *sbuf, *dbuf, *sbuf2;
+  // 256-thread CTAs (FP64): the self-collision pairs of timestep t are split
+  // between threads t + 64 and t + 128 (idle in the evaluation otherwise)
+  static constexpr bool SPLIT = TH >= 192;
   int steps;
   __host__ __device__ static size_t bytes(int steps, int ns) {
     const size_t N = (size_t)steps * NQ;
     const size_t band = N * LW;
-    const size_t uni_b = (size_t)(6 * G::K + 3 * ns) * steps + (size_t)steps * ((NT + NQ) * 2 + 2 * NQ);
+    const size_t uni_b = (size_t)(6 * G::K + 3 * ns) * steps + (size_t)steps * ((NT + NQ) * (SPLIT ? 3 : 2) + 2 * NQ);
     return kHead + sizeof(T) * (TH + 2 * NQ + 5 * N + (size_t)steps * HB + (band > uni_b ? band : uni_b));
   }
   __device__ TrajView(unsigned char* base, int steps_, int ns) : steps(steps_) {
@@ -136,7 +139,8 @@ struct TrajView {
     pbufA = p; p += steps * NT;
     pbufg = p; p += steps * NQ;
     sbuf = p; p += steps * (NT + NQ);  // block t parts of thread t + 64's rows (self, swept)
-    dbuf = p;  // diagonal block t-1 parts of the smoothness / velocity rows of pair (t-1, t)
+    dbuf = p; p += steps * 2 * NQ;  // diagonal block t-1 parts of the smoothness / velocity rows of pair (t-1, t)
+    sbuf2 = p;  // (SPLIT) block t parts of thread t + 128's self pairs
   }
   // pair q of the trailing update, in the order (ri = NQ, ci = 0..ri), (ri = NQ + 1, ...), ...
   __device__ void build_pairs() const {
@@ -351,7 +355,8 @@ __device__ typename G::T traj_eval(const ChainParams<typename G::T, G::K>& C, co
 #pragma unroll
     for (int i = 0; i < NQ; ++i) gs[i] = T(0);
     if (self_rows)
-      cost += col_rows<G, JAC, ObstacleTable<T>, true, 2>(C, P, S.lane(u), As, gs, 0, nullptr, nullptr, S.obs);
+      cost += col_rows<G, JAC, ObstacleTable<T>, true, 2>(C, P, S.lane(u), As, gs, 0, nullptr, nullptr, S.obs, 0,
+                                                          TrajView<G>::SPLIT ? P.np / 2 : P.np);
     if (swept_rows && u >= 1) {
       T pA[NT], pg[NQ];  // block u-1 part
 #pragma unroll
@@ -371,6 +376,24 @@ __device__ typename G::T traj_eval(const ChainParams<typename G::T, G::K>& C, co
       for (int i = 0; i < NT; ++i) S.sbuf[u * (NT + NQ) + i] = As[i];
 #pragma unroll
       for (int i = 0; i < NQ; ++i) S.sbuf[u * (NT + NQ) + NT + i] = gs[i];
+    }
+  }
+  if constexpr (TrajView<G>::SPLIT) {  // thread t + 128: the second half of timestep t's self pairs
+    if (tid >= 128 && tid - 128 < Tn && self_rows && P.np / 2 < P.np) {
+      const int u = tid - 128;
+      T As2[NT], gs2[NQ];
+#pragma unroll
+      for (int i = 0; i < NT; ++i) As2[i] = T(0);
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) gs2[i] = T(0);
+      cost += col_rows<G, JAC, ObstacleTable<T>, true, 2>(C, P, S.lane(u), As2, gs2, 0, nullptr, nullptr, S.obs,
+                                                          P.np / 2, P.np);
+      if (JAC) {
+#pragma unroll
+        for (int i = 0; i < NT; ++i) S.sbuf2[u * (NT + NQ) + i] = As2[i];
+#pragma unroll
+        for (int i = 0; i < NQ; ++i) S.sbuf2[u * (NT + NQ) + NT + i] = gs2[i];
+      }
     }
   }
   if (t < Tn) {
@@ -474,6 +497,12 @@ __device__ typename G::T traj_eval(const ChainParams<typename G::T, G::K>& C, co
       for (int i = 0; i < NT; ++i) Ad[i] += S.sbuf[t * (NT + NQ) + i];
 #pragma unroll
       for (int i = 0; i < NQ; ++i) gd[i] += S.sbuf[t * (NT + NQ) + NT + i];
+    }
+    if (TrajView<G>::SPLIT && self_rows && P.np / 2 < P.np) {
+#pragma unroll
+      for (int i = 0; i < NT; ++i) Ad[i] += S.sbuf2[t * (NT + NQ) + i];
+#pragma unroll
+      for (int i = 0; i < NQ; ++i) gd[i] += S.sbuf2[t * (NT + NQ) + NT + i];
     }
 #pragma unroll
     for (int a = 0; a < NQ; ++a) {
