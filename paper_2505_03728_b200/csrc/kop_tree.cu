@@ -506,6 +506,9 @@ constexpr int tree_warps() { return sizeof(T) == 4 ? KOP_TREE_WARPS32 : KOP_TREE
 #ifndef KOP_TREE_BEAM_WARPS64
 #define KOP_TREE_BEAM_WARPS64 6
 #endif
+#ifndef KOP_TREE_S2_TARGETS32
+#define KOP_TREE_S2_TARGETS32 2
+#endif
 template <typename T>
 constexpr int tree_beam_warps() { return sizeof(T) == 4 ? KOP_TREE_BEAM_WARPS32 : KOP_TREE_BEAM_WARPS64; }
 
@@ -858,37 +861,43 @@ k_tree_beam_stage2(const TreeLmParams<T> P, const TreeLmParams<double> Pd, const
                    int64_t B, const T* __restrict__ recs, int S, const int32_t* __restrict__ surv, int steps1,
                    int steps2, int keep, double pos_tol, double rot_tol, double* __restrict__ q_out,
                    double* __restrict__ cost_out, double* __restrict__ hist_out, double* __restrict__ pos_err,
-                   double* __restrict__ rot_err, uint8_t* __restrict__ success) {
+                   double* __restrict__ rot_err, uint8_t* __restrict__ success, int tpc) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   KOP_SMEM_ENTRY(smem_raw);
-  const int lane = threadIdx.x & 31, r = threadIdx.x >> 5;  // warp r = survivor of stage-1 rank r
-  const int64_t b = blockIdx.x;
+  // tpc targets per CTA (one staged table for all), `keep` warps each: warp r of
+  // group grp = survivor of stage-1 rank r of target b
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, grp = w / keep, r = w - grp * keep;
+  const int64_t b = (int64_t)blockIdx.x * tpc + grp;
+  const bool live = b < B;
   TreeTable<T>& Q = *reinterpret_cast<TreeTable<T>*>(smem_raw);
   const size_t tab = (sizeof(TreeTable<T>) + 15) / 16 * 16;
-  TreeScratch<T, NE>& Sc = reinterpret_cast<TreeScratch<T, NE>*>(smem_raw + tab)[r];
-  T* wcost = reinterpret_cast<T*>(smem_raw + tab + sizeof(TreeScratch<T, NE>) * keep);
-  int* wsel = reinterpret_cast<int*>(wcost + keep);
+  TreeScratch<T, NE>& Sc = reinterpret_cast<TreeScratch<T, NE>*>(smem_raw + tab)[w];
+  T* wcost = reinterpret_cast<T*>(smem_raw + tab + sizeof(TreeScratch<T, NE>) * keep * tpc);
+  int* wsel = reinterpret_cast<int*>(wcost + keep * tpc);
   stage_tree_table(P, Q);
   __syncthreads();
   const int n = P.n, rec = tree_beam_rec(n, steps1);
-  const T* in = recs + (b * S + surv[b * keep + r]) * rec;
-  for (int i = lane; i < NE * 48; i += 32) (&Sc.ee[0][0])[i] = T(0);
-  Sc.q[lane] = lane < n ? in[lane] : T(0);
-  __syncwarp();
-  const double* tg = targets + b * 7 * P.ne;
-  T lam = in[n];
-  T hv = T(0);  // lane h keeps stage-2 hist[h]; J re-derived, the carried cost is stage 1's
-  const T cost = tree_beam_run(P, Q, tg, Sc, lane, steps2, false, in[n + 1], lam, 0, hv);
-  if (lane == 0) wcost[r] = cost;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int best = 0;
-    for (int k = 1; k < keep; ++k)
-      if (wcost[k] < wcost[best] || (wcost[best] != wcost[best] && wcost[k] == wcost[k])) best = k;
-    *wsel = best;
+  const T* in = recs + (live ? (b * S + surv[b * keep + r]) * rec : 0);
+  const double* tg = targets + (live ? b : 0) * 7 * P.ne;
+  T cost = T(0), hv = T(0);  // lane h keeps stage-2 hist[h]; J re-derived, the carried cost is stage 1's
+  if (live) {
+    for (int i = lane; i < NE * 48; i += 32) (&Sc.ee[0][0])[i] = T(0);
+    Sc.q[lane] = lane < n ? in[lane] : T(0);
+    __syncwarp();
+    T lam = in[n];
+    cost = tree_beam_run(P, Q, tg, Sc, lane, steps2, false, in[n + 1], lam, 0, hv);
+    if (lane == 0) wcost[w] = cost;
   }
   __syncthreads();
-  if (r != *wsel) return;
+  if (live && lane == 0 && r == 0) {
+    const T* wc = wcost + grp * keep;
+    int best = 0;
+    for (int k = 1; k < keep; ++k)
+      if (wc[k] < wc[best] || (wc[best] != wc[best] && wc[k] == wc[k])) best = k;
+    wsel[grp] = best;
+  }
+  __syncthreads();
+  if (!live || r != wsel[grp]) return;
   if (lane < n) q_out[b * n + lane] = double(Sc.q[lane]);
   if (lane == 0) cost_out[b] = double(cost);
   if (hist_out) {
@@ -943,13 +952,17 @@ cudaError_t launch_tree_beam_ne(const TreeLmParams<T>& P, const TreeLmParams<dou
   if (e != cudaSuccess) return e;
   k_tree_beam_prune<T><<<(unsigned)((L.B + 3) / 4), 128, 0, st>>>(recs, rec, P.n, L.B, L.S, L.keep, surv);
   if ((e = cudaGetLastError()) != cudaSuccess) return e;
-  const size_t smem2 = tab + sizeof(TreeScratch<T, NE>) * L.keep + (sizeof(T) + sizeof(int)) * 32 + 16;
+  // FP32: two targets per CTA (2 x keep warps share the staged table: 24 resident warps per SM
+  // instead of 20 for keep = 4); FP64 scratch fills the SM either way
+  const int tpc = (sizeof(T) == 4 && 2 * L.keep <= 8) ? KOP_TREE_S2_TARGETS32 : 1;
+  const size_t smem2 =
+      tab + sizeof(TreeScratch<T, NE>) * L.keep * tpc + (sizeof(T) + sizeof(int)) * 32 + 16;
   cudaFuncSetAttribute(k_tree_beam_stage2<T, NE>, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
   if (smem2 > 48 * 1024)
     cudaFuncSetAttribute(k_tree_beam_stage2<T, NE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2);
-  k_tree_beam_stage2<T, NE><<<(unsigned)L.B, 32 * L.keep, smem2, st>>>(
+  k_tree_beam_stage2<T, NE><<<(unsigned)((L.B + tpc - 1) / tpc), 32 * L.keep * tpc, smem2, st>>>(
       P, Pd, L.targets, L.B, recs, L.S, surv, L.steps1, L.steps2, L.keep, L.pos_tol, L.rot_tol, L.q_out, L.cost_out,
-      L.hist_out, L.pos_err, L.rot_err, L.success);
+      L.hist_out, L.pos_err, L.rot_err, L.success, tpc);
   return cudaGetLastError();
 }
 
