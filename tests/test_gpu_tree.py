@@ -274,3 +274,18 @@ def test_tree_solve_folded_fixed_joints_matches_oracle():
     rep = k.solve(k.Problem(k.VariableSet.of(q=np.asarray(m.rest_pose, float).copy()), costs))
     _, c_ref, _, _, _ = to.solve_multi_pose(ch, poses, ch.rest)
     np.testing.assert_allclose(rep.final_cost, c_ref, rtol=1e-5, atol=1e-12)
+
+
+@pytest.mark.parametrize("keep", [1, 3, 4])
+def test_tree_ik_beam_batch_invariance_odd_batches(hum, keep):
+    """Per-target results do not depend on the batch: 37 targets in one call equal
+    the same targets split 20 + 17 (odd batches leave stage 2's packed FP32 CTAs
+    with an empty target slot), for several keep widths."""
+    chh = o.load_chain_files(k.robot_path("humanoid29.urdf"))
+    _, _, _, tg = _hum_targets(hum, chh, 37, 9)
+    kw = dict(rng_seed=5, keep=keep, precision="fp32")
+    full = k.solve_ik_beam_multi(hum, EES, tg, **kw)
+    a = k.solve_ik_beam_multi(hum, EES, tg[:20], **kw)
+    b = k.solve_ik_beam_multi(hum, EES, tg[20:], **kw)
+    for f in ("q", "cost", "history", "pos_error", "rot_error", "success"):
+        np.testing.assert_array_equal(getattr(full, f), np.concatenate([getattr(a, f), getattr(b, f)]), err_msg=f)
