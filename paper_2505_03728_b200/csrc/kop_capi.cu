@@ -1063,7 +1063,7 @@ int kop_lm_solve(const KopModel* m, int32_t link, const KopCollisionCosts* cc, c
   if (o->max_iterations <= 0 || !(o->initial_damping > 0)) return fail(KOP_EINVAL, "max_iterations and initial_damping must be positive");
   if (!(o->damping_increase > 1.0)) return fail(KOP_EINVAL, "damping_increase must exceed 1");
   if (!(o->damping_decrease > 0.0 && o->damping_decrease < 1.0)) return fail(KOP_EINVAL, "damping_decrease must be in (0, 1)");
-  if (o->max_rejections < 1) return fail(KOP_EINVAL, "max_rejections must be positive");
+  if (o->max_rejections < 0) return fail(KOP_EINVAL, "max_rejections must be nonnegative");
   if (batch < 0) return fail(KOP_EINVAL, "negative batch");
   if (batch == 0) return KOP_OK;
   if (!targets || !q0 || !q_out || !cost_out || !init_cost_out || !iterations_out || !termination_out)
@@ -1263,7 +1263,7 @@ int kop_multi_pose_solve_base(const KopModel* m, const KopPoseCosts* pc, const K
   if (o->max_iterations <= 0 || !(o->initial_damping > 0)) return fail(KOP_EINVAL, "max_iterations and initial_damping must be positive");
   if (!(o->damping_increase > 1.0)) return fail(KOP_EINVAL, "damping_increase must exceed 1");
   if (!(o->damping_decrease > 0.0 && o->damping_decrease < 1.0)) return fail(KOP_EINVAL, "damping_decrease must be in (0, 1)");
-  if (o->max_rejections < 1) return fail(KOP_EINVAL, "max_rejections must be positive");
+  if (o->max_rejections < 0) return fail(KOP_EINVAL, "max_rejections must be nonnegative");
   if (batch < 0) return fail(KOP_EINVAL, "negative batch");
   if (batch == 0) return KOP_OK;
   if (!targets || !q0 || !q_out || !cost_out || !init_cost_out || !iterations_out || !termination_out)
@@ -1404,7 +1404,7 @@ int kop_traj_solve(const KopModel* m, int32_t link, const KopTrajCosts* c, const
   if (o->max_iterations <= 0 || !(o->initial_damping > 0)) return fail(KOP_EINVAL, "max_iterations and initial_damping must be positive");
   if (!(o->damping_increase > 1.0)) return fail(KOP_EINVAL, "damping_increase must exceed 1");
   if (!(o->damping_decrease > 0.0 && o->damping_decrease < 1.0)) return fail(KOP_EINVAL, "damping_decrease must be in (0, 1)");
-  if (o->max_rejections < 1) return fail(KOP_EINVAL, "max_rejections must be positive");
+  if (o->max_rejections < 0) return fail(KOP_EINVAL, "max_rejections must be nonnegative");
   if (batch < 0) return fail(KOP_EINVAL, "negative batch");
   if (batch == 0) return KOP_OK;
   if (!anchors || (num_obstacles > 0 && !obstacles) || !q_out || !cost_out || !init_cost_out ||

@@ -211,6 +211,7 @@ k_col_solve(const ChainParams<typename G::T, G::K> C, const CostParams<typename 
 #pragma unroll
           for (int i = 0; i < NQ; ++i) gmax = tmax(gmax, fabs(g[i]));
           if (gmax < T(O.grad_tol)) term = kGradientConverged;
+          else if (O.max_rejections <= 0) term = kRejectionsExhausted;  // no trial allowed (solver.py:389)
         }
       }
     }

@@ -289,3 +289,49 @@ def test_tree_ik_beam_batch_invariance_odd_batches(hum, keep):
     b = k.solve_ik_beam_multi(hum, EES, tg[20:], **kw)
     for f in ("q", "cost", "history", "pos_error", "rot_error", "success"):
         np.testing.assert_array_equal(getattr(full, f), np.concatenate([getattr(a, f), getattr(b, f)]), err_msg=f)
+
+
+@pytest.mark.parametrize("rej", [0, 1, 3])
+def test_tree_solve_rejection_budget_matches_oracle(rej):
+    """The tree solve's rejection loop (one evaluation site, kop_tree.cu) with small
+    budgets -- including none -- against the oracle's classic LM (solver.py:389-419),
+    FP64: cost history, iteration count and termination."""
+    m = k.parse_urdf(_FOLD_TREE)
+    ch = o.load_chain(_FOLD_TREE)
+    rng = np.random.default_rng(47)
+    lq, lp, _, _ = o.fk(ch, rng.uniform(ch.lower, ch.upper, (1, ch.n)))
+    w = k.CostWeights()
+    costs, poses = [], []
+    for e in ("tipA", "tipB"):
+        li = ch.link(e)
+        costs.append(k.pose_cost(m, "q", e, k.Transform3.from_parts(lq[0, li], lp[0, li]),
+                                 position_weight=w.pose_position, orientation_weight=w.pose_orientation))
+        poses.append((li, o.qcanon(lq[0, li]), lp[0, li], w.pose_position, w.pose_orientation))
+    costs += [k.limit_cost(m, "q", weight=w.limit), k.rest_cost("q", m.rest_pose, weight=w.rest)]
+    q0 = np.asarray(m.rest_pose, float).copy()
+    rep = k.solve(k.Problem(k.VariableSet.of(q=q0.copy()), costs), k.SolveOptions(max_rejections=rej))
+    _, c_ref, hist, iters, term = to.solve_multi_pose(ch, poses, q0, max_rejections=rej)
+    assert rep.iterations_run == iters and rep.termination == term
+    np.testing.assert_allclose(rep.cost_history, hist, rtol=1e-8, atol=1e-14)
+
+
+@pytest.mark.parametrize("rej", [0, 1, 3])
+def test_chain_solve_rejection_budget_matches_oracle(rej):
+    """Same budgets on the chain path (k_col_solve's trial machine: a Panda pose
+    problem routes there) against the oracle's classic LM, FP64."""
+    m = k.load_robot(k.robot_path("arm7.urdf"), k.robot_path("arm7.sidecar.json"))
+    ch = o.load_chain_files(k.robot_path("arm7.urdf"))
+    li = ch.link("flange")
+    rng = np.random.default_rng(53)
+    lq, lp, _, _ = o.fk(ch, rng.uniform(ch.lower, ch.upper, (1, ch.n)))
+    w = k.CostWeights()
+    costs = [k.pose_cost(m, "q", "flange", k.Transform3.from_parts(lq[0, li], lp[0, li]),
+                         position_weight=w.pose_position, orientation_weight=w.pose_orientation),
+             k.limit_cost(m, "q", weight=w.limit), k.rest_cost("q", m.rest_pose, weight=w.rest)]
+    q0 = np.asarray(m.rest_pose, float).copy()
+    rep = k.solve(k.Problem(k.VariableSet.of(q=q0.copy()), costs), k.SolveOptions(max_rejections=rej))
+    poses = [(li, o.qcanon(lq[0, li]), lp[0, li], w.pose_position, w.pose_orientation)]
+    _, c_ref, hist, iters, term = to.solve_multi_pose(ch, poses, q0, rest=np.asarray(m.rest_pose, float),
+                                                      max_rejections=rej)
+    assert rep.iterations_run == iters and rep.termination == term
+    np.testing.assert_allclose(rep.cost_history, hist, rtol=1e-8, atol=1e-14)
