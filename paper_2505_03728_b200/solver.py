@@ -606,7 +606,8 @@ def _options(options: SolveOptions):
     o.max_iterations, o.initial_damping = options.max_iterations, options.initial_damping
     o.damping_increase, o.damping_decrease = options.damping_increase, options.damping_decrease
     o.gradient_tolerance, o.step_tolerance = options.gradient_tolerance, options.step_tolerance
-    o.max_rejections, o.precision = options.max_rejections, _precision(options.precision)
+    # range(max_rejections) in solver.py:389: a negative budget allows no trial, like 0
+    o.max_rejections, o.precision = max(0, int(options.max_rejections)), _precision(options.precision)
     return o
 
 

@@ -226,7 +226,7 @@ class TrajectoryPlanner:
             self._vlim.ctypes.data_as(C.POINTER(C.c_double)), self._rest.ctypes.data_as(C.POINTER(C.c_double)))
         o = self.opts
         self.lm = KopLmOptions(o.max_iterations, o.initial_damping, o.damping_increase, o.damping_decrease,
-                               o.gradient_tolerance, o.step_tolerance, o.max_rejections, _precision(precision))
+                               o.gradient_tolerance, o.step_tolerance, max(0, int(o.max_rejections)), _precision(precision))
         # endpoint IK weights (tasks.py:281-289)
         ikw = ck.CostWeights.from_json({**w.to_json(), "rest": max(w.rest, 0.01)})
         if ikw.pose_position == 0.0:
